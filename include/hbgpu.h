@@ -1,0 +1,256 @@
+/*
+ * hbgpu.h -- C ABI of the B200-native HB residual-and-smoothing library
+ * (libhbgpu.so, built from paper_1304_7654_b200/csrc/).
+ *
+ * Plain pointers, sizes and a cudaStream_t passed as void*; no torch types.
+ * Every function returns 0 on success and a nonzero hbgpu status otherwise;
+ * hbgpu_last_error() describes the last failure on the calling thread.
+ * All device pointers are caller-owned; the library never allocates device
+ * memory except the CUDA graph it may instantiate inside an engine.
+ *
+ * Each entry point names the reference interface it replaces (file:line
+ * under /root/reference/pkg/src/hbproxy/).
+ */
+#ifndef HBGPU_H
+#define HBGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HBGPU_ABI_VERSION 1
+#define HBGPU_NPDE 4
+/* largest snapshot count handled by the register-window stage kernels;
+ * larger P runs the generic kernel */
+#define HBGPU_MAX_TEMPLATED_P 17
+/* largest snapshot count of the library (forcing amplitudes travel as a
+ * kernel parameter of HBGPU_MAX_P*4 doubles) */
+#define HBGPU_MAX_P 127
+/* elements of the device row lead: cell i (0 = west halo) of row j sits at
+ * row_base + HBGPU_ROW_LEAD + i, so interior cell i=1 is 32-byte aligned */
+#define HBGPU_ROW_LEAD 3
+
+enum {
+    HBGPU_OK = 0,
+    HBGPU_ERR_CUDA = 1,
+    HBGPU_ERR_ARG = 2,
+    HBGPU_ERR_NCCL = 3,
+    HBGPU_ERR_UNSUPPORTED = 4
+};
+
+/* ---- device data layout -------------------------------------------------
+ * A "slot" is one device allocation holding the full state of every block a
+ * rank owns.  Block b's value (n, p, j, i) -- plane n, pde p, array row j in
+ * [0, nj+1], array column i in [0, ni+1] -- lives at element
+ *     base + (n*4 + p)*ps + j*pitch + HBGPU_ROW_LEAD + i
+ * of the slot.  Three slots rotate through the RK stages.                  */
+typedef struct hbgpu_block {
+    int64_t base;        /* element offset of (0,0,0,-LEAD) in every slot   */
+    int64_t ps;          /* elements between consecutive (n, p) planes      */
+    int32_t ni, nj;      /* interior cells                                  */
+    int32_t pitch;       /* row stride, elements (multiple of 4)            */
+    int32_t gid;         /* global block id                                 */
+    int32_t tiles_i;     /* ceil(ni / 32)                                   */
+    int32_t tiles_j;     /* ceil(nj / tile_rows)                            */
+    int32_t cta_begin;   /* first CTA of this block in the stage grid       */
+    int32_t ncta;        /* tiles_i * tiles_j                               */
+    double nu_h2;        /* NU / (h*h)          (hbcore.py:257)             */
+    double adv_2h;       /* ADVECTION / (2*h)   (hbcore.py:257)             */
+    double h;
+    int64_t sxy_off;     /* element offset of this block's (nj, ni) sxy     */
+    int64_t face_off[4]; /* entry offset into the face-target pool per face
+                            (south, north, west, east), -1 = no cut cell    */
+} hbgpu_block;
+
+/* Halo target of one interior face cell (fused halo forwarding):
+ *   ps >  0 : local halo cell, element `off` of the output slot at (n,p)=(0,0),
+ *             stride ps between (n,p) planes;
+ *   ps == 0 : no target (non-cut boundary cell);
+ *   ps <  0 : remote, send-buffer element off + n*4 + p (element-major,
+ *             exchange.py:248-252).                                        */
+typedef struct hbgpu_face_target {
+    int64_t off;
+    int64_t ps;
+} hbgpu_face_target;
+
+/* One halo copy direction for the standalone halo kernel (priming exchange,
+ * unpack after a receive, exchange_halos).  Value v = n*4 + p of element e
+ * moves from src_base[src_off + e*src_es + v*src_vs] to
+ * dst_base[dst_off + e*dst_es + v*dst_vs]; `src_kind`/`dst_kind` select the
+ * base: 0 = the state slot, 1 = send buffer, 2 = receive buffer.           */
+typedef struct hbgpu_halo_dir {
+    int64_t src_off, src_es, src_vs;
+    int64_t dst_off, dst_es, dst_vs;
+    int32_t length;
+    int32_t src_kind, dst_kind;
+    int32_t pad;
+} hbgpu_halo_dir;
+
+/* Force-integration segment: one (block, face) body face, in reference
+ * order (blocks ascending, body_faces order; hbcore.py:369-381).          */
+typedef struct hbgpu_force_seg {
+    int64_t start;       /* element offset of face cell 1 at (n,p)=(0,0)   */
+    int64_t stride;      /* elements between consecutive face cells        */
+    int64_t ps;          /* elements between (n, p) planes                 */
+    int32_t length;      /* face extent                                    */
+    int32_t body;
+    double h;
+} hbgpu_force_seg;
+
+/* Remote transfer of one cut direction (NCCL send or receive). */
+typedef struct hbgpu_peer_msg {
+    int32_t peer;        /* rank */
+    int32_t pad;
+    int64_t offset;      /* element offset in the send / receive buffer     */
+    int64_t count;       /* doubles                                        */
+} hbgpu_peer_msg;
+
+/* ---- kernel-level drop-ins (reference dense layout) ----------------------
+ * q/q0: (planes, npde, nj2, ni2) C-order fp64; resid/src: (planes, npde,
+ * nj2-2, ni2-2).  Bounds are the reference's array coordinates.           */
+
+/* replaces hbcore._residual_kernel (hbcore.py:184-221) */
+int hbgpu_residual(const double *q, const double *dmat, const double *src,
+                   double nu_h2, double adv_2h, double *out,
+                   int64_t planes, int64_t npde, int64_t nj2, int64_t ni2,
+                   int64_t n_lo, int64_t n_hi, int64_t j_lo, int64_t j_hi,
+                   void *stream);
+
+/* replaces hbcore._update_kernel (hbcore.py:224-245).  Instead of the
+ * poisoned accumulator the kernel atomically lowers *first_bad (device,
+ * initialise to UINT64_MAX) to the linear interior index
+ * ((n*npde + p)*nj + (j-1))*ni + (i-1) of any non-finite value it writes. */
+int hbgpu_update(double *q, double *q0, const double *resid, double coef,
+                 int snapshot, int64_t planes, int64_t npde, int64_t nj2,
+                 int64_t ni2, int64_t n_lo, int64_t n_hi, int64_t j_lo,
+                 int64_t j_hi, unsigned long long *first_bad, void *stream);
+
+/* replaces the np.argwhere scan of hbcore._raise_divergence (hbcore.py:279-284):
+ * lowers *first_bad to the first non-finite interior value of q.          */
+int hbgpu_first_nonfinite(const double *q, int64_t planes, int64_t npde,
+                          int64_t nj2, int64_t ni2,
+                          unsigned long long *first_bad, void *stream);
+
+/* ---- production kernels on the slot layout ------------------------------ */
+
+typedef struct hbgpu_stage_args {
+    const double *in;          /* slot read by the stencil (q_{s-1})       */
+    const double *q0;          /* slot holding the iteration start (q_0)   */
+    double *out;               /* slot written (q_s), may equal q0         */
+    double *sendbuf;           /* remote halo payloads (may be NULL)       */
+    const hbgpu_block *blocks; /* device array [nblocks]                   */
+    const int32_t *cta_block;  /* device array [total_ctas]: CTA -> block  */
+    const double *sxy;         /* device forcing tables                    */
+    const hbgpu_face_target *faces; /* device face-target pool             */
+    double *norm_part;         /* device [total_ctas] (stage 0) or NULL    */
+    unsigned long long *status;/* device [nblocks] divergence keys         */
+    const int32_t *iter;       /* device iteration counter                 */
+    const double *dmat;        /* device P*P (generic kernel only)         */
+    int32_t nblocks;
+    int32_t total_ctas;
+    int32_t planes;
+    int32_t stage;             /* 0..3                                      */
+    int32_t tile_rows;
+    int32_t pad;
+    double coef;               /* alpha_s * dtau                            */
+    double D[HBGPU_MAX_TEMPLATED_P * HBGPU_MAX_TEMPLATED_P];
+    double ap[HBGPU_MAX_P * HBGPU_NPDE];
+} hbgpu_stage_args;
+
+/* one fused RK stage over every owned block: residual (hbcore.py:184-221),
+ * update (hbcore.py:224-245), local halo forwarding and remote pack
+ * (exchange.py:248-261), divergence keys, residual-norm partials */
+int hbgpu_stage(const hbgpu_stage_args *args, void *stream);
+
+/* standalone halo moves (exchange.py:295-316 local copy / pack / unpack) */
+int hbgpu_halo(double *slot, double *sendbuf, const double *recvbuf,
+               const hbgpu_halo_dir *dirs, int32_t ndirs, int32_t max_len,
+               int32_t planes, void *stream);
+
+/* per-block sums of the stage-0 norm partials -> sumsq[iter*nblocks + b] */
+int hbgpu_norm_fold(const hbgpu_block *blocks, int32_t nblocks,
+                    const double *norm_part, double *sumsq,
+                    const int32_t *iter, void *stream);
+
+/* per-rank force partials (hbcore.py:359-382) into
+ * hist[iter][k][n][body] (k = cl, cd, cm), then iter += 1               */
+int hbgpu_forces(const double *slot, const hbgpu_force_seg *segs,
+                 int32_t nsegs, int32_t planes, int32_t nbody, double *hist,
+                 int32_t *iter, void *stream);
+
+/* rank-ordered sum (runtime.py:290-294): out[k] = in[0][k] + in[1][k] + ...
+ * over `nranks` stacked buffers of `count` doubles                        */
+int hbgpu_ordered_fold(const double *stacked, int32_t nranks, int64_t count,
+                       double *out, void *stream);
+
+/* ---- engine: the per-rank iteration schedule (driver.py:110-149) -------- */
+
+typedef struct hbgpu_engine_desc {
+    double *slot[3];                 /* A (q0 / result), B, C              */
+    double *sendbuf, *recvbuf;
+    const hbgpu_block *blocks;       /* device */
+    const int32_t *cta_block;        /* device */
+    const double *sxy;               /* device */
+    const hbgpu_face_target *faces;  /* device */
+    const double *dmat;              /* device */
+    double *norm_part;               /* device [total_ctas] */
+    double *sumsq;                   /* device [max_iters * nblocks] */
+    unsigned long long *status;      /* device [nblocks] */
+    int32_t *iter;                   /* device, 1 element */
+    const hbgpu_halo_dir *prime_dirs;  int32_t nprime;  int32_t prime_max_len;
+    const hbgpu_halo_dir *unpack_dirs; int32_t nunpack; int32_t unpack_max_len;
+    const hbgpu_force_seg *segs;     int32_t nsegs;  /* device */
+    double *force_hist;              /* device [max_iters*3*planes*nbody] */
+    const hbgpu_peer_msg *sends;     int32_t nsends; /* HOST arrays */
+    const hbgpu_peer_msg *recvs;     int32_t nrecvs;
+    void *comm;                      /* from hbgpu_comm_init, NULL if 1 rank */
+    int32_t nblocks, total_ctas, planes, nbody, tile_rows, max_iters;
+    double coef[4];
+    double D[HBGPU_MAX_TEMPLATED_P * HBGPU_MAX_TEMPLATED_P];
+    double ap[HBGPU_MAX_P * HBGPU_NPDE];
+} hbgpu_engine_desc;
+
+/* The engine runs on its own non-blocking stream (CUDA graphs cannot be
+ * captured on the legacy default stream); every call orders that stream
+ * after the caller's `stream` on entry and the caller's stream after it on
+ * exit, so the engine behaves as if it ran on `stream`. */
+typedef struct hbgpu_engine hbgpu_engine;
+
+int hbgpu_engine_create(const hbgpu_engine_desc *desc, hbgpu_engine **out);
+/* priming halo exchange of slot A (driver.py:129) */
+int hbgpu_engine_prime(hbgpu_engine *eng, void *stream);
+/* `iterations` full iterations: 4 x (stage [+ NCCL + unpack]), norm fold,
+ * forces.  use_graph != 0 replays a CUDA graph of one iteration.          */
+int hbgpu_engine_iterate(hbgpu_engine *eng, int32_t iterations, int32_t use_graph,
+                         void *stream);
+/* kernels this engine launches per iteration (for launch accounting) */
+int hbgpu_engine_launches_per_iteration(const hbgpu_engine *eng);
+int hbgpu_engine_destroy(hbgpu_engine *eng);
+
+/* ---- NCCL plumbing (NCCL is dlopen'ed on first use) ---------------------- */
+int hbgpu_comm_unique_id(unsigned char id[128]);
+int hbgpu_comm_init(const unsigned char id[128], int32_t nranks, int32_t rank,
+                    int32_t device, void **comm);
+/* all-gather of `count` doubles per rank (ranks stacked in rank order) */
+int hbgpu_comm_allgather(void *comm, const double *send, double *recv,
+                         int64_t count, void *stream);
+int hbgpu_comm_destroy(void *comm);
+
+/* ---- misc ---------------------------------------------------------------- */
+/* sizeof / offsetof of the ABI structs, for binding checks:
+ * out[0..5] = sizeof(hbgpu_block, hbgpu_face_target, hbgpu_halo_dir,
+ * hbgpu_force_seg, hbgpu_peer_msg, hbgpu_stage_args), out[6] =
+ * sizeof(hbgpu_engine_desc), out[7] = offsetof(hbgpu_engine_desc, coef),
+ * out[8] = offsetof(hbgpu_stage_args, coef); returns the count written */
+int hbgpu_abi_layout(int64_t *out, int32_t n);
+int hbgpu_abi_version(void);
+const char *hbgpu_last_error(void);
+/* kernel launches issued by this library since load (all entry points) */
+uint64_t hbgpu_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HBGPU_H */

@@ -1,0 +1,195 @@
+/*
+ * hb_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain-C restatement of the reference's two numba kernels, used as the CPU
+ * checker for the CUDA path (tests/, __graft_entry__.smoke(), and bench.py's
+ * cpu_baseline / --impl reference legs).  Nothing in the product package
+ * (paper_1304_7654_b200/) links or calls this file.
+ *
+ * Follows, operation for operation:
+ *   _residual_kernel  /root/reference/pkg/src/hbproxy/hbcore.py:184-221
+ *   _update_kernel    /root/reference/pkg/src/hbproxy/hbcore.py:224-245
+ *
+ * Per interior point the reference rounds, in this order (hbcore.py:7-13,
+ * 197-221):  t=4c; t-=w; t-=e; t-=s; t-=n; t*=nu_h2; u=(e-w)*adv_2h;
+ * o=t+u; for m ascending: o += D[n][m]*q[m]; o += src.  numba compiles it
+ * without fastmath, so there is no FMA contraction; this file is compiled
+ * with -ffp-contract=off for the same reason.  The three passes of the
+ * reference are fused into one pass here: per point the rounding sequence
+ * is identical, only the loop order differs.
+ *
+ * Layout: the reference's C-order float64 arrays, q/q0 of shape
+ * (planes, npde, nj+2, ni+2), resid/src of shape (planes, npde, nj, ni).
+ */
+#include <math.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include <pthread.h>
+
+typedef struct {
+    long planes, npde, nj2, ni2;
+} dims_t;
+
+static inline size_t qidx(const dims_t *d, long n, long p, long j, long i) {
+    return (((size_t)n * d->npde + p) * d->nj2 + j) * d->ni2 + i;
+}
+
+static inline size_t ridx(const dims_t *d, long n, long p, long j, long i) {
+    return (((size_t)n * d->npde + p) * (d->nj2 - 2) + j) * (d->ni2 - 2) + i;
+}
+
+/* one (n, p, row j) of the residual; j in array coordinates */
+static void residual_row(const double *q, const double *dmat, const double *src,
+                         double nu_h2, double adv_2h, double *out,
+                         const dims_t *d, long n, long p, long j) {
+    const long planes = d->planes;
+    const long ni2 = d->ni2;
+    const double *row = q + qidx(d, n, p, j, 0);
+    const double *rs = q + qidx(d, n, p, j - 1, 0);
+    const double *rn = q + qidx(d, n, p, j + 1, 0);
+    double *o = out + ridx(d, n, p, j - 1, 0);
+    const double *sr = src + ridx(d, n, p, j - 1, 0);
+    for (long i = 1; i < ni2 - 1; ++i) {
+        double c = row[i], w = row[i - 1], e = row[i + 1];
+        double s = rs[i], nn = rn[i];
+        double t = 4.0 * c;
+        t = t - w;
+        t = t - e;
+        t = t - s;
+        t = t - nn;
+        t = t * nu_h2;
+        double u = (e - w) * adv_2h;
+        double acc = t + u;
+        for (long m = 0; m < planes; ++m) {
+            double prod = dmat[n * planes + m] * q[qidx(d, m, p, j, i)];
+            acc = acc + prod;
+        }
+        acc = acc + sr[i - 1];
+        o[i - 1] = acc;
+    }
+}
+
+/* _residual_kernel(q, dmat, src, nu_h2, adv_2h, out, n_lo, n_hi, j_lo, j_hi) */
+void oracle_residual(const double *q, const double *dmat, const double *src,
+                     double nu_h2, double adv_2h, double *out,
+                     long planes, long npde, long nj2, long ni2,
+                     long n_lo, long n_hi, long j_lo, long j_hi) {
+    dims_t d = {planes, npde, nj2, ni2};
+    for (long n = n_lo; n < n_hi; ++n)
+        for (long p = 0; p < npde; ++p)
+            for (long j = j_lo; j < j_hi; ++j)
+                residual_row(q, dmat, src, nu_h2, adv_2h, out, &d, n, p, j);
+}
+
+/* _update_kernel(q, q0, resid, coef, snapshot, n_lo, n_hi, j_lo, j_hi) -> acc */
+double oracle_update(double *q, double *q0, const double *resid, double coef,
+                     int snapshot, long planes, long npde, long nj2, long ni2,
+                     long n_lo, long n_hi, long j_lo, long j_hi) {
+    dims_t d = {planes, npde, nj2, ni2};
+    double acc = 0.0;
+    if (snapshot) {
+        for (long n = n_lo; n < n_hi; ++n)
+            for (long p = 0; p < npde; ++p)
+                for (long j = j_lo; j < j_hi; ++j)
+                    for (long i = 0; i < ni2; ++i)
+                        q0[qidx(&d, n, p, j, i)] = q[qidx(&d, n, p, j, i)];
+    }
+    for (long n = n_lo; n < n_hi; ++n)
+        for (long p = 0; p < npde; ++p)
+            for (long j = j_lo; j < j_hi; ++j)
+                for (long i = 1; i < ni2 - 1; ++i) {
+                    double v = q0[qidx(&d, n, p, j, i)] - coef * resid[ridx(&d, n, p, j - 1, i - 1)];
+                    q[qidx(&d, n, p, j, i)] = v;
+                    acc += v - v;
+                }
+    return acc;
+}
+
+/*
+ * Whole-stage driver used by the CPU baseline: for every listed block, the
+ * full-interior residual and then the full-interior update (residual nest,
+ * barrier, update nest -- driver.py:133-136 with hybrid.py:233-249).  Work is
+ * split over (block, plane) pairs across `nthreads` pthreads; the rows of one
+ * plane stay on one thread, so the per-point rounding is unchanged.  Returns
+ * the number of blocks whose update produced a non-finite value.
+ */
+typedef struct {
+    int nblk;
+    double *const *q;
+    double *const *q0;
+    double *const *resid;
+    const double *const *src;
+    const long *ni, *nj;
+    const double *nu_h2, *adv_2h, *dmat;
+    long planes, npde;
+    double coef;
+    int snapshot;
+    int phase;          /* 0 = residual, 1 = update */
+    int nthreads;
+    double *accs;       /* per (block, plane) */
+} stage_job_t;
+
+typedef struct {
+    stage_job_t *job;
+    int tid;
+} stage_arg_t;
+
+static void *stage_worker(void *varg) {
+    stage_arg_t *a = (stage_arg_t *)varg;
+    stage_job_t *s = a->job;
+    long total = (long)s->nblk * s->planes;
+    for (long t = a->tid; t < total; t += s->nthreads) {
+        long b = t / s->planes, n = t % s->planes;
+        dims_t d = {s->planes, s->npde, s->nj[b] + 2, s->ni[b] + 2};
+        if (s->phase == 0) {
+            for (long p = 0; p < s->npde; ++p)
+                for (long j = 1; j < s->nj[b] + 1; ++j)
+                    residual_row(s->q[b], s->dmat, s->src[b], s->nu_h2[b], s->adv_2h[b],
+                                 s->resid[b], &d, n, p, j);
+        } else {
+            s->accs[t] = oracle_update(s->q[b], s->q0[b], s->resid[b], s->coef, s->snapshot,
+                                       s->planes, s->npde, s->nj[b] + 2, s->ni[b] + 2,
+                                       n, n + 1, 1, s->nj[b] + 1);
+        }
+    }
+    return NULL;
+}
+
+static void run_phase(stage_job_t *job) {
+    pthread_t th[256];
+    stage_arg_t args[256];
+    int nt = job->nthreads;
+    for (int t = 0; t < nt; ++t) {
+        args[t].job = job;
+        args[t].tid = t;
+        if (t > 0) pthread_create(&th[t], NULL, stage_worker, &args[t]);
+    }
+    stage_worker(&args[0]);
+    for (int t = 1; t < nt; ++t) pthread_join(th[t], NULL);
+}
+
+int oracle_stage_many(int nblk, double *const *q, double *const *q0,
+                      double *const *resid, const double *const *src,
+                      const long *ni, const long *nj, const double *nu_h2,
+                      const double *adv_2h, const double *dmat, long planes,
+                      long npde, double coef, int snapshot, int nthreads,
+                      double *accs /* nblk * planes scratch */) {
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    stage_job_t job = {nblk, q, q0, resid, src, ni, nj, nu_h2, adv_2h, dmat,
+                       planes, npde, coef, snapshot, 0, nthreads, accs};
+    run_phase(&job);   /* residual nest */
+    job.phase = 1;
+    run_phase(&job);   /* update nest, after the implicit barrier (join) */
+    int bad = 0;
+    for (int b = 0; b < nblk; ++b) {
+        int blk_bad = 0;
+        for (long n = 0; n < planes; ++n) {
+            double a = accs[(long)b * planes + n];
+            if (a != 0.0 || a != a) blk_bad = 1;
+        }
+        bad += blk_bad;
+    }
+    return bad;
+}

@@ -1,0 +1,236 @@
+// hb_aux.cu -- the small kernels around the stage kernel:
+//   * standalone halo moves (priming exchange, unpack, exchange_halos);
+//   * residual-norm folding;
+//   * force integration and the rank-ordered fold;
+//   * the kernel-level drop-ins for _residual_kernel / _update_kernel on the
+//     reference's dense (planes, npde, nj+2, ni+2) layout.
+
+#include "hb_common.cuh"
+
+namespace hbgpu {
+
+// ---- halo moves (exchange.py:195-202, 248-261) ------------------------------
+
+__global__ void halo_kernel(double *slot, double *sendbuf, const double *recvbuf,
+                            const hbgpu_halo_dir *dirs, int nv) {
+    const hbgpu_halo_dir d = dirs[blockIdx.y];
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)d.length * nv) return;
+    const int64_t e = idx / nv;
+    const int64_t v = idx - e * nv;
+    const double *src = d.src_kind == 0 ? slot : (d.src_kind == 1 ? sendbuf : recvbuf);
+    double *dst = d.dst_kind == 0 ? slot : sendbuf;
+    dst[d.dst_off + e * d.dst_es + v * d.dst_vs] = src[d.src_off + e * d.src_es + v * d.src_vs];
+}
+
+// ---- residual norm ----------------------------------------------------------
+
+// per block: sequential sum of its CTAs' partials in CTA order
+__global__ void norm_fold_kernel(const hbgpu_block *blocks, int nblocks, const double *part,
+                                 double *sumsq, const int32_t *iter) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nblocks) return;
+    const hbgpu_block &blk = blocks[b];
+    double s = 0.0;
+    for (int c = 0; c < blk.ncta; ++c) s = radd(s, part[blk.cta_begin + c]);
+    sumsq[(int64_t)(*iter) * nblocks + b] = s;
+}
+
+// ---- forces (hbcore.py:359-382) --------------------------------------------
+
+// one thread per (coefficient k, plane n, body): a strict left-to-right fold
+// of h*q over the body's face segments in reference order.  Then one thread
+// advances the device iteration counter (this is the iteration's last kernel).
+__global__ void forces_kernel(const double *slot, const hbgpu_force_seg *segs, int nsegs,
+                              int planes, int nbody, double *hist, int32_t *iter) {
+    const int it = *iter;
+    const int total = 3 * planes * nbody;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+        const int body = t % nbody;
+        const int n = (t / nbody) % planes;
+        const int k = t / (nbody * planes);
+        double acc = 0.0;
+        for (int s = 0; s < nsegs; ++s) {
+            const hbgpu_force_seg g = segs[s];
+            if (g.body != body) continue;
+            const double *f = slot + g.start + (int64_t)(n * NPDE + k) * g.ps;
+            int c = 0;
+            for (; c + 8 <= g.length; c += 8) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = f[(int64_t)(c + u) * g.stride];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc = radd(acc, rmul(g.h, v[u]));
+            }
+            for (; c < g.length; ++c) acc = radd(acc, rmul(g.h, f[(int64_t)c * g.stride]));
+        }
+        hist[(int64_t)it * total + t] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *iter = it + 1;
+}
+
+// runtime.py:290-294: acc = buf[0]; acc += buf[1]; ...
+__global__ void ordered_fold_kernel(const double *stacked, int nranks, int64_t count, double *out) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= count) return;
+    double acc = stacked[k];
+    for (int r = 1; r < nranks; ++r) acc = radd(acc, stacked[(int64_t)r * count + k]);
+    out[k] = acc;
+}
+
+// ---- dense-layout drop-ins -------------------------------------------------
+
+struct Dense {
+    int64_t planes, npde, nj2, ni2;
+    __device__ int64_t q(int64_t n, int64_t p, int64_t j, int64_t i) const {
+        return ((n * npde + p) * nj2 + j) * ni2 + i;
+    }
+    __device__ int64_t r(int64_t n, int64_t p, int64_t j, int64_t i) const {
+        return ((n * npde + p) * (nj2 - 2) + j) * (ni2 - 2) + i;
+    }
+};
+
+__global__ void residual_dense_kernel(const double *q, const double *dmat, const double *src,
+                                      double nu_h2, double adv_2h, double *out, Dense d,
+                                      int64_t n_lo, int64_t n_hi, int64_t j_lo, int64_t j_hi) {
+    const int64_t ni = d.ni2 - 2;
+    const int64_t rows = j_hi - j_lo;
+    const int64_t total = (n_hi - n_lo) * d.npde * rows * ni;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t % ni + 1;
+        int64_t rest = t / ni;
+        const int64_t j = rest % rows + j_lo;
+        rest /= rows;
+        const int64_t p = rest % d.npde;
+        const int64_t n = rest / d.npde + n_lo;
+        const double *c = q + d.q(n, p, j, i);
+        double o = stencil(c[0], c[-1], c[1], c[-d.ni2], c[d.ni2], nu_h2, adv_2h);
+        for (int64_t m = 0; m < d.planes; ++m)
+            o = radd(o, rmul(dmat[n * d.planes + m], q[d.q(m, p, j, i)]));
+        o = radd(o, src[d.r(n, p, j - 1, i - 1)]);
+        out[d.r(n, p, j - 1, i - 1)] = o;
+    }
+}
+
+// snapshot (all columns of the rows, halo columns included) and update
+// (interior); each element depends only on itself, so one pass suffices.
+__global__ void update_dense_kernel(double *q, double *q0, const double *resid, double coef,
+                                    int snapshot, Dense d, int64_t n_lo, int64_t n_hi,
+                                    int64_t j_lo, int64_t j_hi, unsigned long long *first_bad) {
+    const int64_t ni = d.ni2 - 2, nj = d.nj2 - 2;
+    const int64_t rows = j_hi - j_lo;
+    const int64_t total = (n_hi - n_lo) * d.npde * rows * d.ni2;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t % d.ni2;
+        int64_t rest = t / d.ni2;
+        const int64_t j = rest % rows + j_lo;
+        rest /= rows;
+        const int64_t p = rest % d.npde;
+        const int64_t n = rest / d.npde + n_lo;
+        const int64_t k = d.q(n, p, j, i);
+        if (snapshot) q0[k] = q[k];
+        if (i == 0 || i == d.ni2 - 1) continue;
+        const double v = rsub(q0[k], rmul(coef, resid[d.r(n, p, j - 1, i - 1)]));
+        q[k] = v;
+        if (nonfinite(v))
+            atomicMin(first_bad, (unsigned long long)((((n * d.npde + p) * nj) + (j - 1)) * ni + (i - 1)));
+    }
+}
+
+__global__ void first_nonfinite_kernel(const double *q, Dense d, unsigned long long *first_bad) {
+    const int64_t ni = d.ni2 - 2, nj = d.nj2 - 2;
+    const int64_t total = d.planes * d.npde * nj * ni;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t % ni;
+        int64_t rest = t / ni;
+        const int64_t j = rest % nj;
+        const int64_t np = rest / nj;
+        if (nonfinite(q[(np * d.nj2 + j + 1) * d.ni2 + i + 1])) atomicMin(first_bad, (unsigned long long)t);
+    }
+}
+
+static int grid_for(int64_t total) {
+    int64_t g = (total + 255) / 256;
+    if (g > 148 * 64) g = 148 * 64;
+    return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace hbgpu
+
+using namespace hbgpu;
+
+extern "C" int hbgpu_halo(double *slot, double *sendbuf, const double *recvbuf,
+                          const hbgpu_halo_dir *dirs, int32_t ndirs, int32_t max_len,
+                          int32_t planes, void *stream) {
+    if (ndirs <= 0 || max_len <= 0) return HBGPU_OK;
+    const int nv = planes * NPDE;
+    dim3 grid((unsigned)(((int64_t)max_len * nv + 127) / 128), (unsigned)ndirs);
+    halo_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(slot, sendbuf, recvbuf, dirs, nv);
+    hbgpu_count_launch(1);
+    return hbgpu_check_launch("hbgpu_halo");
+}
+
+extern "C" int hbgpu_norm_fold(const hbgpu_block *blocks, int32_t nblocks, const double *norm_part,
+                               double *sumsq, const int32_t *iter, void *stream) {
+    norm_fold_kernel<<<(nblocks + 127) / 128, 128, 0, (cudaStream_t)stream>>>(blocks, nblocks, norm_part,
+                                                                            sumsq, iter);
+    hbgpu_count_launch(1);
+    return hbgpu_check_launch("hbgpu_norm_fold");
+}
+
+extern "C" int hbgpu_forces(const double *slot, const hbgpu_force_seg *segs, int32_t nsegs,
+                            int32_t planes, int32_t nbody, double *hist, int32_t *iter, void *stream) {
+    int threads = 3 * planes * nbody;
+    threads = threads < 32 ? 32 : (threads > 1024 ? 1024 : ((threads + 31) / 32) * 32);
+    forces_kernel<<<1, threads, 0, (cudaStream_t)stream>>>(slot, segs, nsegs, planes, nbody, hist, iter);
+    hbgpu_count_launch(1);
+    return hbgpu_check_launch("hbgpu_forces");
+}
+
+extern "C" int hbgpu_ordered_fold(const double *stacked, int32_t nranks, int64_t count, double *out,
+                                  void *stream) {
+    if (count <= 0) return HBGPU_OK;
+    ordered_fold_kernel<<<(unsigned)((count + 127) / 128), 128, 0, (cudaStream_t)stream>>>(stacked, nranks,
+                                                                                        count, out);
+    hbgpu_count_launch(1);
+    return hbgpu_check_launch("hbgpu_ordered_fold");
+}
+
+extern "C" int hbgpu_residual(const double *q, const double *dmat, const double *src, double nu_h2,
+                              double adv_2h, double *out, int64_t planes, int64_t npde, int64_t nj2,
+                              int64_t ni2, int64_t n_lo, int64_t n_hi, int64_t j_lo, int64_t j_hi,
+                              void *stream) {
+    if (n_hi <= n_lo || j_hi <= j_lo || ni2 < 3) return HBGPU_OK;
+    Dense d{planes, npde, nj2, ni2};
+    const int64_t total = (n_hi - n_lo) * npde * (j_hi - j_lo) * (ni2 - 2);
+    residual_dense_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(q, dmat, src, nu_h2, adv_2h,
+                                                                           out, d, n_lo, n_hi, j_lo, j_hi);
+    hbgpu_count_launch(1);
+    return hbgpu_check_launch("hbgpu_residual");
+}
+
+extern "C" int hbgpu_update(double *q, double *q0, const double *resid, double coef, int snapshot,
+                            int64_t planes, int64_t npde, int64_t nj2, int64_t ni2, int64_t n_lo,
+                            int64_t n_hi, int64_t j_lo, int64_t j_hi, unsigned long long *first_bad,
+                            void *stream) {
+    if (n_hi <= n_lo || j_hi <= j_lo) return HBGPU_OK;
+    Dense d{planes, npde, nj2, ni2};
+    const int64_t total = (n_hi - n_lo) * npde * (j_hi - j_lo) * ni2;
+    update_dense_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(q, q0, resid, coef, snapshot, d,
+                                                                         n_lo, n_hi, j_lo, j_hi, first_bad);
+    hbgpu_count_launch(1);
+    return hbgpu_check_launch("hbgpu_update");
+}
+
+extern "C" int hbgpu_first_nonfinite(const double *q, int64_t planes, int64_t npde, int64_t nj2,
+                                     int64_t ni2, unsigned long long *first_bad, void *stream) {
+    Dense d{planes, npde, nj2, ni2};
+    const int64_t total = planes * npde * (nj2 - 2) * (ni2 - 2);
+    first_nonfinite_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(q, d, first_bad);
+    hbgpu_count_launch(1);
+    return hbgpu_check_launch("hbgpu_first_nonfinite");
+}

@@ -1,0 +1,51 @@
+// Shared device helpers for libhbgpu (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hbgpu.h"
+
+namespace hbgpu {
+
+constexpr int LEAD = HBGPU_ROW_LEAD;
+constexpr int NPDE = HBGPU_NPDE;
+constexpr int MAXP = HBGPU_MAX_TEMPLATED_P;
+constexpr unsigned long long NO_BAD = ~0ull;
+
+// Every floating-point operation on the path is an explicitly rounded
+// multiply / add / subtract: the reference's kernels are compiled without
+// fastmath (no FMA contraction), and bitwise parity needs the
+// same rounding sequence.  The library is also built with --fmad=false.
+__device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rsub(double a, double b) { return __dsub_rn(a, b); }
+
+// The per-point residual prefix of hbcore.py:197-209:
+//   t = 4c; t -= w; t -= e; t -= s; t -= n; t *= nu_h2; u = (e - w) adv_2h; t + u
+__device__ __forceinline__ double stencil(double c, double w, double e, double s, double n,
+                                          double nu_h2, double adv_2h) {
+    double t = rmul(4.0, c);
+    t = rsub(t, w);
+    t = rsub(t, e);
+    t = rsub(t, s);
+    t = rsub(t, n);
+    t = rmul(t, nu_h2);
+    double u = rmul(rsub(e, w), adv_2h);
+    return radd(t, u);
+}
+
+// Divergence key: first (iteration, stage) in the high bits, then the
+// lexicographic (n, p, j, i) interior index (hbcore.py:279-284), so an
+// atomicMin keeps the reference's "first offending cell" per block.
+__device__ __forceinline__ unsigned long long divergence_key(int gstage, long long lin) {
+    return ((unsigned long long)(unsigned)gstage << 40) | (unsigned long long)lin;
+}
+
+__device__ __forceinline__ bool nonfinite(double v) { return !isfinite(v); }
+
+}  // namespace hbgpu
+
+extern "C" void hbgpu_set_error(const char *fmt, ...);
+extern "C" void hbgpu_count_launch(uint64_t n);
+int hbgpu_check_launch(const char *what);

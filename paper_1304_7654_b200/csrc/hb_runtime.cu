@@ -1,0 +1,351 @@
+// hb_runtime.cu -- error state, launch accounting, NCCL plumbing and the
+// per-rank iteration engine (the schedule of driver.py:110-149, run on one
+// CUDA stream, optionally as a replayed CUDA graph of one iteration).
+
+#include <dlfcn.h>
+#include <stdarg.h>
+#include <stddef.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <vector>
+
+#include "hb_common.cuh"
+
+// NCCL's header from the venv (2.28.x) for the types; the functions are
+// resolved with dlsym on first use, so single-GPU use never needs NCCL.
+#include <nccl.h>
+
+static thread_local char g_err[512] = "";
+static std::atomic<uint64_t> g_launches{0};
+
+extern "C" void hbgpu_set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+extern "C" void hbgpu_count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int hbgpu_check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        hbgpu_set_error("%s: %s", what, cudaGetErrorString(e));
+        return HBGPU_ERR_CUDA;
+    }
+    return HBGPU_OK;
+}
+
+extern "C" const char *hbgpu_last_error(void) { return g_err; }
+extern "C" int hbgpu_abi_version(void) { return HBGPU_ABI_VERSION; }
+extern "C" uint64_t hbgpu_launch_count(void) { return g_launches.load(); }
+
+extern "C" int hbgpu_abi_layout(int64_t *out, int32_t n) {
+    const int64_t v[] = {(int64_t)sizeof(hbgpu_block),       (int64_t)sizeof(hbgpu_face_target),
+                         (int64_t)sizeof(hbgpu_halo_dir),    (int64_t)sizeof(hbgpu_force_seg),
+                         (int64_t)sizeof(hbgpu_peer_msg),    (int64_t)sizeof(hbgpu_stage_args),
+                         (int64_t)sizeof(hbgpu_engine_desc), (int64_t)offsetof(hbgpu_engine_desc, coef),
+                         (int64_t)offsetof(hbgpu_stage_args, coef)};
+    int k = 0;
+    for (; k < n && k < (int)(sizeof(v) / sizeof(v[0])); ++k) out[k] = v[k];
+    return k;
+}
+
+// ---- NCCL via dlopen --------------------------------------------------------
+
+namespace {
+
+struct NcclApi {
+    bool loaded = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi g_nccl;
+
+bool load_nccl() {
+    if (g_nccl.loaded) return true;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        hbgpu_set_error("cannot dlopen libnccl.so.2: %s", dlerror());
+        return false;
+    }
+#define HB_SYM(field, name)                                              \
+    g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name)); \
+    if (!g_nccl.field) {                                                 \
+        hbgpu_set_error("libnccl lacks %s", name);                       \
+        return false;                                                    \
+    }
+    HB_SYM(GetUniqueId, "ncclGetUniqueId");
+    HB_SYM(CommInitRank, "ncclCommInitRank");
+    HB_SYM(CommDestroy, "ncclCommDestroy");
+    HB_SYM(GroupStart, "ncclGroupStart");
+    HB_SYM(GroupEnd, "ncclGroupEnd");
+    HB_SYM(Send, "ncclSend");
+    HB_SYM(Recv, "ncclRecv");
+    HB_SYM(AllGather, "ncclAllGather");
+    HB_SYM(GetErrorString, "ncclGetErrorString");
+#undef HB_SYM
+    g_nccl.loaded = true;
+    return true;
+}
+
+int nccl_fail(const char *what, ncclResult_t r) {
+    hbgpu_set_error("%s: %s", what, g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "nccl error");
+    return HBGPU_ERR_NCCL;
+}
+
+}  // namespace
+
+extern "C" int hbgpu_comm_unique_id(unsigned char id[128]) {
+    if (!load_nccl()) return HBGPU_ERR_NCCL;
+    ncclUniqueId uid;
+    ncclResult_t r = g_nccl.GetUniqueId(&uid);
+    if (r != ncclSuccess) return nccl_fail("ncclGetUniqueId", r);
+    memcpy(id, uid.internal, 128);
+    return HBGPU_OK;
+}
+
+extern "C" int hbgpu_comm_init(const unsigned char id[128], int32_t nranks, int32_t rank, int32_t device,
+                               void **comm) {
+    if (!load_nccl()) return HBGPU_ERR_NCCL;
+    if (cudaSetDevice(device) != cudaSuccess) return hbgpu_check_launch("cudaSetDevice");
+    ncclUniqueId uid;
+    memcpy(uid.internal, id, 128);
+    ncclComm_t c;
+    ncclResult_t r = g_nccl.CommInitRank(&c, nranks, uid, rank);
+    if (r != ncclSuccess) return nccl_fail("ncclCommInitRank", r);
+    *comm = (void *)c;
+    return HBGPU_OK;
+}
+
+extern "C" int hbgpu_comm_allgather(void *comm, const double *send, double *recv, int64_t count,
+                                    void *stream) {
+    if (!load_nccl()) return HBGPU_ERR_NCCL;
+    ncclResult_t r = g_nccl.AllGather(send, recv, (size_t)count, ncclFloat64, (ncclComm_t)comm,
+                                      (cudaStream_t)stream);
+    if (r != ncclSuccess) return nccl_fail("ncclAllGather", r);
+    return HBGPU_OK;
+}
+
+extern "C" int hbgpu_comm_destroy(void *comm) {
+    if (comm == nullptr) return HBGPU_OK;
+    if (!load_nccl()) return HBGPU_ERR_NCCL;
+    ncclResult_t r = g_nccl.CommDestroy((ncclComm_t)comm);
+    if (r != ncclSuccess) return nccl_fail("ncclCommDestroy", r);
+    return HBGPU_OK;
+}
+
+// ---- engine -------------------------------------------------------------------
+
+struct hbgpu_engine {
+    hbgpu_engine_desc d;
+    cudaStream_t work = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    std::vector<hbgpu_peer_msg> sends, recvs;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+};
+
+namespace {
+
+// slot rotation per stage: (in, out); q0 is always slot 0 (A).
+//   stage 0: A -> B, stage 1: B -> C, stage 2: C -> B, stage 3: B -> A (in place on q0)
+constexpr int kIn[4] = {0, 1, 2, 1};
+constexpr int kOut[4] = {1, 2, 1, 0};
+
+int exchange_remote(hbgpu_engine *e, double *slot, cudaStream_t s) {
+    const hbgpu_engine_desc &d = e->d;
+    if (d.comm == nullptr || (e->sends.empty() && e->recvs.empty())) return HBGPU_OK;
+    if (!load_nccl()) return HBGPU_ERR_NCCL;
+    ncclComm_t comm = (ncclComm_t)d.comm;
+    ncclResult_t r = g_nccl.GroupStart();
+    if (r != ncclSuccess) return nccl_fail("ncclGroupStart", r);
+    for (const auto &m : e->sends) {
+        r = g_nccl.Send(d.sendbuf + m.offset, (size_t)m.count, ncclFloat64, m.peer, comm, s);
+        if (r != ncclSuccess) return nccl_fail("ncclSend", r);
+    }
+    for (const auto &m : e->recvs) {
+        r = g_nccl.Recv(d.recvbuf + m.offset, (size_t)m.count, ncclFloat64, m.peer, comm, s);
+        if (r != ncclSuccess) return nccl_fail("ncclRecv", r);
+    }
+    r = g_nccl.GroupEnd();
+    if (r != ncclSuccess) return nccl_fail("ncclGroupEnd", r);
+    return hbgpu_halo(slot, d.sendbuf, d.recvbuf, d.unpack_dirs, d.nunpack, d.unpack_max_len, d.planes, s);
+}
+
+int one_iteration(hbgpu_engine *e, cudaStream_t s) {
+    const hbgpu_engine_desc &d = e->d;
+    hbgpu_stage_args a;
+    memset(&a, 0, sizeof(a));
+    a.q0 = d.slot[0];
+    a.sendbuf = d.sendbuf;
+    a.blocks = d.blocks;
+    a.cta_block = d.cta_block;
+    a.sxy = d.sxy;
+    a.faces = d.faces;
+    a.status = d.status;
+    a.iter = d.iter;
+    a.dmat = d.dmat;
+    a.nblocks = d.nblocks;
+    a.total_ctas = d.total_ctas;
+    a.planes = d.planes;
+    a.tile_rows = d.tile_rows;
+    memcpy(a.D, d.D, sizeof(a.D));
+    memcpy(a.ap, d.ap, sizeof(a.ap));
+    for (int st = 0; st < 4; ++st) {
+        a.in = d.slot[kIn[st]];
+        a.out = d.slot[kOut[st]];
+        a.stage = st;
+        a.coef = d.coef[st];
+        a.norm_part = st == 0 ? d.norm_part : nullptr;
+        int rc = hbgpu_stage(&a, s);
+        if (rc) return rc;
+        rc = exchange_remote(e, d.slot[kOut[st]], s);
+        if (rc) return rc;
+        if (st == 0) {
+            rc = hbgpu_norm_fold(d.blocks, d.nblocks, d.norm_part, d.sumsq, d.iter, s);
+            if (rc) return rc;
+        }
+    }
+    return hbgpu_forces(d.slot[0], d.segs, d.nsegs, d.planes, d.nbody, d.force_hist, d.iter, s);
+}
+
+}  // namespace
+
+extern "C" int hbgpu_engine_create(const hbgpu_engine_desc *desc, hbgpu_engine **out) {
+    if (desc == nullptr || out == nullptr || desc->planes < 1 || desc->nblocks < 1) {
+        hbgpu_set_error("hbgpu_engine_create: bad descriptor");
+        return HBGPU_ERR_ARG;
+    }
+    auto *e = new hbgpu_engine();
+    e->d = *desc;
+    if (desc->nsends > 0) e->sends.assign(desc->sends, desc->sends + desc->nsends);
+    if (desc->nrecvs > 0) e->recvs.assign(desc->recvs, desc->recvs + desc->nrecvs);
+    e->d.sends = nullptr;
+    e->d.recvs = nullptr;
+    if (cudaStreamCreateWithFlags(&e->work, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_out, cudaEventDisableTiming) != cudaSuccess) {
+        int rc = hbgpu_check_launch("hbgpu_engine_create");
+        hbgpu_engine_destroy(e);
+        return rc ? rc : HBGPU_ERR_CUDA;
+    }
+    *out = e;
+    return HBGPU_OK;
+}
+
+namespace {
+// caller stream -> engine stream ordering on entry, and back on exit
+int enter(hbgpu_engine *e, cudaStream_t caller) {
+    if (cudaEventRecord(e->ev_in, caller) != cudaSuccess ||
+        cudaStreamWaitEvent(e->work, e->ev_in, 0) != cudaSuccess)
+        return hbgpu_check_launch("hbgpu_engine enter");
+    return HBGPU_OK;
+}
+int leave(hbgpu_engine *e, cudaStream_t caller, int rc) {
+    if (cudaEventRecord(e->ev_out, e->work) != cudaSuccess ||
+        cudaStreamWaitEvent(caller, e->ev_out, 0) != cudaSuccess) {
+        int lrc = hbgpu_check_launch("hbgpu_engine leave");
+        return rc ? rc : lrc;
+    }
+    return rc;
+}
+}  // namespace
+
+extern "C" int hbgpu_engine_prime(hbgpu_engine *e, void *stream) {
+    cudaStream_t caller = (cudaStream_t)stream;
+    int rc = enter(e, caller);
+    if (rc) return rc;
+    const hbgpu_engine_desc &d = e->d;
+    rc = hbgpu_halo(d.slot[0], d.sendbuf, d.recvbuf, d.prime_dirs, d.nprime, d.prime_max_len, d.planes, e->work);
+    if (!rc) rc = exchange_remote(e, d.slot[0], e->work);
+    return leave(e, caller, rc);
+}
+
+extern "C" int hbgpu_engine_launches_per_iteration(const hbgpu_engine *e) {
+    int per_stage = 1 + ((e->d.comm && !e->recvs.empty() && e->d.nunpack > 0) ? 1 : 0);
+    return 4 * per_stage + 2;
+}
+
+static int iterate_on(hbgpu_engine *e, int32_t iterations, int32_t use_graph, cudaStream_t s);
+
+extern "C" int hbgpu_engine_iterate(hbgpu_engine *e, int32_t iterations, int32_t use_graph, void *stream) {
+    cudaStream_t caller = (cudaStream_t)stream;
+    int rc = enter(e, caller);
+    if (rc) return rc;
+    rc = iterate_on(e, iterations, use_graph, e->work);
+    return leave(e, caller, rc);
+}
+
+static int iterate_on(hbgpu_engine *e, int32_t iterations, int32_t use_graph, cudaStream_t s) {
+    if (!use_graph) {
+        for (int it = 0; it < iterations; ++it) {
+            int rc = one_iteration(e, s);
+            if (rc) return rc;
+        }
+        return HBGPU_OK;
+    }
+    if (e->exec == nullptr) {
+        cudaError_t ce = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+        if (ce != cudaSuccess) {
+            hbgpu_set_error("cudaStreamBeginCapture: %s", cudaGetErrorString(ce));
+            return HBGPU_ERR_CUDA;
+        }
+        uint64_t before = g_launches.load();
+        int rc = one_iteration(e, s);
+        cudaGraph_t g = nullptr;
+        ce = cudaStreamEndCapture(s, &g);
+        // captured launches are counted when the graph replays
+        g_launches.store(before);
+        if (rc) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        if (ce != cudaSuccess) {
+            hbgpu_set_error("cudaStreamEndCapture: %s", cudaGetErrorString(ce));
+            return HBGPU_ERR_CUDA;
+        }
+        ce = cudaGraphInstantiate(&e->exec, g, 0);
+        if (ce != cudaSuccess) {
+            cudaGraphDestroy(g);
+            hbgpu_set_error("cudaGraphInstantiate: %s", cudaGetErrorString(ce));
+            return HBGPU_ERR_CUDA;
+        }
+        e->graph = g;
+    }
+    const int per_it = hbgpu_engine_launches_per_iteration(e);
+    for (int it = 0; it < iterations; ++it) {
+        cudaError_t ce = cudaGraphLaunch(e->exec, s);
+        if (ce != cudaSuccess) {
+            hbgpu_set_error("cudaGraphLaunch: %s", cudaGetErrorString(ce));
+            return HBGPU_ERR_CUDA;
+        }
+        hbgpu_count_launch(per_it);
+    }
+    return HBGPU_OK;
+}
+
+extern "C" int hbgpu_engine_destroy(hbgpu_engine *e) {
+    if (e == nullptr) return HBGPU_OK;
+    if (e->exec) cudaGraphExecDestroy(e->exec);
+    if (e->graph) cudaGraphDestroy(e->graph);
+    if (e->work) {
+        cudaStreamSynchronize(e->work);
+        cudaStreamDestroy(e->work);
+    }
+    if (e->ev_in) cudaEventDestroy(e->ev_in);
+    if (e->ev_out) cudaEventDestroy(e->ev_out);
+    delete e;
+    return HBGPU_OK;
+}

@@ -1,0 +1,238 @@
+"""Per-rank device layout and the tables the kernels consume.
+
+Pure host logic (numpy only), so it is unit-tested on CPU.  For the blocks a
+rank owns it fixes:
+
+* the slot layout: block b's value (n, p, j, i) at element
+  base_b + (n*4 + p)*ps_b + j*pitch_b + ROW_LEAD + i, rows padded to a
+  multiple of 4 doubles and ROW_LEAD = 3 so every interior row starts on a
+  32-byte sector; block bases are 256-byte aligned.  Three slots (A, B, C)
+  share the layout;
+* the stage grid: CTAs of 4 warps (warp = pde), 32 columns x tile_rows rows;
+* the face-target pool (fused halo forwarding, see cutplan.py);
+* the standalone halo directions (priming exchange / pack / unpack);
+* the send / receive buffer segments, grouped per peer rank, one NCCL
+  message per peer and stage;
+* the force segments in the reference's summation order (hbcore.py:369-381).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import native
+from .cutplan import rank_routes
+from .hbop import forcing_table, stencil_coefficients
+
+ROW_LEAD = native.ROW_LEAD
+NPDE = native.NPDE
+WARP_COLS = 32
+BLOCK_ALIGN = 32          # elements (256 B)
+TARGET_CTAS = 148 * 8     # enough resident warps on 148 SMs at ~2 CTAs/SM
+MAX_TILE_ROWS = 128
+MIN_TILE_ROWS = 8
+
+
+def _round_up(x, m):
+    return (x + m - 1) // m * m
+
+
+def choose_tile_rows(blocks):
+    rows = sum(-(-b.ni // WARP_COLS) * b.nj for b in blocks)
+    tj = rows // max(1, TARGET_CTAS)
+    tj = max(MIN_TILE_ROWS, min(MAX_TILE_ROWS, tj))
+    return tj
+
+
+@dataclass
+class RankLayout:
+    planes: int
+    blocks: list                    # owned BlockSpec, ascending id
+    local_index: dict               # gid -> local index
+    pitch: list
+    ps: list
+    base: list
+    slot_elems: int
+    tile_rows: int
+    block_table: np.ndarray
+    cta_block: np.ndarray
+    total_ctas: int
+    sxy: np.ndarray
+    faces: np.ndarray
+    prime_dirs: np.ndarray
+    unpack_dirs: np.ndarray
+    force_segs: np.ndarray
+    sends: list = field(default_factory=list)     # (peer, offset, count)
+    recvs: list = field(default_factory=list)
+    sendbuf_elems: int = 0
+    recvbuf_elems: int = 0
+
+    def elem(self, gid, n, p, j, i):
+        """Slot element index of (n, p, j, i) -- array coordinates -- of block gid."""
+        lb = self.local_index[gid]
+        return self.base[lb] + (n * NPDE + p) * self.ps[lb] + j * self.pitch[lb] + ROW_LEAD + i
+
+    def block_view_index(self, gid):
+        """(start, planes*npde, nj+2, pitch) to view a slot as the block's array."""
+        lb = self.local_index[gid]
+        b = self.blocks[lb]
+        return self.base[lb], self.planes * NPDE, b.nj + 2, self.pitch[lb]
+
+
+def _interior_cell(spec, face, k):
+    """(j, i) array coordinates of interior face cell k (1-based along the face)."""
+    return {"south": (1, k), "north": (spec.nj, k), "west": (k, 1), "east": (k, spec.ni)}[face]
+
+
+def _halo_cell(spec, face, k):
+    return {"south": (0, k), "north": (spec.nj + 1, k), "west": (k, 0),
+            "east": (k, spec.ni + 1)}[face]
+
+
+def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None):
+    owned = [topology.blocks[g] for g in partition.blocks_of(rank)]
+    owned.sort(key=lambda b: b.id)
+    if not owned:
+        raise ValueError(f"rank {rank} owns no blocks")
+    local_index = {b.id: k for k, b in enumerate(owned)}
+    tj = tile_rows or choose_tile_rows(owned)
+
+    pitch, ps, base = [], [], []
+    off = 0
+    for b in owned:
+        pt = _round_up(ROW_LEAD + b.ni + 2, 4)
+        pitch.append(pt)
+        ps.append((b.nj + 2) * pt)
+        base.append(off)
+        off = _round_up(off + planes * NPDE * (b.nj + 2) * pt, BLOCK_ALIGN)
+    slot_elems = off
+
+    table = np.zeros(len(owned), dtype=native.BLOCK_DTYPE)
+    cta_block = []
+    sxy_parts, sxy_off = [], 0
+    cta = 0
+    for k, b in enumerate(owned):
+        ti = -(-b.ni // WARP_COLS)
+        tjn = -(-b.nj // tj)
+        nu_h2, adv_2h = stencil_coefficients(b.h)
+        for name, value in (("base", base[k]), ("ps", ps[k]), ("ni", b.ni), ("nj", b.nj),
+                            ("pitch", pitch[k]), ("gid", b.id), ("tiles_i", ti),
+                            ("tiles_j", tjn), ("cta_begin", cta), ("ncta", ti * tjn),
+                            ("nu_h2", nu_h2), ("adv_2h", adv_2h), ("h", b.h),
+                            ("sxy_off", sxy_off)):
+            table[name][k] = value
+        table["face_off"][k] = -1
+        cta_block += [k] * (ti * tjn)
+        cta += ti * tjn
+        sxy_parts.append(forcing_table(b).ravel())
+        sxy_off += b.ni * b.nj
+
+    layout = RankLayout(planes=planes, blocks=owned, local_index=local_index, pitch=pitch, ps=ps,
+                        base=base, slot_elems=slot_elems, tile_rows=tj, block_table=table,
+                        cta_block=np.asarray(cta_block, dtype=np.int32), total_ctas=cta,
+                        sxy=np.concatenate(sxy_parts), faces=np.zeros(0, native.FACE_TARGET_DTYPE),
+                        prime_dirs=np.zeros(0, native.HALO_DIR_DTYPE),
+                        unpack_dirs=np.zeros(0, native.HALO_DIR_DTYPE),
+                        force_segs=np.zeros(0, native.FORCE_SEG_DTYPE))
+    _build_routes(layout, topology, plan, rank)
+    _build_force_segments(layout)
+    return layout
+
+
+def _face_stride(layout, gid, face):
+    lb = layout.local_index[gid]
+    return 1 if face in ("south", "north") else layout.pitch[lb]
+
+
+def _build_routes(layout, topology, plan, rank):
+    ds = plan.datasize
+    routes = rank_routes(plan, rank)
+    blocks = topology.blocks
+    planes = layout.planes
+
+    # send / receive segments grouped by peer (ascending), plan order inside
+    def segments(dirs, peer_of):
+        order = sorted(range(len(dirs)), key=lambda k: (peer_of(dirs[k]), k))
+        offs, msgs, pos = {}, [], 0
+        for k in order:
+            d = dirs[k]
+            offs[k] = pos
+            n = d.length * ds
+            if msgs and msgs[-1][0] == peer_of(d):
+                msgs[-1][2] += n
+            else:
+                msgs.append([peer_of(d), pos, n])
+            pos += n
+        return offs, [tuple(m) for m in msgs], pos
+
+    send_off, layout.sends, layout.sendbuf_elems = segments(routes.sends, lambda d: d.recv_rank)
+    recv_off, layout.recvs, layout.recvbuf_elems = segments(routes.recvs, lambda d: d.sender_rank)
+
+    # face-target pool: one entry per cell of every owned face that feeds a cut
+    face_base = {}
+    pool = []
+    feeding = [(d, True) for d in routes.local] + [(d, False) for d in routes.sends]
+    for d, _ in feeding:
+        key = (d.src_block, d.src_face)
+        if key not in face_base:
+            face_base[key] = len(pool)
+            pool += [(0, 0)] * blocks[d.src_block].face_extent(d.src_face)
+    send_index = {id(d): k for k, d in enumerate(routes.sends)}
+    for d, is_local in feeding:
+        fb = face_base[(d.src_block, d.src_face)]
+        for e in range(d.length):
+            k = d.src_index(e)
+            if is_local:
+                hj, hi = _halo_cell(blocks[d.dst_block], d.dst_face, d.dst_index(e))
+                pool[fb + k - 1] = (layout.elem(d.dst_block, 0, 0, hj, hi),
+                                    layout.ps[layout.local_index[d.dst_block]])
+            else:
+                pool[fb + k - 1] = (send_off[send_index[id(d)]] + e * ds, -1)
+    faces = np.zeros(len(pool), dtype=native.FACE_TARGET_DTYPE)
+    if pool:
+        arr = np.asarray(pool, dtype=np.int64)
+        faces["off"], faces["ps"] = arr[:, 0], arr[:, 1]
+    layout.faces = faces
+    from .topology import FACE_INDEX
+    for (gid, face), fb in face_base.items():
+        layout.block_table["face_off"][layout.local_index[gid], FACE_INDEX[face]] = fb
+
+    def slot_run(gid, face, first_k, reversed_, halo):
+        spec = blocks[gid]
+        cell = _halo_cell if halo else _interior_cell
+        j, i = cell(spec, face, first_k)
+        step = _face_stride(layout, gid, face)
+        return layout.elem(gid, 0, 0, j, i), (-step if reversed_ else step), \
+            layout.ps[layout.local_index[gid]]
+
+    prime = []
+    for d in routes.local:
+        s_off, s_es, s_vs = slot_run(d.src_block, d.src_face, d.src_index(0), d.src_reversed, False)
+        t_off, t_es, t_vs = slot_run(d.dst_block, d.dst_face, d.dst_index(0), d.dst_reversed, True)
+        prime.append((s_off, s_es, s_vs, t_off, t_es, t_vs, d.length, 0, 0, 0))
+    for k, d in enumerate(routes.sends):
+        s_off, s_es, s_vs = slot_run(d.src_block, d.src_face, d.src_index(0), d.src_reversed, False)
+        prime.append((s_off, s_es, s_vs, send_off[k], ds, 1, d.length, 0, 1, 0))
+    unpack = []
+    for k, d in enumerate(routes.recvs):
+        t_off, t_es, t_vs = slot_run(d.dst_block, d.dst_face, d.dst_index(0), d.dst_reversed, True)
+        unpack.append((recv_off[k], ds, 1, t_off, t_es, t_vs, d.length, 2, 0, 0))
+    layout.prime_dirs = np.array(prime, dtype=native.HALO_DIR_DTYPE) if prime else \
+        np.zeros(0, native.HALO_DIR_DTYPE)
+    layout.unpack_dirs = np.array(unpack, dtype=native.HALO_DIR_DTYPE) if unpack else \
+        np.zeros(0, native.HALO_DIR_DTYPE)
+    del planes
+
+
+def _build_force_segments(layout):
+    segs = []
+    for b in layout.blocks:
+        lb = layout.local_index[b.id]
+        for face, body in b.body_faces:
+            j, i = _interior_cell(b, face, 1)
+            segs.append((layout.elem(b.id, 0, 0, j, i), _face_stride(layout, b.id, face),
+                         layout.ps[lb], b.face_extent(face), body, b.h))
+    layout.force_segs = np.array(segs, dtype=native.FORCE_SEG_DTYPE) if segs else \
+        np.zeros(0, native.FORCE_SEG_DTYPE)

@@ -1,0 +1,487 @@
+"""The run-level drop-in: RunSpec / run_case / CaseRunResult on B200s.
+
+Mirrors the reference's driver (driver.py:34-63 types, 110-200 run loop):
+build topology -> partition blocks over ranks (one rank = one GPU) -> cut
+plan -> initial state -> priming halo exchange -> `iterations` x (4 RK
+stages with halo exchange, force integration) -> fields (halos included)
+and globally reduced forces.  The per-iteration schedule runs inside
+libhbgpu's engine (one CUDA stream, optionally a replayed CUDA graph).
+
+Differences that do not change any returned value:
+* force partials are integrated on the device every iteration and kept as a
+  history; the rank-ordered global sum (runtime.py:290-294) is done once at
+  the end over the whole history, instead of once per iteration.  `forces`
+  is the last iteration's, as in the reference;
+* divergence is detected on the device (per-block keys) and raised after the
+  loop (or at a polling point), with the reference's DivergenceError fields
+  for the first diverging stage.
+
+Additions: `residual_norms` (the per-iteration L2 norm of the stage-one
+residual; not produced by the reference) and
+`force_history`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import hbop, native
+from .cutplan import ExchangeStrategy, build_cut_plan, predicted_message_count
+from .devlayout import build_rank_layout
+from .exceptions import DivergenceError, ProtocolError
+from .topology import build_topology, partition_blocks
+
+NO_BAD = (1 << 64) - 1
+LIN_BITS = 40
+
+
+@dataclass(frozen=True)
+class ForceReduceStrategy:
+    """Kept for RunSpec compatibility (reduce.py:34-45); the device path always
+    uses the single-buffer packing with all three coefficients."""
+
+    mode: str = "buffered"
+    functag: int = 3
+
+
+@dataclass
+class RunSpec:
+    case: object
+    ranks: int = 1
+    threads: int = 1
+    axis: object = None
+    activation: object = None
+    exchange: ExchangeStrategy = field(default_factory=ExchangeStrategy)
+    reduce: ForceReduceStrategy = field(default_factory=ForceReduceStrategy)
+    io: object = None
+    iterations: int | None = None
+    out_dir: str | None = None
+    extra_outputs: tuple = ()
+    machine: str = ""
+    jitter_seed: int | None = None
+    # --- device options -------------------------------------------------
+    initial: object = None       # callable(spec, planes, npde) -> (P, npde, nj, ni)
+    use_graph: bool = True
+    tile_rows: int | None = None
+    device: int | None = None
+
+
+@dataclass
+class ForceCoefficients:
+    """cl / cd / cm, each of shape (planes, nbody) (hbcore.py:329-356)."""
+
+    cl: np.ndarray
+    cd: np.ndarray
+    cm: np.ndarray
+
+    @classmethod
+    def zeros(cls, planes, nbody):
+        return cls(np.zeros((planes, nbody)), np.zeros((planes, nbody)), np.zeros((planes, nbody)))
+
+    @classmethod
+    def from_stack(cls, arr):
+        return cls(arr[0].copy(), arr[1].copy(), arr[2].copy())
+
+    def copy(self):
+        return ForceCoefficients(self.cl.copy(), self.cd.copy(), self.cm.copy())
+
+    @property
+    def planes(self):
+        return self.cl.shape[0]
+
+    @property
+    def nbody(self):
+        return self.cl.shape[1]
+
+    def equal_bits(self, other):
+        return all(np.array_equal(a, b) for a, b in
+                   ((self.cl, other.cl), (self.cd, other.cd), (self.cm, other.cm)))
+
+
+@dataclass
+class RunRecord:
+    case: str
+    machine: str
+    ranks: int
+    threads: int
+    iterations: int
+    wall_s: float
+    msgs: int
+    bytes: int
+    collectives: int
+    write_ops: int
+    activations: int
+    units: int = 0
+
+    @property
+    def units_per_s(self):
+        return self.units / self.wall_s if self.wall_s > 0 else 0.0
+
+
+@dataclass
+class CaseRunResult:
+    fields: dict
+    forces: ForceCoefficients
+    counters: list
+    wall_s: float
+    record: object
+    residual_norms: list = field(default_factory=list)
+    force_history: list = field(default_factory=list)
+
+    def field_bits_equal(self, other):
+        if sorted(self.fields) != sorted(other.fields):
+            return False
+        return all(np.array_equal(self.fields[b], other.fields[b]) for b in self.fields)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class DeviceRank:
+    """One rank's blocks resident on one GPU, plus its libhbgpu engine."""
+
+    def __init__(self, case, topology, partition, plan, rank=0, device=None, comm=None,
+                 initial=None, tile_rows=None, max_iters=1, pinned_ic=None):
+        import torch
+        self.lib = native.require_cuda()
+        self.torch = torch
+        self.case = case
+        self.planes = case.planes
+        self.rank = rank
+        self.comm = comm
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        torch.cuda.set_device(self.device)
+        L = self.layout = build_rank_layout(topology, partition, plan, rank, case.planes, tile_rows)
+        dev = self.device
+        f64 = torch.float64
+        self.slots = [torch.zeros(L.slot_elems, dtype=f64, device=dev) for _ in range(3)]
+        self.sendbuf = torch.zeros(max(1, L.sendbuf_elems), dtype=f64, device=dev)
+        self.recvbuf = torch.zeros(max(1, L.recvbuf_elems), dtype=f64, device=dev)
+
+        def table(arr):
+            raw = np.ascontiguousarray(arr).view(np.uint8).ravel()
+            t = torch.zeros(max(16, raw.size), dtype=torch.uint8)
+            t[:raw.size] = torch.from_numpy(raw.copy())
+            return t.to(dev)
+
+        self.t_blocks = table(L.block_table)
+        self.t_cta = torch.from_numpy(L.cta_block).to(dev)
+        self.t_sxy = torch.from_numpy(L.sxy).to(dev)
+        self.t_faces = table(L.faces)
+        self.t_prime = table(L.prime_dirs)
+        self.t_unpack = table(L.unpack_dirs)
+        self.t_segs = table(L.force_segs)
+        deriv = hbop.spectral_matrix(case.nharms, case.omega)
+        self.dmat = np.ascontiguousarray(deriv.matrix)
+        self.t_dmat = torch.from_numpy(self.dmat.copy()).to(dev)
+        self.ap = hbop.forcing_amplitudes(case.planes, 4)
+        nb = len(L.blocks)
+        self.max_iters = max(1, max_iters)
+        self.norm_part = torch.zeros(L.total_ctas, dtype=f64, device=dev)
+        self.sumsq = torch.zeros(self.max_iters * nb, dtype=f64, device=dev)
+        self.status = torch.full((nb,), -1, dtype=torch.int64, device=dev)
+        self.iter = torch.zeros(1, dtype=torch.int32, device=dev)
+        nforce = 3 * case.planes * case.nbody
+        self.force_hist = torch.zeros(max(1, self.max_iters * nforce), dtype=f64, device=dev)
+        self.upload_initial(initial, pinned_ic)
+        self._make_engine()
+
+    # -- state in / out --------------------------------------------------------
+
+    def block_view(self, slot, gid):
+        L = self.layout
+        start, npl, nj2, pitch = L.block_view_index(gid)
+        return slot[start:start + npl * nj2 * pitch].view(npl, nj2, pitch)
+
+    def upload_initial(self, initial=None, pinned=None):
+        """Interior of slot A <- the initial state; halos and slots B, C zero.
+
+        `pinned`, when given, maps gid -> host (pinned) tensors of shape
+        (P, npde, nj, ni) to copy from (the end-to-end path).
+        """
+        torch = self.torch
+        for s in self.slots:
+            s.zero_()
+        for b in self.layout.blocks:
+            view = self.block_view(self.slots[0], b.id)
+            dst = view[:, 1:b.nj + 1, native.ROW_LEAD + 1:native.ROW_LEAD + 1 + b.ni]
+            if pinned is not None:
+                src = pinned[b.id].reshape(self.planes * 4, b.nj, b.ni)
+                dst.copy_(src.to(self.device, non_blocking=True))
+                continue
+            if initial is None:
+                ic = hbop.initial_values(b, self.planes, 4, 0, self.planes, 1, b.nj + 1)
+            else:
+                ic = initial(b, self.planes, 4)
+            dst.copy_(torch.from_numpy(np.ascontiguousarray(ic, dtype=np.float64)
+                                       .reshape(self.planes * 4, b.nj, b.ni)))
+
+    def fields(self, slot=0, pinned_out=None):
+        """{gid: (P, npde, nj+2, ni+2) numpy array incl. halos} of a slot."""
+        out = {}
+        for b in self.layout.blocks:
+            view = self.block_view(self.slots[slot], b.id)
+            sub = view[:, :, native.ROW_LEAD:native.ROW_LEAD + b.ni + 2]
+            if pinned_out is not None:
+                dst = pinned_out[b.id]
+                dst.view(self.planes * 4, b.nj + 2, b.ni + 2).copy_(sub, non_blocking=True)
+                out[b.id] = dst
+            else:
+                out[b.id] = sub.cpu().numpy().reshape(self.planes, 4, b.nj + 2, b.ni + 2)
+        return out
+
+    # -- engine ----------------------------------------------------------------
+
+    def _make_engine(self):
+        L = self.layout
+        d = native.EngineDesc()
+        for k in range(3):
+            d.slot[k] = self.slots[k].data_ptr()
+        d.sendbuf, d.recvbuf = self.sendbuf.data_ptr(), self.recvbuf.data_ptr()
+        d.blocks, d.cta_block = self.t_blocks.data_ptr(), self.t_cta.data_ptr()
+        d.sxy, d.faces, d.dmat = self.t_sxy.data_ptr(), self.t_faces.data_ptr(), self.t_dmat.data_ptr()
+        d.norm_part, d.sumsq = self.norm_part.data_ptr(), self.sumsq.data_ptr()
+        d.status, d.iter = self.status.data_ptr(), self.iter.data_ptr()
+        d.prime_dirs, d.nprime = self.t_prime.data_ptr(), len(L.prime_dirs)
+        d.prime_max_len = int(L.prime_dirs["length"].max()) if len(L.prime_dirs) else 0
+        d.unpack_dirs, d.nunpack = self.t_unpack.data_ptr(), len(L.unpack_dirs)
+        d.unpack_max_len = int(L.unpack_dirs["length"].max()) if len(L.unpack_dirs) else 0
+        d.segs, d.nsegs = self.t_segs.data_ptr(), len(L.force_segs)
+        d.force_hist = self.force_hist.data_ptr()
+        self._sends = (native.PeerMsg * max(1, len(L.sends)))(
+            *[native.PeerMsg(p, 0, o, c) for p, o, c in L.sends])
+        self._recvs = (native.PeerMsg * max(1, len(L.recvs)))(
+            *[native.PeerMsg(p, 0, o, c) for p, o, c in L.recvs])
+        d.sends, d.nsends = self._sends, len(L.sends)
+        d.recvs, d.nrecvs = self._recvs, len(L.recvs)
+        d.comm = self.comm
+        d.nblocks, d.total_ctas, d.planes = len(L.blocks), L.total_ctas, self.planes
+        d.nbody, d.tile_rows, d.max_iters = self.case.nbody, L.tile_rows, self.max_iters
+        for k, c in enumerate(hbop.RKScheme(self.case.dtau).stage_coefficients()):
+            d.coef[k] = c
+        P = self.planes
+        if P > native.MAX_P:
+            raise NotImplementedError(f"{P} snapshots exceed the library limit {native.MAX_P}")
+        if P <= native.MAX_TEMPLATED_P:
+            flat = self.dmat.ravel()
+            for k in range(P * P):
+                d.D[k] = flat[k]
+        apf = self.ap.ravel()
+        for k in range(P * 4):
+            d.ap[k] = apf[k]
+        self._desc = d
+        eng = ctypes.c_void_p()
+        native.check(self.lib.hbgpu_engine_create(ctypes.byref(d), ctypes.byref(eng)),
+                     "hbgpu_engine_create")
+        self.engine = eng
+
+    def stream(self):
+        return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
+
+    def prime(self):
+        native.check(self.lib.hbgpu_engine_prime(self.engine, self.stream()), "hbgpu_engine_prime")
+
+    def iterate(self, iterations, use_graph=True):
+        native.check(self.lib.hbgpu_engine_iterate(self.engine, int(iterations), int(bool(use_graph)),
+                                                   self.stream()), "hbgpu_engine_iterate")
+
+    def launches_per_iteration(self):
+        return int(self.lib.hbgpu_engine_launches_per_iteration(self.engine))
+
+    def reset_counters(self):
+        self.iter.zero_()
+        self.status.fill_(-1)
+
+    def close(self):
+        if getattr(self, "engine", None):
+            self.lib.hbgpu_engine_destroy(self.engine)
+            self.engine = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- results ---------------------------------------------------------------
+
+    def divergence(self):
+        """(gstage, gid, i, j, p, n) of this rank's first non-finite value, or None."""
+        keys = self.status.cpu().numpy().view(np.uint64)
+        best = None
+        for lb, key in enumerate(keys):
+            key = int(key)
+            if key == NO_BAD:
+                continue
+            gstage, lin = key >> LIN_BITS, key & ((1 << LIN_BITS) - 1)
+            b = self.layout.blocks[lb]
+            cand = (gstage, b.id, lin)
+            if best is None or cand[:2] < best[:2]:
+                best = cand
+        if best is None:
+            return None
+        gstage, gid, lin = best
+        b = self.layout.blocks[self.layout.local_index[gid]]
+        i = lin % b.ni
+        j = (lin // b.ni) % b.nj
+        np_ = lin // (b.ni * b.nj)
+        return gstage, gid, i + 1, j + 1, np_ % 4, np_ // 4
+
+    def norm_history(self, iterations):
+        nb = len(self.layout.blocks)
+        arr = self.sumsq[:iterations * nb].cpu().numpy().reshape(iterations, nb)
+        return {b.id: arr[:, k].copy() for k, b in enumerate(self.layout.blocks)}
+
+    def force_history_array(self, iterations):
+        nf = 3 * self.planes * self.case.nbody
+        return self.force_hist[:iterations * nf].view(iterations, 3, self.planes, self.case.nbody)
+
+
+# ---------------------------------------------------------------------------
+# run_case
+# ---------------------------------------------------------------------------
+
+def _dist():
+    try:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            return dist
+    except Exception:
+        pass
+    return None
+
+
+def make_comm(rank, world, device):
+    """NCCL communicator for libhbgpu's engine, id broadcast over torch.distributed."""
+    import torch.distributed as dist
+    lib = native.load()
+    buf = ctypes.create_string_buffer(128)
+    if rank == 0:
+        native.check(lib.hbgpu_comm_unique_id(buf), "hbgpu_comm_unique_id")
+    obj = [bytes(buf.raw) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    comm = ctypes.c_void_p()
+    native.check(lib.hbgpu_comm_init(obj[0], world, rank, device, ctypes.byref(comm)), "hbgpu_comm_init")
+    return comm
+
+
+def _fold_norms(per_block, iterations):
+    """sqrt of the sum over global blocks in ascending id of each block's R^2 sum."""
+    norms = []
+    for it in range(iterations):
+        total = 0.0
+        for gid in sorted(per_block):
+            total += float(per_block[gid][it])
+        norms.append(math.sqrt(total))
+    return norms
+
+
+def raise_divergence(div):
+    if div is not None:
+        _, gid, i, j, p, n = div
+        raise DivergenceError(gid, i, j, p, n)
+
+
+def run_case(spec):
+    """Execute one configuration end to end; fields come back with halos.
+
+    Under torch.distributed with world size W > 1, each process is one rank
+    on its own GPU and spec.ranks must equal W.  In a single process,
+    spec.ranks > 1 keeps the reference partition for the cut plan and its
+    counters, but all ranks' blocks run on the one GPU (results are
+    partition-invariant bitwise, as the reference's acceptance criterion 4
+    requires).
+    """
+    case = spec.case
+    topology = build_topology(case)
+    partition = partition_blocks(topology, spec.ranks)
+    plan = build_cut_plan(topology, partition, case.nharms, case.npde)
+    iterations = case.iterations if spec.iterations is None else spec.iterations
+    dist = _dist()
+    world = dist.get_world_size() if dist is not None else 1
+    if world > 1 and spec.ranks != world:
+        raise ProtocolError(f"spec.ranks={spec.ranks} but torch.distributed world size is {world}")
+
+    import torch
+    native.require_cuda()
+    t0 = time.perf_counter()
+    if world > 1:
+        rank = dist.get_rank()
+        device = spec.device if spec.device is not None else rank % torch.cuda.device_count()
+        torch.cuda.set_device(device)
+        comm = make_comm(rank, world, device)
+        exec_partition, exec_plan = partition, plan
+    else:
+        rank, comm = 0, None
+        device = spec.device if spec.device is not None else torch.cuda.current_device()
+        exec_partition = partition_blocks(topology, 1)
+        exec_plan = build_cut_plan(topology, exec_partition, case.nharms, case.npde)
+    dr = DeviceRank(case, topology, exec_partition, exec_plan, rank=rank, device=device, comm=comm,
+                    initial=spec.initial, tile_rows=spec.tile_rows, max_iters=max(1, iterations))
+    try:
+        dr.prime()
+        if iterations > 0:
+            dr.iterate(iterations, use_graph=spec.use_graph)
+        torch.cuda.synchronize(dr.device)
+        div = dr.divergence()
+        fields = dr.fields(0)
+        norms_local = dr.norm_history(iterations)
+        hist = dr.force_history_array(iterations)
+        if world > 1:
+            divs = [None] * world
+            dist.all_gather_object(divs, div)
+            divs = [d for d in divs if d is not None]
+            div = min(divs, key=lambda d: d[:2]) if divs else None
+            raise_divergence(div)
+            hist = _reduce_history(dr, hist, world)
+            allnorm = [None] * world
+            dist.all_gather_object(allnorm, norms_local)
+            norms_local = {k: v for part in allnorm for k, v in part.items()}
+        raise_divergence(div)
+        hist_np = hist.cpu().numpy() if iterations > 0 else np.zeros((0, 3, case.planes, case.nbody))
+        torch.cuda.synchronize(dr.device)
+    finally:
+        dr.close()
+        if comm is not None:
+            native.load().hbgpu_comm_destroy(comm)
+    wall = time.perf_counter() - t0
+
+    forces = (ForceCoefficients.from_stack(hist_np[-1]) if iterations > 0
+              else ForceCoefficients.zeros(case.planes, case.nbody))
+    forecast = predicted_message_count(plan)
+    exchanges = 4 * iterations + 1
+    counters = [{"rank": r, "msgs_sent": None, "bytes_sent": None} for r in range(spec.ranks)]
+    record = None
+    if iterations >= 1:
+        units = topology.total_cells() * case.planes * 4 * iterations
+        record = RunRecord(case=case.name or "case", machine=spec.machine, ranks=spec.ranks,
+                           threads=spec.threads, iterations=iterations, wall_s=wall,
+                           msgs=forecast.total_messages * exchanges,
+                           bytes=forecast.total_bytes * exchanges,
+                           collectives=iterations if topology.nbody else 0, write_ops=0,
+                           activations=iterations, units=units)
+    return CaseRunResult(fields=fields, forces=forces, counters=counters, wall_s=wall,
+                         record=record, residual_norms=_fold_norms(norms_local, iterations),
+                         force_history=[ForceCoefficients.from_stack(h) for h in hist_np])
+
+
+def _reduce_history(dr, hist, world):
+    """All-gather every rank's force history and fold it in rank order."""
+    import torch
+    count = hist.numel()
+    if count == 0:
+        return hist
+    stacked = torch.empty(world * count, dtype=torch.float64, device=dr.device)
+    src = hist.contiguous().view(-1)
+    native.check(dr.lib.hbgpu_comm_allgather(dr.comm, _ptr(src), _ptr(stacked), count, dr.stream()),
+                 "hbgpu_comm_allgather")
+    out = torch.empty(count, dtype=torch.float64, device=dr.device)
+    native.check(dr.lib.hbgpu_ordered_fold(_ptr(stacked), world, count, _ptr(out), dr.stream()),
+                 "hbgpu_ordered_fold")
+    return out.view_as(hist)

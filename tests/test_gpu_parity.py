@@ -1,0 +1,110 @@
+"""Run-level parity: run_case on the GPU vs the CPU oracle, bitwise.
+
+Fields (halos included), forces and the residual-norm history of the CUDA
+path are compared with oracle/oracle.py, a restatement of the reference
+pinned to the reference's own outputs (tests/test_oracle_golden.py).
+Bar: bitwise for fields and forces; residual norms within 1e-12 relative
+(tree vs exactly-rounded summation order; north_star allows 1e-10).
+"""
+
+import numpy as np
+import pytest
+
+from paper_1304_7654_b200 import (BlockSpec, CaseConfig, CutSide, CutSpec, DivergenceError,
+                                  RunSpec, baseline_workload, lattice_case, pair_case,
+                                  ring_case, run_case, stacked_pair_case, tc1_mini, tc2_mini,
+                                  tc_tiny)
+
+pytestmark = pytest.mark.gpu
+
+NORM_RTOL = 1e-12
+
+
+def assert_parity(got, want, label):
+    for b in want.fields:
+        g, w = got.fields[b], want.fields[b]
+        if not np.array_equal(g, w):
+            bad = np.argwhere(g != w)
+            raise AssertionError(f"{label}: block {b} differs at {len(bad)} places, first {bad[0]}"
+                                 f" got {g[tuple(bad[0])]!r} want {w[tuple(bad[0])]!r}")
+    forces = np.stack([got.forces.cl, got.forces.cd, got.forces.cm])
+    assert np.array_equal(forces, want.forces), f"{label}: forces differ"
+    if want.norms:
+        np.testing.assert_allclose(got.residual_norms, want.norms, rtol=NORM_RTOL, atol=0,
+                                   err_msg=f"{label}: residual norms")
+
+
+CASES = {
+    "tc-tiny-8": (tc_tiny, 8, None),
+    "pair-reversed": (lambda: pair_case(6, 5, 2, h=0.2, dtau=0.01, reversed_cut=True, nbody=1,
+                                        bodies=((1, "north", 0),)), 6, None),
+    "steady-nharms0": (lambda: CaseConfig(nharms=0, npde=4, iterations=12, dtau=0.01, omega=1.0,
+                                          nbody=0, blocks=[BlockSpec(0, 6, 5, 0.3, -0.7, 0.2)],
+                                          cuts=[]), 12, None),
+    "stacked-ns": (lambda: stacked_pair_case(40, 7, 1, h=0.01, dtau=0.0001, nbody=1,
+                                             bodies=((0, "south", 0),)), 4, None),
+    "tc2-mini-3": (tc2_mini, 3, None),
+    "tc1-mini-4": (tc1_mini, 4, None),
+    "lattice-p7-ragged": (lambda: lattice_case(3, 2, 45, 19, 3, h=0.02, dtau=0.0005, nbody=2,
+                                               bodies=((0, "south", 0), (4, "north", 1))), 5, None),
+    "generic-p21": (lambda: ring_case(3, 33, 9, 10, h=0.05, dtau=0.0005, nbody=1,
+                                      bodies=((2, "south", 0),)), 3, None),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_run_case_matches_oracle(name, cuda, oracle_mod):
+    build, iters, initial = CASES[name]
+    case = build()
+    got = run_case(RunSpec(case=case, ranks=1, iterations=iters, initial=initial))
+    want = oracle_mod.run(case, iters, initial=initial)
+    assert_parity(got, want, name)
+
+
+@pytest.mark.parametrize("key,iters", [("C0", 20), ("C1", 2), ("C2", 2)])
+def test_baseline_workloads_match_oracle(key, iters, cuda, oracle_mod):
+    wl = baseline_workload(key)
+    got = run_case(RunSpec(case=wl.case, ranks=1, iterations=iters, initial=wl.initial))
+    want = oracle_mod.run(wl.case, iters, initial=wl.initial)
+    assert_parity(got, want, key)
+
+
+def test_graph_and_eager_identical(cuda):
+    case = tc2_mini()
+    a = run_case(RunSpec(case=case, ranks=1, iterations=3, use_graph=True))
+    b = run_case(RunSpec(case=case, ranks=1, iterations=3, use_graph=False))
+    assert a.field_bits_equal(b) and a.forces.equal_bits(b.forces)
+
+
+@pytest.mark.parametrize("tile_rows", [8, 13, 64])
+def test_tile_rows_invariance(tile_rows, cuda):
+    case = lattice_case(2, 2, 70, 41, 2, h=0.02, dtau=0.0005)
+    base = run_case(RunSpec(case=case, ranks=1, iterations=3, tile_rows=9))
+    other = run_case(RunSpec(case=case, ranks=1, iterations=3, tile_rows=tile_rows))
+    assert base.field_bits_equal(other)
+    np.testing.assert_allclose(base.residual_norms, other.residual_norms, rtol=1e-13)
+
+
+def test_rank_count_invariance_single_process(cuda):
+    case = tc2_mini()
+    one = run_case(RunSpec(case=case, ranks=1, iterations=3))
+    eight = run_case(RunSpec(case=case, ranks=8, iterations=3))
+    assert one.field_bits_equal(eight) and one.forces.equal_bits(eight.forces)
+
+
+def test_divergence_reports_reference_location(cuda, oracle_mod):
+    case = pair_case(8, 6, 1, h=0.25, dtau=50.0, nbody=0)
+    with pytest.raises(oracle_mod.OracleDivergence) as want:
+        oracle_mod.run(case, 100)
+    with pytest.raises(DivergenceError) as got:
+        run_case(RunSpec(case=case, ranks=1, iterations=100))
+    w, g = want.value, got.value
+    assert (g.block, g.i, g.j, g.p, g.n) == (w.block, w.i, w.j, w.p, w.n)
+
+
+def test_dtau_zero_is_identity(cuda):
+    from paper_1304_7654_b200 import initial_values
+    case = pair_case(4, 4, 1, h=0.25, dtau=0.0)
+    res = run_case(RunSpec(case=case, ranks=1, iterations=3))
+    want = initial_values(case.blocks[0], 3, 4, 0, 3, 1, 5)
+    assert np.array_equal(res.fields[0][:, :, 1:5, 1:5], want)
