@@ -1,0 +1,377 @@
+#!/usr/bin/env python3
+"""Benchmark: cell-snapshot RK-stage updates per second on B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4] [--impl ours|reference]
+
+A "step" is one RK iteration (4 fused stages + halo exchange + force
+integration) over the whole workload; one unit is one interior cell x one HB
+snapshot x one RK stage (all 4 pdes).  Default workload: BASELINE.json
+config 4 (C4: 8x8 blocks of 1024x1024 cells, N_H=4 -> P=9, ~19.5 GB per
+state slot), the largest configuration and the one the scaling target is
+quoted on; it fits one B200.  For N > 1 (torchrun, one rank per GPU) blocks
+are partitioned with the reference's LPT rule (8 per GPU at N = 8): total work
+is fixed -> "scaling": "strong".
+
+Printed on rank 0: one JSON line with value (device-timed, inputs resident),
+roofline of the fused stage kernel, cpu_baseline (the oracle port on this
+host), e2e (run_case with pinned host input/output copies inside the timed
+region), clocks, gpu_launches.
+
+`--impl reference` times the reference's CPU path (the C restatement in
+oracle/, with all host threads) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+ALGO_BYTES = {0: 64, 1: 96, 2: 96, 3: 96}   # per unit per stage
+UNIT = "cell-snapshot RK-stage updates/s"
+METRIC = "cell-snapshot RK-stage updates/sec (fp64, 4 pdes) and % of HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="C4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--tile-rows", type=int, default=None)
+    ap.add_argument("--kernel-reps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-iters", type=int, default=1)
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, smax, reasons = [], None, set()
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[4:8]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_ic(wl, blocks, pinned=True):
+    """Seeded initial state of the given blocks in (pinned) host tensors."""
+    import numpy as np
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+    P = wl.case.planes
+
+    def one(b):
+        t = torch.empty((P, 4, b.nj, b.ni), dtype=torch.float64, pin_memory=pinned)
+        t.numpy()[...] = wl.initial(b, P, 4)
+        return b.id, t
+
+    with ThreadPoolExecutor(max_workers=min(16, max(1, os.cpu_count() or 1))) as ex:
+        return dict(ex.map(one, blocks))
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the oracle port of the reference path
+# ---------------------------------------------------------------------------
+
+def sample_case(wl, nblocks):
+    """The first `nblocks` blocks of the workload with the cuts among them."""
+    import dataclasses
+    from paper_1304_7654_b200.topology import CaseConfig
+    keep = set(range(nblocks))
+    cuts = [c for c in wl.case.cuts if c.side_a.block in keep and c.side_b.block in keep]
+    blocks = [dataclasses.replace(b, body_faces=tuple(bf for bf in b.body_faces))
+              for b in wl.case.blocks[:nblocks]]
+    return CaseConfig(nharms=wl.case.nharms, npde=4, iterations=1, dtau=wl.case.dtau,
+                      omega=wl.case.omega, nbody=wl.case.nbody, blocks=blocks,
+                      cuts=cuts, name=f"{wl.key}-sample{nblocks}")
+
+
+def cpu_sample_blocks(wl):
+    # ~40M cell-snapshots per sampled iteration: 1 block of C3/C4, all of C0..C2
+    budget = 40e6
+    per = wl.case.blocks[0].cells() * wl.case.planes
+    return max(1, min(len(wl.case.blocks), int(budget // per)))
+
+
+def cpu_baseline(wl, iters):
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle  # the checker / CPU baseline only
+    nb = cpu_sample_blocks(wl)
+    case = sample_case(wl, nb)
+    solver = oracle.OracleSolver(case, initial=wl.initial, record_norms=False)
+    solver.prime()
+    t0 = time.perf_counter()
+    solver.iterate(iters)
+    dt = time.perf_counter() - t0
+    units = solver.units_per_iteration * iters
+    return {"value": units / dt, "unit": UNIT, "cores": solver.nthreads, "kind": "port",
+            "sample": f"blocks 0..{nb - 1} of {wl.key} ({nb} of {len(wl.case.blocks)}, cuts among "
+                      f"them), {iters} iteration(s), {units / 1e6:.0f} M units in {dt:.2f} s; "
+                      f"C restatement of hbcore._residual_kernel/_update_kernel (oracle/hb_oracle.c), "
+                      f"pthreads over (block, plane)"}
+
+
+def run_reference_arm(args, wl):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+    nb = cpu_sample_blocks(wl)
+    case = sample_case(wl, nb)
+    solver = oracle.OracleSolver(case, initial=wl.initial, record_norms=False)
+    solver.prime()
+    solver.iterate(args.warmup)
+    t0 = time.perf_counter()
+    solver.iterate(args.steps)
+    dt = time.perf_counter() - t0
+    units = solver.units_per_iteration * args.steps
+    value = units / dt
+    sample = (f"each step = 1 iteration over blocks 0..{nb - 1} of {wl.key} ({nb} of "
+              f"{len(wl.case.blocks)}); C restatement of the reference kernels (oracle/), "
+              f"{solver.nthreads} pthreads")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": wl.key, "description": wl.description, "sample_blocks": nb},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": solver.nthreads,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU side
+# ---------------------------------------------------------------------------
+
+def run_ours(args, wl):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1304_7654_b200 import RunSpec, native, run_case
+    from paper_1304_7654_b200.cutplan import build_cut_plan
+    from paper_1304_7654_b200.solver import DeviceRank, make_comm
+    from paper_1304_7654_b200.topology import build_topology, partition_blocks
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    native.require_cuda()
+    case = wl.case
+    topo = build_topology(case)
+    part = partition_blocks(topo, world)
+    plan = build_cut_plan(topo, part, case.nharms, case.npde)
+    mine = [topo.blocks[g] for g in part.blocks_of(rank)]
+    ic = make_ic(wl, mine)
+    total_units_iter = topo.total_cells() * case.planes * 4
+    comm = make_comm(rank, world, local) if world > 1 else None
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    dr = DeviceRank(case, topo, part, plan, rank=rank, device=local, comm=comm,
+                    tile_rows=args.tile_rows, max_iters=args.warmup + args.steps + 1, pinned_ic=ic)
+    dr.prime()
+    dr.iterate(args.warmup, use_graph=True)
+    torch.cuda.synchronize()
+    l0 = native.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record()
+        dr.iterate(args.steps, use_graph=True)
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier()
+    launches = native.launch_count() - l0
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    div = dr.divergence()
+    if div is not None:
+        raise SystemExit(f"benchmark run diverged: {div}")
+    value = total_units_iter * args.steps / (ms / 1e3)
+
+    # dominant kernel, timed alone on the launching stream: the 4 stage variants
+    my_units_stage = sum(b.cells() for b in mine) * case.planes
+    stage_args = [dr.stage_args(s) for s in range(4)]
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(4 * args.kernel_reps)]
+    dr.launch_stage(stage_args[1])  # warm
+    torch.cuda.synchronize()
+    k = 0
+    for _ in range(args.kernel_reps):
+        for s in range(4):
+            evs[k][0].record()
+            dr.launch_stage(stage_args[s])
+            evs[k][1].record()
+            k += 1
+    torch.cuda.synchronize()
+    stage_ms = [0.0] * 4
+    for k, (a, b) in enumerate(evs):
+        stage_ms[k % 4] += a.elapsed_time(b) / args.kernel_reps
+    algo = sum(ALGO_BYTES[s] for s in range(4)) * my_units_stage   # bytes per 4 launches
+    kernel_s = sum(stage_ms) / 1e3
+    achieved = algo / kernel_s / 1e9
+    peak, peak_src = peaks()
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "stage_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            tj = json.load(fh)
+        if tj.get("workload") == wl.key and tj.get("n_gpus", 1) == world:
+            traffic = tj.get("bytes_per_launch_avg")
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+            "kernel": "hb_stage (fused residual + RK update + halo forward)",
+            "algorithmic_bytes_per_unit": {"stage0": 64, "stages1-3": 96, "avg": 88},
+            "units_per_launch": my_units_stage,
+            "stage_ms": [round(x, 4) for x in stage_ms],
+            "share_of_step": round(sum(stage_ms) / (ms / args.steps), 4)}
+    dr.close()
+    del dr
+    torch.cuda.empty_cache()
+
+    # end to end through run_case: pinned IC H2D + K iterations + D2H of fields
+    e2e = None
+    if not args.no_e2e:
+        out = {b.id: torch.empty((case.planes, 4, b.nj + 2, b.ni + 2), dtype=torch.float64,
+                                 pin_memory=True) for b in mine}
+        h2d = sum(t.numel() * 8 for t in ic.values())
+        d2h = sum(t.numel() * 8 for t in out.values())
+        barrier()
+        t0 = time.perf_counter()
+        res = run_case(RunSpec(case=case, ranks=world, iterations=args.steps, initial_state=ic,
+                               output=out, tile_rows=args.tile_rows, device=local))
+        wall = max_over_ranks(time.perf_counter() - t0)
+        del res
+        e2e = {"value": total_units_iter * args.steps / wall, "unit": UNIT,
+               "h2d_bytes_per_step": h2d * world // args.steps,
+               "d2h_bytes_per_step": d2h * world // args.steps,
+               "wall_s": round(wall, 4),
+               "note": "run_case(): layout + allocation + pinned H2D of the initial state + "
+                       "K iterations + D2H of all fields (halos incl.) + forces/norms"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl, args.cpu_sample_iters)
+    if comm is not None:
+        native.load().hbgpu_comm_destroy(comm)
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": wl.key, "description": wl.description,
+                           "blocks": len(case.blocks), "cells": topo.total_cells(),
+                           "planes": case.planes, "units_per_step": total_units_iter,
+                           "parallelism": f"blocks/{world} gpu (LPT partition)",
+                           "tile_rows": stage_args[0].tile_rows,
+                           "l2": f"inputs larger than L2: {dr_slot_gb(case, mine):.1f} GB per state slot"},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+                "gpu_launches": int(launches)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    np.random.seed(0)
+
+
+def dr_slot_gb(case, blocks):
+    return sum(case.planes * 4 * (b.nj + 2) * (b.ni + 8) * 8 for b in blocks) / 1e9
+
+
+def main():
+    args = parse()
+    from paper_1304_7654_b200 import baseline_workload
+    wl = baseline_workload(args.workload)
+    if args.impl == "reference":
+        run_reference_arm(args, wl)
+    else:
+        run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()

@@ -52,10 +52,11 @@ typedef struct hbgpu_block {
     int32_t ni, nj;      /* interior cells                                  */
     int32_t pitch;       /* row stride, elements (multiple of 4)            */
     int32_t gid;         /* global block id                                 */
-    int32_t tiles_i;     /* ceil(ni / 32)                                   */
+    int32_t tiles_i;     /* column strips: ceil(ni / 32)                    */
     int32_t tiles_j;     /* ceil(nj / tile_rows)                            */
-    int32_t cta_begin;   /* first CTA of this block in the stage grid       */
-    int32_t ncta;        /* tiles_i * tiles_j                               */
+    int32_t tile_begin;  /* first tile of this block in the rank tile list  */
+    int32_t ntiles;      /* tiles_i * tiles_j; a tile is one CTA's 32-column
+                            strip over tile_rows rows, all 4 pdes           */
     double nu_h2;        /* NU / (h*h)          (hbcore.py:257)             */
     double adv_2h;       /* ADVECTION / (2*h)   (hbcore.py:257)             */
     double h;
@@ -141,19 +142,22 @@ typedef struct hbgpu_stage_args {
     double *out;               /* slot written (q_s), may equal q0         */
     double *sendbuf;           /* remote halo payloads (may be NULL)       */
     const hbgpu_block *blocks; /* device array [nblocks]                   */
-    const int32_t *cta_block;  /* device array [total_ctas]: CTA -> block  */
+    const int32_t *tile_block;  /* device array [total_tiles]: tile -> block */
     const double *sxy;         /* device forcing tables                    */
     const hbgpu_face_target *faces; /* device face-target pool             */
-    double *norm_part;         /* device [total_ctas] (stage 0) or NULL    */
+    double *norm_part;         /* device [total_tiles] (stage 0) or NULL    */
     unsigned long long *status;/* device [nblocks] divergence keys         */
     const int32_t *iter;       /* device iteration counter                 */
     const double *dmat;        /* device P*P (generic kernel only)         */
+    const void *tmaps;         /* device [3][nblocks] CUtensorMap of the three
+                                  slots (hbgpu_encode_tensor_maps)         */
     int32_t nblocks;
-    int32_t total_ctas;
+    int32_t total_tiles;
     int32_t planes;
     int32_t stage;             /* 0..3                                      */
     int32_t tile_rows;
-    int32_t pad;
+    int32_t in_slot;           /* which of the three slots `in` is (0..2);
+                                  q0 is slot 0                              */
     double coef;               /* alpha_s * dtau                            */
     double D[HBGPU_MAX_TEMPLATED_P * HBGPU_MAX_TEMPLATED_P];
     double ap[HBGPU_MAX_P * HBGPU_NPDE];
@@ -163,6 +167,18 @@ typedef struct hbgpu_stage_args {
  * update (hbcore.py:224-245), local halo forwarding and remote pack
  * (exchange.py:248-261), divergence keys, residual-norm partials */
 int hbgpu_stage(const hbgpu_stage_args *args, void *stream);
+
+/* resolve kernel attributes / occupancy for a snapshot count ahead of any
+ * CUDA graph capture (hbgpu_engine_create calls it) */
+int hbgpu_stage_prepare(int32_t planes);
+
+/* TMA descriptors for the stage kernel: for slot s (0..2) and block b, a 4-D
+ * tensor map (columns, rows, pde, plane) over the block's part of slot[s],
+ * written as CUtensorMap (128 B) #(s*nblocks + b) into out_host (caller
+ * uploads it to device memory, 64-B aligned).  out_bytes >= 3*nblocks*128. */
+int hbgpu_encode_tensor_maps(double *const slot[3], const hbgpu_block *blocks_host,
+                             int32_t nblocks, int32_t planes, void *out_host,
+                             int64_t out_bytes);
 
 /* standalone halo moves (exchange.py:295-316 local copy / pack / unpack) */
 int hbgpu_halo(double *slot, double *sendbuf, const double *recvbuf,
@@ -191,11 +207,11 @@ typedef struct hbgpu_engine_desc {
     double *slot[3];                 /* A (q0 / result), B, C              */
     double *sendbuf, *recvbuf;
     const hbgpu_block *blocks;       /* device */
-    const int32_t *cta_block;        /* device */
+    const int32_t *tile_block;        /* device */
     const double *sxy;               /* device */
     const hbgpu_face_target *faces;  /* device */
     const double *dmat;              /* device */
-    double *norm_part;               /* device [total_ctas] */
+    double *norm_part;               /* device [total_tiles] */
     double *sumsq;                   /* device [max_iters * nblocks] */
     unsigned long long *status;      /* device [nblocks] */
     int32_t *iter;                   /* device, 1 element */
@@ -206,7 +222,8 @@ typedef struct hbgpu_engine_desc {
     const hbgpu_peer_msg *sends;     int32_t nsends; /* HOST arrays */
     const hbgpu_peer_msg *recvs;     int32_t nrecvs;
     void *comm;                      /* from hbgpu_comm_init, NULL if 1 rank */
-    int32_t nblocks, total_ctas, planes, nbody, tile_rows, max_iters;
+    const void *tmaps;               /* device, from hbgpu_encode_tensor_maps */
+    int32_t nblocks, total_tiles, planes, nbody, tile_rows, max_iters;
     double coef[4];
     double D[HBGPU_MAX_TEMPLATED_P * HBGPU_MAX_TEMPLATED_P];
     double ap[HBGPU_MAX_P * HBGPU_NPDE];

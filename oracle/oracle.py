@@ -237,64 +237,92 @@ class OracleResult:
     forces: np.ndarray             # (3, planes, nbody): cl, cd, cm
     norms: list = field(default_factory=list)
     force_history: list = field(default_factory=list)
+    loop_s: float = 0.0
 
 
-def run(case, iterations=None, initial=None, nthreads=None, record_norms=True,
-        record_forces=False):
-    """Single-rank restatement of driver.run_case/_rank_program.
+class OracleSolver:
+    """Single-rank restatement of driver._rank_program (driver.py:110-149),
+    steppable so bench.py can time iterations.
 
     `case` is any object with the reference CaseConfig attributes.  `initial`
     optionally maps a BlockSpec to the (planes, npde, nj, ni) initial interior
     (the hbcore.initial_values hook); default is the reference's IC.
     """
-    iterations = case.iterations if iterations is None else iterations
-    planes = 2 * case.nharms + 1
-    npde = case.npde
-    blocks = sorted(case.blocks, key=lambda s: s.id)
-    nthreads = nthreads or max(1, len(os.sched_getaffinity(0)))
-    dmat = np.ascontiguousarray(spectral_matrix(case.nharms, case.omega))
-    qs, q0s, rs, srcs = {}, {}, {}, {}
-    for s in blocks:
-        qs[s.id] = np.zeros((planes, npde, s.nj + 2, s.ni + 2))
-        q0s[s.id] = np.zeros_like(qs[s.id])
-        rs[s.id] = np.zeros((planes, npde, s.nj, s.ni))
-        srcs[s.id] = forcing_values(s, planes, npde)
-        ic = initial(s, planes, npde) if initial is not None else initial_values(s, planes, npde)
-        qs[s.id][:, :, 1:s.nj + 1, 1:s.ni + 1] = ic
-    alpha_dtau = [a * case.dtau for a in RK_ALPHAS]
-    nb = len(blocks)
-    arr = lambda vals, t: np.array(vals, dtype=t)
-    q_p = arr([_ptr(qs[s.id]) for s in blocks], np.uintp)
-    q0_p = arr([_ptr(q0s[s.id]) for s in blocks], np.uintp)
-    r_p = arr([_ptr(rs[s.id]) for s in blocks], np.uintp)
-    s_p = arr([_ptr(srcs[s.id]) for s in blocks], np.uintp)
-    ni = arr([s.ni for s in blocks], np.int64)
-    nj = arr([s.nj for s in blocks], np.int64)
-    nu_h2 = arr([NU / (s.h * s.h) for s in blocks], np.float64)
-    adv_2h = arr([ADVECTION / (2.0 * s.h) for s in blocks], np.float64)
-    accs = np.zeros(nb * planes)
-    L = lib()
 
-    exchange(qs, case.cuts)  # priming exchange (driver.py:129)
-    forces = np.zeros((3, planes, case.nbody))
-    result = OracleResult(fields=qs, forces=forces)
-    for it in range(iterations):
-        for stage in range(4):
-            bad = L.oracle_stage_many(nb, _ptr(q_p), _ptr(q0_p), _ptr(r_p), _ptr(s_p),
-                                      _ptr(ni), _ptr(nj), _ptr(nu_h2), _ptr(adv_2h),
-                                      _ptr(dmat), planes, npde, alpha_dtau[stage],
-                                      int(stage == 0), nthreads, _ptr(accs))
-            if stage == 0 and record_norms:
-                result.norms.append(_norm(rs[s.id] for s in blocks))
-            if bad:
-                for k, s in enumerate(blocks):
-                    if not np.all(np.isfinite(qs[s.id][:, :, 1:-1, 1:-1])):
-                        raise OracleDivergence(it, stage, s.id, *divergence_location(qs[s.id]))
-            exchange(qs, case.cuts)
-        forces = compute_forces(qs, blocks, planes, case.nbody)
-        if record_forces:
-            result.force_history.append(forces.copy())
-    result.forces = forces
+    def __init__(self, case, initial=None, nthreads=None, record_norms=True,
+                 record_forces=False):
+        self.case = case
+        self.planes = planes = 2 * case.nharms + 1
+        self.npde = npde = case.npde
+        self.blocks = blocks = sorted(case.blocks, key=lambda s: s.id)
+        self.nthreads = nthreads or max(1, len(os.sched_getaffinity(0)))
+        self.dmat = np.ascontiguousarray(spectral_matrix(case.nharms, case.omega))
+        self.qs, self.q0s, self.rs, self.srcs = {}, {}, {}, {}
+        for s in blocks:
+            self.qs[s.id] = np.zeros((planes, npde, s.nj + 2, s.ni + 2))
+            self.q0s[s.id] = np.zeros_like(self.qs[s.id])
+            self.rs[s.id] = np.zeros((planes, npde, s.nj, s.ni))
+            self.srcs[s.id] = forcing_values(s, planes, npde)
+            ic = initial(s, planes, npde) if initial is not None else initial_values(s, planes, npde)
+            self.qs[s.id][:, :, 1:s.nj + 1, 1:s.ni + 1] = ic
+        self.alpha_dtau = [a * case.dtau for a in RK_ALPHAS]
+        arr = lambda vals, t: np.array(vals, dtype=t)  # noqa: E731
+        self._q = arr([_ptr(self.qs[s.id]) for s in blocks], np.uintp)
+        self._q0 = arr([_ptr(self.q0s[s.id]) for s in blocks], np.uintp)
+        self._r = arr([_ptr(self.rs[s.id]) for s in blocks], np.uintp)
+        self._s = arr([_ptr(self.srcs[s.id]) for s in blocks], np.uintp)
+        self._ni = arr([s.ni for s in blocks], np.int64)
+        self._nj = arr([s.nj for s in blocks], np.int64)
+        self._nu = arr([NU / (s.h * s.h) for s in blocks], np.float64)
+        self._adv = arr([ADVECTION / (2.0 * s.h) for s in blocks], np.float64)
+        self._accs = np.zeros(len(blocks) * planes)
+        self.record_norms, self.record_forces = record_norms, record_forces
+        self.result = OracleResult(fields=self.qs, forces=np.zeros((3, planes, case.nbody)))
+        self.done = 0
+
+    def prime(self):
+        exchange(self.qs, self.case.cuts)  # priming exchange (driver.py:129)
+
+    def iterate(self, iterations):
+        L = lib()
+        nb = len(self.blocks)
+        for _ in range(iterations):
+            for stage in range(4):
+                bad = L.oracle_stage_many(nb, _ptr(self._q), _ptr(self._q0), _ptr(self._r),
+                                          _ptr(self._s), _ptr(self._ni), _ptr(self._nj),
+                                          _ptr(self._nu), _ptr(self._adv), _ptr(self.dmat),
+                                          self.planes, self.npde, self.alpha_dtau[stage],
+                                          int(stage == 0), self.nthreads, _ptr(self._accs))
+                if stage == 0 and self.record_norms:
+                    self.result.norms.append(_norm(self.rs[s.id] for s in self.blocks))
+                if bad:
+                    for s in self.blocks:
+                        if not np.all(np.isfinite(self.qs[s.id][:, :, 1:-1, 1:-1])):
+                            raise OracleDivergence(self.done, stage, s.id,
+                                                   *divergence_location(self.qs[s.id]))
+                exchange(self.qs, self.case.cuts)
+            forces = compute_forces(self.qs, self.blocks, self.planes, self.case.nbody)
+            self.result.forces = forces
+            if self.record_forces:
+                self.result.force_history.append(forces.copy())
+            self.done += 1
+        return self.result
+
+    @property
+    def units_per_iteration(self):
+        return sum(s.ni * s.nj for s in self.blocks) * self.planes * 4
+
+
+def run(case, iterations=None, initial=None, nthreads=None, record_norms=True,
+        record_forces=False):
+    """Single-rank restatement of driver.run_case: prime, iterate, return fields/forces."""
+    import time
+    iterations = case.iterations if iterations is None else iterations
+    solver = OracleSolver(case, initial, nthreads, record_norms, record_forces)
+    t0 = time.perf_counter()
+    solver.prime()
+    result = solver.iterate(iterations)
+    result.loop_s = time.perf_counter() - t0
     return result
 
 

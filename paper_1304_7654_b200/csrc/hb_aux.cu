@@ -25,14 +25,15 @@ __global__ void halo_kernel(double *slot, double *sendbuf, const double *recvbuf
 
 // ---- residual norm ----------------------------------------------------------
 
-// per block: sequential sum of its CTAs' partials in CTA order
+// per block: sequential sum of its (tile, pde) partials in tile order
 __global__ void norm_fold_kernel(const hbgpu_block *blocks, int nblocks, const double *part,
                                  double *sumsq, const int32_t *iter) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= nblocks) return;
     const hbgpu_block &blk = blocks[b];
     double s = 0.0;
-    for (int c = 0; c < blk.ncta; ++c) s = radd(s, part[blk.cta_begin + c]);
+    // one partial per (tile, pde), tiles of a block contiguous
+    for (int c = 0; c < blk.ntiles * NPDE; ++c) s = radd(s, part[(int64_t)blk.tile_begin * NPDE + c]);
     sumsq[(int64_t)(*iter) * nblocks + b] = s;
 }
 

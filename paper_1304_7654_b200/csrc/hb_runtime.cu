@@ -191,14 +191,15 @@ int one_iteration(hbgpu_engine *e, cudaStream_t s) {
     a.q0 = d.slot[0];
     a.sendbuf = d.sendbuf;
     a.blocks = d.blocks;
-    a.cta_block = d.cta_block;
+    a.tile_block = d.tile_block;
     a.sxy = d.sxy;
     a.faces = d.faces;
     a.status = d.status;
     a.iter = d.iter;
     a.dmat = d.dmat;
+    a.tmaps = d.tmaps;
     a.nblocks = d.nblocks;
-    a.total_ctas = d.total_ctas;
+    a.total_tiles = d.total_tiles;
     a.planes = d.planes;
     a.tile_rows = d.tile_rows;
     memcpy(a.D, d.D, sizeof(a.D));
@@ -207,6 +208,7 @@ int one_iteration(hbgpu_engine *e, cudaStream_t s) {
         a.in = d.slot[kIn[st]];
         a.out = d.slot[kOut[st]];
         a.stage = st;
+        a.in_slot = kIn[st];
         a.coef = d.coef[st];
         a.norm_part = st == 0 ? d.norm_part : nullptr;
         int rc = hbgpu_stage(&a, s);
@@ -228,6 +230,8 @@ extern "C" int hbgpu_engine_create(const hbgpu_engine_desc *desc, hbgpu_engine *
         hbgpu_set_error("hbgpu_engine_create: bad descriptor");
         return HBGPU_ERR_ARG;
     }
+    int prc = hbgpu_stage_prepare(desc->planes);
+    if (prc) return prc;
     auto *e = new hbgpu_engine();
     e->d = *desc;
     if (desc->nsends > 0) e->sends.assign(desc->sends, desc->sends + desc->nsends);

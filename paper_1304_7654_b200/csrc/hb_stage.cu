@@ -12,16 +12,27 @@
 //     in the reference's element-major layout (remote cut) -- the
 //     _copy_local / _pack of exchange.py:248-261;
 //   * divergence keys (hbcore.py:244-245, 279-284);
-//   * stage 0: per-CTA partial sums of R^2 for the residual norm.
+//   * stage 0: per-(tile, pde) partial sums of R^2 for the residual norm.
 //
-// Layout and mapping.  A CTA is 4 warps; warp w owns pde p = w and 32
-// consecutive interior columns i; every lane marches down `tile_rows` rows
-// j keeping the rows j-1, j, j+1 of all P snapshots of its column in
-// registers (the stencil's north/south neighbours and the P centres the
-// D-contraction needs).  West/east neighbours come from the adjacent lanes
-// by warp shuffle; only lanes 0 and 31 load them.  Each q value therefore
-// crosses HBM once per stage (plus two halo rows per tile), and a warp's
-// loads and stores are 256 B contiguous rows.
+// Work decomposition.  A tile is one CTA's 32-column strip of one block over
+// `tile_rows` rows.  Consumer warp p (0..3) computes pde p; lane l owns
+// column i0 + l and marches down the rows keeping rows j-1, j, j+1 of all P
+// snapshots of its column in registers (stencil north/south neighbours and
+// the P centres of the D-contraction).
+//
+// Memory pipeline (warp-specialised, TMA).  A fifth warp is the producer:
+// one lane streams the tile's rows into shared memory with 4-D tensor TMA
+// loads (cp.async.bulk.tensor, box = 36 columns x 1 row x 4 pdes x P
+// snapshots = 10.4 KB at P = 9: the strip plus its west/east halo columns,
+// zero-filled past the row end), one ring of R slots for the stencil input
+// and one of Q slots for q_0.  Each slot has a "full" mbarrier (TMA
+// transaction count) and an "empty" mbarrier the four consumer warps arrive
+// on once they no longer read it.  The producer therefore runs R-2 rows ahead
+// of the consumers with only two requests per row, the per-request TMA cost
+// is amortised over ~10 KB, the west/east neighbours come from shared memory,
+// and the amount of memory in flight no longer depends on register pressure.
+// CTAs are persistent (tiles t = blockIdx.x, +gridDim.x, ...) so the ring
+// streams across tile boundaries without draining.
 //
 // Rounding: every operation is an explicitly rounded DMUL/DADD, in the
 // reference's per-point order, including the m == n term (D[n][n] = 0 still
@@ -29,7 +40,68 @@
 
 #include "hb_common.cuh"
 
+#include <cuda.h>
+
 namespace hbgpu {
+
+// ---- PTX: mbarrier + tensor TMA --------------------------------------------------
+
+__device__ __forceinline__ uint32_t saddr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(saddr(b)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void tma_load_4d(void *dst, const void *map, int c0, int c1, int c2, int c3,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(saddr(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(saddr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const void *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+// ---- tiles and halo targets -------------------------------------------------
+
+struct Tile {
+    int bidx;   // local block index
+    int i0;     // first interior column of the strip (1-based)
+    int j0, j1; // first / last interior row
+};
+
+__device__ __forceinline__ Tile decode_tile(const hbgpu_stage_args &a, int t) {
+    Tile T;
+    T.bidx = a.tile_block[t];
+    const hbgpu_block &b = a.blocks[T.bidx];
+    const int local = t - b.tile_begin;
+    T.i0 = (local % b.tiles_i) * 32 + 1;
+    T.j0 = (local / b.tiles_i) * a.tile_rows + 1;
+    T.j1 = min(T.j0 + a.tile_rows - 1, b.nj);
+    return T;
+}
 
 struct FaceHit {
     int64_t off;
@@ -46,6 +118,18 @@ __device__ __forceinline__ FaceHit load_target(const hbgpu_face_target *pool, in
     return t;
 }
 
+// halo targets of cell (i, j): the south/north face target and the west/east one
+__device__ __forceinline__ void cell_targets(const hbgpu_face_target *pool, const hbgpu_block &b, int i,
+                                             int j, bool live, FaceHit &trow, FaceHit &tcol) {
+    trow = FaceHit{0, 0};
+    tcol = FaceHit{0, 0};
+    if (!live) return;
+    if (j == 1) trow = load_target(pool, b.face_off[0], i - 1);
+    else if (j == b.nj) trow = load_target(pool, b.face_off[1], i - 1);
+    if (i == 1) tcol = load_target(pool, b.face_off[2], j - 1);
+    else if (i == b.ni) tcol = load_target(pool, b.face_off[3], j - 1);
+}
+
 __device__ __forceinline__ void forward(const FaceHit &t, double *out, double *sendbuf, int n, int p,
                                         double v) {
     if (t.ps > 0) {
@@ -55,156 +139,234 @@ __device__ __forceinline__ void forward(const FaceHit &t, double *out, double *s
     }
 }
 
-__device__ __forceinline__ double cta_sum(double v, double *smem) {
-    // fixed-shape tree: deterministic for a given launch geometry
+__device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = radd(v, __shfl_down_sync(0xffffffffu, v, o));
-    const int warp = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0) smem[warp] = v;
-    __syncthreads();
-    double s = 0.0;
-    if (threadIdx.x == 0) {
-        s = smem[0];
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) s = radd(s, smem[w]);
-    }
-    return s;
+    return v;
 }
 
-template <int P, bool FIRST>
-__global__ void __launch_bounds__(128) stage_kernel(const __grid_constant__ hbgpu_stage_args a) {
-    __shared__ double red[4];
-    const int cta = blockIdx.x;
-    const int bidx = a.cta_block[cta];
-    const hbgpu_block &blk = a.blocks[bidx];
-    const int ni = blk.ni, nj = blk.nj, pitch = blk.pitch;
-    const int64_t ps = blk.ps;
-    const int64_t ps4 = ps * NPDE;
-    const double nu_h2 = blk.nu_h2, adv_2h = blk.adv_2h;
+// ---- shared-memory geometry -------------------------------------------------------
 
-    const int local = cta - blk.cta_begin;
-    const int ti = local % blk.tiles_i;
-    const int tj = local / blk.tiles_i;
+constexpr int CW = 4;                     // consumer warps (one per pde)
+constexpr int THREADS = (CW + 1) * 32;    // + one producer warp
+constexpr int SEG = 36;                   // columns per box row: i0-2 .. i0+33
+
+template <int P, bool FIRST, int R, int Q>
+struct Smem {
+    static constexpr int SLOT = P * NPDE * SEG;   // doubles: [snapshot][pde][SEG]
+    static constexpr int NQ = FIRST ? 0 : Q;
+    static constexpr size_t BAR_OFF = (size_t)(R + NQ) * SLOT * 8;
+    static constexpr size_t BYTES = BAR_OFF + (size_t)2 * (R + NQ) * 8;
+};
+
+// ---- the pipelined kernel -----------------------------------------------------------
+
+template <int P, bool FIRST, int R, int Q, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) stage_tma_kernel(const __grid_constant__ hbgpu_stage_args a) {
+    using S = Smem<P, FIRST, R, Q>;
+    static_assert(R >= 3 && Q >= 2, "ring too short");
+    extern __shared__ __align__(1024) unsigned char smem[];
+    double *ring = reinterpret_cast<double *>(smem);
+    double *qring = ring + R * S::SLOT;
+    uint64_t *full_in = reinterpret_cast<uint64_t *>(smem + S::BAR_OFF);
+    uint64_t *empty_in = full_in + R;
+    uint64_t *full_q = empty_in + R;
+    uint64_t *empty_q = full_q + S::NQ;
+    const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int p = threadIdx.x >> 5;
-    const int i = ti * 32 + lane + 1;            // 1-based interior column
-    const bool live = i <= ni;
-    const int ic = min(i, ni + 1);               // clamped: dead lanes read the halo column
-    const int j0 = tj * a.tile_rows + 1;
-    const int j1 = min(j0 + a.tile_rows - 1, nj);
-    const int gstage = (*a.iter) * 4 + a.stage + 1;
-
-    const int64_t col = blk.base + (int64_t)p * ps + LEAD + ic;
-    const double *__restrict__ in = a.in + col;
-    const double *q0 = a.q0 + col;
-    double *out = a.out + col;
-    const double *sxy = a.sxy + blk.sxy_off + (i - 1);
-    const double coef = a.coef;
-
-    double up[P], cur[P], dn[P];
-#pragma unroll
-    for (int m = 0; m < P; ++m) {
-        up[m] = __ldg(in + m * ps4 + (int64_t)(j0 - 1) * pitch);
-        cur[m] = __ldg(in + m * ps4 + (int64_t)j0 * pitch);
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < R; ++k) {
+            mbar_init(full_in + k, 1);
+            mbar_init(empty_in + k, CW);
+        }
+        for (int k = 0; k < S::NQ; ++k) {
+            mbar_init(full_q + k, 1);
+            mbar_init(empty_q + k, CW);
+        }
+        fence_mbar_init();
     }
+    __syncthreads();
+    const int ntile = a.total_tiles;
+    const CUtensorMap *maps = reinterpret_cast<const CUtensorMap *>(a.tmaps);
 
-    double nrm = 0.0;
-    // west/east neighbours outside the warp's 32 columns
-    const int64_t wcol = (int64_t)(i - 1) - ic;                 // offset of column i-1
-    const int64_t ecol = (int64_t)min(i + 1, ni + 1) - ic;      // offset of column i+1
-
-    for (int j = j0; j <= j1; ++j) {
-        const int64_t row = (int64_t)j * pitch;
-#pragma unroll
-        for (int m = 0; m < P; ++m) dn[m] = __ldg(in + m * ps4 + row + pitch);
-        double q0v[FIRST ? 1 : P];
-        if (!FIRST) {
-#pragma unroll
-            for (int n = 0; n < P; ++n) q0v[n] = q0[n * ps4 + row];
-        }
-        const double sv = live ? sxy[(int64_t)(j - 1) * ni] : 0.0;
-
-        FaceHit trow{0, 0}, tcol{0, 0};
-        if (live) {
-            if (j == 1) trow = load_target(a.faces, blk.face_off[0], i - 1);
-            else if (j == nj) trow = load_target(a.faces, blk.face_off[1], i - 1);
-            if (i == 1) tcol = load_target(a.faces, blk.face_off[2], j - 1);
-            else if (i == ni) tcol = load_target(a.faces, blk.face_off[3], j - 1);
-        }
-
-#pragma unroll
-        for (int n = 0; n < P; ++n) {
-            const double *rown = in + n * ps4 + row;
-            double w = __shfl_up_sync(0xffffffffu, cur[n], 1);
-            double e = __shfl_down_sync(0xffffffffu, cur[n], 1);
-            if (lane == 0) w = __ldg(rown + wcol);
-            if (lane == 31) e = __ldg(rown + ecol);
-            double o = stencil(cur[n], w, e, up[n], dn[n], nu_h2, adv_2h);
-#pragma unroll
-            for (int m = 0; m < P; ++m) o = radd(o, rmul(a.D[n * P + m], cur[m]));
-            o = radd(o, rmul(a.ap[n * NPDE + p], sv));
-            const double base = FIRST ? cur[n] : q0v[n];
-            const double v = rsub(base, rmul(coef, o));
-            if (live) {
-                out[n * ps4 + row] = v;
-                if (FIRST) nrm = radd(nrm, rmul(o, o));
-                forward(trow, a.out, a.sendbuf, n, p, v);
-                forward(tcol, a.out, a.sendbuf, n, p, v);
-                if (nonfinite(v)) {
-                    long long lin = (((long long)(n * NPDE + p) * nj + (j - 1)) * ni) + (i - 1);
-                    atomicMin(a.status + bidx, divergence_key(gstage, lin));
-                }
+    if (warp == CW) {
+        // ------------------------------ producer ------------------------------
+        if (lane != 0) return;
+        constexpr uint32_t BYTES = S::SLOT * 8;
+        long long ein = 0, eq = 0;
+        auto put_in = [&](const CUtensorMap *m, int x, int row) {
+            const int s = (int)(ein % R);
+            if (ein >= R) mbar_wait(empty_in + s, (uint32_t)(((ein / R) + 1) & 1));
+            mbar_expect_tx(full_in + s, BYTES);
+            tma_load_4d(ring + s * S::SLOT, m, x, row, 0, 0, full_in + s);
+            ++ein;
+        };
+        auto put_q = [&](const CUtensorMap *m, int x, int row) {
+            const int s = (int)(eq % Q);
+            if (eq >= Q) mbar_wait(empty_q + s, (uint32_t)(((eq / Q) + 1) & 1));
+            mbar_expect_tx(full_q + s, BYTES);
+            tma_load_4d(qring + s * S::SLOT, m, x, row, 0, 0, full_q + s);
+            ++eq;
+        };
+        for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+            const Tile tl = decode_tile(a, t);
+            const CUtensorMap *min = maps + a.in_slot * a.nblocks + tl.bidx;
+            const CUtensorMap *mq = maps + tl.bidx;   // q0 is slot 0
+            prefetch_tmap(min);
+            const int x = tl.i0 + LEAD - 2;
+            put_in(min, x, tl.j0 - 1);
+            put_in(min, x, tl.j0);
+            for (int j = tl.j0; j <= tl.j1; ++j) {
+                put_in(min, x, j + 1);
+                if (!FIRST) put_q(mq, x, j);
             }
         }
-#pragma unroll
-        for (int m = 0; m < P; ++m) {
-            up[m] = cur[m];
-            cur[m] = dn[m];
-        }
+        return;
     }
-    if (FIRST && a.norm_part != nullptr) {
-        double s = cta_sum(nrm, red);
-        if (threadIdx.x == 0) a.norm_part[cta] = s;
+
+    // -------------------------------- consumers ---------------------------------
+    const int p = warp;
+    const int gstage = (*a.iter) * 4 + a.stage + 1;
+    const double coef = a.coef;
+    long long ein = 0, eq = 0;
+    for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+        const Tile tl = decode_tile(a, t);
+        const hbgpu_block &b = a.blocks[tl.bidx];
+        const int ni = b.ni, nj = b.nj;
+        const int64_t ps4 = b.ps * NPDE;
+        const double nu_h2 = b.nu_h2, adv_2h = b.adv_2h;
+        const int i = tl.i0 + lane;
+        const bool live = i <= ni;
+        double *out = a.out + b.base + (int64_t)p * b.ps + LEAD + i;
+        const double *sxy = a.sxy + b.sxy_off + (i - 1);
+        double ap[P];
+#pragma unroll
+        for (int n = 0; n < P; ++n) ap[n] = a.ap[n * NPDE + p];
+
+        FaceHit trow, tcol;
+        cell_targets(a.faces, b, i, tl.j0, live, trow, tcol);
+        double sv = live ? sxy[(int64_t)(tl.j0 - 1) * ni] : 0.0;
+
+        // rows j0-1 and j0 -> registers; release row j0-1
+        double up[P], cur[P], dn[P];
+        {
+            const int s0 = (int)(ein % R), s1 = (int)((ein + 1) % R);
+            mbar_wait(full_in + s0, (uint32_t)((ein / R) & 1));
+            mbar_wait(full_in + s1, (uint32_t)(((ein + 1) / R) & 1));
+            const double *r0 = ring + s0 * S::SLOT + p * SEG + lane + 2;
+            const double *r1 = ring + s1 * S::SLOT + p * SEG + lane + 2;
+#pragma unroll
+            for (int m = 0; m < P; ++m) {
+                up[m] = r0[m * NPDE * SEG];
+                cur[m] = r1[m * NPDE * SEG];
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty_in + s0);
+            ++ein;   // ein: entry of the current row j
+        }
+        double nrm = 0.0;
+
+        for (int j = tl.j0; j <= tl.j1; ++j) {
+            // prefetch the next row's forcing value and halo targets
+            FaceHit nrow, ncol;
+            cell_targets(a.faces, b, i, j + 1, live && j < tl.j1, nrow, ncol);
+            const double sv_next = (live && j < tl.j1) ? sxy[(int64_t)j * ni] : 0.0;
+
+            const int sc = (int)(ein % R);
+            const int sn = (int)((ein + 1) % R);
+            mbar_wait(full_in + sn, (uint32_t)(((ein + 1) / R) & 1));
+            const double *rc = ring + sc * S::SLOT + p * SEG + lane;
+            const double *rn = ring + sn * S::SLOT + p * SEG + lane + 2;
+#pragma unroll
+            for (int m = 0; m < P; ++m) dn[m] = rn[m * NPDE * SEG];
+            const double *qv = nullptr;
+            int sq = 0;
+            if (!FIRST) {
+                sq = (int)(eq % Q);
+                mbar_wait(full_q + sq, (uint32_t)((eq / Q) & 1));
+                qv = qring + sq * S::SLOT + p * SEG + lane + 2;
+            }
+            const int64_t row = (int64_t)j * b.pitch;
+#pragma unroll
+            for (int n = 0; n < P; ++n) {
+                const double w = rc[n * NPDE * SEG + 1];
+                const double e = rc[n * NPDE * SEG + 3];
+                double o = stencil(cur[n], w, e, up[n], dn[n], nu_h2, adv_2h);
+#pragma unroll
+                for (int m = 0; m < P; ++m) o = radd(o, rmul(a.D[n * P + m], cur[m]));
+                o = radd(o, rmul(ap[n], sv));
+                const double base = FIRST ? cur[n] : qv[n * NPDE * SEG];
+                const double v = rsub(base, rmul(coef, o));
+                if (live) {
+                    out[n * ps4 + row] = v;
+                    if (FIRST) nrm = radd(nrm, rmul(o, o));
+                    forward(trow, a.out, a.sendbuf, n, p, v);
+                    forward(tcol, a.out, a.sendbuf, n, p, v);
+                    if (nonfinite(v)) {
+                        long long lin = (((long long)(n * NPDE + p) * nj + (j - 1)) * ni) + (i - 1);
+                        atomicMin(a.status + tl.bidx, divergence_key(gstage, lin));
+                    }
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < P; ++m) {
+                up[m] = cur[m];
+                cur[m] = dn[m];
+            }
+            trow = nrow;
+            tcol = ncol;
+            sv = sv_next;
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(empty_in + sc);   // row j no longer read
+                if (!FIRST) mbar_arrive(empty_q + sq);
+            }
+            ++ein;
+            if (!FIRST) ++eq;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_in + (int)(ein % R));   // row j1+1
+        ++ein;
+        if (FIRST && a.norm_part != nullptr) {
+            const double s = warp_sum(nrm);
+            if (lane == 0) a.norm_part[(int64_t)t * NPDE + p] = s;
+        }
     }
 }
 
-// Generic snapshot count (P > HBGPU_MAX_TEMPLATED_P, e.g. the 63-plane
-// tc1-full case): one thread per (column, pde) and row, D from shared memory,
-// operands re-read through L1.  Same arithmetic sequence.
-__global__ void __launch_bounds__(128) stage_kernel_generic(const __grid_constant__ hbgpu_stage_args a) {
+// ---- generic snapshot count (P > HBGPU_MAX_TEMPLATED_P) --------------------------
+// One CTA of 4 warps (one per pde) per tile, operands through L1, D from
+// shared memory.  Same arithmetic sequence; used for e.g. the 63-plane
+// tc1-full catalog case.
+__global__ void __launch_bounds__(CW * 32) stage_kernel_generic(const __grid_constant__ hbgpu_stage_args a) {
     extern __shared__ double sh[];
-    double *D = sh;
-    double *red = sh + a.planes * a.planes;
     const int P = a.planes;
-    for (int k = threadIdx.x; k < P * P; k += blockDim.x) D[k] = a.dmat[k];
+    for (int k = threadIdx.x; k < P * P; k += blockDim.x) sh[k] = a.dmat[k];
     __syncthreads();
-    const int cta = blockIdx.x;
-    const int bidx = a.cta_block[cta];
-    const hbgpu_block &blk = a.blocks[bidx];
-    const int ni = blk.ni, nj = blk.nj, pitch = blk.pitch;
-    const int64_t ps4 = blk.ps * NPDE;
-    const int local = cta - blk.cta_begin;
-    const int ti = local % blk.tiles_i, tj = local / blk.tiles_i;
-    const int lane = threadIdx.x & 31, p = threadIdx.x >> 5;
-    const int i = ti * 32 + lane + 1;
+    const double *D = sh;
+    const int lane = threadIdx.x & 31;
+    const int p = threadIdx.x >> 5;
+    const int t = blockIdx.x;
+    const Tile tl = decode_tile(a, t);
+    const hbgpu_block &b = a.blocks[tl.bidx];
+    const int ni = b.ni, nj = b.nj, pitch = b.pitch;
+    const int64_t ps4 = b.ps * NPDE;
+    const int i = tl.i0 + lane;
     const bool live = i <= ni;
-    const int j0 = tj * a.tile_rows + 1, j1 = min(j0 + a.tile_rows - 1, nj);
     const bool first = a.stage == 0;
     const int gstage = (*a.iter) * 4 + a.stage + 1;
     double nrm = 0.0;
     if (live) {
-        const int64_t col = blk.base + (int64_t)blk.ps * p + LEAD + i;
+        const int64_t col = b.base + (int64_t)b.ps * p + LEAD + i;
         const double *in = a.in + col;
-        for (int j = j0; j <= j1; ++j) {
+        for (int j = tl.j0; j <= tl.j1; ++j) {
             const int64_t row = (int64_t)j * pitch;
-            const double sv = a.sxy[blk.sxy_off + (int64_t)(j - 1) * ni + (i - 1)];
-            FaceHit trow{0, 0}, tcol{0, 0};
-            if (j == 1) trow = load_target(a.faces, blk.face_off[0], i - 1);
-            else if (j == nj) trow = load_target(a.faces, blk.face_off[1], i - 1);
-            if (i == 1) tcol = load_target(a.faces, blk.face_off[2], j - 1);
-            else if (i == ni) tcol = load_target(a.faces, blk.face_off[3], j - 1);
+            const double sv = a.sxy[b.sxy_off + (int64_t)(j - 1) * ni + (i - 1)];
+            FaceHit trow, tcol;
+            cell_targets(a.faces, b, i, j, true, trow, tcol);
             for (int n = 0; n < P; ++n) {
                 const double *c = in + n * ps4 + row;
-                double o = stencil(c[0], c[-1], c[1], c[-pitch], c[pitch], blk.nu_h2, blk.adv_2h);
+                double o = stencil(c[0], c[-1], c[1], c[-pitch], c[pitch], b.nu_h2, b.adv_2h);
                 for (int m = 0; m < P; ++m) o = radd(o, rmul(D[n * P + m], in[m * ps4 + row]));
                 o = radd(o, rmul(a.ap[n * NPDE + p], sv));
                 const double base = first ? c[0] : a.q0[col + n * ps4 + row];
@@ -215,57 +377,170 @@ __global__ void __launch_bounds__(128) stage_kernel_generic(const __grid_constan
                 forward(tcol, a.out, a.sendbuf, n, p, v);
                 if (nonfinite(v)) {
                     long long lin = (((long long)(n * NPDE + p) * nj + (j - 1)) * ni) + (i - 1);
-                    atomicMin(a.status + bidx, divergence_key(gstage, lin));
+                    atomicMin(a.status + tl.bidx, divergence_key(gstage, lin));
                 }
             }
         }
     }
     if (first && a.norm_part != nullptr) {
-        double s = cta_sum(nrm, red);
-        if (threadIdx.x == 0) a.norm_part[cta] = s;
+        const double s = warp_sum(nrm);
+        if (lane == 0) a.norm_part[(int64_t)t * NPDE + p] = s;
     }
 }
 
+// ---- launch -------------------------------------------------------------------
+
+struct Launch {
+    void (*fn)(hbgpu_stage_args) = nullptr;
+    size_t smem = 0;
+    int grid = 0;   // persistent CTAs: SMs x resident CTAs per SM
+    bool ready = false;
+};
+
+template <int P, bool FIRST, int R, int Q, int MINB>
+static int prepare(Launch &L) {
+    if (L.ready) return HBGPU_OK;
+    L.fn = stage_tma_kernel<P, FIRST, R, Q, MINB>;
+    L.smem = Smem<P, FIRST, R, Q>::BYTES;
+    if (cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem) != cudaSuccess)
+        return hbgpu_check_launch("stage kernel smem attribute");
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.fn, THREADS, L.smem) != cudaSuccess ||
+        per_sm < 1)
+        return hbgpu_check_launch("stage kernel occupancy");
+    L.grid = sms * per_sm;
+    L.ready = true;
+    return HBGPU_OK;
+}
+
+// ring depths (R stencil rows, Q q0 rows) and CTAs per SM, per snapshot count:
+// each CTA keeps R-2 + Q-1 rows (~10 KB each at P = 9) in flight
+template <int P> struct Depth { static constexpr int R = 5, Q = 4, MINB = 2; };
+template <> struct Depth<1> { static constexpr int R = 8, Q = 6, MINB = 3; };
+template <> struct Depth<3> { static constexpr int R = 8, Q = 6, MINB = 3; };
+template <> struct Depth<5> { static constexpr int R = 6, Q = 5, MINB = 2; };
+template <> struct Depth<11> { static constexpr int R = 4, Q = 3, MINB = 2; };
+template <> struct Depth<13> { static constexpr int R = 4, Q = 3, MINB = 2; };
+template <> struct Depth<15> { static constexpr int R = 4, Q = 2, MINB = 2; };
+template <> struct Depth<17> { static constexpr int R = 4, Q = 2, MINB = 1; };
+
 template <int P>
-static void launch_p(const hbgpu_stage_args &a, cudaStream_t s) {
-    if (a.stage == 0)
-        stage_kernel<P, true><<<a.total_ctas, 128, 0, s>>>(a);
-    else
-        stage_kernel<P, false><<<a.total_ctas, 128, 0, s>>>(a);
+static int launch_p(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
+    using D = Depth<P>;
+    static Launch first, rest;
+    int rc = prepare<P, true, D::R, D::Q, D::MINB>(first);
+    if (!rc) rc = prepare<P, false, D::R, D::Q, D::MINB>(rest);
+    if (rc || prepare_only) return rc;
+    if (a.tmaps == nullptr) {
+        hbgpu_set_error("hbgpu_stage: args->tmaps is required (hbgpu_encode_tensor_maps)");
+        return HBGPU_ERR_ARG;
+    }
+    Launch &L = a.stage == 0 ? first : rest;
+    const int grid = min(L.grid, a.total_tiles);
+    L.fn<<<grid, THREADS, L.smem, s>>>(a);
+    hbgpu_count_launch(1);
+    return hbgpu_check_launch("hbgpu_stage");
+}
+
+static int dispatch(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
+    switch (a.planes) {
+        case 1: return launch_p<1>(a, s, prepare_only);
+        case 3: return launch_p<3>(a, s, prepare_only);
+        case 5: return launch_p<5>(a, s, prepare_only);
+        case 7: return launch_p<7>(a, s, prepare_only);
+        case 9: return launch_p<9>(a, s, prepare_only);
+        case 11: return launch_p<11>(a, s, prepare_only);
+        case 13: return launch_p<13>(a, s, prepare_only);
+        case 15: return launch_p<15>(a, s, prepare_only);
+        case 17: return launch_p<17>(a, s, prepare_only);
+        default: break;
+    }
+    const size_t sm = sizeof(double) * (size_t)a.planes * a.planes;
+    if (sm > 48 * 1024 &&
+        cudaFuncSetAttribute(stage_kernel_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+            cudaSuccess)
+        return hbgpu_check_launch("generic stage smem attribute");
+    if (prepare_only) return HBGPU_OK;
+    if (a.dmat == nullptr) {
+        hbgpu_set_error("hbgpu_stage: P=%d needs args->dmat", a.planes);
+        return HBGPU_ERR_ARG;
+    }
+    stage_kernel_generic<<<a.total_tiles, CW * 32, sm, s>>>(a);
+    hbgpu_count_launch(1);
+    return hbgpu_check_launch("hbgpu_stage");
+}
+
+// ---- tensor maps ------------------------------------------------------------------
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (fn == nullptr) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
 }
 
 }  // namespace hbgpu
 
+// Function attributes and occupancy are resolved once per kernel instantiation,
+// before any stream capture (the engine calls this at creation).
+extern "C" int hbgpu_stage_prepare(int32_t planes) {
+    hbgpu_stage_args a;
+    a.planes = planes;
+    return hbgpu::dispatch(a, nullptr, true);
+}
+
 extern "C" int hbgpu_stage(const hbgpu_stage_args *args, void *stream) {
-    using namespace hbgpu;
-    if (args == nullptr || args->total_ctas <= 0 || args->planes < 1) {
+    if (args == nullptr || args->total_tiles <= 0 || args->planes < 1 || args->planes > HBGPU_MAX_P ||
+        args->in_slot < 0 || args->in_slot > 2) {
         hbgpu_set_error("hbgpu_stage: bad arguments");
         return HBGPU_ERR_ARG;
     }
-    cudaStream_t s = (cudaStream_t)stream;
-    const hbgpu_stage_args &a = *args;
-    switch (a.planes) {
-        case 1: launch_p<1>(a, s); break;
-        case 3: launch_p<3>(a, s); break;
-        case 5: launch_p<5>(a, s); break;
-        case 7: launch_p<7>(a, s); break;
-        case 9: launch_p<9>(a, s); break;
-        case 11: launch_p<11>(a, s); break;
-        case 13: launch_p<13>(a, s); break;
-        case 15: launch_p<15>(a, s); break;
-        case 17: launch_p<17>(a, s); break;
-        default: {
-            if (a.dmat == nullptr) {
-                hbgpu_set_error("hbgpu_stage: P=%d needs args->dmat", a.planes);
-                return HBGPU_ERR_ARG;
+    return hbgpu::dispatch(*args, (cudaStream_t)stream, false);
+}
+
+extern "C" int hbgpu_encode_tensor_maps(double *const slot[3], const hbgpu_block *blocks, int32_t nblocks,
+                                        int32_t planes, void *out_host, int64_t out_bytes) {
+    using namespace hbgpu;
+    if ((int64_t)sizeof(CUtensorMap) * 3 * nblocks > out_bytes || planes < 1 || planes > 256) {
+        hbgpu_set_error("hbgpu_encode_tensor_maps: output too small or bad planes");
+        return HBGPU_ERR_ARG;
+    }
+    EncodeTiledFn fn = encode_fn();
+    if (fn == nullptr) {
+        hbgpu_set_error("cuTensorMapEncodeTiled unavailable from the driver");
+        return HBGPU_ERR_CUDA;
+    }
+    CUtensorMap *maps = reinterpret_cast<CUtensorMap *>(out_host);
+    for (int s = 0; s < 3; ++s) {
+        for (int k = 0; k < nblocks; ++k) {
+            const hbgpu_block &b = blocks[k];
+            cuuint64_t dims[4] = {(cuuint64_t)b.pitch, (cuuint64_t)(b.nj + 2), (cuuint64_t)NPDE,
+                                  (cuuint64_t)planes};
+            cuuint64_t strides[3] = {(cuuint64_t)b.pitch * 8, (cuuint64_t)b.ps * 8,
+                                     (cuuint64_t)b.ps * 8 * NPDE};
+            cuuint32_t box[4] = {(cuuint32_t)SEG, 1, (cuuint32_t)NPDE, (cuuint32_t)planes};
+            cuuint32_t estr[4] = {1, 1, 1, 1};
+            CUresult r = fn(&maps[s * nblocks + k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
+                            (void *)(slot[s] + b.base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) {
+                hbgpu_set_error("cuTensorMapEncodeTiled failed (%d) for slot %d block %d", (int)r, s, k);
+                return HBGPU_ERR_CUDA;
             }
-            size_t sm = sizeof(double) * ((size_t)a.planes * a.planes + 4);
-            if (sm > 48 * 1024)
-                cudaFuncSetAttribute(stage_kernel_generic, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sm);
-            stage_kernel_generic<<<a.total_ctas, 128, sm, s>>>(a);
         }
     }
-    hbgpu_count_launch(1);
-    return hbgpu_check_launch("hbgpu_stage");
+    return HBGPU_OK;
 }

@@ -8,7 +8,9 @@ rank owns it fixes:
   multiple of 4 doubles and ROW_LEAD = 3 so every interior row starts on a
   32-byte sector; block bases are 256-byte aligned.  Three slots (A, B, C)
   share the layout;
-* the stage grid: CTAs of 4 warps (warp = pde), 32 columns x tile_rows rows;
+* the stage tiles: one tile = one CTA's 32-column strip over tile_rows rows
+  of one block (4 consumer warps = 4 pdes); tile t of block b is strip
+  t % tiles_i, row tile t / tiles_i;
 * the face-target pool (fused halo forwarding, see cutplan.py);
 * the standalone halo directions (priming exchange / pack / unpack);
 * the send / receive buffer segments, grouped per peer rank, one NCCL
@@ -30,9 +32,10 @@ ROW_LEAD = native.ROW_LEAD
 NPDE = native.NPDE
 WARP_COLS = 32
 BLOCK_ALIGN = 32          # elements (256 B)
-TARGET_CTAS = 148 * 8     # enough resident warps on 148 SMs at ~2 CTAs/SM
-MAX_TILE_ROWS = 128
+TARGET_TILES = 148 * 2 * 8   # ~8 tiles per persistent CTA (148 SMs x 2 CTAs)
+MAX_TILE_ROWS = 256
 MIN_TILE_ROWS = 8
+SLOT_TAIL = 64            # elements of zero padding after the last block
 
 
 def _round_up(x, m):
@@ -40,8 +43,10 @@ def _round_up(x, m):
 
 
 def choose_tile_rows(blocks):
+    """Rows per tile: long tiles amortise the two halo rows each tile re-reads;
+    enough tiles keep every persistent warp of the stage kernel busy."""
     rows = sum(-(-b.ni // WARP_COLS) * b.nj for b in blocks)
-    tj = rows // max(1, TARGET_CTAS)
+    tj = rows // TARGET_TILES
     tj = max(MIN_TILE_ROWS, min(MAX_TILE_ROWS, tj))
     return tj
 
@@ -57,8 +62,8 @@ class RankLayout:
     slot_elems: int
     tile_rows: int
     block_table: np.ndarray
-    cta_block: np.ndarray
-    total_ctas: int
+    tile_block: np.ndarray
+    total_tiles: int
     sxy: np.ndarray
     faces: np.ndarray
     prime_dirs: np.ndarray
@@ -107,31 +112,33 @@ def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None):
         ps.append((b.nj + 2) * pt)
         base.append(off)
         off = _round_up(off + planes * NPDE * (b.nj + 2) * pt, BLOCK_ALIGN)
-    slot_elems = off
+    # bulk row copies of the last strip may run a few elements past a row end
+    slot_elems = off + SLOT_TAIL
 
     table = np.zeros(len(owned), dtype=native.BLOCK_DTYPE)
-    cta_block = []
+    tile_block = []
     sxy_parts, sxy_off = [], 0
-    cta = 0
+    ntile = 0
     for k, b in enumerate(owned):
         ti = -(-b.ni // WARP_COLS)
         tjn = -(-b.nj // tj)
         nu_h2, adv_2h = stencil_coefficients(b.h)
         for name, value in (("base", base[k]), ("ps", ps[k]), ("ni", b.ni), ("nj", b.nj),
                             ("pitch", pitch[k]), ("gid", b.id), ("tiles_i", ti),
-                            ("tiles_j", tjn), ("cta_begin", cta), ("ncta", ti * tjn),
+                            ("tiles_j", tjn), ("tile_begin", ntile),
+                            ("ntiles", ti * tjn),
                             ("nu_h2", nu_h2), ("adv_2h", adv_2h), ("h", b.h),
                             ("sxy_off", sxy_off)):
             table[name][k] = value
         table["face_off"][k] = -1
-        cta_block += [k] * (ti * tjn)
-        cta += ti * tjn
+        tile_block += [k] * (ti * tjn)
+        ntile += ti * tjn
         sxy_parts.append(forcing_table(b).ravel())
         sxy_off += b.ni * b.nj
 
     layout = RankLayout(planes=planes, blocks=owned, local_index=local_index, pitch=pitch, ps=ps,
                         base=base, slot_elems=slot_elems, tile_rows=tj, block_table=table,
-                        cta_block=np.asarray(cta_block, dtype=np.int32), total_ctas=cta,
+                        tile_block=np.asarray(tile_block, dtype=np.int32), total_tiles=ntile,
                         sxy=np.concatenate(sxy_parts), faces=np.zeros(0, native.FACE_TARGET_DTYPE),
                         prime_dirs=np.zeros(0, native.HALO_DIR_DTYPE),
                         unpack_dirs=np.zeros(0, native.HALO_DIR_DTYPE),

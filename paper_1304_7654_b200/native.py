@@ -30,8 +30,8 @@ c_i32, c_i64, c_f64, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, cty
 
 BLOCK_DTYPE = np.dtype([
     ("base", "<i8"), ("ps", "<i8"), ("ni", "<i4"), ("nj", "<i4"), ("pitch", "<i4"),
-    ("gid", "<i4"), ("tiles_i", "<i4"), ("tiles_j", "<i4"), ("cta_begin", "<i4"),
-    ("ncta", "<i4"), ("nu_h2", "<f8"), ("adv_2h", "<f8"), ("h", "<f8"),
+    ("gid", "<i4"), ("tiles_i", "<i4"), ("tiles_j", "<i4"), ("tile_begin", "<i4"),
+    ("ntiles", "<i4"), ("nu_h2", "<f8"), ("adv_2h", "<f8"), ("h", "<f8"),
     ("sxy_off", "<i8"), ("face_off", "<i8", (4,))], align=True)
 
 FACE_TARGET_DTYPE = np.dtype([("off", "<i8"), ("ps", "<i8")], align=True)
@@ -53,10 +53,10 @@ class PeerMsg(ctypes.Structure):
 class StageArgs(ctypes.Structure):
     _fields_ = [
         ("in_", c_vp), ("q0", c_vp), ("out", c_vp), ("sendbuf", c_vp),
-        ("blocks", c_vp), ("cta_block", c_vp), ("sxy", c_vp), ("faces", c_vp),
-        ("norm_part", c_vp), ("status", c_vp), ("iter", c_vp), ("dmat", c_vp),
-        ("nblocks", c_i32), ("total_ctas", c_i32), ("planes", c_i32), ("stage", c_i32),
-        ("tile_rows", c_i32), ("pad", c_i32), ("coef", c_f64),
+        ("blocks", c_vp), ("tile_block", c_vp), ("sxy", c_vp), ("faces", c_vp),
+        ("norm_part", c_vp), ("status", c_vp), ("iter", c_vp), ("dmat", c_vp), ("tmaps", c_vp),
+        ("nblocks", c_i32), ("total_tiles", c_i32), ("planes", c_i32), ("stage", c_i32),
+        ("tile_rows", c_i32), ("in_slot", c_i32), ("coef", c_f64),
         ("D", c_f64 * (MAX_TEMPLATED_P * MAX_TEMPLATED_P)),
         ("ap", c_f64 * (MAX_P * NPDE))]
 
@@ -64,7 +64,7 @@ class StageArgs(ctypes.Structure):
 class EngineDesc(ctypes.Structure):
     _fields_ = [
         ("slot", c_vp * 3), ("sendbuf", c_vp), ("recvbuf", c_vp),
-        ("blocks", c_vp), ("cta_block", c_vp), ("sxy", c_vp), ("faces", c_vp), ("dmat", c_vp),
+        ("blocks", c_vp), ("tile_block", c_vp), ("sxy", c_vp), ("faces", c_vp), ("dmat", c_vp),
         ("norm_part", c_vp), ("sumsq", c_vp), ("status", c_vp), ("iter", c_vp),
         ("prime_dirs", c_vp), ("nprime", c_i32), ("prime_max_len", c_i32),
         ("unpack_dirs", c_vp), ("nunpack", c_i32), ("unpack_max_len", c_i32),
@@ -72,8 +72,8 @@ class EngineDesc(ctypes.Structure):
         ("force_hist", c_vp),
         ("sends", ctypes.POINTER(PeerMsg)), ("nsends", c_i32),
         ("recvs", ctypes.POINTER(PeerMsg)), ("nrecvs", c_i32),
-        ("comm", c_vp),
-        ("nblocks", c_i32), ("total_ctas", c_i32), ("planes", c_i32), ("nbody", c_i32),
+        ("comm", c_vp), ("tmaps", c_vp),
+        ("nblocks", c_i32), ("total_tiles", c_i32), ("planes", c_i32), ("nbody", c_i32),
         ("tile_rows", c_i32), ("max_iters", c_i32),
         ("coef", c_f64 * 4),
         ("D", c_f64 * (MAX_TEMPLATED_P * MAX_TEMPLATED_P)),
@@ -86,6 +86,8 @@ SIGNATURES = {
     "hbgpu_update": (c_i32, [c_vp, c_vp, c_vp, c_f64, c_i32] + [c_i64] * 8 + [c_vp, c_vp]),
     "hbgpu_first_nonfinite": (c_i32, [c_vp] + [c_i64] * 4 + [c_vp, c_vp]),
     "hbgpu_stage": (c_i32, [ctypes.POINTER(StageArgs), c_vp]),
+    "hbgpu_stage_prepare": (c_i32, [c_i32]),
+    "hbgpu_encode_tensor_maps": (c_i32, [c_vp * 3, c_vp, c_i32, c_i32, c_vp, c_i64]),
     "hbgpu_halo": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "hbgpu_norm_fold": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "hbgpu_forces": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp]),

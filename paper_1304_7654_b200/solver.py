@@ -66,6 +66,8 @@ class RunSpec:
     jitter_seed: int | None = None
     # --- device options -------------------------------------------------
     initial: object = None       # callable(spec, planes, npde) -> (P, npde, nj, ni)
+    initial_state: dict | None = None   # gid -> host tensor (P, npde, nj, ni), pinned for speed
+    output: dict | None = None          # gid -> host tensor (P, npde, nj+2, ni+2) to fill
     use_graph: bool = True
     tile_rows: int | None = None
     device: int | None = None
@@ -171,7 +173,7 @@ class DeviceRank:
             return t.to(dev)
 
         self.t_blocks = table(L.block_table)
-        self.t_cta = torch.from_numpy(L.cta_block).to(dev)
+        self.t_tiles = torch.from_numpy(L.tile_block).to(dev)
         self.t_sxy = torch.from_numpy(L.sxy).to(dev)
         self.t_faces = table(L.faces)
         self.t_prime = table(L.prime_dirs)
@@ -183,13 +185,14 @@ class DeviceRank:
         self.ap = hbop.forcing_amplitudes(case.planes, 4)
         nb = len(L.blocks)
         self.max_iters = max(1, max_iters)
-        self.norm_part = torch.zeros(L.total_ctas, dtype=f64, device=dev)
+        self.norm_part = torch.zeros(L.total_tiles * 4, dtype=f64, device=dev)
         self.sumsq = torch.zeros(self.max_iters * nb, dtype=f64, device=dev)
         self.status = torch.full((nb,), -1, dtype=torch.int64, device=dev)
         self.iter = torch.zeros(1, dtype=torch.int32, device=dev)
         nforce = 3 * case.planes * case.nbody
         self.force_hist = torch.zeros(max(1, self.max_iters * nforce), dtype=f64, device=dev)
         self.upload_initial(initial, pinned_ic)
+        self._encode_tensor_maps()
         self._make_engine()
 
     # -- state in / out --------------------------------------------------------
@@ -231,12 +234,24 @@ class DeviceRank:
             if pinned_out is not None:
                 dst = pinned_out[b.id]
                 dst.view(self.planes * 4, b.nj + 2, b.ni + 2).copy_(sub, non_blocking=True)
-                out[b.id] = dst
+                out[b.id] = dst.numpy()
             else:
                 out[b.id] = sub.cpu().numpy().reshape(self.planes, 4, b.nj + 2, b.ni + 2)
         return out
 
     # -- engine ----------------------------------------------------------------
+
+    def _encode_tensor_maps(self):
+        """TMA descriptors of the three slots (128 B each), uploaded to the device."""
+        L = self.layout
+        n = len(L.blocks)
+        host = (ctypes.c_ubyte * (3 * n * 128))()
+        slots = (ctypes.c_void_p * 3)(*[s.data_ptr() for s in self.slots])
+        blocks = np.ascontiguousarray(L.block_table)
+        native.check(self.lib.hbgpu_encode_tensor_maps(slots, blocks.ctypes.data, n, self.planes,
+                                                       ctypes.addressof(host), len(host)),
+                     "hbgpu_encode_tensor_maps")
+        self.t_tmaps = self.torch.frombuffer(bytearray(host), dtype=self.torch.uint8).to(self.device)
 
     def _make_engine(self):
         L = self.layout
@@ -244,7 +259,7 @@ class DeviceRank:
         for k in range(3):
             d.slot[k] = self.slots[k].data_ptr()
         d.sendbuf, d.recvbuf = self.sendbuf.data_ptr(), self.recvbuf.data_ptr()
-        d.blocks, d.cta_block = self.t_blocks.data_ptr(), self.t_cta.data_ptr()
+        d.blocks, d.tile_block = self.t_blocks.data_ptr(), self.t_tiles.data_ptr()
         d.sxy, d.faces, d.dmat = self.t_sxy.data_ptr(), self.t_faces.data_ptr(), self.t_dmat.data_ptr()
         d.norm_part, d.sumsq = self.norm_part.data_ptr(), self.sumsq.data_ptr()
         d.status, d.iter = self.status.data_ptr(), self.iter.data_ptr()
@@ -261,7 +276,8 @@ class DeviceRank:
         d.sends, d.nsends = self._sends, len(L.sends)
         d.recvs, d.nrecvs = self._recvs, len(L.recvs)
         d.comm = self.comm
-        d.nblocks, d.total_ctas, d.planes = len(L.blocks), L.total_ctas, self.planes
+        d.tmaps = self.t_tmaps.data_ptr()
+        d.nblocks, d.total_tiles, d.planes = len(L.blocks), L.total_tiles, self.planes
         d.nbody, d.tile_rows, d.max_iters = self.case.nbody, L.tile_rows, self.max_iters
         for k, c in enumerate(hbop.RKScheme(self.case.dtau).stage_coefficients()):
             d.coef[k] = c
@@ -293,6 +309,31 @@ class DeviceRank:
 
     def launches_per_iteration(self):
         return int(self.lib.hbgpu_engine_launches_per_iteration(self.engine))
+
+    # slot rotation of the engine (hb_runtime.cu): stage s reads IN[s], writes OUT[s]
+    STAGE_IN = (0, 1, 2, 1)
+    STAGE_OUT = (1, 2, 1, 0)
+
+    def stage_args(self, stage):
+        """hbgpu_stage arguments of RK stage `stage` as the engine issues them."""
+        d, a = self._desc, native.StageArgs()
+        a.in_ = self.slots[self.STAGE_IN[stage]].data_ptr()
+        a.q0 = self.slots[0].data_ptr()
+        a.out = self.slots[self.STAGE_OUT[stage]].data_ptr()
+        a.sendbuf, a.blocks, a.tile_block = d.sendbuf, d.blocks, d.tile_block
+        a.sxy, a.faces, a.status, a.iter, a.dmat = d.sxy, d.faces, d.status, d.iter, d.dmat
+        a.norm_part = d.norm_part if stage == 0 else None
+        a.nblocks, a.total_tiles, a.planes = d.nblocks, d.total_tiles, d.planes
+        a.stage, a.tile_rows, a.coef = stage, d.tile_rows, d.coef[stage]
+        a.tmaps, a.in_slot = d.tmaps, self.STAGE_IN[stage]
+        ctypes.memmove(ctypes.addressof(a.D), ctypes.addressof(d.D), ctypes.sizeof(a.D))
+        ctypes.memmove(ctypes.addressof(a.ap), ctypes.addressof(d.ap), ctypes.sizeof(a.ap))
+        return a
+
+    def launch_stage(self, args, stream=None):
+        """One hbgpu_stage launch on `stream` (default: torch's current stream)."""
+        s = stream if stream is not None else self.stream()
+        native.check(self.lib.hbgpu_stage(ctypes.byref(args), s), "hbgpu_stage")
 
     def reset_counters(self):
         self.iter.zero_()
@@ -423,14 +464,15 @@ def run_case(spec):
         exec_partition = partition_blocks(topology, 1)
         exec_plan = build_cut_plan(topology, exec_partition, case.nharms, case.npde)
     dr = DeviceRank(case, topology, exec_partition, exec_plan, rank=rank, device=device, comm=comm,
-                    initial=spec.initial, tile_rows=spec.tile_rows, max_iters=max(1, iterations))
+                    initial=spec.initial, tile_rows=spec.tile_rows, max_iters=max(1, iterations),
+                    pinned_ic=spec.initial_state)
     try:
         dr.prime()
         if iterations > 0:
             dr.iterate(iterations, use_graph=spec.use_graph)
         torch.cuda.synchronize(dr.device)
         div = dr.divergence()
-        fields = dr.fields(0)
+        fields = dr.fields(0, pinned_out=spec.output)
         norms_local = dr.norm_history(iterations)
         hist = dr.force_history_array(iterations)
         if world > 1:
