@@ -145,6 +145,22 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// ---- ring positions -----------------------------------------------------------------
+
+struct RingPos {
+    int slot;
+    uint32_t phase;   // mbarrier phase parity of the slot's current fill
+};
+
+template <int N>
+__device__ __forceinline__ RingPos advance(RingPos r) {
+    if (++r.slot == N) {
+        r.slot = 0;
+        r.phase ^= 1u;
+    }
+    return r;
+}
+
 // ---- shared-memory geometry -------------------------------------------------------
 
 constexpr int CW = 4;                     // consumer warps (one per pde)
@@ -193,32 +209,32 @@ __global__ void __launch_bounds__(THREADS, MINB) stage_tma_kernel(const __grid_c
         // ------------------------------ producer ------------------------------
         if (lane != 0) return;
         constexpr uint32_t BYTES = S::SLOT * 8;
-        long long ein = 0, eq = 0;
-        auto put_in = [&](const CUtensorMap *m, int x, int row) {
-            const int s = (int)(ein % R);
-            if (ein >= R) mbar_wait(empty_in + s, (uint32_t)(((ein / R) + 1) & 1));
-            mbar_expect_tx(full_in + s, BYTES);
-            tma_load_4d(ring + s * S::SLOT, m, x, row, 0, 0, full_in + s);
-            ++ein;
-        };
-        auto put_q = [&](const CUtensorMap *m, int x, int row) {
-            const int s = (int)(eq % Q);
-            if (eq >= Q) mbar_wait(empty_q + s, (uint32_t)(((eq / Q) + 1) & 1));
-            mbar_expect_tx(full_q + s, BYTES);
-            tma_load_4d(qring + s * S::SLOT, m, x, row, 0, 0, full_q + s);
-            ++eq;
-        };
+        RingPos pin{0, 0}, pq{0, 0};
+        int issued_in = 0, issued_q = 0;   // saturate at the ring size
         for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
             const Tile tl = decode_tile(a, t);
             const CUtensorMap *min = maps + a.in_slot * a.nblocks + tl.bidx;
             const CUtensorMap *mq = maps + tl.bidx;   // q0 is slot 0
             prefetch_tmap(min);
             const int x = tl.i0 + LEAD - 2;
-            put_in(min, x, tl.j0 - 1);
-            put_in(min, x, tl.j0);
+            auto put_in = [&](int row) {
+                if (issued_in >= R) mbar_wait(empty_in + pin.slot, pin.phase ^ 1u);
+                else ++issued_in;
+                mbar_expect_tx(full_in + pin.slot, BYTES);
+                tma_load_4d(ring + pin.slot * S::SLOT, min, x, row, 0, 0, full_in + pin.slot);
+                pin = advance<R>(pin);
+            };
+            put_in(tl.j0 - 1);
+            put_in(tl.j0);
             for (int j = tl.j0; j <= tl.j1; ++j) {
-                put_in(min, x, j + 1);
-                if (!FIRST) put_q(mq, x, j);
+                put_in(j + 1);
+                if (!FIRST) {
+                    if (issued_q >= Q) mbar_wait(empty_q + pq.slot, pq.phase ^ 1u);
+                    else ++issued_q;
+                    mbar_expect_tx(full_q + pq.slot, BYTES);
+                    tma_load_4d(qring + pq.slot * S::SLOT, mq, x, j, 0, 0, full_q + pq.slot);
+                    pq = advance<Q>(pq);
+                }
             }
         }
         return;
@@ -228,65 +244,66 @@ __global__ void __launch_bounds__(THREADS, MINB) stage_tma_kernel(const __grid_c
     const int p = warp;
     const int gstage = (*a.iter) * 4 + a.stage + 1;
     const double coef = a.coef;
-    long long ein = 0, eq = 0;
+    double ap[P];
+#pragma unroll
+    for (int n = 0; n < P; ++n) ap[n] = a.ap[n * NPDE + p];
+    RingPos cin{0, 0}, cq{0, 0};
     for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
         const Tile tl = decode_tile(a, t);
-        const hbgpu_block &b = a.blocks[tl.bidx];
+        // by value: the output stores must not force re-reads of the descriptor
+        const hbgpu_block b = a.blocks[tl.bidx];
         const int ni = b.ni, nj = b.nj;
         const int64_t ps4 = b.ps * NPDE;
         const double nu_h2 = b.nu_h2, adv_2h = b.adv_2h;
         const int i = tl.i0 + lane;
         const bool live = i <= ni;
-        double *out = a.out + b.base + (int64_t)p * b.ps + LEAD + i;
-        const double *sxy = a.sxy + b.sxy_off + (i - 1);
-        double ap[P];
-#pragma unroll
-        for (int n = 0; n < P; ++n) ap[n] = a.ap[n * NPDE + p];
+        double *const out = a.out + b.base + (int64_t)p * b.ps + LEAD + i;
+        const double *const sxy = a.sxy + b.sxy_off + (i - 1);
 
         FaceHit trow, tcol;
         cell_targets(a.faces, b, i, tl.j0, live, trow, tcol);
-        double sv = live ? sxy[(int64_t)(tl.j0 - 1) * ni] : 0.0;
+        double sv = live ? __ldg(sxy + (int64_t)(tl.j0 - 1) * ni) : 0.0;
 
         // rows j0-1 and j0 -> registers; release row j0-1
         double up[P], cur[P], dn[P];
         {
-            const int s0 = (int)(ein % R), s1 = (int)((ein + 1) % R);
-            mbar_wait(full_in + s0, (uint32_t)((ein / R) & 1));
-            mbar_wait(full_in + s1, (uint32_t)(((ein + 1) / R) & 1));
-            const double *r0 = ring + s0 * S::SLOT + p * SEG + lane + 2;
-            const double *r1 = ring + s1 * S::SLOT + p * SEG + lane + 2;
+            const RingPos c1 = advance<R>(cin);
+            mbar_wait(full_in + cin.slot, cin.phase);
+            mbar_wait(full_in + c1.slot, c1.phase);
+            const double *r0 = ring + cin.slot * S::SLOT + p * SEG + lane + 2;
+            const double *r1 = ring + c1.slot * S::SLOT + p * SEG + lane + 2;
 #pragma unroll
             for (int m = 0; m < P; ++m) {
                 up[m] = r0[m * NPDE * SEG];
                 cur[m] = r1[m * NPDE * SEG];
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(empty_in + s0);
-            ++ein;   // ein: entry of the current row j
+            if (lane == 0) mbar_arrive(empty_in + cin.slot);
+            cin = c1;   // entry of the current row j
         }
         double nrm = 0.0;
 
         for (int j = tl.j0; j <= tl.j1; ++j) {
             // prefetch the next row's forcing value and halo targets
+            const bool more = j < tl.j1;
             FaceHit nrow, ncol;
-            cell_targets(a.faces, b, i, j + 1, live && j < tl.j1, nrow, ncol);
-            const double sv_next = (live && j < tl.j1) ? sxy[(int64_t)j * ni] : 0.0;
+            cell_targets(a.faces, b, i, j + 1, live && more, nrow, ncol);
+            const double sv_next = (live && more) ? __ldg(sxy + (int64_t)j * ni) : 0.0;
 
-            const int sc = (int)(ein % R);
-            const int sn = (int)((ein + 1) % R);
-            mbar_wait(full_in + sn, (uint32_t)(((ein + 1) / R) & 1));
-            const double *rc = ring + sc * S::SLOT + p * SEG + lane;
-            const double *rn = ring + sn * S::SLOT + p * SEG + lane + 2;
+            const RingPos nx = advance<R>(cin);
+            mbar_wait(full_in + nx.slot, nx.phase);
+            const double *rc = ring + cin.slot * S::SLOT + p * SEG + lane;
+            const double *rn = ring + nx.slot * S::SLOT + p * SEG + lane + 2;
 #pragma unroll
             for (int m = 0; m < P; ++m) dn[m] = rn[m * NPDE * SEG];
             const double *qv = nullptr;
-            int sq = 0;
             if (!FIRST) {
-                sq = (int)(eq % Q);
-                mbar_wait(full_q + sq, (uint32_t)((eq / Q) & 1));
-                qv = qring + sq * S::SLOT + p * SEG + lane + 2;
+                mbar_wait(full_q + cq.slot, cq.phase);
+                qv = qring + cq.slot * S::SLOT + p * SEG + lane + 2;
             }
-            const int64_t row = (int64_t)j * b.pitch;
+
+            // all P outputs first: P independent rounding chains, no branches
+            double v[P];
 #pragma unroll
             for (int n = 0; n < P; ++n) {
                 const double w = rc[n * NPDE * SEG + 1];
@@ -296,17 +313,32 @@ __global__ void __launch_bounds__(THREADS, MINB) stage_tma_kernel(const __grid_c
                 for (int m = 0; m < P; ++m) o = radd(o, rmul(a.D[n * P + m], cur[m]));
                 o = radd(o, rmul(ap[n], sv));
                 const double base = FIRST ? cur[n] : qv[n * NPDE * SEG];
-                const double v = rsub(base, rmul(coef, o));
-                if (live) {
-                    out[n * ps4 + row] = v;
-                    if (FIRST) nrm = radd(nrm, rmul(o, o));
-                    forward(trow, a.out, a.sendbuf, n, p, v);
-                    forward(tcol, a.out, a.sendbuf, n, p, v);
-                    if (nonfinite(v)) {
+                v[n] = rsub(base, rmul(coef, o));
+                if (FIRST) nrm = radd(nrm, live ? rmul(o, o) : 0.0);
+            }
+
+            const int64_t row = (int64_t)j * b.pitch;
+            if (live) {
+#pragma unroll
+                for (int n = 0; n < P; ++n) out[n * ps4 + row] = v[n];
+            }
+            if (trow.ps != 0) {
+#pragma unroll
+                for (int n = 0; n < P; ++n) forward(trow, a.out, a.sendbuf, n, p, v[n]);
+            }
+            if (tcol.ps != 0) {
+#pragma unroll
+                for (int n = 0; n < P; ++n) forward(tcol, a.out, a.sendbuf, n, p, v[n]);
+            }
+            bool bad = false;
+#pragma unroll
+            for (int n = 0; n < P; ++n) bad |= nonfinite(v[n]);
+            if (bad && live) {
+                for (int n = 0; n < P; ++n)
+                    if (nonfinite(v[n])) {
                         long long lin = (((long long)(n * NPDE + p) * nj + (j - 1)) * ni) + (i - 1);
                         atomicMin(a.status + tl.bidx, divergence_key(gstage, lin));
                     }
-                }
             }
 #pragma unroll
             for (int m = 0; m < P; ++m) {
@@ -318,15 +350,15 @@ __global__ void __launch_bounds__(THREADS, MINB) stage_tma_kernel(const __grid_c
             sv = sv_next;
             __syncwarp();
             if (lane == 0) {
-                mbar_arrive(empty_in + sc);   // row j no longer read
-                if (!FIRST) mbar_arrive(empty_q + sq);
+                mbar_arrive(empty_in + cin.slot);   // row j no longer read
+                if (!FIRST) mbar_arrive(empty_q + cq.slot);
             }
-            ++ein;
-            if (!FIRST) ++eq;
+            cin = nx;
+            if (!FIRST) cq = advance<Q>(cq);
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(empty_in + (int)(ein % R));   // row j1+1
-        ++ein;
+        if (lane == 0) mbar_arrive(empty_in + cin.slot);   // row j1+1
+        cin = advance<R>(cin);
         if (FIRST && a.norm_part != nullptr) {
             const double s = warp_sum(nrm);
             if (lane == 0) a.norm_part[(int64_t)t * NPDE + p] = s;
