@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-iters", type=int, default=1)
+    ap.add_argument("--zero-ic", action="store_true",
+                    help="development only: zero initial state (skips the seeded IC build)")
     return ap.parse_args()
 
 
@@ -124,16 +126,18 @@ def dist_env():
     return world, rank, local
 
 
-def make_ic(wl, blocks, pinned=True):
+def make_ic(wl, blocks, pinned=True, zero=False):
     """Seeded initial state of the given blocks in (pinned) host tensors."""
-    import numpy as np
     import torch
     from concurrent.futures import ThreadPoolExecutor
     P = wl.case.planes
 
     def one(b):
         t = torch.empty((P, 4, b.nj, b.ni), dtype=torch.float64, pin_memory=pinned)
-        t.numpy()[...] = wl.initial(b, P, 4)
+        if zero:
+            t.zero_()
+        else:
+            t.numpy()[...] = wl.initial(b, P, 4)
         return b.id, t
 
     with ThreadPoolExecutor(max_workers=min(16, max(1, os.cpu_count() or 1))) as ex:
@@ -238,7 +242,7 @@ def run_ours(args, wl):
     part = partition_blocks(topo, world)
     plan = build_cut_plan(topo, part, case.nharms, case.npde)
     mine = [topo.blocks[g] for g in part.blocks_of(rank)]
-    ic = make_ic(wl, mine)
+    ic = make_ic(wl, mine, zero=args.zero_ic)
     total_units_iter = topo.total_cells() * case.planes * 4
     comm = make_comm(rank, world, local) if world > 1 else None
 

@@ -57,10 +57,13 @@ typedef struct hbgpu_block {
     int32_t tile_begin;  /* first tile of this block in the rank tile list  */
     int32_t ntiles;      /* tiles_i * tiles_j; a tile is one CTA's 32-column
                             strip over tile_rows rows, all 4 pdes           */
+    int32_t sxy_pitch;   /* row stride of the sxy table (ni rounded up to 4) */
+    int32_t pad0;
     double nu_h2;        /* NU / (h*h)          (hbcore.py:257)             */
     double adv_2h;       /* ADVECTION / (2*h)   (hbcore.py:257)             */
     double h;
-    int64_t sxy_off;     /* element offset of this block's (nj, ni) sxy     */
+    int64_t sxy_off;     /* element offset of the block's sxy table (32-B aligned,
+                            nj rows of sxy_pitch)                        */
     int64_t face_off[4]; /* entry offset into the face-target pool per face
                             (south, north, west, east), -1 = no cut cell    */
 } hbgpu_block;
@@ -149,8 +152,8 @@ typedef struct hbgpu_stage_args {
     unsigned long long *status;/* device [nblocks] divergence keys         */
     const int32_t *iter;       /* device iteration counter                 */
     const double *dmat;        /* device P*P (generic kernel only)         */
-    const void *tmaps;         /* device [3][nblocks] CUtensorMap of the three
-                                  slots (hbgpu_encode_tensor_maps)         */
+    const void *tmaps;         /* device [4][nblocks] CUtensorMap
+                                  (hbgpu_encode_tensor_maps)               */
     int32_t nblocks;
     int32_t total_tiles;
     int32_t planes;
@@ -172,11 +175,14 @@ int hbgpu_stage(const hbgpu_stage_args *args, void *stream);
  * CUDA graph capture (hbgpu_engine_create calls it) */
 int hbgpu_stage_prepare(int32_t planes);
 
-/* TMA descriptors for the stage kernel: for slot s (0..2) and block b, a 4-D
- * tensor map (columns, rows, pde, plane) over the block's part of slot[s],
- * written as CUtensorMap (128 B) #(s*nblocks + b) into out_host (caller
- * uploads it to device memory, 64-B aligned).  out_bytes >= 3*nblocks*128. */
-int hbgpu_encode_tensor_maps(double *const slot[3], const hbgpu_block *blocks_host,
+/* TMA descriptors for the stage kernel: 4-D tensor maps (columns, rows,
+ * pde, plane) over each block's part of a slot, written as CUtensorMap
+ * (128 B) #(set*nblocks + b) into out_host (caller uploads it to device
+ * memory, 64-B aligned): sets 0..2 = 36-column stencil boxes over slot[0..2],
+ * set 3 = 32-column q0 box over slot[0], set 4 = 2-D (column, row) 32-column
+ * box over the block's sxy forcing table.  out_bytes >= 5*nblocks*128.    */
+int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy,
+                             const hbgpu_block *blocks_host,
                              int32_t nblocks, int32_t planes, void *out_host,
                              int64_t out_bytes);
 

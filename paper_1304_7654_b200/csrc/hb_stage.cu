@@ -41,6 +41,7 @@
 #include "hb_common.cuh"
 
 #include <cuda.h>
+#include <stdlib.h>
 
 namespace hbgpu {
 
@@ -78,6 +79,13 @@ __device__ __forceinline__ void tma_load_4d(void *dst, const void *map, int c0, 
         "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(saddr(dst)),
         "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(saddr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const void *map, int c0, int c1, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(saddr(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(saddr(bar))
         : "memory");
 }
 __device__ __forceinline__ void prefetch_tmap(const void *map) {
@@ -165,13 +173,16 @@ __device__ __forceinline__ RingPos advance(RingPos r) {
 
 constexpr int CW = 4;                     // consumer warps (one per pde)
 constexpr int THREADS = (CW + 1) * 32;    // + one producer warp
-constexpr int SEG = 36;                   // columns per box row: i0-2 .. i0+33
+constexpr int SEG = 36;                   // stencil box row: columns i0-2 .. i0+33
+constexpr int QSEG = 32;                  // q0 box row: columns i0 .. i0+31 (sector aligned)
 
 template <int P, bool FIRST, int R, int Q>
 struct Smem {
-    static constexpr int SLOT = P * NPDE * SEG;   // doubles: [snapshot][pde][SEG]
+    static constexpr int BOX = P * NPDE * SEG;     // doubles: [snapshot][pde][SEG]
+    static constexpr int SLOT = BOX + 32;          // + the sxy row of the previous row
+    static constexpr int QSLOT = P * NPDE * QSEG;  // doubles: [snapshot][pde][QSEG]
     static constexpr int NQ = FIRST ? 0 : Q;
-    static constexpr size_t BAR_OFF = (size_t)(R + NQ) * SLOT * 8;
+    static constexpr size_t BAR_OFF = ((size_t)R * SLOT + (size_t)NQ * QSLOT) * 8;
     static constexpr size_t BYTES = BAR_OFF + (size_t)2 * (R + NQ) * 8;
 };
 
@@ -208,31 +219,36 @@ __global__ void __launch_bounds__(THREADS, MINB) stage_tma_kernel(const __grid_c
     if (warp == CW) {
         // ------------------------------ producer ------------------------------
         if (lane != 0) return;
-        constexpr uint32_t BYTES = S::SLOT * 8;
+        constexpr uint32_t BYTES = S::BOX * 8, QBYTES = S::QSLOT * 8, SBYTES = 32 * 8;
         RingPos pin{0, 0}, pq{0, 0};
         int issued_in = 0, issued_q = 0;   // saturate at the ring size
         for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
             const Tile tl = decode_tile(a, t);
             const CUtensorMap *min = maps + a.in_slot * a.nblocks + tl.bidx;
-            const CUtensorMap *mq = maps + tl.bidx;   // q0 is slot 0
+            const CUtensorMap *mq = maps + 3 * a.nblocks + tl.bidx;   // q0: slot 0, 32-col box
+            const CUtensorMap *ms = maps + 4 * a.nblocks + tl.bidx;   // sxy table
             prefetch_tmap(min);
             const int x = tl.i0 + LEAD - 2;
-            auto put_in = [&](int row) {
+            // stencil rows; the entry of row r also carries sxy row r-1, the
+            // forcing of the row computed while r is the "north" row
+            auto put_in = [&](int row, bool with_sxy) {
                 if (issued_in >= R) mbar_wait(empty_in + pin.slot, pin.phase ^ 1u);
                 else ++issued_in;
-                mbar_expect_tx(full_in + pin.slot, BYTES);
-                tma_load_4d(ring + pin.slot * S::SLOT, min, x, row, 0, 0, full_in + pin.slot);
+                double *dst = ring + pin.slot * S::SLOT;
+                mbar_expect_tx(full_in + pin.slot, with_sxy ? BYTES + SBYTES : BYTES);
+                tma_load_4d(dst, min, x, row, 0, 0, full_in + pin.slot);
+                if (with_sxy) tma_load_2d(dst + S::BOX, ms, tl.i0 - 1, row - 2, full_in + pin.slot);
                 pin = advance<R>(pin);
             };
-            put_in(tl.j0 - 1);
-            put_in(tl.j0);
+            put_in(tl.j0 - 1, false);
+            put_in(tl.j0, false);
             for (int j = tl.j0; j <= tl.j1; ++j) {
-                put_in(j + 1);
+                put_in(j + 1, true);
                 if (!FIRST) {
                     if (issued_q >= Q) mbar_wait(empty_q + pq.slot, pq.phase ^ 1u);
                     else ++issued_q;
-                    mbar_expect_tx(full_q + pq.slot, BYTES);
-                    tma_load_4d(qring + pq.slot * S::SLOT, mq, x, j, 0, 0, full_q + pq.slot);
+                    mbar_expect_tx(full_q + pq.slot, QBYTES);
+                    tma_load_4d(qring + pq.slot * S::QSLOT, mq, x + 2, j, 0, 0, full_q + pq.slot);
                     pq = advance<Q>(pq);
                 }
             }
@@ -258,11 +274,9 @@ __global__ void __launch_bounds__(THREADS, MINB) stage_tma_kernel(const __grid_c
         const int i = tl.i0 + lane;
         const bool live = i <= ni;
         double *const out = a.out + b.base + (int64_t)p * b.ps + LEAD + i;
-        const double *const sxy = a.sxy + b.sxy_off + (i - 1);
 
         FaceHit trow, tcol;
         cell_targets(a.faces, b, i, tl.j0, live, trow, tcol);
-        double sv = live ? __ldg(sxy + (int64_t)(tl.j0 - 1) * ni) : 0.0;
 
         // rows j0-1 and j0 -> registers; release row j0-1
         double up[P], cur[P], dn[P];
@@ -288,10 +302,10 @@ __global__ void __launch_bounds__(THREADS, MINB) stage_tma_kernel(const __grid_c
             const bool more = j < tl.j1;
             FaceHit nrow, ncol;
             cell_targets(a.faces, b, i, j + 1, live && more, nrow, ncol);
-            const double sv_next = (live && more) ? __ldg(sxy + (int64_t)j * ni) : 0.0;
 
             const RingPos nx = advance<R>(cin);
             mbar_wait(full_in + nx.slot, nx.phase);
+            const double sv = ring[nx.slot * S::SLOT + S::BOX + lane];   // sxy of row j
             const double *rc = ring + cin.slot * S::SLOT + p * SEG + lane;
             const double *rn = ring + nx.slot * S::SLOT + p * SEG + lane + 2;
 #pragma unroll
@@ -299,22 +313,51 @@ __global__ void __launch_bounds__(THREADS, MINB) stage_tma_kernel(const __grid_c
             const double *qv = nullptr;
             if (!FIRST) {
                 mbar_wait(full_q + cq.slot, cq.phase);
-                qv = qring + cq.slot * S::SLOT + p * SEG + lane + 2;
+                qv = qring + cq.slot * S::QSLOT + p * QSEG + lane;
             }
 
-            // all P outputs first: P independent rounding chains, no branches
-            double v[P];
+            // All P outputs in lockstep, branch-free: each step below is P
+            // independent rounded operations (one per snapshot), so the P
+            // dependency chains overlap.  Per point the rounding sequence is
+            // the reference's: stencil, then m ascending, then forcing
+            // (hbcore.py:193-221 is this same pass structure).
+            double v[P], o[P];
+            {
+                double w[P], e[P];
+#pragma unroll
+                for (int n = 0; n < P; ++n) {
+                    w[n] = rc[n * NPDE * SEG + 1];
+                    e[n] = rc[n * NPDE * SEG + 3];
+                }
+#pragma unroll
+                for (int n = 0; n < P; ++n) o[n] = rmul(4.0, cur[n]);
+#pragma unroll
+                for (int n = 0; n < P; ++n) o[n] = rsub(o[n], w[n]);
+#pragma unroll
+                for (int n = 0; n < P; ++n) o[n] = rsub(o[n], e[n]);
+#pragma unroll
+                for (int n = 0; n < P; ++n) o[n] = rsub(o[n], up[n]);
+#pragma unroll
+                for (int n = 0; n < P; ++n) o[n] = rsub(o[n], dn[n]);
+#pragma unroll
+                for (int n = 0; n < P; ++n) o[n] = rmul(o[n], nu_h2);
+#pragma unroll
+                for (int n = 0; n < P; ++n) o[n] = radd(o[n], rmul(rsub(e[n], w[n]), adv_2h));
+            }
+#pragma unroll
+            for (int m = 0; m < P; ++m) {
+#pragma unroll
+                for (int n = 0; n < P; ++n) o[n] = radd(o[n], rmul(a.D[n * P + m], cur[m]));
+            }
 #pragma unroll
             for (int n = 0; n < P; ++n) {
-                const double w = rc[n * NPDE * SEG + 1];
-                const double e = rc[n * NPDE * SEG + 3];
-                double o = stencil(cur[n], w, e, up[n], dn[n], nu_h2, adv_2h);
+                o[n] = radd(o[n], rmul(ap[n], sv));
+                const double base = FIRST ? cur[n] : qv[n * NPDE * QSEG];
+                v[n] = rsub(base, rmul(coef, o[n]));
+            }
+            if (FIRST) {
 #pragma unroll
-                for (int m = 0; m < P; ++m) o = radd(o, rmul(a.D[n * P + m], cur[m]));
-                o = radd(o, rmul(ap[n], sv));
-                const double base = FIRST ? cur[n] : qv[n * NPDE * SEG];
-                v[n] = rsub(base, rmul(coef, o));
-                if (FIRST) nrm = radd(nrm, live ? rmul(o, o) : 0.0);
+                for (int n = 0; n < P; ++n) nrm = radd(nrm, live ? rmul(o[n], o[n]) : 0.0);
             }
 
             const int64_t row = (int64_t)j * b.pitch;
@@ -347,7 +390,6 @@ __global__ void __launch_bounds__(THREADS, MINB) stage_tma_kernel(const __grid_c
             }
             trow = nrow;
             tcol = ncol;
-            sv = sv_next;
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(empty_in + cin.slot);   // row j no longer read
@@ -393,7 +435,7 @@ __global__ void __launch_bounds__(CW * 32) stage_kernel_generic(const __grid_con
         const double *in = a.in + col;
         for (int j = tl.j0; j <= tl.j1; ++j) {
             const int64_t row = (int64_t)j * pitch;
-            const double sv = a.sxy[b.sxy_off + (int64_t)(j - 1) * ni + (i - 1)];
+            const double sv = a.sxy[b.sxy_off + (int64_t)(j - 1) * b.sxy_pitch + (i - 1)];
             FaceHit trow, tcol;
             cell_targets(a.faces, b, i, j, true, trow, tcol);
             for (int n = 0; n < P; ++n) {
@@ -449,7 +491,8 @@ static int prepare(Launch &L) {
 
 // ring depths (R stencil rows, Q q0 rows) and CTAs per SM, per snapshot count:
 // each CTA keeps R-2 + Q-1 rows (~10 KB each at P = 9) in flight
-template <int P> struct Depth { static constexpr int R = 5, Q = 4, MINB = 2; };
+// (P = 7, 9 measured on C3 / C4: (4, 3) > (5, 4) > (6, 5) > (8, 7, 1 CTA))
+template <int P> struct Depth { static constexpr int R = 4, Q = 3, MINB = 2; };
 template <> struct Depth<1> { static constexpr int R = 8, Q = 6, MINB = 3; };
 template <> struct Depth<3> { static constexpr int R = 8, Q = 6, MINB = 3; };
 template <> struct Depth<5> { static constexpr int R = 6, Q = 5, MINB = 2; };
@@ -458,12 +501,33 @@ template <> struct Depth<13> { static constexpr int R = 4, Q = 3, MINB = 2; };
 template <> struct Depth<15> { static constexpr int R = 4, Q = 2, MINB = 2; };
 template <> struct Depth<17> { static constexpr int R = 4, Q = 2, MINB = 1; };
 
+// HBGPU_RING=<variant> selects an alternative ring depth for P = 7 and 9
+// (measurements only): 1 = (R 6, Q 5), 2 = (R 5, Q 4), 3 = (R 8, Q 7, 1 CTA/SM)
+static int ring_variant() {
+    const char *env = getenv("HBGPU_RING");
+    return env ? atoi(env) : 0;
+}
+
+template <int P, int R, int Q, int MINB>
+static int launch_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only);
+
 template <int P>
 static int launch_p(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
     using D = Depth<P>;
+    if constexpr (P == 7 || P == 9) {
+        static const int variant = ring_variant();
+        if (variant == 1) return launch_cfg<P, 6, 5, 2>(a, s, prepare_only);
+        if (variant == 2) return launch_cfg<P, 5, 4, 2>(a, s, prepare_only);
+        if (variant == 3) return launch_cfg<P, 8, 7, 1>(a, s, prepare_only);
+    }
+    return launch_cfg<P, D::R, D::Q, D::MINB>(a, s, prepare_only);
+}
+
+template <int P, int R, int Q, int MINB>
+static int launch_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
     static Launch first, rest;
-    int rc = prepare<P, true, D::R, D::Q, D::MINB>(first);
-    if (!rc) rc = prepare<P, false, D::R, D::Q, D::MINB>(rest);
+    int rc = prepare<P, true, R, Q, MINB>(first);
+    if (!rc) rc = prepare<P, false, R, Q, MINB>(rest);
     if (rc || prepare_only) return rc;
     if (a.tmaps == nullptr) {
         hbgpu_set_error("hbgpu_stage: args->tmaps is required (hbgpu_encode_tensor_maps)");
@@ -542,34 +606,58 @@ extern "C" int hbgpu_stage(const hbgpu_stage_args *args, void *stream) {
     return hbgpu::dispatch(*args, (cudaStream_t)stream, false);
 }
 
-extern "C" int hbgpu_encode_tensor_maps(double *const slot[3], const hbgpu_block *blocks, int32_t nblocks,
-                                        int32_t planes, void *out_host, int64_t out_bytes) {
+extern "C" int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy, const hbgpu_block *blocks,
+                                        int32_t nblocks, int32_t planes, void *out_host, int64_t out_bytes) {
     using namespace hbgpu;
-    if ((int64_t)sizeof(CUtensorMap) * 3 * nblocks > out_bytes || planes < 1 || planes > 256) {
+    if ((int64_t)sizeof(CUtensorMap) * 5 * nblocks > out_bytes || planes < 1 || planes > 256) {
         hbgpu_set_error("hbgpu_encode_tensor_maps: output too small or bad planes");
         return HBGPU_ERR_ARG;
     }
     EncodeTiledFn fn = encode_fn();
+    // L2 sector promotion of the TMA fetches (rows are 32-B aligned only; 256-B
+    // promotion drags in unused neighbour sectors).  HBGPU_L2_PROMOTION = 0, 64,
+    // 128 or 256 overrides for measurements.
+    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;   // best measured on C4 (64 > none = 128 > 256)
+    if (const char *env = getenv("HBGPU_L2_PROMOTION")) {
+        const int v = atoi(env);
+        promo = v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+              : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+              : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    }
     if (fn == nullptr) {
         hbgpu_set_error("cuTensorMapEncodeTiled unavailable from the driver");
         return HBGPU_ERR_CUDA;
     }
     CUtensorMap *maps = reinterpret_cast<CUtensorMap *>(out_host);
-    for (int s = 0; s < 3; ++s) {
+    // sets 0..2: stencil boxes (36 columns) over slots 0..2; set 3: q0 box
+    // (32 columns) over slot 0; set 4: 2-D sxy table box (32 columns x 1 row)
+    for (int s = 0; s < 5; ++s) {
         for (int k = 0; k < nblocks; ++k) {
             const hbgpu_block &b = blocks[k];
-            cuuint64_t dims[4] = {(cuuint64_t)b.pitch, (cuuint64_t)(b.nj + 2), (cuuint64_t)NPDE,
-                                  (cuuint64_t)planes};
-            cuuint64_t strides[3] = {(cuuint64_t)b.pitch * 8, (cuuint64_t)b.ps * 8,
-                                     (cuuint64_t)b.ps * 8 * NPDE};
-            cuuint32_t box[4] = {(cuuint32_t)SEG, 1, (cuuint32_t)NPDE, (cuuint32_t)planes};
-            cuuint32_t estr[4] = {1, 1, 1, 1};
-            CUresult r = fn(&maps[s * nblocks + k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
-                            (void *)(slot[s] + b.base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            CUresult r;
+            if (s < 4) {
+                cuuint64_t dims[4] = {(cuuint64_t)b.pitch, (cuuint64_t)(b.nj + 2), (cuuint64_t)NPDE,
+                                      (cuuint64_t)planes};
+                cuuint64_t strides[3] = {(cuuint64_t)b.pitch * 8, (cuuint64_t)b.ps * 8,
+                                         (cuuint64_t)b.ps * 8 * NPDE};
+                cuuint32_t box[4] = {(cuuint32_t)(s < 3 ? SEG : QSEG), 1, (cuuint32_t)NPDE,
+                                     (cuuint32_t)planes};
+                cuuint32_t estr[4] = {1, 1, 1, 1};
+                r = fn(&maps[s * nblocks + k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
+                       (void *)(slot[s < 3 ? s : 0] + b.base), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            } else {
+                cuuint64_t dims[2] = {(cuuint64_t)b.ni, (cuuint64_t)b.nj};
+                cuuint64_t strides[1] = {(cuuint64_t)b.sxy_pitch * 8};
+                cuuint32_t box[2] = {32, 1};
+                cuuint32_t estr[2] = {1, 1};
+                r = fn(&maps[s * nblocks + k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                       (void *)(sxy + b.sxy_off), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            }
             if (r != CUDA_SUCCESS) {
-                hbgpu_set_error("cuTensorMapEncodeTiled failed (%d) for slot %d block %d", (int)r, s, k);
+                hbgpu_set_error("cuTensorMapEncodeTiled failed (%d) for set %d block %d", (int)r, s, k);
                 return HBGPU_ERR_CUDA;
             }
         }

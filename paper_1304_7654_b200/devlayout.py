@@ -123,18 +123,21 @@ def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None):
         ti = -(-b.ni // WARP_COLS)
         tjn = -(-b.nj // tj)
         nu_h2, adv_2h = stencil_coefficients(b.h)
+        spitch = _round_up(b.ni, 4)
         for name, value in (("base", base[k]), ("ps", ps[k]), ("ni", b.ni), ("nj", b.nj),
                             ("pitch", pitch[k]), ("gid", b.id), ("tiles_i", ti),
                             ("tiles_j", tjn), ("tile_begin", ntile),
                             ("ntiles", ti * tjn),
                             ("nu_h2", nu_h2), ("adv_2h", adv_2h), ("h", b.h),
-                            ("sxy_off", sxy_off)):
+                            ("sxy_off", sxy_off), ("sxy_pitch", spitch)):
             table[name][k] = value
         table["face_off"][k] = -1
         tile_block += [k] * (ti * tjn)
         ntile += ti * tjn
-        sxy_parts.append(forcing_table(b).ravel())
-        sxy_off += b.ni * b.nj
+        padded = np.zeros((b.nj, spitch))
+        padded[:, :b.ni] = forcing_table(b)
+        sxy_parts.append(padded.ravel())
+        sxy_off += b.nj * spitch
 
     layout = RankLayout(planes=planes, blocks=owned, local_index=local_index, pitch=pitch, ps=ps,
                         base=base, slot_elems=slot_elems, tile_rows=tj, block_table=table,

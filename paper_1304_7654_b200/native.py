@@ -31,7 +31,8 @@ c_i32, c_i64, c_f64, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, cty
 BLOCK_DTYPE = np.dtype([
     ("base", "<i8"), ("ps", "<i8"), ("ni", "<i4"), ("nj", "<i4"), ("pitch", "<i4"),
     ("gid", "<i4"), ("tiles_i", "<i4"), ("tiles_j", "<i4"), ("tile_begin", "<i4"),
-    ("ntiles", "<i4"), ("nu_h2", "<f8"), ("adv_2h", "<f8"), ("h", "<f8"),
+    ("ntiles", "<i4"), ("sxy_pitch", "<i4"), ("pad0", "<i4"), ("nu_h2", "<f8"),
+    ("adv_2h", "<f8"), ("h", "<f8"),
     ("sxy_off", "<i8"), ("face_off", "<i8", (4,))], align=True)
 
 FACE_TARGET_DTYPE = np.dtype([("off", "<i8"), ("ps", "<i8")], align=True)
@@ -87,7 +88,7 @@ SIGNATURES = {
     "hbgpu_first_nonfinite": (c_i32, [c_vp] + [c_i64] * 4 + [c_vp, c_vp]),
     "hbgpu_stage": (c_i32, [ctypes.POINTER(StageArgs), c_vp]),
     "hbgpu_stage_prepare": (c_i32, [c_i32]),
-    "hbgpu_encode_tensor_maps": (c_i32, [c_vp * 3, c_vp, c_i32, c_i32, c_vp, c_i64]),
+    "hbgpu_encode_tensor_maps": (c_i32, [c_vp * 3, c_vp, c_vp, c_i32, c_i32, c_vp, c_i64]),
     "hbgpu_halo": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "hbgpu_norm_fold": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "hbgpu_forces": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp]),

@@ -242,13 +242,14 @@ class DeviceRank:
     # -- engine ----------------------------------------------------------------
 
     def _encode_tensor_maps(self):
-        """TMA descriptors of the three slots (128 B each), uploaded to the device."""
+        """TMA descriptors (4 sets x blocks, 128 B each), uploaded to the device."""
         L = self.layout
         n = len(L.blocks)
-        host = (ctypes.c_ubyte * (3 * n * 128))()
+        host = (ctypes.c_ubyte * (5 * n * 128))()
         slots = (ctypes.c_void_p * 3)(*[s.data_ptr() for s in self.slots])
         blocks = np.ascontiguousarray(L.block_table)
-        native.check(self.lib.hbgpu_encode_tensor_maps(slots, blocks.ctypes.data, n, self.planes,
+        native.check(self.lib.hbgpu_encode_tensor_maps(slots, self.t_sxy.data_ptr(),
+                                                       blocks.ctypes.data, n, self.planes,
                                                        ctypes.addressof(host), len(host)),
                      "hbgpu_encode_tensor_maps")
         self.t_tmaps = self.torch.frombuffer(bytearray(host), dtype=self.torch.uint8).to(self.device)
