@@ -29,8 +29,14 @@ extern "C" {
  * kernel parameter of HBGPU_MAX_P*4 doubles) */
 #define HBGPU_MAX_P 127
 /* elements of the device row lead: cell i (0 = west halo) of row j sits at
- * row_base + HBGPU_ROW_LEAD + i, so interior cell i=1 is 32-byte aligned */
-#define HBGPU_ROW_LEAD 3
+ * row_base + HBGPU_ROW_LEAD + i, so interior cell i=1 -- and every stage
+ * strip -- starts on a 64-byte DRAM access granule (rows are padded to a
+ * multiple of 8 doubles) */
+#define HBGPU_ROW_LEAD 7
+/* interior columns per stage-kernel strip (one CTA: 2 warps per pde) */
+#define HBGPU_STRIP 64
+/* consumer warps per stage tile (= residual-norm partials per tile) */
+#define HBGPU_TILE_WARPS (HBGPU_NPDE * HBGPU_STRIP / 32)
 
 enum {
     HBGPU_OK = 0,
@@ -50,13 +56,13 @@ typedef struct hbgpu_block {
     int64_t base;        /* element offset of (0,0,0,-LEAD) in every slot   */
     int64_t ps;          /* elements between consecutive (n, p) planes      */
     int32_t ni, nj;      /* interior cells                                  */
-    int32_t pitch;       /* row stride, elements (multiple of 4)            */
+    int32_t pitch;       /* row stride, elements (multiple of 8)            */
     int32_t gid;         /* global block id                                 */
-    int32_t tiles_i;     /* column strips: ceil(ni / 32)                    */
+    int32_t tiles_i;     /* column strips: ceil(ni / HBGPU_STRIP)           */
     int32_t tiles_j;     /* ceil(nj / tile_rows)                            */
     int32_t tile_begin;  /* first tile of this block in the rank tile list  */
-    int32_t ntiles;      /* tiles_i * tiles_j; a tile is one CTA's 32-column
-                            strip over tile_rows rows, all 4 pdes           */
+    int32_t ntiles;      /* tiles_i * tiles_j; a tile is one CTA's strip
+                            over tile_rows rows, all 4 pdes                 */
     int32_t sxy_pitch;   /* row stride of the sxy table (ni rounded up to 4) */
     int32_t pad0;
     double nu_h2;        /* NU / (h*h)          (hbcore.py:257)             */
@@ -178,9 +184,10 @@ int hbgpu_stage_prepare(int32_t planes);
 /* TMA descriptors for the stage kernel: 4-D tensor maps (columns, rows,
  * pde, plane) over each block's part of a slot, written as CUtensorMap
  * (128 B) #(set*nblocks + b) into out_host (caller uploads it to device
- * memory, 64-B aligned): sets 0..2 = 36-column stencil boxes over slot[0..2],
- * set 3 = 32-column q0 box over slot[0], set 4 = 2-D (column, row) 32-column
- * box over the block's sxy forcing table.  out_bytes >= 5*nblocks*128.    */
+ * memory, 64-B aligned): sets 0..2 = stencil boxes (strip + 2 halo columns
+ * each side) over slot[0..2], set 3 = strip-wide q0 box over slot[0], set
+ * 4 = 2-D (column, row) strip-wide box over the block's sxy forcing table.
+ * out_bytes >= 5*nblocks*128.                                              */
 int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy,
                              const hbgpu_block *blocks_host,
                              int32_t nblocks, int32_t planes, void *out_host,

@@ -25,7 +25,7 @@ __global__ void halo_kernel(double *slot, double *sendbuf, const double *recvbuf
 
 // ---- residual norm ----------------------------------------------------------
 
-// per block: sequential sum of its (tile, pde) partials in tile order
+// per block: sequential sum of its (tile, consumer warp) partials in tile order
 __global__ void norm_fold_kernel(const hbgpu_block *blocks, int nblocks, const double *part,
                                  double *sumsq, const int32_t *iter) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -33,7 +33,8 @@ __global__ void norm_fold_kernel(const hbgpu_block *blocks, int nblocks, const d
     const hbgpu_block &blk = blocks[b];
     double s = 0.0;
     // one partial per (tile, pde), tiles of a block contiguous
-    for (int c = 0; c < blk.ntiles * NPDE; ++c) s = radd(s, part[(int64_t)blk.tile_begin * NPDE + c]);
+    constexpr int W = HBGPU_TILE_WARPS;
+    for (int c = 0; c < blk.ntiles * W; ++c) s = radd(s, part[(int64_t)blk.tile_begin * W + c]);
     sumsq[(int64_t)(*iter) * nblocks + b] = s;
 }
 

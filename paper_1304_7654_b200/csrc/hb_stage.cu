@@ -12,27 +12,28 @@
 //     in the reference's element-major layout (remote cut) -- the
 //     _copy_local / _pack of exchange.py:248-261;
 //   * divergence keys (hbcore.py:244-245, 279-284);
-//   * stage 0: per-(tile, pde) partial sums of R^2 for the residual norm.
+//   * stage 0: per-(tile, warp) partial sums of R^2 for the residual norm.
 //
-// Work decomposition.  A tile is one CTA's 32-column strip of one block over
-// `tile_rows` rows.  Consumer warp p (0..3) computes pde p; lane l owns
-// column i0 + l and marches down the rows keeping rows j-1, j, j+1 of all P
-// snapshots of its column in registers (stencil north/south neighbours and
-// the P centres of the D-contraction).
+// Work decomposition.  A tile is one CTA's strip of HBGPU_STRIP (64)
+// columns of one block over `tile_rows` rows.  Consumer warp w computes pde
+// w % 4 on columns [i0 + 32 (w / 4), +32); lane l owns one column and marches
+// down the rows keeping rows j-1, j, j+1 of all P snapshots of its column in
+// registers (stencil north/south neighbours and the P centres of the
+// D-contraction).
 //
-// Memory pipeline (warp-specialised, TMA).  A fifth warp is the producer:
-// one lane streams the tile's rows into shared memory with 4-D tensor TMA
-// loads (cp.async.bulk.tensor, box = 36 columns x 1 row x 4 pdes x P
-// snapshots = 10.4 KB at P = 9: the strip plus its west/east halo columns,
-// zero-filled past the row end), one ring of R slots for the stencil input
-// and one of Q slots for q_0.  Each slot has a "full" mbarrier (TMA
-// transaction count) and an "empty" mbarrier the four consumer warps arrive
-// on once they no longer read it.  The producer therefore runs R-2 rows ahead
-// of the consumers with only two requests per row, the per-request TMA cost
-// is amortised over ~10 KB, the west/east neighbours come from shared memory,
-// and the amount of memory in flight no longer depends on register pressure.
-// CTAs are persistent (tiles t = blockIdx.x, +gridDim.x, ...) so the ring
-// streams across tile boundaries without draining.
+// Memory pipeline (warp-specialised, TMA).  A ninth warp is the producer: one
+// lane streams the tile's rows into shared memory with tensor TMA loads
+// (cp.async.bulk.tensor): per row, one 4-D box of 68 columns x 4 pdes x P
+// snapshots (19.6 KB at P = 9: the strip plus two halo columns each side,
+// zero-filled past the row end) into a ring of R stencil slots, the strip's
+// 64-column q_0 row box into a ring of Q slots, and the 64-column sxy forcing
+// row riding on the stencil slot's barrier.  Every slot has a "full" mbarrier
+// (TMA transaction count) and an "empty" one the consumer warps arrive on
+// once they stop reading it.  With ROW_LEAD = 7 every strip starts on a
+// 64-byte DRAM granule: a q_0 row costs exactly its 512 bytes and a stencil
+// row one extra granule on each side, shared with the neighbouring strips.
+// CTAs are persistent (tiles t = blockIdx.x, +gridDim.x, ...) and the rings
+// stream across tile boundaries without draining.
 //
 // Rounding: every operation is an explicitly rounded DMUL/DADD, in the
 // reference's per-point order, including the m == n term (D[n][n] = 0 still
@@ -92,6 +93,16 @@ __device__ __forceinline__ void prefetch_tmap(const void *map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
 
+// ---- geometry ---------------------------------------------------------------------
+
+constexpr int STRIP = HBGPU_STRIP;              // interior columns per tile
+constexpr int HALVES = STRIP / 32;              // warps per pde
+constexpr int CW = NPDE * HALVES;               // consumer warps
+constexpr int THREADS = (CW + 1) * 32;          // + one producer warp
+constexpr int SEG = STRIP + 4;                  // stencil box row: columns i0-2 .. i0+STRIP+1
+constexpr int QSEG = STRIP;                     // q0 / sxy box row: columns i0 .. i0+STRIP-1
+static_assert(CW == HBGPU_TILE_WARPS, "tile warp count");
+
 // ---- tiles and halo targets -------------------------------------------------
 
 struct Tile {
@@ -105,7 +116,7 @@ __device__ __forceinline__ Tile decode_tile(const hbgpu_stage_args &a, int t) {
     T.bidx = a.tile_block[t];
     const hbgpu_block &b = a.blocks[T.bidx];
     const int local = t - b.tile_begin;
-    T.i0 = (local % b.tiles_i) * 32 + 1;
+    T.i0 = (local % b.tiles_i) * STRIP + 1;
     T.j0 = (local / b.tiles_i) * a.tile_rows + 1;
     T.j1 = min(T.j0 + a.tile_rows - 1, b.nj);
     return T;
@@ -169,27 +180,21 @@ __device__ __forceinline__ RingPos advance(RingPos r) {
     return r;
 }
 
-// ---- shared-memory geometry -------------------------------------------------------
-
-constexpr int CW = 4;                     // consumer warps (one per pde)
-constexpr int THREADS = (CW + 1) * 32;    // + one producer warp
-constexpr int SEG = 36;                   // stencil box row: columns i0-2 .. i0+33
-constexpr int QSEG = 32;                  // q0 box row: columns i0 .. i0+31 (sector aligned)
-
 template <int P, bool FIRST, int R, int Q>
 struct Smem {
     static constexpr int BOX = P * NPDE * SEG;     // doubles: [snapshot][pde][SEG]
-    static constexpr int SLOT = BOX + 32;          // + the sxy row of the previous row
+    static constexpr int SLOT = BOX + QSEG;        // + the sxy row of the row computed with it
     static constexpr int QSLOT = P * NPDE * QSEG;  // doubles: [snapshot][pde][QSEG]
     static constexpr int NQ = FIRST ? 0 : Q;
     static constexpr size_t BAR_OFF = ((size_t)R * SLOT + (size_t)NQ * QSLOT) * 8;
     static constexpr size_t BYTES = BAR_OFF + (size_t)2 * (R + NQ) * 8;
+    static_assert((SLOT * 8) % 128 == 0 && (QSLOT * 8) % 128 == 0, "TMA slots need 128-B alignment");
 };
 
 // ---- the pipelined kernel -----------------------------------------------------------
 
-template <int P, bool FIRST, int R, int Q, int MINB>
-__global__ void __launch_bounds__(THREADS, MINB) stage_tma_kernel(const __grid_constant__ hbgpu_stage_args a) {
+template <int P, bool FIRST, int R, int Q>
+__global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_constant__ hbgpu_stage_args a) {
     using S = Smem<P, FIRST, R, Q>;
     static_assert(R >= 3 && Q >= 2, "ring too short");
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -219,13 +224,13 @@ __global__ void __launch_bounds__(THREADS, MINB) stage_tma_kernel(const __grid_c
     if (warp == CW) {
         // ------------------------------ producer ------------------------------
         if (lane != 0) return;
-        constexpr uint32_t BYTES = S::BOX * 8, QBYTES = S::QSLOT * 8, SBYTES = 32 * 8;
+        constexpr uint32_t BYTES = S::BOX * 8, QBYTES = S::QSLOT * 8, SBYTES = QSEG * 8;
         RingPos pin{0, 0}, pq{0, 0};
         int issued_in = 0, issued_q = 0;   // saturate at the ring size
         for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
             const Tile tl = decode_tile(a, t);
             const CUtensorMap *min = maps + a.in_slot * a.nblocks + tl.bidx;
-            const CUtensorMap *mq = maps + 3 * a.nblocks + tl.bidx;   // q0: slot 0, 32-col box
+            const CUtensorMap *mq = maps + 3 * a.nblocks + tl.bidx;   // q0: slot 0, strip box
             const CUtensorMap *ms = maps + 4 * a.nblocks + tl.bidx;   // sxy table
             prefetch_tmap(min);
             const int x = tl.i0 + LEAD - 2;
@@ -257,7 +262,8 @@ __global__ void __launch_bounds__(THREADS, MINB) stage_tma_kernel(const __grid_c
     }
 
     // -------------------------------- consumers ---------------------------------
-    const int p = warp;
+    const int p = warp % NPDE;
+    const int col0 = 32 * (warp / NPDE) + lane;   // this lane's column within the strip
     const int gstage = (*a.iter) * 4 + a.stage + 1;
     const double coef = a.coef;
     double ap[P];
@@ -271,7 +277,7 @@ __global__ void __launch_bounds__(THREADS, MINB) stage_tma_kernel(const __grid_c
         const int ni = b.ni, nj = b.nj;
         const int64_t ps4 = b.ps * NPDE;
         const double nu_h2 = b.nu_h2, adv_2h = b.adv_2h;
-        const int i = tl.i0 + lane;
+        const int i = tl.i0 + col0;
         const bool live = i <= ni;
         double *const out = a.out + b.base + (int64_t)p * b.ps + LEAD + i;
 
@@ -284,8 +290,8 @@ __global__ void __launch_bounds__(THREADS, MINB) stage_tma_kernel(const __grid_c
             const RingPos c1 = advance<R>(cin);
             mbar_wait(full_in + cin.slot, cin.phase);
             mbar_wait(full_in + c1.slot, c1.phase);
-            const double *r0 = ring + cin.slot * S::SLOT + p * SEG + lane + 2;
-            const double *r1 = ring + c1.slot * S::SLOT + p * SEG + lane + 2;
+            const double *r0 = ring + cin.slot * S::SLOT + p * SEG + col0 + 2;
+            const double *r1 = ring + c1.slot * S::SLOT + p * SEG + col0 + 2;
 #pragma unroll
             for (int m = 0; m < P; ++m) {
                 up[m] = r0[m * NPDE * SEG];
@@ -298,22 +304,21 @@ __global__ void __launch_bounds__(THREADS, MINB) stage_tma_kernel(const __grid_c
         double nrm = 0.0;
 
         for (int j = tl.j0; j <= tl.j1; ++j) {
-            // prefetch the next row's forcing value and halo targets
-            const bool more = j < tl.j1;
+            // prefetch the next row's halo targets (boundary cells only)
             FaceHit nrow, ncol;
-            cell_targets(a.faces, b, i, j + 1, live && more, nrow, ncol);
+            cell_targets(a.faces, b, i, j + 1, live && j < tl.j1, nrow, ncol);
 
             const RingPos nx = advance<R>(cin);
             mbar_wait(full_in + nx.slot, nx.phase);
-            const double sv = ring[nx.slot * S::SLOT + S::BOX + lane];   // sxy of row j
-            const double *rc = ring + cin.slot * S::SLOT + p * SEG + lane;
-            const double *rn = ring + nx.slot * S::SLOT + p * SEG + lane + 2;
+            const double *rc = ring + cin.slot * S::SLOT + p * SEG + col0;
+            const double *rn = ring + nx.slot * S::SLOT + p * SEG + col0 + 2;
+            const double sv = ring[nx.slot * S::SLOT + S::BOX + col0];   // sxy of row j
 #pragma unroll
             for (int m = 0; m < P; ++m) dn[m] = rn[m * NPDE * SEG];
             const double *qv = nullptr;
             if (!FIRST) {
                 mbar_wait(full_q + cq.slot, cq.phase);
-                qv = qring + cq.slot * S::QSLOT + p * QSEG + lane;
+                qv = qring + cq.slot * S::QSLOT + p * QSEG + col0;
             }
 
             // All P outputs in lockstep, branch-free: each step below is P
@@ -403,29 +408,30 @@ __global__ void __launch_bounds__(THREADS, MINB) stage_tma_kernel(const __grid_c
         cin = advance<R>(cin);
         if (FIRST && a.norm_part != nullptr) {
             const double s = warp_sum(nrm);
-            if (lane == 0) a.norm_part[(int64_t)t * NPDE + p] = s;
+            if (lane == 0) a.norm_part[(int64_t)t * CW + warp] = s;
         }
     }
 }
 
 // ---- generic snapshot count (P > HBGPU_MAX_TEMPLATED_P) --------------------------
-// One CTA of 4 warps (one per pde) per tile, operands through L1, D from
-// shared memory.  Same arithmetic sequence; used for e.g. the 63-plane
-// tc1-full catalog case.
+// One CTA of CW warps (same warp -> (pde, half-strip) map) per tile, operands
+// through L1, D from shared memory.  Same arithmetic sequence; used for e.g.
+// the 63-plane tc1-full catalog case.
 __global__ void __launch_bounds__(CW * 32) stage_kernel_generic(const __grid_constant__ hbgpu_stage_args a) {
     extern __shared__ double sh[];
     const int P = a.planes;
     for (int k = threadIdx.x; k < P * P; k += blockDim.x) sh[k] = a.dmat[k];
     __syncthreads();
     const double *D = sh;
+    const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int p = threadIdx.x >> 5;
+    const int p = warp % NPDE;
     const int t = blockIdx.x;
     const Tile tl = decode_tile(a, t);
     const hbgpu_block &b = a.blocks[tl.bidx];
     const int ni = b.ni, nj = b.nj, pitch = b.pitch;
     const int64_t ps4 = b.ps * NPDE;
-    const int i = tl.i0 + lane;
+    const int i = tl.i0 + 32 * (warp / NPDE) + lane;
     const bool live = i <= ni;
     const bool first = a.stage == 0;
     const int gstage = (*a.iter) * 4 + a.stage + 1;
@@ -458,7 +464,7 @@ __global__ void __launch_bounds__(CW * 32) stage_kernel_generic(const __grid_con
     }
     if (first && a.norm_part != nullptr) {
         const double s = warp_sum(nrm);
-        if (lane == 0) a.norm_part[(int64_t)t * NPDE + p] = s;
+        if (lane == 0) a.norm_part[(int64_t)t * CW + warp] = s;
     }
 }
 
@@ -471,10 +477,10 @@ struct Launch {
     bool ready = false;
 };
 
-template <int P, bool FIRST, int R, int Q, int MINB>
+template <int P, bool FIRST, int R, int Q>
 static int prepare(Launch &L) {
     if (L.ready) return HBGPU_OK;
-    L.fn = stage_tma_kernel<P, FIRST, R, Q, MINB>;
+    L.fn = stage_tma_kernel<P, FIRST, R, Q>;
     L.smem = Smem<P, FIRST, R, Q>::BYTES;
     if (cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem) != cudaSuccess)
         return hbgpu_check_launch("stage kernel smem attribute");
@@ -489,45 +495,29 @@ static int prepare(Launch &L) {
     return HBGPU_OK;
 }
 
-// ring depths (R stencil rows, Q q0 rows) and CTAs per SM, per snapshot count:
-// each CTA keeps R-2 + Q-1 rows (~10 KB each at P = 9) in flight
-// (P = 7, 9 measured on C3 / C4: (4, 3) > (5, 4) > (6, 5) > (8, 7, 1 CTA))
-template <int P> struct Depth { static constexpr int R = 4, Q = 3, MINB = 2; };
-template <> struct Depth<1> { static constexpr int R = 8, Q = 6, MINB = 3; };
-template <> struct Depth<3> { static constexpr int R = 8, Q = 6, MINB = 3; };
-template <> struct Depth<5> { static constexpr int R = 6, Q = 5, MINB = 2; };
-template <> struct Depth<11> { static constexpr int R = 4, Q = 3, MINB = 2; };
-template <> struct Depth<13> { static constexpr int R = 4, Q = 3, MINB = 2; };
-template <> struct Depth<15> { static constexpr int R = 4, Q = 2, MINB = 2; };
-template <> struct Depth<17> { static constexpr int R = 4, Q = 2, MINB = 1; };
+// Ring depths per snapshot count: R stencil rows for the update stages, RF
+// for the first stage (no q0 ring, so its rows go deeper), Q q0 rows.  One
+// CTA (8 consumer warps) per SM at P >= 7; the smem budget is ~227 KB.
+template <int P> struct Depth { static constexpr int R = 4, RF = 7, Q = 3; };
+template <> struct Depth<1> { static constexpr int R = 8, RF = 12, Q = 6; };
+template <> struct Depth<3> { static constexpr int R = 8, RF = 12, Q = 6; };
+template <> struct Depth<5> { static constexpr int R = 6, RF = 10, Q = 5; };
+template <> struct Depth<13> { static constexpr int R = 4, RF = 6, Q = 2; };
+template <> struct Depth<15> { static constexpr int R = 4, RF = 5, Q = 2; };
+template <> struct Depth<17> { static constexpr int R = 4, RF = 5, Q = 2; };
 
 // HBGPU_RING=<variant> selects an alternative ring depth for P = 7 and 9
-// (measurements only): 1 = (R 6, Q 5), 2 = (R 5, Q 4), 3 = (R 8, Q 7, 1 CTA/SM)
+// (measurements only): 1 = (R 5, RF 8, Q 4), 2 = (R 3, RF 5, Q 2), 3 = (R 6, RF 6, Q 5)
 static int ring_variant() {
     const char *env = getenv("HBGPU_RING");
     return env ? atoi(env) : 0;
 }
 
-template <int P, int R, int Q, int MINB>
-static int launch_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only);
-
-template <int P>
-static int launch_p(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
-    using D = Depth<P>;
-    if constexpr (P == 7 || P == 9) {
-        static const int variant = ring_variant();
-        if (variant == 1) return launch_cfg<P, 6, 5, 2>(a, s, prepare_only);
-        if (variant == 2) return launch_cfg<P, 5, 4, 2>(a, s, prepare_only);
-        if (variant == 3) return launch_cfg<P, 8, 7, 1>(a, s, prepare_only);
-    }
-    return launch_cfg<P, D::R, D::Q, D::MINB>(a, s, prepare_only);
-}
-
-template <int P, int R, int Q, int MINB>
+template <int P, int R, int RF, int Q>
 static int launch_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
     static Launch first, rest;
-    int rc = prepare<P, true, R, Q, MINB>(first);
-    if (!rc) rc = prepare<P, false, R, Q, MINB>(rest);
+    int rc = prepare<P, true, RF, Q>(first);
+    if (!rc) rc = prepare<P, false, R, Q>(rest);
     if (rc || prepare_only) return rc;
     if (a.tmaps == nullptr) {
         hbgpu_set_error("hbgpu_stage: args->tmaps is required (hbgpu_encode_tensor_maps)");
@@ -538,6 +528,18 @@ static int launch_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_on
     L.fn<<<grid, THREADS, L.smem, s>>>(a);
     hbgpu_count_launch(1);
     return hbgpu_check_launch("hbgpu_stage");
+}
+
+template <int P>
+static int launch_p(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
+    using D = Depth<P>;
+    if constexpr (P == 7 || P == 9) {
+        static const int variant = ring_variant();
+        if (variant == 1) return launch_cfg<P, 5, 8, 4>(a, s, prepare_only);
+        if (variant == 2) return launch_cfg<P, 3, 5, 2>(a, s, prepare_only);
+        if (variant == 3) return launch_cfg<P, 6, 6, 5>(a, s, prepare_only);
+    }
+    return launch_cfg<P, D::R, D::RF, D::Q>(a, s, prepare_only);
 }
 
 static int dispatch(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
@@ -614,23 +616,22 @@ extern "C" int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy
         return HBGPU_ERR_ARG;
     }
     EncodeTiledFn fn = encode_fn();
-    // L2 sector promotion of the TMA fetches (rows are 32-B aligned only; 256-B
-    // promotion drags in unused neighbour sectors).  HBGPU_L2_PROMOTION = 0, 64,
-    // 128 or 256 overrides for measurements.
-    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;   // best measured on C4 (64 > none = 128 > 256)
+    if (fn == nullptr) {
+        hbgpu_set_error("cuTensorMapEncodeTiled unavailable from the driver");
+        return HBGPU_ERR_CUDA;
+    }
+    // L2 sector promotion of the TMA fetches; HBGPU_L2_PROMOTION = 0, 64, 128
+    // or 256 overrides (measurements: 64 B best on C4 with 32-B aligned rows)
+    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
     if (const char *env = getenv("HBGPU_L2_PROMOTION")) {
         const int v = atoi(env);
         promo = v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
               : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
               : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
     }
-    if (fn == nullptr) {
-        hbgpu_set_error("cuTensorMapEncodeTiled unavailable from the driver");
-        return HBGPU_ERR_CUDA;
-    }
     CUtensorMap *maps = reinterpret_cast<CUtensorMap *>(out_host);
-    // sets 0..2: stencil boxes (36 columns) over slots 0..2; set 3: q0 box
-    // (32 columns) over slot 0; set 4: 2-D sxy table box (32 columns x 1 row)
+    // sets 0..2: stencil boxes (SEG columns) over slots 0..2; set 3: q0 box
+    // (QSEG columns) over slot 0; set 4: 2-D sxy table box (QSEG columns x 1 row)
     for (int s = 0; s < 5; ++s) {
         for (int k = 0; k < nblocks; ++k) {
             const hbgpu_block &b = blocks[k];
@@ -650,7 +651,7 @@ extern "C" int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy
             } else {
                 cuuint64_t dims[2] = {(cuuint64_t)b.ni, (cuuint64_t)b.nj};
                 cuuint64_t strides[1] = {(cuuint64_t)b.sxy_pitch * 8};
-                cuuint32_t box[2] = {32, 1};
+                cuuint32_t box[2] = {(cuuint32_t)QSEG, 1};
                 cuuint32_t estr[2] = {1, 1};
                 r = fn(&maps[s * nblocks + k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
                        (void *)(sxy + b.sxy_off), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,

@@ -5,11 +5,11 @@ rank owns it fixes:
 
 * the slot layout: block b's value (n, p, j, i) at element
   base_b + (n*4 + p)*ps_b + j*pitch_b + ROW_LEAD + i, rows padded to a
-  multiple of 4 doubles and ROW_LEAD = 3 so every interior row starts on a
-  32-byte sector; block bases are 256-byte aligned.  Three slots (A, B, C)
-  share the layout;
-* the stage tiles: one tile = one CTA's 32-column strip over tile_rows rows
-  of one block (4 consumer warps = 4 pdes); tile t of block b is strip
+  multiple of 8 doubles and ROW_LEAD = 7 so every interior row -- and every
+  64-column strip -- starts on a 64-byte DRAM granule; block bases are
+  256-byte aligned.  Three slots (A, B, C) share the layout;
+* the stage tiles: one tile = one CTA's 64-column strip over tile_rows rows
+  of one block (8 consumer warps: 2 per pde); tile t of block b is strip
   t % tiles_i, row tile t / tiles_i;
 * the face-target pool (fused halo forwarding, see cutplan.py);
 * the standalone halo directions (priming exchange / pack / unpack);
@@ -30,9 +30,9 @@ from .hbop import forcing_table, stencil_coefficients
 
 ROW_LEAD = native.ROW_LEAD
 NPDE = native.NPDE
-WARP_COLS = 32
+STRIP = native.STRIP     # interior columns per stage tile
 BLOCK_ALIGN = 32          # elements (256 B)
-TARGET_TILES = 148 * 2 * 8   # ~8 tiles per persistent CTA (148 SMs x 2 CTAs)
+TARGET_TILES = 148 * 8    # ~8 tiles per persistent CTA (148 SMs x 1 CTA)
 MAX_TILE_ROWS = 256
 MIN_TILE_ROWS = 8
 SLOT_TAIL = 64            # elements of zero padding after the last block
@@ -45,7 +45,7 @@ def _round_up(x, m):
 def choose_tile_rows(blocks):
     """Rows per tile: long tiles amortise the two halo rows each tile re-reads;
     enough tiles keep every persistent warp of the stage kernel busy."""
-    rows = sum(-(-b.ni // WARP_COLS) * b.nj for b in blocks)
+    rows = sum(-(-b.ni // STRIP) * b.nj for b in blocks)
     tj = rows // TARGET_TILES
     tj = max(MIN_TILE_ROWS, min(MAX_TILE_ROWS, tj))
     return tj
@@ -107,7 +107,7 @@ def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None):
     pitch, ps, base = [], [], []
     off = 0
     for b in owned:
-        pt = _round_up(ROW_LEAD + b.ni + 2, 4)
+        pt = _round_up(ROW_LEAD + b.ni + 2, 8)
         pitch.append(pt)
         ps.append((b.nj + 2) * pt)
         base.append(off)
@@ -120,7 +120,7 @@ def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None):
     sxy_parts, sxy_off = [], 0
     ntile = 0
     for k, b in enumerate(owned):
-        ti = -(-b.ni // WARP_COLS)
+        ti = -(-b.ni // STRIP)
         tjn = -(-b.nj // tj)
         nu_h2, adv_2h = stencil_coefficients(b.h)
         spitch = _round_up(b.ni, 4)

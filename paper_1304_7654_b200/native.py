@@ -21,7 +21,9 @@ LIB_PATH = os.path.join(PKG_DIR, "libhbgpu.so")
 NPDE = 4
 MAX_TEMPLATED_P = 17
 MAX_P = 127
-ROW_LEAD = 3
+ROW_LEAD = 7
+STRIP = 64
+TILE_WARPS = NPDE * STRIP // 32
 ABI_VERSION = 1
 
 c_i32, c_i64, c_f64, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p

@@ -185,7 +185,7 @@ class DeviceRank:
         self.ap = hbop.forcing_amplitudes(case.planes, 4)
         nb = len(L.blocks)
         self.max_iters = max(1, max_iters)
-        self.norm_part = torch.zeros(L.total_tiles * 4, dtype=f64, device=dev)
+        self.norm_part = torch.zeros(L.total_tiles * native.TILE_WARPS, dtype=f64, device=dev)
         self.sumsq = torch.zeros(self.max_iters * nb, dtype=f64, device=dev)
         self.status = torch.full((nb,), -1, dtype=torch.int64, device=dev)
         self.iter = torch.zeros(1, dtype=torch.int32, device=dev)

@@ -66,9 +66,9 @@ def test_layout_alignment_and_tiles():
     part = partition_blocks(topo, 1)
     L = build_rank_layout(topo, part, build_cut_plan(topo, part, 3, 4), 0, case.planes, tile_rows=8)
     for k, b in enumerate(L.blocks):
-        assert L.base[k] % 32 == 0 and L.pitch[k] % 4 == 0
-        assert L.elem(b.id, 0, 0, 0, 1) % 4 == 0        # interior column 1: 32-B sector aligned
-        assert L.pitch[k] >= b.ni + 2 + 3
+        assert L.base[k] % 32 == 0 and L.pitch[k] % 8 == 0
+        assert L.elem(b.id, 0, 0, 0, 1) % 8 == 0        # interior column 1: 64-B granule aligned
+        assert L.pitch[k] >= b.ni + 2 + 7
         t = L.block_table[k]
         assert t["ntiles"] == t["tiles_i"] * t["tiles_j"]
         assert t["sxy_off"] % 4 == 0 and t["sxy_pitch"] >= b.ni
