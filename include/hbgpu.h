@@ -50,11 +50,14 @@ enum {
  * A "slot" is one device allocation holding the full state of every block a
  * rank owns.  Block b's value (n, p, j, i) -- plane n, pde p, array row j in
  * [0, nj+1], array column i in [0, ni+1] -- lives at element
- *     base + (n*4 + p)*ps + j*pitch + HBGPU_ROW_LEAD + i
- * of the slot.  Three slots rotate through the RK stages.                  */
+ *     base + (n*4 + p)*ps + j*rs + HBGPU_ROW_LEAD + i
+ * of the slot.  Three slots rotate through the RK stages.  Two layouts:
+ * plane-major (ps = (nj+2)*pitch, rs = pitch) and row-interleaved
+ * (ps = pitch, rs = 4*P*pitch: row j of all (n, p) planes contiguous).     */
 typedef struct hbgpu_block {
     int64_t base;        /* element offset of (0,0,0,-LEAD) in every slot   */
     int64_t ps;          /* elements between consecutive (n, p) planes      */
+    int64_t rs;          /* elements between consecutive rows j            */
     int32_t ni, nj;      /* interior cells                                  */
     int32_t pitch;       /* row stride, elements (multiple of 8)            */
     int32_t gid;         /* global block id                                 */
@@ -167,7 +170,12 @@ typedef struct hbgpu_stage_args {
     int32_t tile_rows;
     int32_t in_slot;           /* which of the three slots `in` is (0..2);
                                   q0 is slot 0                              */
+    int32_t interleaved;       /* 1 = row-interleaved slot layout          */
+    int32_t pad1;
     double coef;               /* alpha_s * dtau                            */
+    /* D row-major P x P with a +0.0 diagonal (hbcore.py:88-94); ap[n*4 + p]
+     * = amp[n] (1 + p/4), zero except on planes 1 and 2 (hbcore.py:170-175):
+     * the kernel adds those zero terms as exact signed zeros              */
     double D[HBGPU_MAX_TEMPLATED_P * HBGPU_MAX_TEMPLATED_P];
     double ap[HBGPU_MAX_P * HBGPU_NPDE];
 } hbgpu_stage_args;
@@ -237,6 +245,7 @@ typedef struct hbgpu_engine_desc {
     void *comm;                      /* from hbgpu_comm_init, NULL if 1 rank */
     const void *tmaps;               /* device, from hbgpu_encode_tensor_maps */
     int32_t nblocks, total_tiles, planes, nbody, tile_rows, max_iters;
+    int32_t interleaved, pad1;       /* slot layout, see hbgpu_block        */
     double coef[4];
     double D[HBGPU_MAX_TEMPLATED_P * HBGPU_MAX_TEMPLATED_P];
     double ap[HBGPU_MAX_P * HBGPU_NPDE];

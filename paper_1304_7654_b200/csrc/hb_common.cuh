@@ -44,6 +44,24 @@ __device__ __forceinline__ unsigned long long divergence_key(int gstage, long lo
 
 __device__ __forceinline__ bool nonfinite(double v) { return !isfinite(v); }
 
+// radd(o, rmul(0.0, x)) for finite x, without touching the fp64 pipe.
+// 0*x is +0 when x's sign bit is clear and -0 otherwise; o + (+-0) == o
+// except -0 + +0 == +0.  So the result differs from o only when o is -0 and
+// x's sign bit is clear.  Used for the D[n][n] == 0 coupling term and the
+// zero-amplitude forcing planes.  (A non-finite x can only appear after a
+// stage has already produced a non-finite value, i.e. after divergence, and
+// then o is non-finite as well, so the divergence location is unchanged.)
+__device__ __forceinline__ double add_signed_zero(double o, double x) {
+    const long long ob = __double_as_longlong(o);
+    const long long xb = __double_as_longlong(x);
+    return (ob == (long long)0x8000000000000000ULL && xb >= 0) ? 0.0 : o;
+}
+
+// The reference forcing (hbcore.py:165-177) has nonzero amplitude on planes
+// 1 and 2 only; every other plane's forcing term is a signed zero.  The host
+// refuses amplitude tables that break this (solver.DeviceRank).
+__host__ __device__ constexpr bool forced_plane(int n) { return n == 1 || n == 2; }
+
 }  // namespace hbgpu
 
 extern "C" void hbgpu_set_error(const char *fmt, ...);

@@ -209,6 +209,7 @@ int one_iteration(hbgpu_engine *e, cudaStream_t s) {
         a.out = d.slot[kOut[st]];
         a.stage = st;
         a.in_slot = kIn[st];
+        a.interleaved = d.interleaved;
         a.coef = d.coef[st];
         a.norm_part = st == 0 ? d.norm_part : nullptr;
         int rc = hbgpu_stage(&a, s);

@@ -43,6 +43,7 @@
 
 #include <cuda.h>
 #include <stdlib.h>
+#include <string.h>
 
 namespace hbgpu {
 
@@ -193,7 +194,7 @@ struct Smem {
 
 // ---- the pipelined kernel -----------------------------------------------------------
 
-template <int P, bool FIRST, int R, int Q>
+template <int P, bool FIRST, int R, int Q, int MODE = 0>
 __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_constant__ hbgpu_stage_args a) {
     using S = Smem<P, FIRST, R, Q>;
     static_assert(R >= 3 && Q >= 2, "ring too short");
@@ -241,7 +242,8 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
                 else ++issued_in;
                 double *dst = ring + pin.slot * S::SLOT;
                 mbar_expect_tx(full_in + pin.slot, with_sxy ? BYTES + SBYTES : BYTES);
-                tma_load_4d(dst, min, x, row, 0, 0, full_in + pin.slot);
+                if (a.interleaved) tma_load_4d(dst, min, x, 0, 0, row, full_in + pin.slot);
+                else tma_load_4d(dst, min, x, row, 0, 0, full_in + pin.slot);
                 if (with_sxy) tma_load_2d(dst + S::BOX, ms, tl.i0 - 1, row - 2, full_in + pin.slot);
                 pin = advance<R>(pin);
             };
@@ -253,7 +255,10 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
                     if (issued_q >= Q) mbar_wait(empty_q + pq.slot, pq.phase ^ 1u);
                     else ++issued_q;
                     mbar_expect_tx(full_q + pq.slot, QBYTES);
-                    tma_load_4d(qring + pq.slot * S::QSLOT, mq, x + 2, j, 0, 0, full_q + pq.slot);
+                    if (a.interleaved)
+                        tma_load_4d(qring + pq.slot * S::QSLOT, mq, x + 2, 0, 0, j, full_q + pq.slot);
+                    else
+                        tma_load_4d(qring + pq.slot * S::QSLOT, mq, x + 2, j, 0, 0, full_q + pq.slot);
                     pq = advance<Q>(pq);
                 }
             }
@@ -349,23 +354,28 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
 #pragma unroll
                 for (int n = 0; n < P; ++n) o[n] = radd(o[n], rmul(rsub(e[n], w[n]), adv_2h));
             }
+            // D[n][n] == 0 and the zero-amplitude forcing planes add a signed
+            // zero: add_signed_zero reproduces that rounding step exactly on
+            // the integer pipe (see hb_common.cuh)
 #pragma unroll
             for (int m = 0; m < P; ++m) {
 #pragma unroll
-                for (int n = 0; n < P; ++n) o[n] = radd(o[n], rmul(a.D[n * P + m], cur[m]));
+                for (int n = 0; n < P; ++n)
+                    o[n] = (m == n) ? add_signed_zero(o[n], cur[m]) : radd(o[n], rmul(a.D[n * P + m], cur[m]));
             }
 #pragma unroll
             for (int n = 0; n < P; ++n) {
-                o[n] = radd(o[n], rmul(ap[n], sv));
+                o[n] = forced_plane(n) ? radd(o[n], rmul(ap[n], sv)) : add_signed_zero(o[n], sv);
                 const double base = FIRST ? cur[n] : qv[n * NPDE * QSEG];
                 v[n] = rsub(base, rmul(coef, o[n]));
+                if (MODE == 1) v[n] = base;   // measurement variant: same traffic, no arithmetic
             }
             if (FIRST) {
 #pragma unroll
                 for (int n = 0; n < P; ++n) nrm = radd(nrm, live ? rmul(o[n], o[n]) : 0.0);
             }
 
-            const int64_t row = (int64_t)j * b.pitch;
+            const int64_t row = (int64_t)j * b.rs;
             if (live) {
 #pragma unroll
                 for (int n = 0; n < P; ++n) out[n * ps4 + row] = v[n];
@@ -429,7 +439,8 @@ __global__ void __launch_bounds__(CW * 32) stage_kernel_generic(const __grid_con
     const int t = blockIdx.x;
     const Tile tl = decode_tile(a, t);
     const hbgpu_block &b = a.blocks[tl.bidx];
-    const int ni = b.ni, nj = b.nj, pitch = b.pitch;
+    const int ni = b.ni, nj = b.nj;
+    const int64_t rstride = b.rs;
     const int64_t ps4 = b.ps * NPDE;
     const int i = tl.i0 + 32 * (warp / NPDE) + lane;
     const bool live = i <= ni;
@@ -440,13 +451,13 @@ __global__ void __launch_bounds__(CW * 32) stage_kernel_generic(const __grid_con
         const int64_t col = b.base + (int64_t)b.ps * p + LEAD + i;
         const double *in = a.in + col;
         for (int j = tl.j0; j <= tl.j1; ++j) {
-            const int64_t row = (int64_t)j * pitch;
+            const int64_t row = (int64_t)j * rstride;
             const double sv = a.sxy[b.sxy_off + (int64_t)(j - 1) * b.sxy_pitch + (i - 1)];
             FaceHit trow, tcol;
             cell_targets(a.faces, b, i, j, true, trow, tcol);
             for (int n = 0; n < P; ++n) {
                 const double *c = in + n * ps4 + row;
-                double o = stencil(c[0], c[-1], c[1], c[-pitch], c[pitch], b.nu_h2, b.adv_2h);
+                double o = stencil(c[0], c[-1], c[1], c[-rstride], c[rstride], b.nu_h2, b.adv_2h);
                 for (int m = 0; m < P; ++m) o = radd(o, rmul(D[n * P + m], in[m * ps4 + row]));
                 o = radd(o, rmul(a.ap[n * NPDE + p], sv));
                 const double base = first ? c[0] : a.q0[col + n * ps4 + row];
@@ -477,10 +488,10 @@ struct Launch {
     bool ready = false;
 };
 
-template <int P, bool FIRST, int R, int Q>
+template <int P, bool FIRST, int R, int Q, int MODE = 0>
 static int prepare(Launch &L) {
     if (L.ready) return HBGPU_OK;
-    L.fn = stage_tma_kernel<P, FIRST, R, Q>;
+    L.fn = stage_tma_kernel<P, FIRST, R, Q, MODE>;
     L.smem = Smem<P, FIRST, R, Q>::BYTES;
     if (cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem) != cudaSuccess)
         return hbgpu_check_launch("stage kernel smem attribute");
@@ -513,11 +524,11 @@ static int ring_variant() {
     return env ? atoi(env) : 0;
 }
 
-template <int P, int R, int RF, int Q>
+template <int P, int R, int RF, int Q, int MODE = 0>
 static int launch_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
     static Launch first, rest;
-    int rc = prepare<P, true, RF, Q>(first);
-    if (!rc) rc = prepare<P, false, R, Q>(rest);
+    int rc = prepare<P, true, RF, Q, MODE>(first);
+    if (!rc) rc = prepare<P, false, R, Q, MODE>(rest);
     if (rc || prepare_only) return rc;
     if (a.tmaps == nullptr) {
         hbgpu_set_error("hbgpu_stage: args->tmaps is required (hbgpu_encode_tensor_maps)");
@@ -538,6 +549,7 @@ static int launch_p(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only
         if (variant == 1) return launch_cfg<P, 5, 8, 4>(a, s, prepare_only);
         if (variant == 2) return launch_cfg<P, 3, 5, 2>(a, s, prepare_only);
         if (variant == 3) return launch_cfg<P, 6, 6, 5>(a, s, prepare_only);
+        if (P == 9 && variant == 9) return launch_cfg<P, D::R, D::RF, D::Q, 1>(a, s, prepare_only);
     }
     return launch_cfg<P, D::R, D::RF, D::Q>(a, s, prepare_only);
 }
@@ -637,12 +649,30 @@ extern "C" int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy
             const hbgpu_block &b = blocks[k];
             CUresult r;
             if (s < 4) {
-                cuuint64_t dims[4] = {(cuuint64_t)b.pitch, (cuuint64_t)(b.nj + 2), (cuuint64_t)NPDE,
-                                      (cuuint64_t)planes};
-                cuuint64_t strides[3] = {(cuuint64_t)b.pitch * 8, (cuuint64_t)b.ps * 8,
-                                         (cuuint64_t)b.ps * 8 * NPDE};
-                cuuint32_t box[4] = {(cuuint32_t)(s < 3 ? SEG : QSEG), 1, (cuuint32_t)NPDE,
-                                     (cuuint32_t)planes};
+                // dimension order follows the layout so the strides nest:
+                // plane-major (cols, rows, pde, plane), interleaved (cols, pde,
+                // plane, rows); both land in smem as [plane][pde][cols]
+                const bool inter = b.rs > b.ps;
+                const cuuint32_t w = (cuuint32_t)(s < 3 ? SEG : QSEG);
+                cuuint64_t dims[4], strides[3];
+                cuuint32_t box[4];
+                if (inter) {
+                    cuuint64_t d[4] = {(cuuint64_t)b.pitch, (cuuint64_t)NPDE, (cuuint64_t)planes,
+                                       (cuuint64_t)(b.nj + 2)};
+                    cuuint64_t st[3] = {(cuuint64_t)b.ps * 8, (cuuint64_t)b.ps * 8 * NPDE, (cuuint64_t)b.rs * 8};
+                    cuuint32_t bx[4] = {w, (cuuint32_t)NPDE, (cuuint32_t)planes, 1};
+                    memcpy(dims, d, sizeof(d));
+                    memcpy(strides, st, sizeof(st));
+                    memcpy(box, bx, sizeof(bx));
+                } else {
+                    cuuint64_t d[4] = {(cuuint64_t)b.pitch, (cuuint64_t)(b.nj + 2), (cuuint64_t)NPDE,
+                                       (cuuint64_t)planes};
+                    cuuint64_t st[3] = {(cuuint64_t)b.rs * 8, (cuuint64_t)b.ps * 8, (cuuint64_t)b.ps * 8 * NPDE};
+                    cuuint32_t bx[4] = {w, 1, (cuuint32_t)NPDE, (cuuint32_t)planes};
+                    memcpy(dims, d, sizeof(d));
+                    memcpy(strides, st, sizeof(st));
+                    memcpy(box, bx, sizeof(bx));
+                }
                 cuuint32_t estr[4] = {1, 1, 1, 1};
                 r = fn(&maps[s * nblocks + k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
                        (void *)(slot[s < 3 ? s : 0] + b.base), dims, strides, box, estr,

@@ -20,6 +20,7 @@ rank owns it fixes:
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -36,6 +37,9 @@ TARGET_TILES = 148 * 8    # ~8 tiles per persistent CTA (148 SMs x 1 CTA)
 MAX_TILE_ROWS = 256
 MIN_TILE_ROWS = 8
 SLOT_TAIL = 64            # elements of zero padding after the last block
+# slot layout default: row-interleaved (row j of every (n, p) plane contiguous)
+# unless HBGPU_LAYOUT=plane selects the plane-major layout
+INTERLEAVED = os.environ.get("HBGPU_LAYOUT", "interleaved") != "plane"
 
 
 def _round_up(x, m):
@@ -57,7 +61,8 @@ class RankLayout:
     blocks: list                    # owned BlockSpec, ascending id
     local_index: dict               # gid -> local index
     pitch: list
-    ps: list
+    ps: list                        # elements between (n, p) planes
+    rs: list                        # elements between rows j
     base: list
     slot_elems: int
     tile_rows: int
@@ -73,17 +78,26 @@ class RankLayout:
     recvs: list = field(default_factory=list)
     sendbuf_elems: int = 0
     recvbuf_elems: int = 0
+    interleaved: bool = False
 
     def elem(self, gid, n, p, j, i):
         """Slot element index of (n, p, j, i) -- array coordinates -- of block gid."""
         lb = self.local_index[gid]
-        return self.base[lb] + (n * NPDE + p) * self.ps[lb] + j * self.pitch[lb] + ROW_LEAD + i
+        return self.base[lb] + (n * NPDE + p) * self.ps[lb] + j * self.rs[lb] + ROW_LEAD + i
 
-    def block_view_index(self, gid):
-        """(start, planes*npde, nj+2, pitch) to view a slot as the block's array."""
+    def block_view(self, gid):
+        """(offset, shape, strides) in elements viewing a slot as the block's
+        (planes, npde, nj+2, ni+2) array, halos included."""
         lb = self.local_index[gid]
         b = self.blocks[lb]
-        return self.base[lb], self.planes * NPDE, b.nj + 2, self.pitch[lb]
+        return (self.base[lb] + ROW_LEAD, (self.planes, NPDE, b.nj + 2, b.ni + 2),
+                (NPDE * self.ps[lb], self.ps[lb], self.rs[lb], 1))
+
+    def block_extent(self, gid):
+        """(start, length) of the block's region of a slot."""
+        lb = self.local_index[gid]
+        b = self.blocks[lb]
+        return self.base[lb], self.planes * NPDE * (b.nj + 2) * self.pitch[lb]
 
 
 def _interior_cell(spec, face, k):
@@ -96,20 +110,29 @@ def _halo_cell(spec, face, k):
             "east": (k, spec.ni + 1)}[face]
 
 
-def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None):
+def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None,
+                      interleaved=None):
+    """Device layout of one rank's blocks.
+
+    interleaved=False: plane-major slots, (n, p) planes of (nj+2) x pitch;
+    interleaved=True: row j of all (n, p) planes stored contiguously.
+    Default: the INTERLEAVED module setting.
+    """
     owned = [topology.blocks[g] for g in partition.blocks_of(rank)]
     owned.sort(key=lambda b: b.id)
     if not owned:
         raise ValueError(f"rank {rank} owns no blocks")
     local_index = {b.id: k for k, b in enumerate(owned)}
     tj = tile_rows or choose_tile_rows(owned)
+    inter = INTERLEAVED if interleaved is None else bool(interleaved)
 
-    pitch, ps, base = [], [], []
+    pitch, ps, rs, base = [], [], [], []
     off = 0
     for b in owned:
         pt = _round_up(ROW_LEAD + b.ni + 2, 8)
         pitch.append(pt)
-        ps.append((b.nj + 2) * pt)
+        ps.append(pt if inter else (b.nj + 2) * pt)
+        rs.append(planes * NPDE * pt if inter else pt)
         base.append(off)
         off = _round_up(off + planes * NPDE * (b.nj + 2) * pt, BLOCK_ALIGN)
     # bulk row copies of the last strip may run a few elements past a row end
@@ -124,7 +147,7 @@ def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None):
         tjn = -(-b.nj // tj)
         nu_h2, adv_2h = stencil_coefficients(b.h)
         spitch = _round_up(b.ni, 4)
-        for name, value in (("base", base[k]), ("ps", ps[k]), ("ni", b.ni), ("nj", b.nj),
+        for name, value in (("base", base[k]), ("ps", ps[k]), ("rs", rs[k]), ("ni", b.ni), ("nj", b.nj),
                             ("pitch", pitch[k]), ("gid", b.id), ("tiles_i", ti),
                             ("tiles_j", tjn), ("tile_begin", ntile),
                             ("ntiles", ti * tjn),
@@ -140,7 +163,8 @@ def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None):
         sxy_off += b.nj * spitch
 
     layout = RankLayout(planes=planes, blocks=owned, local_index=local_index, pitch=pitch, ps=ps,
-                        base=base, slot_elems=slot_elems, tile_rows=tj, block_table=table,
+                        rs=rs, base=base, slot_elems=slot_elems, tile_rows=tj, block_table=table,
+                        interleaved=inter,
                         tile_block=np.asarray(tile_block, dtype=np.int32), total_tiles=ntile,
                         sxy=np.concatenate(sxy_parts), faces=np.zeros(0, native.FACE_TARGET_DTYPE),
                         prime_dirs=np.zeros(0, native.HALO_DIR_DTYPE),
@@ -153,7 +177,7 @@ def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None):
 
 def _face_stride(layout, gid, face):
     lb = layout.local_index[gid]
-    return 1 if face in ("south", "north") else layout.pitch[lb]
+    return 1 if face in ("south", "north") else layout.rs[lb]
 
 
 def _build_routes(layout, topology, plan, rank):

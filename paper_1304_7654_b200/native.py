@@ -31,7 +31,7 @@ c_i32, c_i64, c_f64, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, cty
 # ---- device table dtypes (C structs stored in device arrays) ---------------
 
 BLOCK_DTYPE = np.dtype([
-    ("base", "<i8"), ("ps", "<i8"), ("ni", "<i4"), ("nj", "<i4"), ("pitch", "<i4"),
+    ("base", "<i8"), ("ps", "<i8"), ("rs", "<i8"), ("ni", "<i4"), ("nj", "<i4"), ("pitch", "<i4"),
     ("gid", "<i4"), ("tiles_i", "<i4"), ("tiles_j", "<i4"), ("tile_begin", "<i4"),
     ("ntiles", "<i4"), ("sxy_pitch", "<i4"), ("pad0", "<i4"), ("nu_h2", "<f8"),
     ("adv_2h", "<f8"), ("h", "<f8"),
@@ -59,7 +59,8 @@ class StageArgs(ctypes.Structure):
         ("blocks", c_vp), ("tile_block", c_vp), ("sxy", c_vp), ("faces", c_vp),
         ("norm_part", c_vp), ("status", c_vp), ("iter", c_vp), ("dmat", c_vp), ("tmaps", c_vp),
         ("nblocks", c_i32), ("total_tiles", c_i32), ("planes", c_i32), ("stage", c_i32),
-        ("tile_rows", c_i32), ("in_slot", c_i32), ("coef", c_f64),
+        ("tile_rows", c_i32), ("in_slot", c_i32), ("interleaved", c_i32), ("pad1", c_i32),
+        ("coef", c_f64),
         ("D", c_f64 * (MAX_TEMPLATED_P * MAX_TEMPLATED_P)),
         ("ap", c_f64 * (MAX_P * NPDE))]
 
@@ -77,7 +78,7 @@ class EngineDesc(ctypes.Structure):
         ("recvs", ctypes.POINTER(PeerMsg)), ("nrecvs", c_i32),
         ("comm", c_vp), ("tmaps", c_vp),
         ("nblocks", c_i32), ("total_tiles", c_i32), ("planes", c_i32), ("nbody", c_i32),
-        ("tile_rows", c_i32), ("max_iters", c_i32),
+        ("tile_rows", c_i32), ("max_iters", c_i32), ("interleaved", c_i32), ("pad1", c_i32),
         ("coef", c_f64 * 4),
         ("D", c_f64 * (MAX_TEMPLATED_P * MAX_TEMPLATED_P)),
         ("ap", c_f64 * (MAX_P * NPDE))]

@@ -198,9 +198,10 @@ class DeviceRank:
     # -- state in / out --------------------------------------------------------
 
     def block_view(self, slot, gid):
-        L = self.layout
-        start, npl, nj2, pitch = L.block_view_index(gid)
-        return slot[start:start + npl * nj2 * pitch].view(npl, nj2, pitch)
+        """The block's (planes, npde, nj+2, ni+2) array (halos included) as a
+        strided view of a slot, for either slot layout."""
+        off, shape, strides = self.layout.block_view(gid)
+        return slot.as_strided(shape, strides, off)
 
     def upload_initial(self, initial=None, pinned=None):
         """Interior of slot A <- the initial state; halos and slots B, C zero.
@@ -212,31 +213,27 @@ class DeviceRank:
         for s in self.slots:
             s.zero_()
         for b in self.layout.blocks:
-            view = self.block_view(self.slots[0], b.id)
-            dst = view[:, 1:b.nj + 1, native.ROW_LEAD + 1:native.ROW_LEAD + 1 + b.ni]
+            dst = self.block_view(self.slots[0], b.id)[:, :, 1:b.nj + 1, 1:b.ni + 1]
             if pinned is not None:
-                src = pinned[b.id].reshape(self.planes * 4, b.nj, b.ni)
-                dst.copy_(src.to(self.device, non_blocking=True))
+                dst.copy_(pinned[b.id].to(self.device, non_blocking=True))
                 continue
             if initial is None:
                 ic = hbop.initial_values(b, self.planes, 4, 0, self.planes, 1, b.nj + 1)
             else:
                 ic = initial(b, self.planes, 4)
-            dst.copy_(torch.from_numpy(np.ascontiguousarray(ic, dtype=np.float64)
-                                       .reshape(self.planes * 4, b.nj, b.ni)))
+            dst.copy_(torch.from_numpy(np.ascontiguousarray(ic, dtype=np.float64)))
 
     def fields(self, slot=0, pinned_out=None):
         """{gid: (P, npde, nj+2, ni+2) numpy array incl. halos} of a slot."""
         out = {}
         for b in self.layout.blocks:
             view = self.block_view(self.slots[slot], b.id)
-            sub = view[:, :, native.ROW_LEAD:native.ROW_LEAD + b.ni + 2]
             if pinned_out is not None:
                 dst = pinned_out[b.id]
-                dst.view(self.planes * 4, b.nj + 2, b.ni + 2).copy_(sub, non_blocking=True)
+                dst.copy_(view.contiguous(), non_blocking=True)
                 out[b.id] = dst.numpy()
             else:
-                out[b.id] = sub.cpu().numpy().reshape(self.planes, 4, b.nj + 2, b.ni + 2)
+                out[b.id] = view.cpu().numpy()
         return out
 
     # -- engine ----------------------------------------------------------------
@@ -280,11 +277,18 @@ class DeviceRank:
         d.tmaps = self.t_tmaps.data_ptr()
         d.nblocks, d.total_tiles, d.planes = len(L.blocks), L.total_tiles, self.planes
         d.nbody, d.tile_rows, d.max_iters = self.case.nbody, L.tile_rows, self.max_iters
+        d.interleaved = int(L.interleaved)
         for k, c in enumerate(hbop.RKScheme(self.case.dtau).stage_coefficients()):
             d.coef[k] = c
         P = self.planes
         if P > native.MAX_P:
             raise NotImplementedError(f"{P} snapshots exceed the library limit {native.MAX_P}")
+        # the stage kernel adds the D[n][n] term and the forcing of planes other
+        # than 1 and 2 as signed zeros (hb_common.cuh add_signed_zero)
+        diag = np.diagonal(self.dmat)
+        unforced = [n for n in range(P) if n not in (1, 2)]
+        if np.any(diag.view(np.uint64) != 0) or np.any(self.ap[unforced].view(np.uint64) != 0):
+            raise ValueError("operator tables break the +0.0 diagonal / planes-1,2 forcing invariant")
         if P <= native.MAX_TEMPLATED_P:
             flat = self.dmat.ravel()
             for k in range(P * P):
@@ -326,7 +330,7 @@ class DeviceRank:
         a.norm_part = d.norm_part if stage == 0 else None
         a.nblocks, a.total_tiles, a.planes = d.nblocks, d.total_tiles, d.planes
         a.stage, a.tile_rows, a.coef = stage, d.tile_rows, d.coef[stage]
-        a.tmaps, a.in_slot = d.tmaps, self.STAGE_IN[stage]
+        a.tmaps, a.in_slot, a.interleaved = d.tmaps, self.STAGE_IN[stage], d.interleaved
         ctypes.memmove(ctypes.addressof(a.D), ctypes.addressof(d.D), ctypes.sizeof(a.D))
         ctypes.memmove(ctypes.addressof(a.ap), ctypes.addressof(d.ap), ctypes.sizeof(a.ap))
         return a

@@ -37,10 +37,10 @@ class RankEmulator:
         self.force_hist = []
 
     def view(self, slot, gid):
-        start, npl, nj2, pitch = self.L.block_view_index(gid)
-        b = self.L.blocks[self.L.local_index[gid]]
-        arr = self.slots[slot][start:start + npl * nj2 * pitch].reshape(self.P, 4, nj2, pitch)
-        return arr[:, :, :, ROW_LEAD:ROW_LEAD + b.ni + 2]
+        off, shape, strides = self.L.block_view(gid)
+        base = self.slots[slot]
+        return np.lib.stride_tricks.as_strided(base[off:], shape, tuple(8 * s for s in strides),
+                                               writeable=True)
 
     def _buf(self, kind, slot):
         return {0: self.slots[slot], 1: self.sendbuf, 2: self.recvbuf}[kind]
