@@ -264,6 +264,14 @@ int hbgpu_engine_prime(hbgpu_engine *eng, void *stream);
  * forces.  use_graph != 0 replays a CUDA graph of one iteration.          */
 int hbgpu_engine_iterate(hbgpu_engine *eng, int32_t iterations, int32_t use_graph,
                          void *stream);
+/* The same schedule split at its exchange points, for a caller that moves
+ * the remote halo payloads itself (several ranks' engines in one process):
+ * phase -1 = priming halo moves of slot A (local copies + pack), 0..3 = the
+ * fused stage kernel of that RK stage (+ norm fold after stage 0), 4 =
+ * forces and the iteration counter.  hbgpu_engine_unpack(e, phase) then
+ * scatters the receive buffer into the slot that phase wrote.            */
+int hbgpu_engine_step(hbgpu_engine *eng, int32_t phase, void *stream);
+int hbgpu_engine_unpack(hbgpu_engine *eng, int32_t phase, void *stream);
 /* kernels this engine launches per iteration (for launch accounting) */
 int hbgpu_engine_launches_per_iteration(const hbgpu_engine *eng);
 int hbgpu_engine_destroy(hbgpu_engine *eng);

@@ -184,7 +184,8 @@ int exchange_remote(hbgpu_engine *e, double *slot, cudaStream_t s) {
     return hbgpu_halo(slot, d.sendbuf, d.recvbuf, d.unpack_dirs, d.nunpack, d.unpack_max_len, d.planes, s);
 }
 
-int one_iteration(hbgpu_engine *e, cudaStream_t s) {
+// the fused stage kernel of RK stage `st` (+ the norm fold after stage 0)
+int run_stage(hbgpu_engine *e, int st, cudaStream_t s) {
     const hbgpu_engine_desc &d = e->d;
     hbgpu_stage_args a;
     memset(&a, 0, sizeof(a));
@@ -204,22 +205,24 @@ int one_iteration(hbgpu_engine *e, cudaStream_t s) {
     a.tile_rows = d.tile_rows;
     memcpy(a.D, d.D, sizeof(a.D));
     memcpy(a.ap, d.ap, sizeof(a.ap));
+    a.in = d.slot[kIn[st]];
+    a.out = d.slot[kOut[st]];
+    a.stage = st;
+    a.in_slot = kIn[st];
+    a.interleaved = d.interleaved;
+    a.coef = d.coef[st];
+    a.norm_part = st == 0 ? d.norm_part : nullptr;
+    int rc = hbgpu_stage(&a, s);
+    if (!rc && st == 0) rc = hbgpu_norm_fold(d.blocks, d.nblocks, d.norm_part, d.sumsq, d.iter, s);
+    return rc;
+}
+
+int one_iteration(hbgpu_engine *e, cudaStream_t s) {
+    const hbgpu_engine_desc &d = e->d;
     for (int st = 0; st < 4; ++st) {
-        a.in = d.slot[kIn[st]];
-        a.out = d.slot[kOut[st]];
-        a.stage = st;
-        a.in_slot = kIn[st];
-        a.interleaved = d.interleaved;
-        a.coef = d.coef[st];
-        a.norm_part = st == 0 ? d.norm_part : nullptr;
-        int rc = hbgpu_stage(&a, s);
+        int rc = run_stage(e, st, s);
+        if (!rc) rc = exchange_remote(e, d.slot[kOut[st]], s);
         if (rc) return rc;
-        rc = exchange_remote(e, d.slot[kOut[st]], s);
-        if (rc) return rc;
-        if (st == 0) {
-            rc = hbgpu_norm_fold(d.blocks, d.nblocks, d.norm_part, d.sumsq, d.iter, s);
-            if (rc) return rc;
-        }
     }
     return hbgpu_forces(d.slot[0], d.segs, d.nsegs, d.planes, d.nbody, d.force_hist, d.iter, s);
 }
@@ -275,6 +278,47 @@ extern "C" int hbgpu_engine_prime(hbgpu_engine *e, void *stream) {
     const hbgpu_engine_desc &d = e->d;
     rc = hbgpu_halo(d.slot[0], d.sendbuf, d.recvbuf, d.prime_dirs, d.nprime, d.prime_max_len, d.planes, e->work);
     if (!rc) rc = exchange_remote(e, d.slot[0], e->work);
+    return leave(e, caller, rc);
+}
+
+// ---- stepwise schedule: the same iteration split at its exchange points, for
+// callers that move the remote halo payloads themselves (one process driving
+// several ranks' engines, e.g. the loopback transport of solver.run_case).
+// phase: -1 = priming exchange (halo kernel: local copies + pack of slot A),
+//        0..3 = fused stage kernel of that RK stage (+ norm fold after 0),
+//        4 = forces + iteration counter.
+// unpack(e, phase) scatters the receive buffer into the slot phase wrote.
+
+extern "C" int hbgpu_engine_step(hbgpu_engine *e, int32_t phase, void *stream) {
+    cudaStream_t caller = (cudaStream_t)stream;
+    int rc = enter(e, caller);
+    if (rc) return rc;
+    const hbgpu_engine_desc &d = e->d;
+    if (phase == -1)
+        rc = hbgpu_halo(d.slot[0], d.sendbuf, d.recvbuf, d.prime_dirs, d.nprime, d.prime_max_len, d.planes,
+                        e->work);
+    else if (phase >= 0 && phase < 4)
+        rc = run_stage(e, phase, e->work);
+    else if (phase == 4)
+        rc = hbgpu_forces(d.slot[0], d.segs, d.nsegs, d.planes, d.nbody, d.force_hist, d.iter, e->work);
+    else {
+        hbgpu_set_error("hbgpu_engine_step: bad phase %d", phase);
+        rc = HBGPU_ERR_ARG;
+    }
+    return leave(e, caller, rc);
+}
+
+extern "C" int hbgpu_engine_unpack(hbgpu_engine *e, int32_t phase, void *stream) {
+    cudaStream_t caller = (cudaStream_t)stream;
+    if (phase < -1 || phase > 3) {
+        hbgpu_set_error("hbgpu_engine_unpack: bad phase %d", phase);
+        return HBGPU_ERR_ARG;
+    }
+    int rc = enter(e, caller);
+    if (rc) return rc;
+    const hbgpu_engine_desc &d = e->d;
+    double *slot = phase < 0 ? d.slot[0] : d.slot[kOut[phase]];
+    rc = hbgpu_halo(slot, d.sendbuf, d.recvbuf, d.unpack_dirs, d.nunpack, d.unpack_max_len, d.planes, e->work);
     return leave(e, caller, rc);
 }
 

@@ -100,6 +100,8 @@ SIGNATURES = {
     "hbgpu_engine_prime": (c_i32, [c_vp, c_vp]),
     "hbgpu_engine_iterate": (c_i32, [c_vp, c_i32, c_i32, c_vp]),
     "hbgpu_engine_launches_per_iteration": (c_i32, [c_vp]),
+    "hbgpu_engine_step": (c_i32, [c_vp, c_i32, c_vp]),
+    "hbgpu_engine_unpack": (c_i32, [c_vp, c_i32, c_vp]),
     "hbgpu_engine_destroy": (c_i32, [c_vp]),
     "hbgpu_comm_unique_id": (c_i32, [ctypes.c_char_p]),
     "hbgpu_comm_init": (c_i32, [ctypes.c_char_p, c_i32, c_i32, c_i32, ctypes.POINTER(c_vp)]),

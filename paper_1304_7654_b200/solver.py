@@ -71,6 +71,10 @@ class RunSpec:
     use_graph: bool = True
     tile_rows: int | None = None
     device: int | None = None
+    # single process, ranks > 1: "fold" runs all blocks in one engine;
+    # "loopback" runs one engine per rank on this GPU with device-copy
+    # transport (exercises the multi-GPU halo path)
+    transport: str = "fold"
 
 
 @dataclass
@@ -309,6 +313,9 @@ class DeviceRank:
         native.check(self.lib.hbgpu_engine_prime(self.engine, self.stream()), "hbgpu_engine_prime")
 
     def iterate(self, iterations, use_graph=True):
+        if self.comm is None and (self.layout.sends or self.layout.recvs):
+            raise ProtocolError("this rank has remote cuts but no communicator; "
+                                "step it with hbgpu_engine_step/unpack (loopback) instead")
         native.check(self.lib.hbgpu_engine_iterate(self.engine, int(iterations), int(bool(use_graph)),
                                                    self.stream()), "hbgpu_engine_iterate")
 
@@ -458,45 +465,14 @@ def run_case(spec):
     native.require_cuda()
     t0 = time.perf_counter()
     if world > 1:
-        rank = dist.get_rank()
-        device = spec.device if spec.device is not None else rank % torch.cuda.device_count()
-        torch.cuda.set_device(device)
-        comm = make_comm(rank, world, device)
-        exec_partition, exec_plan = partition, plan
+        fields, hist_np, norms_local = _execute_distributed(spec, topology, partition, plan,
+                                                            iterations, dist, world)
+    elif spec.ranks > 1 and spec.transport == "loopback":
+        fields, hist_np, norms_local = _execute_loopback(spec, topology, partition, plan, iterations)
     else:
-        rank, comm = 0, None
-        device = spec.device if spec.device is not None else torch.cuda.current_device()
-        exec_partition = partition_blocks(topology, 1)
-        exec_plan = build_cut_plan(topology, exec_partition, case.nharms, case.npde)
-    dr = DeviceRank(case, topology, exec_partition, exec_plan, rank=rank, device=device, comm=comm,
-                    initial=spec.initial, tile_rows=spec.tile_rows, max_iters=max(1, iterations),
-                    pinned_ic=spec.initial_state)
-    try:
-        dr.prime()
-        if iterations > 0:
-            dr.iterate(iterations, use_graph=spec.use_graph)
-        torch.cuda.synchronize(dr.device)
-        div = dr.divergence()
-        fields = dr.fields(0, pinned_out=spec.output)
-        norms_local = dr.norm_history(iterations)
-        hist = dr.force_history_array(iterations)
-        if world > 1:
-            divs = [None] * world
-            dist.all_gather_object(divs, div)
-            divs = [d for d in divs if d is not None]
-            div = min(divs, key=lambda d: d[:2]) if divs else None
-            raise_divergence(div)
-            hist = _reduce_history(dr, hist, world)
-            allnorm = [None] * world
-            dist.all_gather_object(allnorm, norms_local)
-            norms_local = {k: v for part in allnorm for k, v in part.items()}
-        raise_divergence(div)
-        hist_np = hist.cpu().numpy() if iterations > 0 else np.zeros((0, 3, case.planes, case.nbody))
-        torch.cuda.synchronize(dr.device)
-    finally:
-        dr.close()
-        if comm is not None:
-            native.load().hbgpu_comm_destroy(comm)
+        one = partition_blocks(topology, 1)
+        fields, hist_np, norms_local = _execute_single(
+            spec, topology, one, build_cut_plan(topology, one, case.nharms, case.npde), iterations)
     wall = time.perf_counter() - t0
 
     forces = (ForceCoefficients.from_stack(hist_np[-1]) if iterations > 0
@@ -516,6 +492,130 @@ def run_case(spec):
     return CaseRunResult(fields=fields, forces=forces, counters=counters, wall_s=wall,
                          record=record, residual_norms=_fold_norms(norms_local, iterations),
                          force_history=[ForceCoefficients.from_stack(h) for h in hist_np])
+
+
+def _new_rank(spec, topology, partition, plan, rank, device, comm, iterations):
+    return DeviceRank(spec.case, topology, partition, plan, rank=rank, device=device, comm=comm,
+                      initial=spec.initial, tile_rows=spec.tile_rows, max_iters=max(1, iterations),
+                      pinned_ic=spec.initial_state)
+
+
+def _history(dr, iterations):
+    case = dr.case
+    if iterations == 0:
+        return np.zeros((0, 3, case.planes, case.nbody))
+    return dr.force_history_array(iterations).cpu().numpy()
+
+
+def _execute_single(spec, topology, partition, plan, iterations):
+    """All blocks on this process's GPU, one engine, graph-replayed iterations."""
+    import torch
+    device = spec.device if spec.device is not None else torch.cuda.current_device()
+    dr = _new_rank(spec, topology, partition, plan, 0, device, None, iterations)
+    try:
+        dr.prime()
+        if iterations > 0:
+            dr.iterate(iterations, use_graph=spec.use_graph)
+        torch.cuda.synchronize(dr.device)
+        raise_divergence(dr.divergence())
+        fields = dr.fields(0, pinned_out=spec.output)
+        hist = _history(dr, iterations)
+        norms = dr.norm_history(iterations)
+        torch.cuda.synchronize(dr.device)
+    finally:
+        dr.close()
+    return fields, hist, norms
+
+
+def _execute_distributed(spec, topology, partition, plan, iterations, dist, world):
+    """One rank per process/GPU; remote halos over NCCL inside the engine."""
+    import torch
+    rank = dist.get_rank()
+    device = spec.device if spec.device is not None else rank % torch.cuda.device_count()
+    torch.cuda.set_device(device)
+    comm = make_comm(rank, world, device)
+    dr = _new_rank(spec, topology, partition, plan, rank, device, comm, iterations)
+    try:
+        dr.prime()
+        if iterations > 0:
+            dr.iterate(iterations, use_graph=spec.use_graph)
+        torch.cuda.synchronize(dr.device)
+        divs = [None] * world
+        dist.all_gather_object(divs, dr.divergence())
+        divs = [d for d in divs if d is not None]
+        raise_divergence(min(divs, key=lambda d: d[:2]) if divs else None)
+        fields = dr.fields(0, pinned_out=spec.output)
+        hist = dr.force_history_array(iterations)
+        hist = _reduce_history(dr, hist, world).cpu().numpy() if iterations > 0 else _history(dr, 0)
+        allnorm = [None] * world
+        dist.all_gather_object(allnorm, dr.norm_history(iterations))
+        norms = {k: v for part in allnorm for k, v in part.items()}
+        torch.cuda.synchronize(dr.device)
+    finally:
+        dr.close()
+        native.load().hbgpu_comm_destroy(comm)
+    return fields, hist, norms
+
+
+def _execute_loopback(spec, topology, partition, plan, iterations):
+    """spec.ranks engines on this GPU, one per rank of the reference partition,
+    stepped stage by stage; the remote halo payloads move between their send
+    and receive buffers by device copies in place of NCCL.  This runs the
+    multi-GPU data path -- fused pack in the stage kernel, per-peer segments,
+    unpack -- on one device."""
+    import torch
+    device = spec.device if spec.device is not None else torch.cuda.current_device()
+    nr = spec.ranks
+    ranks = []
+    try:
+        for r in range(nr):
+            ranks.append(_new_rank(spec, topology, partition, plan, r, device, None, iterations))
+        lib = native.load()
+        recv_index = [{peer: (off, cnt) for peer, off, cnt in dr.layout.recvs} for dr in ranks]
+
+        def transport():
+            for r, dr in enumerate(ranks):
+                for peer, off, cnt in dr.layout.sends:
+                    roff, rcnt = recv_index[peer][r]
+                    if rcnt != cnt:
+                        raise ProtocolError(f"rank {r} -> {peer}: {cnt} != {rcnt} doubles")
+                    ranks[peer].recvbuf[roff:roff + cnt].copy_(dr.sendbuf[off:off + cnt])
+
+        def phase(p, exchange):
+            for dr in ranks:
+                native.check(lib.hbgpu_engine_step(dr.engine, p, dr.stream()), "hbgpu_engine_step")
+            if exchange:
+                transport()
+                for dr in ranks:
+                    native.check(lib.hbgpu_engine_unpack(dr.engine, p, dr.stream()), "hbgpu_engine_unpack")
+
+        phase(-1, True)
+        for _ in range(iterations):
+            for st in range(4):
+                phase(st, True)
+            phase(4, False)
+        torch.cuda.synchronize(device)
+        divs = [d for d in (dr.divergence() for dr in ranks) if d is not None]
+        raise_divergence(min(divs, key=lambda d: d[:2]) if divs else None)
+        fields, norms = {}, {}
+        for dr in ranks:
+            fields.update(dr.fields(0, pinned_out=spec.output))
+            norms.update(dr.norm_history(iterations))
+        if iterations > 0:
+            stacked = torch.stack([dr.force_history_array(iterations).reshape(-1) for dr in ranks])
+            count = stacked.shape[1]
+            out = torch.empty(count, dtype=torch.float64, device=stacked.device)
+            if count:
+                native.check(lib.hbgpu_ordered_fold(_ptr(stacked), nr, count, _ptr(out), ranks[0].stream()),
+                             "hbgpu_ordered_fold")
+            hist = out.cpu().numpy().reshape(iterations, 3, spec.case.planes, spec.case.nbody)
+        else:
+            hist = _history(ranks[0], 0)
+        torch.cuda.synchronize(device)
+    finally:
+        for dr in ranks:
+            dr.close()
+    return fields, hist, norms
 
 
 def _reduce_history(dr, hist, world):
