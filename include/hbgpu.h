@@ -33,10 +33,12 @@ extern "C" {
  * strip -- starts on a 64-byte DRAM access granule (rows are padded to a
  * multiple of 8 doubles) */
 #define HBGPU_ROW_LEAD 7
-/* interior columns per stage-kernel strip (one CTA: 2 warps per pde) */
+/* consumer warps per stage tile (= residual-norm partials per tile).  A
+ * tile covers tile_pdes pdes (4 or 1) and 256 / tile_pdes columns: each of
+ * the 8 warps owns 32 columns of one pde. */
+#define HBGPU_TILE_WARPS 8
+/* interior columns per strip for tile_pdes = 4 (the narrow-block default) */
 #define HBGPU_STRIP 64
-/* consumer warps per stage tile (= residual-norm partials per tile) */
-#define HBGPU_TILE_WARPS (HBGPU_NPDE * HBGPU_STRIP / 32)
 
 enum {
     HBGPU_OK = 0,
@@ -61,11 +63,12 @@ typedef struct hbgpu_block {
     int32_t ni, nj;      /* interior cells                                  */
     int32_t pitch;       /* row stride, elements (multiple of 8)            */
     int32_t gid;         /* global block id                                 */
-    int32_t tiles_i;     /* column strips: ceil(ni / HBGPU_STRIP)           */
+    int32_t tiles_i;     /* column strips: ceil(ni / (256 / tile_pdes))     */
     int32_t tiles_j;     /* ceil(nj / tile_rows)                            */
     int32_t tile_begin;  /* first tile of this block in the rank tile list  */
-    int32_t ntiles;      /* tiles_i * tiles_j; a tile is one CTA's strip
-                            over tile_rows rows, all 4 pdes                 */
+    int32_t ntiles;      /* tiles_i * (4 / tile_pdes) * tiles_j; tile t of
+                            the block: strip t % tiles_i, pde group
+                            (t / tiles_i) % (4 / tile_pdes), row tile rest  */
     int32_t sxy_pitch;   /* row stride of the sxy table (ni rounded up to 4) */
     int32_t pad0;
     double nu_h2;        /* NU / (h*h)          (hbcore.py:257)             */
@@ -171,7 +174,8 @@ typedef struct hbgpu_stage_args {
     int32_t in_slot;           /* which of the three slots `in` is (0..2);
                                   q0 is slot 0                              */
     int32_t interleaved;       /* 1 = row-interleaved slot layout          */
-    int32_t pad1;
+    int32_t tile_pdes;         /* pdes per tile: 4 (64-col strips) or 1
+                                  (256-col strips)                          */
     double coef;               /* alpha_s * dtau                            */
     /* D row-major P x P with a +0.0 diagonal (hbcore.py:88-94); ap[n*4 + p]
      * = amp[n] (1 + p/4), zero except on planes 1 and 2 (hbcore.py:170-175):
@@ -193,13 +197,14 @@ int hbgpu_stage_prepare(int32_t planes);
  * pde, plane) over each block's part of a slot, written as CUtensorMap
  * (128 B) #(set*nblocks + b) into out_host (caller uploads it to device
  * memory, 64-B aligned): sets 0..2 = stencil boxes (strip + 2 halo columns
- * each side) over slot[0..2], set 3 = strip-wide q0 box over slot[0], set
- * 4 = 2-D (column, row) strip-wide box over the block's sxy forcing table.
- * out_bytes >= 5*nblocks*128.                                              */
+ * each side, split in two boxes when wider than TMA's 256) over slot[0..2],
+ * set 3 = strip-wide q0 box over slot[0], set 4 = 2-D (column, row)
+ * strip-wide box over the block's sxy forcing table.  tile_pdes (4 or 1)
+ * fixes the strip geometry.  out_bytes >= 5*nblocks*128.                   */
 int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy,
                              const hbgpu_block *blocks_host,
-                             int32_t nblocks, int32_t planes, void *out_host,
-                             int64_t out_bytes);
+                             int32_t nblocks, int32_t planes, int32_t tile_pdes,
+                             void *out_host, int64_t out_bytes);
 
 /* standalone halo moves (exchange.py:295-316 local copy / pack / unpack) */
 int hbgpu_halo(double *slot, double *sendbuf, const double *recvbuf,
@@ -245,7 +250,7 @@ typedef struct hbgpu_engine_desc {
     void *comm;                      /* from hbgpu_comm_init, NULL if 1 rank */
     const void *tmaps;               /* device, from hbgpu_encode_tensor_maps */
     int32_t nblocks, total_tiles, planes, nbody, tile_rows, max_iters;
-    int32_t interleaved, pad1;       /* slot layout, see hbgpu_block        */
+    int32_t interleaved, tile_pdes;  /* slot layout, tile geometry          */
     double coef[4];
     double D[HBGPU_MAX_TEMPLATED_P * HBGPU_MAX_TEMPLATED_P];
     double ap[HBGPU_MAX_P * HBGPU_NPDE];

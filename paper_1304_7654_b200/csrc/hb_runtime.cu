@@ -210,6 +210,7 @@ int run_stage(hbgpu_engine *e, int st, cudaStream_t s) {
     a.stage = st;
     a.in_slot = kIn[st];
     a.interleaved = d.interleaved;
+    a.tile_pdes = d.tile_pdes;
     a.coef = d.coef[st];
     a.norm_part = st == 0 ? d.norm_part : nullptr;
     int rc = hbgpu_stage(&a, s);

@@ -14,30 +14,32 @@
 //   * divergence keys (hbcore.py:244-245, 279-284);
 //   * stage 0: per-(tile, warp) partial sums of R^2 for the residual norm.
 //
-// Work decomposition.  A tile is one CTA's strip of HBGPU_STRIP (64)
-// columns of one block over `tile_rows` rows.  Consumer warp w computes pde
-// w % 4 on columns [i0 + 32 (w / 4), +32); lane l owns one column and marches
-// down the rows keeping rows j-1, j, j+1 of all P snapshots of its column in
-// registers (stencil north/south neighbours and the P centres of the
-// D-contraction).
+// Work decomposition.  A tile is one CTA's strip of one block over
+// `tile_rows` rows: PT pdes x 256/PT columns (PT = 4: 64 columns of every
+// pde; PT = 1: 256 columns of one pde, for blocks at least 192 wide).  Each of
+// the 8 consumer warps owns 32 columns of one pde; lane l owns one column and
+// marches down the rows keeping rows j-1, j, j+1 of all P snapshots of its
+// column in registers (stencil north/south neighbours and the P centres of
+// the D-contraction).
 //
 // Memory pipeline (warp-specialised, TMA).  A ninth warp is the producer: one
 // lane streams the tile's rows into shared memory with tensor TMA loads
-// (cp.async.bulk.tensor): per row, one 4-D box of 68 columns x 4 pdes x P
-// snapshots (19.6 KB at P = 9: the strip plus two halo columns each side,
-// zero-filled past the row end) into a ring of R stencil slots, the strip's
-// 64-column q_0 row box into a ring of Q slots, and the 64-column sxy forcing
-// row riding on the stencil slot's barrier.  Every slot has a "full" mbarrier
-// (TMA transaction count) and an "empty" one the consumer warps arrive on
-// once they stop reading it.  With ROW_LEAD = 7 every strip starts on a
-// 64-byte DRAM granule: a q_0 row costs exactly its 512 bytes and a stencil
-// row one extra granule on each side, shared with the neighbouring strips.
-// CTAs are persistent (tiles t = blockIdx.x, +gridDim.x, ...) and the rings
-// stream across tile boundaries without draining.
+// (cp.async.bulk.tensor): per row, the stencil box (the strip plus two halo
+// columns each side, x PT pdes x P snapshots; split in two boxes when wider
+// than TMA's 256-element limit) into a ring of R slots, the strip's q_0 row
+// into a ring of Q slots, and the sxy forcing row riding on the stencil
+// slot's barrier.  Every slot has a "full" mbarrier (TMA transaction count)
+// and an "empty" one the consumer warps arrive on once they stop reading it.
+// With ROW_LEAD = 7 every strip starts on a 64-byte DRAM granule: a q_0 row
+// costs exactly its bytes and a stencil row one extra granule each side,
+// shared with the neighbouring strips (2/32 extra at PT = 1).  CTAs are
+// persistent (tiles t = blockIdx.x, +gridDim.x, ...) and the rings stream
+// across tile boundaries without draining.
 //
 // Rounding: every operation is an explicitly rounded DMUL/DADD, in the
-// reference's per-point order, including the m == n term (D[n][n] = 0 still
-// contributes a signed zero) and the +ap*sxy term on zero-amplitude planes.
+// reference's per-point order.  The m == n coupling term (D[n][n] = 0) and
+// the zero-amplitude forcing planes contribute signed zeros, reproduced
+// exactly by add_signed_zero (hb_common.cuh).
 
 #include "hb_common.cuh"
 
@@ -96,29 +98,54 @@ __device__ __forceinline__ void prefetch_tmap(const void *map) {
 
 // ---- geometry ---------------------------------------------------------------------
 
-constexpr int STRIP = HBGPU_STRIP;              // interior columns per tile
-constexpr int HALVES = STRIP / 32;              // warps per pde
-constexpr int CW = NPDE * HALVES;               // consumer warps
+constexpr int CW = HBGPU_TILE_WARPS;            // consumer warps per tile
 constexpr int THREADS = (CW + 1) * 32;          // + one producer warp
-constexpr int SEG = STRIP + 4;                  // stencil box row: columns i0-2 .. i0+STRIP+1
-constexpr int QSEG = STRIP;                     // q0 / sxy box row: columns i0 .. i0+STRIP-1
-static_assert(CW == HBGPU_TILE_WARPS, "tile warp count");
+
+// Tile geometry for PT pdes per tile (4 or 1).
+template <int PT>
+struct Geo {
+    static constexpr int TCOLS = 256 / PT;                     // strip columns
+    static constexpr int NSPLIT = (TCOLS + 4 > 256) ? 2 : 1;   // stencil boxes per row
+    static constexpr int BW = TCOLS / NSPLIT + 4;              // stencil box width
+    static constexpr int CWPR = TCOLS / 32 / NSPLIT;           // column warps per box
+    static_assert(PT == 1 || PT == 4, "tile_pdes is 1 or 4");
+    static_assert(BW <= 256, "TMA box limit");
+};
+
+template <int P, bool FIRST, int R, int Q, int PT>
+struct Smem {
+    using G = Geo<PT>;
+    static constexpr int BOXD = P * PT * G::BW;                          // doubles per box
+    static constexpr int REGION = (BOXD * 8 + 127) / 128 * 128 / 8;      // 128-B aligned
+    static constexpr int SXY = G::NSPLIT * REGION;                       // sxy row offset
+    static constexpr int SLOT = SXY + G::TCOLS;                          // stencil slot
+    static constexpr int QSLOT = P * PT * G::TCOLS;                      // q0 slot
+    static constexpr int NQ = FIRST ? 0 : Q;
+    static constexpr size_t BAR_OFF = ((size_t)R * SLOT + (size_t)NQ * QSLOT) * 8;
+    static constexpr size_t BYTES = BAR_OFF + (size_t)2 * (R + NQ) * 8;
+    static_assert((SLOT * 8) % 128 == 0 && (QSLOT * 8) % 128 == 0, "TMA slots need 128-B alignment");
+};
 
 // ---- tiles and halo targets -------------------------------------------------
 
 struct Tile {
     int bidx;   // local block index
     int i0;     // first interior column of the strip (1-based)
+    int pde0;   // first pde of the tile
     int j0, j1; // first / last interior row
 };
 
+template <int PT>
 __device__ __forceinline__ Tile decode_tile(const hbgpu_stage_args &a, int t) {
     Tile T;
     T.bidx = a.tile_block[t];
     const hbgpu_block &b = a.blocks[T.bidx];
     const int local = t - b.tile_begin;
-    T.i0 = (local % b.tiles_i) * STRIP + 1;
-    T.j0 = (local / b.tiles_i) * a.tile_rows + 1;
+    T.i0 = (local % b.tiles_i) * Geo<PT>::TCOLS + 1;
+    const int rest = local / b.tiles_i;
+    constexpr int GROUPS = NPDE / PT;
+    T.pde0 = (rest % GROUPS) * PT;
+    T.j0 = (rest / GROUPS) * a.tile_rows + 1;
     T.j1 = min(T.j0 + a.tile_rows - 1, b.nj);
     return T;
 }
@@ -181,22 +208,20 @@ __device__ __forceinline__ RingPos advance(RingPos r) {
     return r;
 }
 
-template <int P, bool FIRST, int R, int Q>
-struct Smem {
-    static constexpr int BOX = P * NPDE * SEG;     // doubles: [snapshot][pde][SEG]
-    static constexpr int SLOT = BOX + QSEG;        // + the sxy row of the row computed with it
-    static constexpr int QSLOT = P * NPDE * QSEG;  // doubles: [snapshot][pde][QSEG]
-    static constexpr int NQ = FIRST ? 0 : Q;
-    static constexpr size_t BAR_OFF = ((size_t)R * SLOT + (size_t)NQ * QSLOT) * 8;
-    static constexpr size_t BYTES = BAR_OFF + (size_t)2 * (R + NQ) * 8;
-    static_assert((SLOT * 8) % 128 == 0 && (QSLOT * 8) % 128 == 0, "TMA slots need 128-B alignment");
-};
+// TMA coordinates of (column x, first pde, row) for either slot layout
+template <int PT>
+__device__ __forceinline__ void load_rows(void *dst, const void *map, int x, int pde0, int row, bool inter,
+                                          uint64_t *bar) {
+    if (inter) tma_load_4d(dst, map, x, pde0, 0, row, bar);
+    else tma_load_4d(dst, map, x, row, pde0, 0, bar);
+}
 
 // ---- the pipelined kernel -----------------------------------------------------------
 
-template <int P, bool FIRST, int R, int Q, int MODE = 0>
+template <int P, bool FIRST, int R, int Q, int PT, int MODE>
 __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_constant__ hbgpu_stage_args a) {
-    using S = Smem<P, FIRST, R, Q>;
+    using S = Smem<P, FIRST, R, Q, PT>;
+    using G = Geo<PT>;
     static_assert(R >= 3 && Q >= 2, "ring too short");
     extern __shared__ __align__(1024) unsigned char smem[];
     double *ring = reinterpret_cast<double *>(smem);
@@ -221,15 +246,16 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
     __syncthreads();
     const int ntile = a.total_tiles;
     const CUtensorMap *maps = reinterpret_cast<const CUtensorMap *>(a.tmaps);
+    const bool inter = a.interleaved != 0;
 
     if (warp == CW) {
         // ------------------------------ producer ------------------------------
         if (lane != 0) return;
-        constexpr uint32_t BYTES = S::BOX * 8, QBYTES = S::QSLOT * 8, SBYTES = QSEG * 8;
+        constexpr uint32_t BYTES = S::BOXD * 8 * G::NSPLIT, QBYTES = S::QSLOT * 8, SBYTES = G::TCOLS * 8;
         RingPos pin{0, 0}, pq{0, 0};
         int issued_in = 0, issued_q = 0;   // saturate at the ring size
         for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
-            const Tile tl = decode_tile(a, t);
+            const Tile tl = decode_tile<PT>(a, t);
             const CUtensorMap *min = maps + a.in_slot * a.nblocks + tl.bidx;
             const CUtensorMap *mq = maps + 3 * a.nblocks + tl.bidx;   // q0: slot 0, strip box
             const CUtensorMap *ms = maps + 4 * a.nblocks + tl.bidx;   // sxy table
@@ -242,9 +268,11 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
                 else ++issued_in;
                 double *dst = ring + pin.slot * S::SLOT;
                 mbar_expect_tx(full_in + pin.slot, with_sxy ? BYTES + SBYTES : BYTES);
-                if (a.interleaved) tma_load_4d(dst, min, x, 0, 0, row, full_in + pin.slot);
-                else tma_load_4d(dst, min, x, row, 0, 0, full_in + pin.slot);
-                if (with_sxy) tma_load_2d(dst + S::BOX, ms, tl.i0 - 1, row - 2, full_in + pin.slot);
+#pragma unroll
+                for (int k = 0; k < G::NSPLIT; ++k)
+                    load_rows<PT>(dst + k * S::REGION, min, x + k * (G::TCOLS / G::NSPLIT), tl.pde0, row,
+                                  inter, full_in + pin.slot);
+                if (with_sxy) tma_load_2d(dst + S::SXY, ms, tl.i0 - 1, row - 2, full_in + pin.slot);
                 pin = advance<R>(pin);
             };
             put_in(tl.j0 - 1, false);
@@ -255,10 +283,7 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
                     if (issued_q >= Q) mbar_wait(empty_q + pq.slot, pq.phase ^ 1u);
                     else ++issued_q;
                     mbar_expect_tx(full_q + pq.slot, QBYTES);
-                    if (a.interleaved)
-                        tma_load_4d(qring + pq.slot * S::QSLOT, mq, x + 2, 0, 0, j, full_q + pq.slot);
-                    else
-                        tma_load_4d(qring + pq.slot * S::QSLOT, mq, x + 2, j, 0, 0, full_q + pq.slot);
+                    load_rows<PT>(qring + pq.slot * S::QSLOT, mq, x + 2, tl.pde0, j, inter, full_q + pq.slot);
                     pq = advance<Q>(pq);
                 }
             }
@@ -267,16 +292,25 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
     }
 
     // -------------------------------- consumers ---------------------------------
-    const int p = warp % NPDE;
-    const int col0 = 32 * (warp / NPDE) + lane;   // this lane's column within the strip
+    const int pp = warp % PT;                     // pde within the tile
+    const int cw = warp / PT;                     // column warp within the strip
+    const int col0 = 32 * cw + lane;              // this lane's column within the strip
+    // offset of this lane's column (+2 halo columns) inside a stencil slot
+    const int in_off = (cw / G::CWPR) * S::REGION + pp * G::BW + 32 * (cw % G::CWPR) + lane + 2;
+    const int q_off = pp * G::TCOLS + col0;
     const int gstage = (*a.iter) * 4 + a.stage + 1;
     const double coef = a.coef;
-    double ap[P];
-#pragma unroll
-    for (int n = 0; n < P; ++n) ap[n] = a.ap[n * NPDE + p];
     RingPos cin{0, 0}, cq{0, 0};
+    int ap_pde = -1;
+    double ap[P];
     for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
-        const Tile tl = decode_tile(a, t);
+        const Tile tl = decode_tile<PT>(a, t);
+        const int p = tl.pde0 + pp;
+        if (p != ap_pde) {
+#pragma unroll
+            for (int n = 0; n < P; ++n) ap[n] = a.ap[n * NPDE + p];
+            ap_pde = p;
+        }
         // by value: the output stores must not force re-reads of the descriptor
         const hbgpu_block b = a.blocks[tl.bidx];
         const int ni = b.ni, nj = b.nj;
@@ -295,12 +329,12 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
             const RingPos c1 = advance<R>(cin);
             mbar_wait(full_in + cin.slot, cin.phase);
             mbar_wait(full_in + c1.slot, c1.phase);
-            const double *r0 = ring + cin.slot * S::SLOT + p * SEG + col0 + 2;
-            const double *r1 = ring + c1.slot * S::SLOT + p * SEG + col0 + 2;
+            const double *r0 = ring + cin.slot * S::SLOT + in_off;
+            const double *r1 = ring + c1.slot * S::SLOT + in_off;
 #pragma unroll
             for (int m = 0; m < P; ++m) {
-                up[m] = r0[m * NPDE * SEG];
-                cur[m] = r1[m * NPDE * SEG];
+                up[m] = r0[m * PT * G::BW];
+                cur[m] = r1[m * PT * G::BW];
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty_in + cin.slot);
@@ -315,15 +349,15 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
 
             const RingPos nx = advance<R>(cin);
             mbar_wait(full_in + nx.slot, nx.phase);
-            const double *rc = ring + cin.slot * S::SLOT + p * SEG + col0;
-            const double *rn = ring + nx.slot * S::SLOT + p * SEG + col0 + 2;
-            const double sv = ring[nx.slot * S::SLOT + S::BOX + col0];   // sxy of row j
+            const double *rc = ring + cin.slot * S::SLOT + in_off;
+            const double *rn = ring + nx.slot * S::SLOT + in_off;
+            const double sv = ring[nx.slot * S::SLOT + S::SXY + col0];   // sxy of row j
 #pragma unroll
-            for (int m = 0; m < P; ++m) dn[m] = rn[m * NPDE * SEG];
+            for (int m = 0; m < P; ++m) dn[m] = rn[m * PT * G::BW];
             const double *qv = nullptr;
             if (!FIRST) {
                 mbar_wait(full_q + cq.slot, cq.phase);
-                qv = qring + cq.slot * S::QSLOT + p * QSEG + col0;
+                qv = qring + cq.slot * S::QSLOT + q_off;
             }
 
             // All P outputs in lockstep, branch-free: each step below is P
@@ -336,8 +370,8 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
                 double w[P], e[P];
 #pragma unroll
                 for (int n = 0; n < P; ++n) {
-                    w[n] = rc[n * NPDE * SEG + 1];
-                    e[n] = rc[n * NPDE * SEG + 3];
+                    w[n] = rc[n * PT * G::BW - 1];
+                    e[n] = rc[n * PT * G::BW + 1];
                 }
 #pragma unroll
                 for (int n = 0; n < P; ++n) o[n] = rmul(4.0, cur[n]);
@@ -366,7 +400,7 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
 #pragma unroll
             for (int n = 0; n < P; ++n) {
                 o[n] = forced_plane(n) ? radd(o[n], rmul(ap[n], sv)) : add_signed_zero(o[n], sv);
-                const double base = FIRST ? cur[n] : qv[n * NPDE * QSEG];
+                const double base = FIRST ? cur[n] : qv[n * PT * G::TCOLS];
                 v[n] = rsub(base, rmul(coef, o[n]));
                 if (MODE == 1) v[n] = base;   // measurement variant: same traffic, no arithmetic
             }
@@ -424,9 +458,10 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
 }
 
 // ---- generic snapshot count (P > HBGPU_MAX_TEMPLATED_P) --------------------------
-// One CTA of CW warps (same warp -> (pde, half-strip) map) per tile, operands
+// One CTA of CW warps (same warp -> (pde, columns) map) per tile, operands
 // through L1, D from shared memory.  Same arithmetic sequence; used for e.g.
 // the 63-plane tc1-full catalog case.
+template <int PT>
 __global__ void __launch_bounds__(CW * 32) stage_kernel_generic(const __grid_constant__ hbgpu_stage_args a) {
     extern __shared__ double sh[];
     const int P = a.planes;
@@ -435,14 +470,14 @@ __global__ void __launch_bounds__(CW * 32) stage_kernel_generic(const __grid_con
     const double *D = sh;
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int p = warp % NPDE;
     const int t = blockIdx.x;
-    const Tile tl = decode_tile(a, t);
+    const Tile tl = decode_tile<PT>(a, t);
+    const int p = tl.pde0 + warp % PT;
     const hbgpu_block &b = a.blocks[tl.bidx];
     const int ni = b.ni, nj = b.nj;
     const int64_t rstride = b.rs;
     const int64_t ps4 = b.ps * NPDE;
-    const int i = tl.i0 + 32 * (warp / NPDE) + lane;
+    const int i = tl.i0 + 32 * (warp / PT) + lane;
     const bool live = i <= ni;
     const bool first = a.stage == 0;
     const int gstage = (*a.iter) * 4 + a.stage + 1;
@@ -488,11 +523,11 @@ struct Launch {
     bool ready = false;
 };
 
-template <int P, bool FIRST, int R, int Q, int MODE = 0>
+template <int P, bool FIRST, int R, int Q, int PT, int MODE>
 static int prepare(Launch &L) {
     if (L.ready) return HBGPU_OK;
-    L.fn = stage_tma_kernel<P, FIRST, R, Q, MODE>;
-    L.smem = Smem<P, FIRST, R, Q>::BYTES;
+    L.fn = stage_tma_kernel<P, FIRST, R, Q, PT, MODE>;
+    L.smem = Smem<P, FIRST, R, Q, PT>::BYTES;
     if (cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem) != cudaSuccess)
         return hbgpu_check_launch("stage kernel smem attribute");
     int dev = 0, sms = 0, per_sm = 0;
@@ -508,7 +543,7 @@ static int prepare(Launch &L) {
 
 // Ring depths per snapshot count: R stencil rows for the update stages, RF
 // for the first stage (no q0 ring, so its rows go deeper), Q q0 rows.  One
-// CTA (8 consumer warps) per SM at P >= 7; the smem budget is ~227 KB.
+// CTA (8 consumer warps) per SM; the smem budget is ~227 KB.
 template <int P> struct Depth { static constexpr int R = 4, RF = 7, Q = 3; };
 template <> struct Depth<1> { static constexpr int R = 8, RF = 12, Q = 6; };
 template <> struct Depth<3> { static constexpr int R = 8, RF = 12, Q = 6; };
@@ -517,18 +552,12 @@ template <> struct Depth<13> { static constexpr int R = 4, RF = 6, Q = 2; };
 template <> struct Depth<15> { static constexpr int R = 4, RF = 5, Q = 2; };
 template <> struct Depth<17> { static constexpr int R = 4, RF = 5, Q = 2; };
 
-// HBGPU_RING=<variant> selects an alternative ring depth for P = 7 and 9
-// (measurements only): 1 = (R 5, RF 8, Q 4), 2 = (R 3, RF 5, Q 2), 3 = (R 6, RF 6, Q 5)
-static int ring_variant() {
-    const char *env = getenv("HBGPU_RING");
-    return env ? atoi(env) : 0;
-}
-
-template <int P, int R, int RF, int Q, int MODE = 0>
+template <int P, int PT, int MODE>
 static int launch_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
+    using D = Depth<P>;
     static Launch first, rest;
-    int rc = prepare<P, true, RF, Q, MODE>(first);
-    if (!rc) rc = prepare<P, false, R, Q, MODE>(rest);
+    int rc = prepare<P, true, D::RF, D::Q, PT, MODE>(first);
+    if (!rc) rc = prepare<P, false, D::R, D::Q, PT, MODE>(rest);
     if (rc || prepare_only) return rc;
     if (a.tmaps == nullptr) {
         hbgpu_set_error("hbgpu_stage: args->tmaps is required (hbgpu_encode_tensor_maps)");
@@ -541,20 +570,28 @@ static int launch_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_on
     return hbgpu_check_launch("hbgpu_stage");
 }
 
+// HBGPU_NOMATH=1 (measurements only, P = 9): the same pipeline and traffic
+// with the arithmetic replaced by a copy of q0
+static bool nomath() {
+    const char *env = getenv("HBGPU_NOMATH");
+    return env != nullptr && atoi(env) == 1;
+}
+
 template <int P>
 static int launch_p(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
-    using D = Depth<P>;
-    if constexpr (P == 7 || P == 9) {
-        static const int variant = ring_variant();
-        if (variant == 1) return launch_cfg<P, 5, 8, 4>(a, s, prepare_only);
-        if (variant == 2) return launch_cfg<P, 3, 5, 2>(a, s, prepare_only);
-        if (variant == 3) return launch_cfg<P, 6, 6, 5>(a, s, prepare_only);
-        if (P == 9 && variant == 9) return launch_cfg<P, D::R, D::RF, D::Q, 1>(a, s, prepare_only);
+    if constexpr (P == 9) {
+        static const bool nm = nomath();
+        if (nm) return a.tile_pdes == 1 ? launch_cfg<P, 1, 1>(a, s, prepare_only)
+                                        : launch_cfg<P, 4, 1>(a, s, prepare_only);
     }
-    return launch_cfg<P, D::R, D::RF, D::Q>(a, s, prepare_only);
+    return a.tile_pdes == 1 ? launch_cfg<P, 1, 0>(a, s, prepare_only) : launch_cfg<P, 4, 0>(a, s, prepare_only);
 }
 
 static int dispatch(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
+    if (a.tile_pdes != 1 && a.tile_pdes != 4) {
+        hbgpu_set_error("hbgpu_stage: tile_pdes must be 1 or 4, got %d", a.tile_pdes);
+        return HBGPU_ERR_ARG;
+    }
     switch (a.planes) {
         case 1: return launch_p<1>(a, s, prepare_only);
         case 3: return launch_p<3>(a, s, prepare_only);
@@ -567,17 +604,17 @@ static int dispatch(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only
         case 17: return launch_p<17>(a, s, prepare_only);
         default: break;
     }
+    auto kern = a.tile_pdes == 1 ? stage_kernel_generic<1> : stage_kernel_generic<4>;
     const size_t sm = sizeof(double) * (size_t)a.planes * a.planes;
-    if (sm > 48 * 1024 &&
-        cudaFuncSetAttribute(stage_kernel_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
-            cudaSuccess)
+    if (sm > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+                              cudaSuccess)
         return hbgpu_check_launch("generic stage smem attribute");
     if (prepare_only) return HBGPU_OK;
     if (a.dmat == nullptr) {
         hbgpu_set_error("hbgpu_stage: P=%d needs args->dmat", a.planes);
         return HBGPU_ERR_ARG;
     }
-    stage_kernel_generic<<<a.total_tiles, CW * 32, sm, s>>>(a);
+    kern<<<a.total_tiles, CW * 32, sm, s>>>(a);
     hbgpu_count_launch(1);
     return hbgpu_check_launch("hbgpu_stage");
 }
@@ -607,8 +644,14 @@ static EncodeTiledFn encode_fn() {
 // before any stream capture (the engine calls this at creation).
 extern "C" int hbgpu_stage_prepare(int32_t planes) {
     hbgpu_stage_args a;
+    memset(&a, 0, sizeof(a));
     a.planes = planes;
-    return hbgpu::dispatch(a, nullptr, true);
+    int rc = HBGPU_OK;
+    for (int pt : {1, 4}) {
+        a.tile_pdes = pt;
+        rc = rc ? rc : hbgpu::dispatch(a, nullptr, true);
+    }
+    return rc;
 }
 
 extern "C" int hbgpu_stage(const hbgpu_stage_args *args, void *stream) {
@@ -621,10 +664,12 @@ extern "C" int hbgpu_stage(const hbgpu_stage_args *args, void *stream) {
 }
 
 extern "C" int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy, const hbgpu_block *blocks,
-                                        int32_t nblocks, int32_t planes, void *out_host, int64_t out_bytes) {
+                                        int32_t nblocks, int32_t planes, int32_t tile_pdes, void *out_host,
+                                        int64_t out_bytes) {
     using namespace hbgpu;
-    if ((int64_t)sizeof(CUtensorMap) * 5 * nblocks > out_bytes || planes < 1 || planes > 256) {
-        hbgpu_set_error("hbgpu_encode_tensor_maps: output too small or bad planes");
+    if ((int64_t)sizeof(CUtensorMap) * 5 * nblocks > out_bytes || planes < 1 || planes > 256 ||
+        (tile_pdes != 1 && tile_pdes != 4)) {
+        hbgpu_set_error("hbgpu_encode_tensor_maps: output too small, bad planes or tile_pdes");
         return HBGPU_ERR_ARG;
     }
     EncodeTiledFn fn = encode_fn();
@@ -633,7 +678,7 @@ extern "C" int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy
         return HBGPU_ERR_CUDA;
     }
     // L2 sector promotion of the TMA fetches; HBGPU_L2_PROMOTION = 0, 64, 128
-    // or 256 overrides (measurements: 64 B best on C4 with 32-B aligned rows)
+    // or 256 overrides (measurements: 64 B best on C4)
     CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
     if (const char *env = getenv("HBGPU_L2_PROMOTION")) {
         const int v = atoi(env);
@@ -641,9 +686,11 @@ extern "C" int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy
               : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
               : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
     }
+    const cuuint32_t tcols = (cuuint32_t)(256 / tile_pdes);
+    const cuuint32_t bw = tile_pdes == 1 ? Geo<1>::BW : Geo<4>::BW;
     CUtensorMap *maps = reinterpret_cast<CUtensorMap *>(out_host);
-    // sets 0..2: stencil boxes (SEG columns) over slots 0..2; set 3: q0 box
-    // (QSEG columns) over slot 0; set 4: 2-D sxy table box (QSEG columns x 1 row)
+    // sets 0..2: stencil boxes over slots 0..2; set 3: q0 box over slot 0;
+    // set 4: 2-D sxy table box (strip columns x 1 row)
     for (int s = 0; s < 5; ++s) {
         for (int k = 0; k < nblocks; ++k) {
             const hbgpu_block &b = blocks[k];
@@ -653,14 +700,15 @@ extern "C" int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy
                 // plane-major (cols, rows, pde, plane), interleaved (cols, pde,
                 // plane, rows); both land in smem as [plane][pde][cols]
                 const bool inter = b.rs > b.ps;
-                const cuuint32_t w = (cuuint32_t)(s < 3 ? SEG : QSEG);
+                const cuuint32_t w = s < 3 ? bw : tcols;
+                const cuuint32_t npd = (cuuint32_t)tile_pdes;
                 cuuint64_t dims[4], strides[3];
                 cuuint32_t box[4];
                 if (inter) {
                     cuuint64_t d[4] = {(cuuint64_t)b.pitch, (cuuint64_t)NPDE, (cuuint64_t)planes,
                                        (cuuint64_t)(b.nj + 2)};
                     cuuint64_t st[3] = {(cuuint64_t)b.ps * 8, (cuuint64_t)b.ps * 8 * NPDE, (cuuint64_t)b.rs * 8};
-                    cuuint32_t bx[4] = {w, (cuuint32_t)NPDE, (cuuint32_t)planes, 1};
+                    cuuint32_t bx[4] = {w, npd, (cuuint32_t)planes, 1};
                     memcpy(dims, d, sizeof(d));
                     memcpy(strides, st, sizeof(st));
                     memcpy(box, bx, sizeof(bx));
@@ -668,7 +716,7 @@ extern "C" int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy
                     cuuint64_t d[4] = {(cuuint64_t)b.pitch, (cuuint64_t)(b.nj + 2), (cuuint64_t)NPDE,
                                        (cuuint64_t)planes};
                     cuuint64_t st[3] = {(cuuint64_t)b.rs * 8, (cuuint64_t)b.ps * 8, (cuuint64_t)b.ps * 8 * NPDE};
-                    cuuint32_t bx[4] = {w, 1, (cuuint32_t)NPDE, (cuuint32_t)planes};
+                    cuuint32_t bx[4] = {w, 1, npd, (cuuint32_t)planes};
                     memcpy(dims, d, sizeof(d));
                     memcpy(strides, st, sizeof(st));
                     memcpy(box, bx, sizeof(bx));
@@ -681,7 +729,7 @@ extern "C" int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy
             } else {
                 cuuint64_t dims[2] = {(cuuint64_t)b.ni, (cuuint64_t)b.nj};
                 cuuint64_t strides[1] = {(cuuint64_t)b.sxy_pitch * 8};
-                cuuint32_t box[2] = {(cuuint32_t)QSEG, 1};
+                cuuint32_t box[2] = {tcols, 1};
                 cuuint32_t estr[2] = {1, 1};
                 r = fn(&maps[s * nblocks + k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
                        (void *)(sxy + b.sxy_off), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,

@@ -31,7 +31,7 @@ from .hbop import forcing_table, stencil_coefficients
 
 ROW_LEAD = native.ROW_LEAD
 NPDE = native.NPDE
-STRIP = native.STRIP     # interior columns per stage tile
+WIDE_MIN_NI = 192         # blocks at least this wide use 256-column, 1-pde tiles
 BLOCK_ALIGN = 32          # elements (256 B)
 TARGET_TILES = 148 * 8    # ~8 tiles per persistent CTA (148 SMs x 1 CTA)
 MAX_TILE_ROWS = 256
@@ -46,10 +46,24 @@ def _round_up(x, m):
     return (x + m - 1) // m * m
 
 
-def choose_tile_rows(blocks):
+def choose_tile_pdes(blocks):
+    """4 pdes x 64 columns per tile, or 1 pde x 256 columns when every block
+    is wide enough: a tile re-reads one 64-byte halo granule on each side of
+    each row, 2 / 8 extra stencil reads for 64 columns but 2 / 32 for 256."""
+    if os.environ.get("HBGPU_TILE_PDES") in ("1", "4"):
+        return int(os.environ["HBGPU_TILE_PDES"])
+    return 1 if min(b.ni for b in blocks) >= WIDE_MIN_NI else 4
+
+
+def tiles_per_row(blocks, tile_pdes):
+    return {b.id: -(-b.ni // native.TILE_COLS[tile_pdes]) * (NPDE // tile_pdes) for b in blocks}
+
+
+def choose_tile_rows(blocks, tile_pdes=4):
     """Rows per tile: long tiles amortise the two halo rows each tile re-reads;
-    enough tiles keep every persistent warp of the stage kernel busy."""
-    rows = sum(-(-b.ni // STRIP) * b.nj for b in blocks)
+    enough tiles keep every persistent CTA of the stage kernel busy."""
+    per_row = tiles_per_row(blocks, tile_pdes)
+    rows = sum(per_row[b.id] * b.nj for b in blocks)
     tj = rows // TARGET_TILES
     tj = max(MIN_TILE_ROWS, min(MAX_TILE_ROWS, tj))
     return tj
@@ -79,6 +93,7 @@ class RankLayout:
     sendbuf_elems: int = 0
     recvbuf_elems: int = 0
     interleaved: bool = False
+    tile_pdes: int = 4
 
     def elem(self, gid, n, p, j, i):
         """Slot element index of (n, p, j, i) -- array coordinates -- of block gid."""
@@ -111,7 +126,7 @@ def _halo_cell(spec, face, k):
 
 
 def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None,
-                      interleaved=None):
+                      interleaved=None, tile_pdes=None):
     """Device layout of one rank's blocks.
 
     interleaved=False: plane-major slots, (n, p) planes of (nj+2) x pitch;
@@ -123,7 +138,8 @@ def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None,
     if not owned:
         raise ValueError(f"rank {rank} owns no blocks")
     local_index = {b.id: k for k, b in enumerate(owned)}
-    tj = tile_rows or choose_tile_rows(owned)
+    tpd = tile_pdes or choose_tile_pdes(owned)
+    tj = tile_rows or choose_tile_rows(owned, tpd)
     inter = INTERLEAVED if interleaved is None else bool(interleaved)
 
     pitch, ps, rs, base = [], [], [], []
@@ -143,20 +159,21 @@ def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None,
     sxy_parts, sxy_off = [], 0
     ntile = 0
     for k, b in enumerate(owned):
-        ti = -(-b.ni // STRIP)
+        ti = -(-b.ni // native.TILE_COLS[tpd])
         tjn = -(-b.nj // tj)
+        nt = ti * tjn * (NPDE // tpd)          # strips x row tiles x pde groups
         nu_h2, adv_2h = stencil_coefficients(b.h)
         spitch = _round_up(b.ni, 4)
         for name, value in (("base", base[k]), ("ps", ps[k]), ("rs", rs[k]), ("ni", b.ni), ("nj", b.nj),
                             ("pitch", pitch[k]), ("gid", b.id), ("tiles_i", ti),
                             ("tiles_j", tjn), ("tile_begin", ntile),
-                            ("ntiles", ti * tjn),
+                            ("ntiles", nt),
                             ("nu_h2", nu_h2), ("adv_2h", adv_2h), ("h", b.h),
                             ("sxy_off", sxy_off), ("sxy_pitch", spitch)):
             table[name][k] = value
         table["face_off"][k] = -1
-        tile_block += [k] * (ti * tjn)
-        ntile += ti * tjn
+        tile_block += [k] * nt
+        ntile += nt
         padded = np.zeros((b.nj, spitch))
         padded[:, :b.ni] = forcing_table(b)
         sxy_parts.append(padded.ravel())
@@ -164,7 +181,7 @@ def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None,
 
     layout = RankLayout(planes=planes, blocks=owned, local_index=local_index, pitch=pitch, ps=ps,
                         rs=rs, base=base, slot_elems=slot_elems, tile_rows=tj, block_table=table,
-                        interleaved=inter,
+                        interleaved=inter, tile_pdes=tpd,
                         tile_block=np.asarray(tile_block, dtype=np.int32), total_tiles=ntile,
                         sxy=np.concatenate(sxy_parts), faces=np.zeros(0, native.FACE_TARGET_DTYPE),
                         prime_dirs=np.zeros(0, native.HALO_DIR_DTYPE),

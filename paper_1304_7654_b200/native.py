@@ -23,7 +23,8 @@ MAX_TEMPLATED_P = 17
 MAX_P = 127
 ROW_LEAD = 7
 STRIP = 64
-TILE_WARPS = NPDE * STRIP // 32
+TILE_WARPS = 8                # consumer warps per stage tile
+TILE_COLS = {4: 64, 1: 256}   # tile_pdes -> interior columns per strip
 ABI_VERSION = 1
 
 c_i32, c_i64, c_f64, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
@@ -59,7 +60,7 @@ class StageArgs(ctypes.Structure):
         ("blocks", c_vp), ("tile_block", c_vp), ("sxy", c_vp), ("faces", c_vp),
         ("norm_part", c_vp), ("status", c_vp), ("iter", c_vp), ("dmat", c_vp), ("tmaps", c_vp),
         ("nblocks", c_i32), ("total_tiles", c_i32), ("planes", c_i32), ("stage", c_i32),
-        ("tile_rows", c_i32), ("in_slot", c_i32), ("interleaved", c_i32), ("pad1", c_i32),
+        ("tile_rows", c_i32), ("in_slot", c_i32), ("interleaved", c_i32), ("tile_pdes", c_i32),
         ("coef", c_f64),
         ("D", c_f64 * (MAX_TEMPLATED_P * MAX_TEMPLATED_P)),
         ("ap", c_f64 * (MAX_P * NPDE))]
@@ -78,7 +79,7 @@ class EngineDesc(ctypes.Structure):
         ("recvs", ctypes.POINTER(PeerMsg)), ("nrecvs", c_i32),
         ("comm", c_vp), ("tmaps", c_vp),
         ("nblocks", c_i32), ("total_tiles", c_i32), ("planes", c_i32), ("nbody", c_i32),
-        ("tile_rows", c_i32), ("max_iters", c_i32), ("interleaved", c_i32), ("pad1", c_i32),
+        ("tile_rows", c_i32), ("max_iters", c_i32), ("interleaved", c_i32), ("tile_pdes", c_i32),
         ("coef", c_f64 * 4),
         ("D", c_f64 * (MAX_TEMPLATED_P * MAX_TEMPLATED_P)),
         ("ap", c_f64 * (MAX_P * NPDE))]
@@ -91,7 +92,7 @@ SIGNATURES = {
     "hbgpu_first_nonfinite": (c_i32, [c_vp] + [c_i64] * 4 + [c_vp, c_vp]),
     "hbgpu_stage": (c_i32, [ctypes.POINTER(StageArgs), c_vp]),
     "hbgpu_stage_prepare": (c_i32, [c_i32]),
-    "hbgpu_encode_tensor_maps": (c_i32, [c_vp * 3, c_vp, c_vp, c_i32, c_i32, c_vp, c_i64]),
+    "hbgpu_encode_tensor_maps": (c_i32, [c_vp * 3, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_i64]),
     "hbgpu_halo": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "hbgpu_norm_fold": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "hbgpu_forces": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp]),

@@ -251,6 +251,7 @@ class DeviceRank:
         blocks = np.ascontiguousarray(L.block_table)
         native.check(self.lib.hbgpu_encode_tensor_maps(slots, self.t_sxy.data_ptr(),
                                                        blocks.ctypes.data, n, self.planes,
+                                                       L.tile_pdes,
                                                        ctypes.addressof(host), len(host)),
                      "hbgpu_encode_tensor_maps")
         self.t_tmaps = self.torch.frombuffer(bytearray(host), dtype=self.torch.uint8).to(self.device)
@@ -281,7 +282,7 @@ class DeviceRank:
         d.tmaps = self.t_tmaps.data_ptr()
         d.nblocks, d.total_tiles, d.planes = len(L.blocks), L.total_tiles, self.planes
         d.nbody, d.tile_rows, d.max_iters = self.case.nbody, L.tile_rows, self.max_iters
-        d.interleaved = int(L.interleaved)
+        d.interleaved, d.tile_pdes = int(L.interleaved), int(L.tile_pdes)
         for k, c in enumerate(hbop.RKScheme(self.case.dtau).stage_coefficients()):
             d.coef[k] = c
         P = self.planes
@@ -338,6 +339,7 @@ class DeviceRank:
         a.nblocks, a.total_tiles, a.planes = d.nblocks, d.total_tiles, d.planes
         a.stage, a.tile_rows, a.coef = stage, d.tile_rows, d.coef[stage]
         a.tmaps, a.in_slot, a.interleaved = d.tmaps, self.STAGE_IN[stage], d.interleaved
+        a.tile_pdes = d.tile_pdes
         ctypes.memmove(ctypes.addressof(a.D), ctypes.addressof(d.D), ctypes.sizeof(a.D))
         ctypes.memmove(ctypes.addressof(a.ap), ctypes.addressof(d.ap), ctypes.sizeof(a.ap))
         return a
