@@ -404,9 +404,12 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
                 v[n] = rsub(base, rmul(coef, o[n]));
                 if (MODE == 1) v[n] = base;   // measurement variant: same traffic, no arithmetic
             }
-            if (FIRST) {
+            if (FIRST && live) {
+                // the residual norm is not a reference quantity (no bitwise
+                // contract; tolerance 1e-12 vs an exactly rounded sum), so it
+                // may use fused multiply-adds
 #pragma unroll
-                for (int n = 0; n < P; ++n) nrm = radd(nrm, live ? rmul(o[n], o[n]) : 0.0);
+                for (int n = 0; n < P; ++n) nrm = __fma_rn(o[n], o[n], nrm);
             }
 
             const int64_t row = (int64_t)j * b.rs;
