@@ -227,6 +227,7 @@ def run_ours(args, wl):
 
     from paper_1304_7654_b200 import RunSpec, native, run_case
     from paper_1304_7654_b200.cutplan import build_cut_plan
+    from paper_1304_7654_b200 import solver as solver_mod
     from paper_1304_7654_b200.solver import DeviceRank, make_comm
     from paper_1304_7654_b200.topology import build_topology, partition_blocks
 
@@ -336,6 +337,7 @@ def run_ours(args, wl):
                "h2d_bytes_per_step": h2d * world // args.steps,
                "d2h_bytes_per_step": d2h * world // args.steps,
                "wall_s": round(wall, 4),
+               "phases_s": {k: round(v, 4) for k, v in solver_mod.LAST_TIMINGS.items()},
                "note": "run_case(): layout + allocation + pinned H2D of the initial state + "
                        "K iterations + D2H of all fields (halos incl.) + forces/norms"}
 

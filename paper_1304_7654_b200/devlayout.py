@@ -27,7 +27,7 @@ import numpy as np
 
 from . import native
 from .cutplan import rank_routes
-from .hbop import forcing_table, stencil_coefficients
+from .hbop import forcing_vectors, stencil_coefficients
 
 ROW_LEAD = native.ROW_LEAD
 NPDE = native.NPDE
@@ -83,7 +83,8 @@ class RankLayout:
     block_table: np.ndarray
     tile_block: np.ndarray
     total_tiles: int
-    sxy: np.ndarray
+    sxy: list                       # per block (sin 2 pi x_i, sin 2 pi y_j)
+    sxy_size: int                   # elements of the device forcing-table pool
     faces: np.ndarray
     prime_dirs: np.ndarray
     unpack_dirs: np.ndarray
@@ -174,16 +175,16 @@ def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None,
         table["face_off"][k] = -1
         tile_block += [k] * nt
         ntile += nt
-        padded = np.zeros((b.nj, spitch))
-        padded[:, :b.ni] = forcing_table(b)
-        sxy_parts.append(padded.ravel())
+        # the (nj, sxy_pitch) forcing table is formed on the device from these
+        # two vectors (solver.DeviceRank): sxy[j, i] = sx[i] * sy[j]
+        sxy_parts.append(forcing_vectors(b))
         sxy_off += b.nj * spitch
 
     layout = RankLayout(planes=planes, blocks=owned, local_index=local_index, pitch=pitch, ps=ps,
                         rs=rs, base=base, slot_elems=slot_elems, tile_rows=tj, block_table=table,
                         interleaved=inter, tile_pdes=tpd,
                         tile_block=np.asarray(tile_block, dtype=np.int32), total_tiles=ntile,
-                        sxy=np.concatenate(sxy_parts), faces=np.zeros(0, native.FACE_TARGET_DTYPE),
+                        sxy=sxy_parts, sxy_size=sxy_off, faces=np.zeros(0, native.FACE_TARGET_DTYPE),
                         prime_dirs=np.zeros(0, native.HALO_DIR_DTYPE),
                         unpack_dirs=np.zeros(0, native.HALO_DIR_DTYPE),
                         force_segs=np.zeros(0, native.FORCE_SEG_DTYPE))
@@ -223,28 +224,30 @@ def _build_routes(layout, topology, plan, rank):
 
     # face-target pool: one entry per cell of every owned face that feeds a cut
     face_base = {}
-    pool = []
+    size = 0
     feeding = [(d, True) for d in routes.local] + [(d, False) for d in routes.sends]
     for d, _ in feeding:
         key = (d.src_block, d.src_face)
         if key not in face_base:
-            face_base[key] = len(pool)
-            pool += [(0, 0)] * blocks[d.src_block].face_extent(d.src_face)
+            face_base[key] = size
+            size += blocks[d.src_block].face_extent(d.src_face)
+    faces = np.zeros(size, dtype=native.FACE_TARGET_DTYPE)
     send_index = {id(d): k for k, d in enumerate(routes.sends)}
     for d, is_local in feeding:
         fb = face_base[(d.src_block, d.src_face)]
-        for e in range(d.length):
-            k = d.src_index(e)
-            if is_local:
-                hj, hi = _halo_cell(blocks[d.dst_block], d.dst_face, d.dst_index(e))
-                pool[fb + k - 1] = (layout.elem(d.dst_block, 0, 0, hj, hi),
-                                    layout.ps[layout.local_index[d.dst_block]])
-            else:
-                pool[fb + k - 1] = (send_off[send_index[id(d)]] + e * ds, -1)
-    faces = np.zeros(len(pool), dtype=native.FACE_TARGET_DTYPE)
-    if pool:
-        arr = np.asarray(pool, dtype=np.int64)
-        faces["off"], faces["ps"] = arr[:, 0], arr[:, 1]
+        e = np.arange(d.length, dtype=np.int64)
+        k = (d.src_hi - e) if d.src_reversed else (d.src_lo + e)      # source face index
+        if is_local:
+            kd = (d.dst_hi - e) if d.dst_reversed else (d.dst_lo + e)  # halo face index
+            spec = blocks[d.dst_block]
+            lb = layout.local_index[d.dst_block]
+            hj, hi = {"south": (0, kd), "north": (spec.nj + 1, kd), "west": (kd, 0),
+                      "east": (kd, spec.ni + 1)}[d.dst_face]
+            faces["off"][fb + k - 1] = layout.base[lb] + hj * layout.rs[lb] + ROW_LEAD + hi
+            faces["ps"][fb + k - 1] = layout.ps[lb]
+        else:
+            faces["off"][fb + k - 1] = send_off[send_index[id(d)]] + e * ds
+            faces["ps"][fb + k - 1] = -1
     layout.faces = faces
     from .topology import FACE_INDEX
     for (gid, face), fb in face_base.items():

@@ -8,9 +8,10 @@ inputs bit for bit on the same host.
 
 The forcing array of the reference, amp[n] * pfac[p] * sxy[j, i] evaluated
 left to right (hbcore.py:165-177), is stored factored as a per-(plane, pde)
-scalar ap[n][p] = amp[n] * pfac[p] and one (nj, ni) table sxy per block; the
-kernel forms ap * sxy with one rounded multiply, which reproduces the
-reference's array exactly, signed zeros included.
+scalar ap[n][p] = amp[n] * pfac[p] and, per block, the two vectors
+sin(2 pi x_i) and sin(2 pi y_j) whose rounded product is the reference's
+sxy[j, i]; the kernel forms sxy and then ap * sxy with one rounded multiply
+each, which reproduces the reference's array exactly, signed zeros included.
 """
 
 from __future__ import annotations
@@ -116,10 +117,18 @@ def forcing_amplitudes(planes, npde=NPDE):
     return np.ascontiguousarray(amp[:, None] * pfac[None, :])
 
 
-def forcing_table(spec):
-    """sxy[j, i] = sin(2 pi x_i) * sin(2 pi y_j) as the reference forms it."""
+def forcing_vectors(spec):
+    """(sin(2 pi x_i), sin(2 pi y_j)): the two factors of the forcing table."""
     xc, yc = cell_centres(spec)
-    return np.ascontiguousarray(np.sin(TWO_PI * xc)[None, :] * np.sin(TWO_PI * yc)[:, None])
+    return np.sin(TWO_PI * xc), np.sin(TWO_PI * yc)
+
+
+def forcing_table(spec):
+    """sxy[j, i] = sin(2 pi x_i) * sin(2 pi y_j) as the reference forms it
+    (hbcore.py:169): one rounded product per element, which the stage
+    kernel recomputes from forcing_vectors instead of storing the table."""
+    sx, sy = forcing_vectors(spec)
+    return np.ascontiguousarray(sx[None, :] * sy[:, None])
 
 
 def forcing_values(spec, planes, npde=NPDE):

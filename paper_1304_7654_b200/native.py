@@ -16,7 +16,8 @@ import numpy as np
 from .exceptions import NativeUnavailable
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libhbgpu.so")
+# HBGPU_LIB selects another build of the library (A/B measurements)
+LIB_PATH = os.environ.get("HBGPU_LIB") or os.path.join(PKG_DIR, "libhbgpu.so")
 
 NPDE = 4
 MAX_TEMPLATED_P = 17

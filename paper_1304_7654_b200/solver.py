@@ -37,6 +37,9 @@ from .exceptions import DivergenceError, ProtocolError
 from .topology import build_topology, partition_blocks
 
 NO_BAD = (1 << 64) - 1
+# phase wall times (s) of the last single-GPU run_case: layout, alloc,
+# upload, engine, compute, download
+LAST_TIMINGS = {}
 LIN_BITS = 40
 
 
@@ -163,7 +166,9 @@ class DeviceRank:
         self.comm = comm
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         torch.cuda.set_device(self.device)
+        t0 = time.perf_counter()
         L = self.layout = build_rank_layout(topology, partition, plan, rank, case.planes, tile_rows)
+        self.timings = {"layout": time.perf_counter() - t0}
         dev = self.device
         f64 = torch.float64
         self.slots = [torch.zeros(L.slot_elems, dtype=f64, device=dev) for _ in range(3)]
@@ -178,7 +183,14 @@ class DeviceRank:
 
         self.t_blocks = table(L.block_table)
         self.t_tiles = torch.from_numpy(L.tile_block).to(dev)
-        self.t_sxy = torch.from_numpy(L.sxy).to(dev)
+        # forcing tables sxy[j, i] = sx[i] * sy[j], formed on the device (one
+        # rounded product per element, as hbcore.py:169 forms it)
+        self.t_sxy = torch.zeros(max(1, L.sxy_size), dtype=f64, device=dev)
+        for k, (sx, sy) in enumerate(L.sxy):
+            off, sp = int(L.block_table["sxy_off"][k]), int(L.block_table["sxy_pitch"][k])
+            tbl = self.t_sxy[off:off + sy.size * sp].view(sy.size, sp)
+            tbl[:, :sx.size] = (torch.from_numpy(sx).to(dev)[None, :] *
+                                torch.from_numpy(sy).to(dev)[:, None])
         self.t_faces = table(L.faces)
         self.t_prime = table(L.prime_dirs)
         self.t_unpack = table(L.unpack_dirs)
@@ -195,9 +207,15 @@ class DeviceRank:
         self.iter = torch.zeros(1, dtype=torch.int32, device=dev)
         nforce = 3 * case.planes * case.nbody
         self.force_hist = torch.zeros(max(1, self.max_iters * nforce), dtype=f64, device=dev)
+        torch.cuda.synchronize(dev)
+        t1 = time.perf_counter()
         self.upload_initial(initial, pinned_ic)
+        torch.cuda.synchronize(dev)
+        t2 = time.perf_counter()
         self._encode_tensor_maps()
         self._make_engine()
+        self.timings.update(alloc=t1 - t0 - self.timings["layout"], upload=t2 - t1,
+                            engine=time.perf_counter() - t2)
 
     # -- state in / out --------------------------------------------------------
 
@@ -515,15 +533,21 @@ def _execute_single(spec, topology, partition, plan, iterations):
     device = spec.device if spec.device is not None else torch.cuda.current_device()
     dr = _new_rank(spec, topology, partition, plan, 0, device, None, iterations)
     try:
+        torch.cuda.synchronize(dr.device)
+        t0 = time.perf_counter()
         dr.prime()
         if iterations > 0:
             dr.iterate(iterations, use_graph=spec.use_graph)
         torch.cuda.synchronize(dr.device)
+        t1 = time.perf_counter()
         raise_divergence(dr.divergence())
         fields = dr.fields(0, pinned_out=spec.output)
         hist = _history(dr, iterations)
         norms = dr.norm_history(iterations)
         torch.cuda.synchronize(dr.device)
+        dr.timings.update(compute=t1 - t0, download=time.perf_counter() - t1)
+        LAST_TIMINGS.clear()
+        LAST_TIMINGS.update(dr.timings)
     finally:
         dr.close()
     return fields, hist, norms

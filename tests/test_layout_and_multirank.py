@@ -72,6 +72,9 @@ def test_layout_alignment_and_tiles():
         t = L.block_table[k]
         assert t["ntiles"] == t["tiles_i"] * t["tiles_j"]
         assert t["sxy_off"] % 4 == 0 and t["sxy_pitch"] >= b.ni
+        sx, sy = L.sxy[k]
+        from paper_1304_7654_b200.hbop import forcing_table
+        assert np.array_equal(sx[None, :] * sy[:, None], forcing_table(b))
     assert len(L.tile_block) == L.total_tiles == sum(int(t) for t in L.block_table["ntiles"])
     # every face cell on a cut has exactly one target; others none
     assert np.count_nonzero(L.faces["ps"]) == sum(2 * c.length for c in topo.cuts)
