@@ -4,12 +4,15 @@ Pure host logic (numpy only), so it is unit-tested on CPU.  For the blocks a
 rank owns it fixes:
 
 * the slot layout: block b's value (n, p, j, i) at element
-  base_b + (n*4 + p)*ps_b + j*pitch_b + ROW_LEAD + i, rows padded to a
+  base_b + (n*4 + p)*ps_b + j*rs_b + ROW_LEAD + i, rows padded to a
   multiple of 8 doubles and ROW_LEAD = 7 so every interior row -- and every
-  64-column strip -- starts on a 64-byte DRAM granule; block bases are
-  256-byte aligned.  Three slots (A, B, C) share the layout;
-* the stage tiles: one tile = one CTA's 64-column strip over tile_rows rows
-  of one block (8 consumer warps: 2 per pde); tile t of block b is strip
+  strip -- starts on a 64-byte DRAM granule; block bases are 256-byte
+  aligned.  Row-interleaved (default): ps = pitch, rs = 4*P*pitch;
+  plane-major (HBGPU_LAYOUT=plane): ps = (nj+2)*pitch, rs = pitch.
+  Three slots (A, B, C) share the layout;
+* the stage tiles: one tile = one CTA's strip over tile_rows rows of one
+  block -- 64 columns x 4 pdes (tile_pdes 4) or 256 columns x 1 pde
+  (tile_pdes 1, every block ni >= WIDE_MIN_NI); tile t of block b is strip
   t % tiles_i, row tile t / tiles_i;
 * the face-target pool (fused halo forwarding, see cutplan.py);
 * the standalone halo directions (priming exchange / pack / unpack);
