@@ -390,12 +390,20 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
             }
             // D[n][n] == 0 and the zero-amplitude forcing planes add a signed
             // zero: add_signed_zero reproduces that rounding step exactly on
-            // the integer pipe (see hb_common.cuh)
+            // the integer pipe (see hb_common.cuh).  D is a circulant,
+            // exactly antisymmetric matrix (D[m+k][m] == -D[m-k][m] bit for
+            // bit, checked on the host), so column m's product for row m+k
+            // is, negated, row m-k's: one DMUL feeds a DADD and a DSUB with
+            // the reference's rounding (x + (-y) == x - y, (-d) y == -(d y)).
 #pragma unroll
             for (int m = 0; m < P; ++m) {
+                o[m] = add_signed_zero(o[m], cur[m]);
 #pragma unroll
-                for (int n = 0; n < P; ++n)
-                    o[n] = (m == n) ? add_signed_zero(o[n], cur[m]) : radd(o[n], rmul(a.D[n * P + m], cur[m]));
+                for (int k = 1; k <= P / 2; ++k) {
+                    const double prod = rmul(a.D[((m + k) % P) * P + m], cur[m]);
+                    o[(m + k) % P] = radd(o[(m + k) % P], prod);
+                    o[(m + P - k) % P] = rsub(o[(m + P - k) % P], prod);
+                }
             }
 #pragma unroll
             for (int n = 0; n < P; ++n) {
@@ -590,9 +598,31 @@ static int launch_p(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only
     return a.tile_pdes == 1 ? launch_cfg<P, 1, 0>(a, s, prepare_only) : launch_cfg<P, 4, 0>(a, s, prepare_only);
 }
 
+// The templated kernel shares each D product between rows m+k and m-k; that
+// is exact only for the spectral matrix's bitwise antisymmetric circulant
+// structure (hbcore.py:88-94 wraps d into [-N_H, N_H], so D[d] = -D[-d]).
+static bool circulant_antisymmetric(const double *D, int P) {
+    for (int m = 0; m < P; ++m) {
+        uint64_t diag;
+        memcpy(&diag, D + m * P + m, 8);
+        if (diag != 0) return false;
+        for (int k = 1; k <= P / 2; ++k) {
+            uint64_t x, y;
+            memcpy(&x, D + ((m + k) % P) * P + m, 8);
+            memcpy(&y, D + ((m + P - k) % P) * P + m, 8);
+            if (x != (y ^ 0x8000000000000000ull)) return false;
+        }
+    }
+    return true;
+}
+
 static int dispatch(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
     if (a.tile_pdes != 1 && a.tile_pdes != 4) {
         hbgpu_set_error("hbgpu_stage: tile_pdes must be 1 or 4, got %d", a.tile_pdes);
+        return HBGPU_ERR_ARG;
+    }
+    if (!prepare_only && a.planes <= HBGPU_MAX_TEMPLATED_P && !circulant_antisymmetric(a.D, a.planes)) {
+        hbgpu_set_error("hbgpu_stage: D must be the spectral matrix (+0.0 diagonal, D[m+k][m] == -D[m-k][m])");
         return HBGPU_ERR_ARG;
     }
     switch (a.planes) {

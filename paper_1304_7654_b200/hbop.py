@@ -68,6 +68,27 @@ def spectral_matrix(nharms, omega):
     return SpectralDeriv(matrix=mat, omega=omega, nharms=nharms)
 
 
+def circulant_antisymmetric(mat):
+    """True when D[(m+k)%P][m] is bitwise -D[(m-k)%P][m] and the diagonal is +0.0.
+
+    spectral_matrix has this structure exactly (the wrapped d of ref
+    hbcore.py:88-94 makes D a function of d with D(-d) = -D(d)); the stage
+    kernel relies on it to share one product between two rows.
+    """
+    mat = np.ascontiguousarray(mat, dtype=np.float64)
+    size = mat.shape[0]
+    bits = mat.view(np.uint64)
+    idx = np.arange(size)
+    if np.any(bits[idx, idx] != 0):
+        return False
+    for k in range(1, size // 2 + 1):
+        plus = bits[(idx + k) % size, idx]
+        minus = bits[(idx - k) % size, idx]
+        if np.any(plus != (minus ^ np.uint64(1 << 63))):
+            return False
+    return True
+
+
 @dataclass(frozen=True)
 class RKScheme:
     """q_s = q_0 - alpha_s dtau R(q_{s-1}), alphas (1/4, 1/3, 1/2, 1)."""

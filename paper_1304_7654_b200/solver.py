@@ -312,6 +312,10 @@ class DeviceRank:
         unforced = [n for n in range(P) if n not in (1, 2)]
         if np.any(diag.view(np.uint64) != 0) or np.any(self.ap[unforced].view(np.uint64) != 0):
             raise ValueError("operator tables break the +0.0 diagonal / planes-1,2 forcing invariant")
+        # ... and shares each D product between rows m+k and m-k (exact for
+        # the spectral matrix's bitwise antisymmetric circulant structure)
+        if P <= native.MAX_TEMPLATED_P and not hbop.circulant_antisymmetric(self.dmat):
+            raise ValueError("D is not bitwise antisymmetric circulant (D[m+k][m] == -D[m-k][m])")
         if P <= native.MAX_TEMPLATED_P:
             flat = self.dmat.ravel()
             for k in range(P * P):

@@ -148,6 +148,21 @@ def test_spectral_antisymmetric_exactly_and_row_sums():
             assert np.abs(d.sum(axis=1)).max() <= 1e-14
 
 
+def test_spectral_circulant_structure_the_stage_kernel_shares_products_on():
+    """The fused stage kernel computes D[m+k][m]*q[m] once and subtracts it for
+    row m-k: exact only if the reference's D is bitwise antisymmetric circulant."""
+    from paper_1304_7654_b200.hbop import circulant_antisymmetric
+    for nh in range(64):
+        for omega in (1.0, 0.12, 2.3, 1e-3):
+            assert circulant_antisymmetric(spectral_matrix(nh, omega).matrix)
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "kernels.npz"))
+    for key in ("p3/dmat", "p5/dmat", "p9/dmat"):       # the reference's own matrices
+        assert circulant_antisymmetric(gold[key])
+    bent = spectral_matrix(4, 1.0).matrix.copy()
+    bent[3, 1] = np.nextafter(bent[3, 1], 9.0)
+    assert not circulant_antisymmetric(bent)
+
+
 @pytest.mark.parametrize("nharms", range(1, 9))
 def test_spectral_derivative_vs_fft(nharms):
     omega = 2.3
