@@ -164,8 +164,8 @@ typedef struct hbgpu_stage_args {
     unsigned long long *status;/* device [nblocks] divergence keys         */
     const int32_t *iter;       /* device iteration counter                 */
     const double *dmat;        /* device P*P (generic kernel only)         */
-    const void *tmaps;         /* device [4][nblocks] CUtensorMap
-                                  (hbgpu_encode_tensor_maps)               */
+    const void *tmaps;         /* device [HBGPU_TMAP_SETS][nblocks]
+                                  CUtensorMap (hbgpu_encode_tensor_maps)    */
     int32_t nblocks;
     int32_t total_tiles;
     int32_t planes;
@@ -176,6 +176,8 @@ typedef struct hbgpu_stage_args {
     int32_t interleaved;       /* 1 = row-interleaved slot layout          */
     int32_t tile_pdes;         /* pdes per tile: 4 (64-col strips) or 1
                                   (256-col strips)                          */
+    int32_t out_slot;          /* which of the three slots `out` is (0..2) */
+    int32_t pad0;
     double coef;               /* alpha_s * dtau                            */
     /* D row-major P x P with a +0.0 diagonal (hbcore.py:88-94); ap[n*4 + p]
      * = amp[n] (1 + p/4), zero except on planes 1 and 2 (hbcore.py:170-175):
@@ -199,8 +201,12 @@ int hbgpu_stage_prepare(int32_t planes);
  * memory, 64-B aligned): sets 0..2 = stencil boxes (strip + 2 halo columns
  * each side, split in two boxes when wider than TMA's 256) over slot[0..2],
  * set 3 = strip-wide q0 box over slot[0], set 4 = 2-D (column, row)
- * strip-wide box over the block's sxy forcing table.  tile_pdes (4 or 1)
- * fixes the strip geometry.  out_bytes >= 5*nblocks*128.                   */
+ * strip-wide box over the block's sxy forcing table, sets 5..7 = strip-wide
+ * store boxes over slot[0..2] whose column extent ends at cell ni (the
+ * store clips the strip's columns past the block and never touches the
+ * halo ring).  tile_pdes (4 or 1) fixes the strip geometry.
+ * out_bytes >= HBGPU_TMAP_SETS*nblocks*128.                                 */
+#define HBGPU_TMAP_SETS 8
 int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy,
                              const hbgpu_block *blocks_host,
                              int32_t nblocks, int32_t planes, int32_t tile_pdes,

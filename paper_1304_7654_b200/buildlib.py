@@ -57,7 +57,9 @@ def build(force=False, verbose=False):
     logs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [nvcc, *ARCH_FLAGS, *NVCC_FLAGS, *inc, "-c", src, "-o", obj]
+        # HBGPU_NVCC_EXTRA: extra flags for measurement builds (e.g. -D overrides)
+        extra = os.environ.get("HBGPU_NVCC_EXTRA", "").split()
+        cmd = [nvcc, *ARCH_FLAGS, *NVCC_FLAGS, *extra, *inc, "-c", src, "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         logs.append(res.stdout + res.stderr)
         if res.returncode != 0:

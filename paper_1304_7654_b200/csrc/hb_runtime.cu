@@ -209,6 +209,7 @@ int run_stage(hbgpu_engine *e, int st, cudaStream_t s) {
     a.out = d.slot[kOut[st]];
     a.stage = st;
     a.in_slot = kIn[st];
+    a.out_slot = kOut[st];
     a.interleaved = d.interleaved;
     a.tile_pdes = d.tile_pdes;
     a.coef = d.coef[st];

@@ -92,6 +92,19 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const void *map, int c0, 
         "l"(map), "r"(c0), "r"(c1), "r"(saddr(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_store_4d(const void *map, int c0, int c1, int c2, int c3, const void *src) {
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(map),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(saddr(src))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// wait until every committed bulk store has finished READING shared memory
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// make this thread's generic-proxy shared-memory writes visible to TMA
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 __device__ __forceinline__ void prefetch_tmap(const void *map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -99,7 +112,15 @@ __device__ __forceinline__ void prefetch_tmap(const void *map) {
 // ---- geometry ---------------------------------------------------------------------
 
 constexpr int CW = HBGPU_TILE_WARPS;            // consumer warps per tile
-constexpr int THREADS = (CW + 1) * 32;          // + one producer warp
+constexpr int THREADS = (CW + 2) * 32;          // + one TMA load warp + one TMA store warp
+// Output rows of the update stages leave by TMA store from the q0 slot they
+// replace.  The first stage is fp64-issue bound: its plain stores cost less
+// than staging + proxy fence, so NOUT = 0 keeps them (a measurement build can
+// set HBGPU_FIRST_STAGING=2 to stage its rows in two extra slots).
+#ifndef HBGPU_FIRST_STAGING
+#define HBGPU_FIRST_STAGING 0
+#endif
+constexpr int NOUT = HBGPU_FIRST_STAGING;
 
 // Tile geometry for PT pdes per tile (4 or 1).
 template <int PT>
@@ -121,10 +142,21 @@ struct Smem {
     static constexpr int SLOT = SXY + G::TCOLS;                          // stencil slot
     static constexpr int QSLOT = P * PT * G::TCOLS;                      // q0 slot
     static constexpr int NQ = FIRST ? 0 : Q;
-    static constexpr size_t BAR_OFF = ((size_t)R * SLOT + (size_t)NQ * QSLOT) * 8;
-    static constexpr size_t BYTES = BAR_OFF + (size_t)2 * (R + NQ) * 8;
+    // output rows are staged for the TMA store in the q0 slot they replace;
+    // the first stage has no q0 ring: NOUT own slots, or plain stores
+    static constexpr int NO = FIRST ? NOUT : 0;
+    static constexpr int NS = FIRST ? NO : NQ;   // staging slots (either kind)
+    static constexpr size_t BAR_OFF = ((size_t)R * SLOT + (size_t)(NQ + NO) * QSLOT) * 8;
+    static constexpr size_t BYTES = BAR_OFF + (size_t)(2 * (R + NQ) + NS + NO) * 8;
     static_assert((SLOT * 8) % 128 == 0 && (QSLOT * 8) % 128 == 0, "TMA slots need 128-B alignment");
 };
+
+// Interior columns 1..store_cols(ni) of a row go out by TMA store; the rest
+// (at most 7, ni not a multiple of 8) by plain stores.  The store tensor map
+// ends on a 64-B boundary: a bulk store may write whole granules, and the
+// granule holding cell ni also holds the east halo cell ni+1, which the
+// neighbouring block's tile forwards into concurrently.
+__host__ __device__ __forceinline__ int store_cols(int ni) { return ni / 8 * 8; }
 
 // ---- tiles and halo targets -------------------------------------------------
 
@@ -215,6 +247,10 @@ __device__ __forceinline__ void load_rows(void *dst, const void *map, int x, int
     if (inter) tma_load_4d(dst, map, x, pde0, 0, row, bar);
     else tma_load_4d(dst, map, x, row, pde0, 0, bar);
 }
+__device__ __forceinline__ void store_rows(const void *map, const void *src, int x, int pde0, int row, bool inter) {
+    if (inter) tma_store_4d(map, x, pde0, 0, row, src);
+    else tma_store_4d(map, x, row, pde0, 0, src);
+}
 
 // ---- the pipelined kernel -----------------------------------------------------------
 
@@ -226,10 +262,13 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
     extern __shared__ __align__(1024) unsigned char smem[];
     double *ring = reinterpret_cast<double *>(smem);
     double *qring = ring + R * S::SLOT;
+    double *oring = qring + S::NQ * S::QSLOT;    // first stage: output staging
     uint64_t *full_in = reinterpret_cast<uint64_t *>(smem + S::BAR_OFF);
     uint64_t *empty_in = full_in + R;
     uint64_t *full_q = empty_in + R;
-    uint64_t *empty_q = full_q + S::NQ;
+    uint64_t *empty_q = full_q + S::NQ;          // q0 slot stored out and free
+    uint64_t *staged = empty_q + S::NQ;          // output row written to smem
+    uint64_t *out_free = staged + S::NS;         // first stage: staging slot free
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -239,8 +278,10 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
         }
         for (int k = 0; k < S::NQ; ++k) {
             mbar_init(full_q + k, 1);
-            mbar_init(empty_q + k, CW);
+            mbar_init(empty_q + k, 1);
         }
+        for (int k = 0; k < S::NS; ++k) mbar_init(staged + k, CW * 32);
+        for (int k = 0; k < S::NO; ++k) mbar_init(out_free + k, 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -290,6 +331,32 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
         }
         return;
     }
+    constexpr bool TSTORE = !FIRST || S::NO > 0;   // rows leave by TMA store
+    if (warp == CW + 1) {
+        if (!TSTORE) return;
+        // ------------------------------ store warp ------------------------------
+        // one TMA store per output row once all consumer threads have staged
+        // it; the staging slot is handed back (to the q0 loads, or to the
+        // consumers in the first stage) when the store has read it
+        if (lane != 0) return;
+        RingPos ps{0, 0};
+        for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+            const Tile tl = decode_tile<PT>(a, t);
+            const CUtensorMap *mo = maps + (5 + a.out_slot) * a.nblocks + tl.bidx;
+            prefetch_tmap(mo);
+            for (int j = tl.j0; j <= tl.j1; ++j) {
+                mbar_wait(staged + ps.slot, ps.phase);
+                const double *src = FIRST ? oring + ps.slot * S::QSLOT : qring + ps.slot * S::QSLOT;
+                store_rows(mo, src, tl.i0 + LEAD, tl.pde0, j, inter);
+                bulk_commit();
+                bulk_wait_read_all();
+                mbar_arrive(FIRST ? out_free + ps.slot : empty_q + ps.slot);
+                ps = advance<S::NS>(ps);
+            }
+        }
+        bulk_wait_all();
+        return;
+    }
 
     // -------------------------------- consumers ---------------------------------
     const int pp = warp % PT;                     // pde within the tile
@@ -300,7 +367,8 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
     const int q_off = pp * G::TCOLS + col0;
     const int gstage = (*a.iter) * 4 + a.stage + 1;
     const double coef = a.coef;
-    RingPos cin{0, 0}, cq{0, 0};
+    RingPos cin{0, 0}, cq{0, 0}, co{0, 0};
+    int used_out = 0;   // first stage: staging slots handed out so far (saturates)
     int ap_pde = -1;
     double ap[P];
     for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
@@ -314,11 +382,13 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
         // by value: the output stores must not force re-reads of the descriptor
         const hbgpu_block b = a.blocks[tl.bidx];
         const int ni = b.ni, nj = b.nj;
-        const int64_t ps4 = b.ps * NPDE;
         const double nu_h2 = b.nu_h2, adv_2h = b.adv_2h;
         const int i = tl.i0 + col0;
         const bool live = i <= ni;
-        double *const out = a.out + b.base + (int64_t)p * b.ps + LEAD + i;
+        // plain stores: columns past the TMA store extent, or every column
+        const bool tail = live && (!TSTORE || i > store_cols(ni));
+        double *const tail_out = a.out + b.base + (int64_t)p * b.ps + LEAD + i;
+        const int64_t ps4 = b.ps * NPDE;
 
         FaceHit trow, tcol;
         cell_targets(a.faces, b, i, tl.j0, live, trow, tcol);
@@ -420,10 +490,27 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
                 for (int n = 0; n < P; ++n) nrm = __fma_rn(o[n], o[n], nrm);
             }
 
-            const int64_t row = (int64_t)j * b.rs;
-            if (live) {
+            if (TSTORE) {
+                // stage the output row for the TMA store: in place of the q0
+                // row it replaces, or (first stage) in an output staging slot
+                double *stage_row;
+                if (FIRST) {
+                    if (used_out >= S::NO) mbar_wait(out_free + co.slot, co.phase ^ 1u);
+                    else ++used_out;
+                    stage_row = oring + co.slot * S::QSLOT + q_off;
+                } else {
+                    stage_row = qring + cq.slot * S::QSLOT + q_off;
+                }
 #pragma unroll
-                for (int n = 0; n < P; ++n) out[n * ps4 + row] = v[n];
+                for (int n = 0; n < P; ++n) stage_row[n * PT * G::TCOLS] = v[n];
+                fence_proxy_async_smem();
+                mbar_arrive(staged + (FIRST ? co.slot : cq.slot));
+                if (FIRST) co = advance<S::NO>(co);
+            }
+            const int64_t row = (int64_t)j * b.rs;
+            if (tail) {
+#pragma unroll
+                for (int n = 0; n < P; ++n) tail_out[n * ps4 + row] = v[n];
             }
             if (trow.ps != 0) {
 #pragma unroll
@@ -451,10 +538,7 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
             trow = nrow;
             tcol = ncol;
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(empty_in + cin.slot);   // row j no longer read
-                if (!FIRST) mbar_arrive(empty_q + cq.slot);
-            }
+            if (lane == 0) mbar_arrive(empty_in + cin.slot);   // row j no longer read
             cin = nx;
             if (!FIRST) cq = advance<Q>(cq);
         }
@@ -555,7 +639,18 @@ static int prepare(Launch &L) {
 // Ring depths per snapshot count: R stencil rows for the update stages, RF
 // for the first stage (no q0 ring, so its rows go deeper), Q q0 rows.  One
 // CTA (8 consumer warps) per SM; the smem budget is ~227 KB.
-template <int P> struct Depth { static constexpr int R = 4, RF = 7, Q = 3; };
+#ifndef HBGPU_DEPTH_R   // measurement builds may override the default depths
+#define HBGPU_DEPTH_R 4
+#endif
+#ifndef HBGPU_DEPTH_RF
+#define HBGPU_DEPTH_RF 7
+#endif
+#ifndef HBGPU_DEPTH_Q
+#define HBGPU_DEPTH_Q 3
+#endif
+template <int P> struct Depth {
+    static constexpr int R = HBGPU_DEPTH_R, RF = HBGPU_DEPTH_RF, Q = HBGPU_DEPTH_Q;
+};
 template <> struct Depth<1> { static constexpr int R = 8, RF = 12, Q = 6; };
 template <> struct Depth<3> { static constexpr int R = 8, RF = 12, Q = 6; };
 template <> struct Depth<5> { static constexpr int R = 6, RF = 10, Q = 5; };
@@ -700,7 +795,7 @@ extern "C" int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy
                                         int32_t nblocks, int32_t planes, int32_t tile_pdes, void *out_host,
                                         int64_t out_bytes) {
     using namespace hbgpu;
-    if ((int64_t)sizeof(CUtensorMap) * 5 * nblocks > out_bytes || planes < 1 || planes > 256 ||
+    if ((int64_t)sizeof(CUtensorMap) * HBGPU_TMAP_SETS * nblocks > out_bytes || planes < 1 || planes > 256 ||
         (tile_pdes != 1 && tile_pdes != 4)) {
         hbgpu_set_error("hbgpu_encode_tensor_maps: output too small, bad planes or tile_pdes");
         return HBGPU_ERR_ARG;
@@ -723,22 +818,28 @@ extern "C" int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy
     const cuuint32_t bw = tile_pdes == 1 ? Geo<1>::BW : Geo<4>::BW;
     CUtensorMap *maps = reinterpret_cast<CUtensorMap *>(out_host);
     // sets 0..2: stencil boxes over slots 0..2; set 3: q0 box over slot 0;
-    // set 4: 2-D sxy table box (strip columns x 1 row)
-    for (int s = 0; s < 5; ++s) {
+    // set 4: 2-D sxy table box (strip columns x 1 row); sets 5..7: store
+    // boxes over slots 0..2, column extent clipped after cell ni
+    for (int s = 0; s < HBGPU_TMAP_SETS; ++s) {
         for (int k = 0; k < nblocks; ++k) {
             const hbgpu_block &b = blocks[k];
             CUresult r;
-            if (s < 4) {
+            if (s != 4) {
                 // dimension order follows the layout so the strides nest:
                 // plane-major (cols, rows, pde, plane), interleaved (cols, pde,
                 // plane, rows); both land in smem as [plane][pde][cols]
                 const bool inter = b.rs > b.ps;
                 const cuuint32_t w = s < 3 ? bw : tcols;
                 const cuuint32_t npd = (cuuint32_t)tile_pdes;
+                // store extent: columns up to store_cols(ni), a 64-B boundary,
+                // so no store granule reaches the east halo cell (the kernel
+                // writes the <= 7 columns past it with plain stores)
+                const cuuint64_t cols = s >= 5 ? (cuuint64_t)(LEAD + 1 + store_cols(b.ni)) : (cuuint64_t)b.pitch;
+                const int slot_k = s < 3 ? s : s == 3 ? 0 : s - 5;
                 cuuint64_t dims[4], strides[3];
                 cuuint32_t box[4];
                 if (inter) {
-                    cuuint64_t d[4] = {(cuuint64_t)b.pitch, (cuuint64_t)NPDE, (cuuint64_t)planes,
+                    cuuint64_t d[4] = {cols, (cuuint64_t)NPDE, (cuuint64_t)planes,
                                        (cuuint64_t)(b.nj + 2)};
                     cuuint64_t st[3] = {(cuuint64_t)b.ps * 8, (cuuint64_t)b.ps * 8 * NPDE, (cuuint64_t)b.rs * 8};
                     cuuint32_t bx[4] = {w, npd, (cuuint32_t)planes, 1};
@@ -746,7 +847,7 @@ extern "C" int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy
                     memcpy(strides, st, sizeof(st));
                     memcpy(box, bx, sizeof(bx));
                 } else {
-                    cuuint64_t d[4] = {(cuuint64_t)b.pitch, (cuuint64_t)(b.nj + 2), (cuuint64_t)NPDE,
+                    cuuint64_t d[4] = {cols, (cuuint64_t)(b.nj + 2), (cuuint64_t)NPDE,
                                        (cuuint64_t)planes};
                     cuuint64_t st[3] = {(cuuint64_t)b.rs * 8, (cuuint64_t)b.ps * 8, (cuuint64_t)b.ps * 8 * NPDE};
                     cuuint32_t bx[4] = {w, 1, npd, (cuuint32_t)planes};
@@ -756,7 +857,7 @@ extern "C" int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy
                 }
                 cuuint32_t estr[4] = {1, 1, 1, 1};
                 r = fn(&maps[s * nblocks + k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
-                       (void *)(slot[s < 3 ? s : 0] + b.base), dims, strides, box, estr,
+                       (void *)(slot[slot_k] + b.base), dims, strides, box, estr,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             } else {

@@ -27,6 +27,7 @@ STRIP = 64
 TILE_WARPS = 8                # consumer warps per stage tile
 TILE_COLS = {4: 64, 1: 256}   # tile_pdes -> interior columns per strip
 ABI_VERSION = 1
+TMAP_SETS = 8                  # tensor-map sets per block (hbgpu_encode_tensor_maps)
 
 c_i32, c_i64, c_f64, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
 
@@ -62,7 +63,7 @@ class StageArgs(ctypes.Structure):
         ("norm_part", c_vp), ("status", c_vp), ("iter", c_vp), ("dmat", c_vp), ("tmaps", c_vp),
         ("nblocks", c_i32), ("total_tiles", c_i32), ("planes", c_i32), ("stage", c_i32),
         ("tile_rows", c_i32), ("in_slot", c_i32), ("interleaved", c_i32), ("tile_pdes", c_i32),
-        ("coef", c_f64),
+        ("out_slot", c_i32), ("pad0", c_i32), ("coef", c_f64),
         ("D", c_f64 * (MAX_TEMPLATED_P * MAX_TEMPLATED_P)),
         ("ap", c_f64 * (MAX_P * NPDE))]
 

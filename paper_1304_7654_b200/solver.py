@@ -261,10 +261,10 @@ class DeviceRank:
     # -- engine ----------------------------------------------------------------
 
     def _encode_tensor_maps(self):
-        """TMA descriptors (4 sets x blocks, 128 B each), uploaded to the device."""
+        """TMA descriptors (TMAP_SETS sets x blocks, 128 B each), uploaded to the device."""
         L = self.layout
         n = len(L.blocks)
-        host = (ctypes.c_ubyte * (5 * n * 128))()
+        host = (ctypes.c_ubyte * (native.TMAP_SETS * n * 128))()
         slots = (ctypes.c_void_p * 3)(*[s.data_ptr() for s in self.slots])
         blocks = np.ascontiguousarray(L.block_table)
         native.check(self.lib.hbgpu_encode_tensor_maps(slots, self.t_sxy.data_ptr(),
@@ -361,6 +361,7 @@ class DeviceRank:
         a.nblocks, a.total_tiles, a.planes = d.nblocks, d.total_tiles, d.planes
         a.stage, a.tile_rows, a.coef = stage, d.tile_rows, d.coef[stage]
         a.tmaps, a.in_slot, a.interleaved = d.tmaps, self.STAGE_IN[stage], d.interleaved
+        a.out_slot = self.STAGE_OUT[stage]
         a.tile_pdes = d.tile_pdes
         ctypes.memmove(ctypes.addressof(a.D), ctypes.addressof(d.D), ctypes.sizeof(a.D))
         ctypes.memmove(ctypes.addressof(a.ap), ctypes.addressof(d.ap), ctypes.sizeof(a.ap))

@@ -69,6 +69,18 @@ def test_baseline_workloads_match_oracle(key, iters, cuda, oracle_mod):
     assert_parity(got, want, key)
 
 
+@pytest.mark.parametrize("ni", [5, 41, 42, 43, 44, 45, 46, 47, 48, 193, 199, 255, 256, 257, 263])
+def test_ragged_widths_match_oracle(ni, cuda, oracle_mod):
+    """Every residue of ni mod 8 at both strip geometries (64 x 4 pdes below
+    192 columns, 256 x 1 above): the TMA store extent ends on the 64-B boundary
+    at or before cell ni, and the forwarded east halo cell ni+1 -- in the same
+    granule as cell ni when ni % 8 != 0 -- must survive every stage."""
+    case = ring_case(2, ni, 5, 1, h=0.05, dtau=0.0005, nbody=1, bodies=((1, "south", 0),))
+    got = run_case(RunSpec(case=case, ranks=1, iterations=3))
+    want = oracle_mod.run(case, 3)
+    assert_parity(got, want, f"ring2-ni{ni}")
+
+
 def test_graph_and_eager_identical(cuda):
     case = tc2_mini()
     a = run_case(RunSpec(case=case, ranks=1, iterations=3, use_graph=True))
