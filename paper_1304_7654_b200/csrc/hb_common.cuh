@@ -44,18 +44,19 @@ __device__ __forceinline__ unsigned long long divergence_key(int gstage, long lo
 
 __device__ __forceinline__ bool nonfinite(double v) { return !isfinite(v); }
 
-// radd(o, rmul(0.0, x)) for finite x, without touching the fp64 pipe.
-// 0*x is +0 when x's sign bit is clear and -0 otherwise; o + (+-0) == o
-// except -0 + +0 == +0.  So the result differs from o only when o is -0 and
-// x's sign bit is clear.  Used for the D[n][n] == 0 coupling term and the
-// zero-amplitude forcing planes.  (A non-finite x can only appear after a
-// stage has already produced a non-finite value, i.e. after divergence, and
-// then o is non-finite as well, so the divergence location is unchanged.)
-__device__ __forceinline__ double add_signed_zero(double o, double x) {
-    const long long ob = __double_as_longlong(o);
-    const long long xb = __double_as_longlong(x);
-    return (ob == (long long)0x8000000000000000ULL && xb >= 0) ? 0.0 : o;
+// rmul(+0.0, x) for finite x: a zero carrying x's sign bit, built on the
+// integer pipe (one LOP3).  radd(o, zero_times(x)) is then exactly the
+// reference's o + 0.0*x -- o + (+-0) == o except -0 + +0 == +0 -- for the
+// D[n][n] == 0 coupling term and the zero-amplitude forcing planes.  (A
+// non-finite x can only appear after a stage has already produced a
+// non-finite value, i.e. after divergence, and then o is non-finite as well,
+// so the divergence location is unchanged.)
+__device__ __forceinline__ double zero_times(double x) {
+    return __longlong_as_double(__double_as_longlong(x) & (long long)0x8000000000000000ULL);
 }
+
+// !nonfinite(v) as one fp64 compare: false for +-inf and NaN (unordered)
+__device__ __forceinline__ bool finite_fp(double v) { return fabs(v) <= 1.7976931348623157e308; }
 
 // The reference forcing (hbcore.py:165-177) has nonzero amplitude on planes
 // 1 and 2 only; every other plane's forcing term is a signed zero.  The host

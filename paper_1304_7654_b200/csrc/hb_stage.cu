@@ -121,6 +121,11 @@ constexpr int THREADS = (CW + 2) * 32;          // + one TMA load warp + one TMA
 #define HBGPU_FIRST_STAGING 0
 #endif
 constexpr int NOUT = HBGPU_FIRST_STAGING;
+// measurement builds only (wrong results): bit 0 drops the sxy loads, bit 1
+// loads the stencil row as one aligned strip-wide box, bit 2 drops the q0 loads
+#ifndef HBGPU_EXP
+#define HBGPU_EXP 0
+#endif
 
 // Tile geometry for PT pdes per tile (4 or 1).
 template <int PT>
@@ -308,11 +313,18 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
                 if (issued_in >= R) mbar_wait(empty_in + pin.slot, pin.phase ^ 1u);
                 else ++issued_in;
                 double *dst = ring + pin.slot * S::SLOT;
-                mbar_expect_tx(full_in + pin.slot, with_sxy ? BYTES + SBYTES : BYTES);
+                if (HBGPU_EXP & 1) with_sxy = false;
+                if (HBGPU_EXP & 2) {   // measurement: one aligned strip-wide box
+                    mbar_expect_tx(full_in + pin.slot, with_sxy ? QBYTES / P / PT * P * PT + SBYTES : QBYTES);
+                    load_rows<PT>(dst, maps + (5 + a.in_slot) * a.nblocks + tl.bidx, x + 2, tl.pde0, row, inter,
+                                  full_in + pin.slot);
+                } else {
+                    mbar_expect_tx(full_in + pin.slot, with_sxy ? BYTES + SBYTES : BYTES);
 #pragma unroll
-                for (int k = 0; k < G::NSPLIT; ++k)
-                    load_rows<PT>(dst + k * S::REGION, min, x + k * (G::TCOLS / G::NSPLIT), tl.pde0, row,
-                                  inter, full_in + pin.slot);
+                    for (int k = 0; k < G::NSPLIT; ++k)
+                        load_rows<PT>(dst + k * S::REGION, min, x + k * (G::TCOLS / G::NSPLIT), tl.pde0, row,
+                                      inter, full_in + pin.slot);
+                }
                 if (with_sxy) tma_load_2d(dst + S::SXY, ms, tl.i0 - 1, row - 2, full_in + pin.slot);
                 pin = advance<R>(pin);
             };
@@ -323,8 +335,12 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
                 if (!FIRST) {
                     if (issued_q >= Q) mbar_wait(empty_q + pq.slot, pq.phase ^ 1u);
                     else ++issued_q;
-                    mbar_expect_tx(full_q + pq.slot, QBYTES);
-                    load_rows<PT>(qring + pq.slot * S::QSLOT, mq, x + 2, tl.pde0, j, inter, full_q + pq.slot);
+                    if (HBGPU_EXP & 4) {   // measurement: no q0 traffic
+                        mbar_arrive(full_q + pq.slot);
+                    } else {
+                        mbar_expect_tx(full_q + pq.slot, QBYTES);
+                        load_rows<PT>(qring + pq.slot * S::QSLOT, mq, x + 2, tl.pde0, j, inter, full_q + pq.slot);
+                    }
                     pq = advance<Q>(pq);
                 }
             }
@@ -371,6 +387,9 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
     int used_out = 0;   // first stage: staging slots handed out so far (saturates)
     int ap_pde = -1;
     double ap[P];
+    double dk[P / 2 + 1];   // dk[k] = D[m+k][m] for every m (circulant)
+#pragma unroll
+    for (int k = 1; k <= P / 2; ++k) dk[k] = a.D[k * P];
     for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
         const Tile tl = decode_tile<PT>(a, t);
         const int p = tl.pde0 + pp;
@@ -458,26 +477,27 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
 #pragma unroll
                 for (int n = 0; n < P; ++n) o[n] = radd(o[n], rmul(rsub(e[n], w[n]), adv_2h));
             }
-            // D[n][n] == 0 and the zero-amplitude forcing planes add a signed
-            // zero: add_signed_zero reproduces that rounding step exactly on
-            // the integer pipe (see hb_common.cuh).  D is a circulant,
-            // exactly antisymmetric matrix (D[m+k][m] == -D[m-k][m] bit for
-            // bit, checked on the host), so column m's product for row m+k
-            // is, negated, row m-k's: one DMUL feeds a DADD and a DSUB with
-            // the reference's rounding (x + (-y) == x - y, (-d) y == -(d y)).
+            // D is the spectral matrix: circulant and exactly antisymmetric
+            // (D[m+k][m] == dk[k] == -D[m-k][m] bit for bit, checked on the
+            // host), so column m's product for row m+k is, negated, row
+            // m-k's: one DMUL feeds a DADD and a DSUB with the reference's
+            // rounding (x + (-y) == x - y, (-d) y == -(d y)).  The D[m][m]
+            // == +0 term and the zero-amplitude forcing planes add 0*x, a
+            // signed zero formed on the integer pipe (zero_times).
 #pragma unroll
             for (int m = 0; m < P; ++m) {
-                o[m] = add_signed_zero(o[m], cur[m]);
+                o[m] = radd(o[m], zero_times(cur[m]));
 #pragma unroll
                 for (int k = 1; k <= P / 2; ++k) {
-                    const double prod = rmul(a.D[((m + k) % P) * P + m], cur[m]);
+                    const double prod = rmul(dk[k], cur[m]);
                     o[(m + k) % P] = radd(o[(m + k) % P], prod);
                     o[(m + P - k) % P] = rsub(o[(m + P - k) % P], prod);
                 }
             }
+            const double sv0 = zero_times(sv);
 #pragma unroll
             for (int n = 0; n < P; ++n) {
-                o[n] = forced_plane(n) ? radd(o[n], rmul(ap[n], sv)) : add_signed_zero(o[n], sv);
+                o[n] = radd(o[n], forced_plane(n) ? rmul(ap[n], sv) : sv0);
                 const double base = FIRST ? cur[n] : qv[n * PT * G::TCOLS];
                 v[n] = rsub(base, rmul(coef, o[n]));
                 if (MODE == 1) v[n] = base;   // measurement variant: same traffic, no arithmetic
@@ -520,9 +540,10 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
 #pragma unroll
                 for (int n = 0; n < P; ++n) forward(tcol, a.out, a.sendbuf, n, p, v[n]);
             }
-            bool bad = false;
+            bool ok = true;
 #pragma unroll
-            for (int n = 0; n < P; ++n) bad |= nonfinite(v[n]);
+            for (int n = 0; n < P; ++n) ok = ok && (MODE == 1 || finite_fp(v[n]));
+            const bool bad = !ok;
             if (bad && live) {
                 for (int n = 0; n < P; ++n)
                     if (nonfinite(v[n])) {
@@ -693,19 +714,22 @@ static int launch_p(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only
     return a.tile_pdes == 1 ? launch_cfg<P, 1, 0>(a, s, prepare_only) : launch_cfg<P, 4, 0>(a, s, prepare_only);
 }
 
-// The templated kernel shares each D product between rows m+k and m-k; that
-// is exact only for the spectral matrix's bitwise antisymmetric circulant
-// structure (hbcore.py:88-94 wraps d into [-N_H, N_H], so D[d] = -D[-d]).
+// The templated kernel multiplies by dk[k] = D[k][0] for every D[m+k][m] and
+// shares each product between rows m+k and m-k; that is exact only for the
+// spectral matrix's bitwise circulant, antisymmetric structure (hbcore.py:
+// 88-94 computes D from the wrapped d = n - m in [-N_H, N_H] alone, and
+// D(-d) = -D(d) exactly).
 static bool circulant_antisymmetric(const double *D, int P) {
     for (int m = 0; m < P; ++m) {
         uint64_t diag;
         memcpy(&diag, D + m * P + m, 8);
         if (diag != 0) return false;
         for (int k = 1; k <= P / 2; ++k) {
-            uint64_t x, y;
+            uint64_t x, y, d0;
             memcpy(&x, D + ((m + k) % P) * P + m, 8);
             memcpy(&y, D + ((m + P - k) % P) * P + m, 8);
-            if (x != (y ^ 0x8000000000000000ull)) return false;
+            memcpy(&d0, D + k * P, 8);
+            if (x != d0 || x != (y ^ 0x8000000000000000ull)) return false;
         }
     }
     return true;
@@ -717,7 +741,7 @@ static int dispatch(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only
         return HBGPU_ERR_ARG;
     }
     if (!prepare_only && a.planes <= HBGPU_MAX_TEMPLATED_P && !circulant_antisymmetric(a.D, a.planes)) {
-        hbgpu_set_error("hbgpu_stage: D must be the spectral matrix (+0.0 diagonal, D[m+k][m] == -D[m-k][m])");
+        hbgpu_set_error("hbgpu_stage: D must be the spectral matrix (+0.0 diagonal, D[m+k][m] == D[k][0] == -D[m-k][m])");
         return HBGPU_ERR_ARG;
     }
     switch (a.planes) {

@@ -10,8 +10,9 @@ The forcing array of the reference, amp[n] * pfac[p] * sxy[j, i] evaluated
 left to right (hbcore.py:165-177), is stored factored as a per-(plane, pde)
 scalar ap[n][p] = amp[n] * pfac[p] and, per block, the two vectors
 sin(2 pi x_i) and sin(2 pi y_j) whose rounded product is the reference's
-sxy[j, i]; the kernel forms sxy and then ap * sxy with one rounded multiply
-each, which reproduces the reference's array exactly, signed zeros included.
+sxy[j, i]; the device forms the sxy table from them once (one rounded multiply
+per element) and the stage kernel forms ap * sxy with one more, which
+reproduces the reference's array exactly, signed zeros included.
 """
 
 from __future__ import annotations
@@ -69,11 +70,13 @@ def spectral_matrix(nharms, omega):
 
 
 def circulant_antisymmetric(mat):
-    """True when D[(m+k)%P][m] is bitwise -D[(m-k)%P][m] and the diagonal is +0.0.
+    """True when D[(m+k)%P][m] is bitwise D[k][0] and -D[(m-k)%P][m], and the
+    diagonal is +0.0.
 
     spectral_matrix has this structure exactly (the wrapped d of ref
-    hbcore.py:88-94 makes D a function of d with D(-d) = -D(d)); the stage
-    kernel relies on it to share one product between two rows.
+    hbcore.py:88-94 makes D a function of d alone, with D(-d) = -D(d)); the
+    stage kernel relies on it to multiply by N_H constants and to share one
+    product between two rows.
     """
     mat = np.ascontiguousarray(mat, dtype=np.float64)
     size = mat.shape[0]
@@ -84,7 +87,7 @@ def circulant_antisymmetric(mat):
     for k in range(1, size // 2 + 1):
         plus = bits[(idx + k) % size, idx]
         minus = bits[(idx - k) % size, idx]
-        if np.any(plus != (minus ^ np.uint64(1 << 63))):
+        if np.any(plus != bits[k, 0]) or np.any(plus != (minus ^ np.uint64(1 << 63))):
             return False
     return True
 
@@ -146,8 +149,8 @@ def forcing_vectors(spec):
 
 def forcing_table(spec):
     """sxy[j, i] = sin(2 pi x_i) * sin(2 pi y_j) as the reference forms it
-    (hbcore.py:169): one rounded product per element, which the stage
-    kernel recomputes from forcing_vectors instead of storing the table."""
+    (hbcore.py:169): one rounded product per element -- what the device
+    table built from forcing_vectors holds."""
     sx, sy = forcing_vectors(spec)
     return np.ascontiguousarray(sx[None, :] * sy[:, None])
 
