@@ -233,6 +233,31 @@ int hbgpu_forces(const double *slot, const hbgpu_force_seg *segs,
 int hbgpu_ordered_fold(const double *stacked, int32_t nranks, int64_t count,
                        double *out, void *stream);
 
+/* ---- output records (outio.py:79-123 layout, 221-241 writer) ------------
+ * One record of a restart or flowtec file: a 4-byte little-endian length
+ * prefix (payload bytes), the float64 payload, the same 4-byte suffix.
+ * Restart payload of (block, plane n): q[n][p][j][i] for j rows outer, i
+ * columns, p innermost (the interior only).  Flowtec payload: per cell
+ * (x_i, y_j, q[n][0][j][i], q[n][1][j][i]), rows outer.                     */
+enum { HBGPU_RECORD_RESTART = 0, HBGPU_RECORD_FLOWTEC = 1 };
+
+typedef struct hbgpu_out_record {
+    int32_t block;    /* local block index into the blocks table            */
+    int32_t plane;    /* HB snapshot n                                       */
+    int32_t kind;     /* HBGPU_RECORD_RESTART or HBGPU_RECORD_FLOWTEC        */
+    int32_t pad;
+    int64_t dst;      /* byte offset of the record's length prefix in dst    */
+    int64_t xy;       /* flowtec: element offset of the block's x centres
+                         (ni values) followed by its y centres (nj) in xy    */
+} hbgpu_out_record;
+
+/* Write `nrecs` records (markers + payload, byte-exact file images) from a
+ * slot into dst (device memory; records may be 4-byte aligned only).      */
+int hbgpu_pack_records(const double *slot, const hbgpu_block *blocks,
+                       const hbgpu_out_record *recs, int32_t nrecs,
+                       int32_t max_cells, const double *xy, void *dst,
+                       void *stream);
+
 /* ---- engine: the per-rank iteration schedule (driver.py:110-149) -------- */
 
 typedef struct hbgpu_engine_desc {

@@ -47,7 +47,7 @@ extern "C" int hbgpu_abi_layout(int64_t *out, int32_t n) {
                          (int64_t)sizeof(hbgpu_halo_dir),    (int64_t)sizeof(hbgpu_force_seg),
                          (int64_t)sizeof(hbgpu_peer_msg),    (int64_t)sizeof(hbgpu_stage_args),
                          (int64_t)sizeof(hbgpu_engine_desc), (int64_t)offsetof(hbgpu_engine_desc, coef),
-                         (int64_t)offsetof(hbgpu_stage_args, coef)};
+                         (int64_t)offsetof(hbgpu_stage_args, coef), (int64_t)sizeof(hbgpu_out_record)};
     int k = 0;
     for (; k < n && k < (int)(sizeof(v) / sizeof(v[0])); ++k) out[k] = v[k];
     return k;

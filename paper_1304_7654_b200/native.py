@@ -47,6 +47,11 @@ HALO_DIR_DTYPE = np.dtype([
     ("dst_off", "<i8"), ("dst_es", "<i8"), ("dst_vs", "<i8"),
     ("length", "<i4"), ("src_kind", "<i4"), ("dst_kind", "<i4"), ("pad", "<i4")], align=True)
 
+OUT_RECORD_DTYPE = np.dtype([
+    ("block", "<i4"), ("plane", "<i4"), ("kind", "<i4"), ("pad", "<i4"),
+    ("dst", "<i8"), ("xy", "<i8")], align=True)
+RECORD_RESTART, RECORD_FLOWTEC = 0, 1
+
 FORCE_SEG_DTYPE = np.dtype([
     ("start", "<i8"), ("stride", "<i8"), ("ps", "<i8"), ("length", "<i4"),
     ("body", "<i4"), ("h", "<f8")], align=True)
@@ -99,6 +104,7 @@ SIGNATURES = {
     "hbgpu_norm_fold": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "hbgpu_forces": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "hbgpu_ordered_fold": (c_i32, [c_vp, c_i32, c_i64, c_vp, c_vp]),
+    "hbgpu_pack_records": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "hbgpu_engine_create": (c_i32, [ctypes.POINTER(EngineDesc), ctypes.POINTER(c_vp)]),
     "hbgpu_engine_prime": (c_i32, [c_vp, c_vp]),
     "hbgpu_engine_iterate": (c_i32, [c_vp, c_i32, c_i32, c_vp]),
@@ -142,7 +148,8 @@ def abi_layout_python():
     """The same numbers hbgpu_abi_layout reports, from the Python mirrors."""
     return [BLOCK_DTYPE.itemsize, FACE_TARGET_DTYPE.itemsize, HALO_DIR_DTYPE.itemsize,
             FORCE_SEG_DTYPE.itemsize, ctypes.sizeof(PeerMsg), ctypes.sizeof(StageArgs),
-            ctypes.sizeof(EngineDesc), EngineDesc.coef.offset, StageArgs.coef.offset]
+            ctypes.sizeof(EngineDesc), EngineDesc.coef.offset, StageArgs.coef.offset,
+            OUT_RECORD_DTYPE.itemsize]
 
 
 def abi_layout_native():

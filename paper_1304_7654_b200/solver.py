@@ -30,7 +30,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import hbop, native
+from . import hbop, native, outio
 from .cutplan import ExchangeStrategy, build_cut_plan, predicted_message_count
 from .devlayout import build_rank_layout
 from .exceptions import DivergenceError, ProtocolError
@@ -61,7 +61,7 @@ class RunSpec:
     activation: object = None
     exchange: ExchangeStrategy = field(default_factory=ExchangeStrategy)
     reduce: ForceReduceStrategy = field(default_factory=ForceReduceStrategy)
-    io: object = None
+    io: object = None            # outio.WriteMode (None = buffered)
     iterations: int | None = None
     out_dir: str | None = None
     extra_outputs: tuple = ()
@@ -488,16 +488,27 @@ def run_case(spec):
 
     import torch
     native.require_cuda()
+    # output files exist at their final size before any rank writes
+    # (driver.py:160-167); every rank writes its own records after the loop
+    targets = _output_targets(spec)
+    layouts = outio.all_layouts(topology, case.nharms, case.npde) if targets else ()
+    if targets:
+        if world == 1 or dist.get_rank() == 0:
+            for out_dir, _ in targets:
+                outio.create_output_files(out_dir, layouts)
+        if world > 1:
+            dist.barrier()
+    out = (layouts, targets)
     t0 = time.perf_counter()
     if world > 1:
         fields, hist_np, norms_local = _execute_distributed(spec, topology, partition, plan,
-                                                            iterations, dist, world)
+                                                            iterations, dist, world, out)
     elif spec.ranks > 1 and spec.transport == "loopback":
-        fields, hist_np, norms_local = _execute_loopback(spec, topology, partition, plan, iterations)
+        fields, hist_np, norms_local = _execute_loopback(spec, topology, partition, plan, iterations, out)
     else:
         one = partition_blocks(topology, 1)
         fields, hist_np, norms_local = _execute_single(
-            spec, topology, one, build_cut_plan(topology, one, case.nharms, case.npde), iterations)
+            spec, topology, one, build_cut_plan(topology, one, case.nharms, case.npde), iterations, out)
     wall = time.perf_counter() - t0
 
     forces = (ForceCoefficients.from_stack(hist_np[-1]) if iterations > 0
@@ -512,8 +523,10 @@ def run_case(spec):
                            threads=spec.threads, iterations=iterations, wall_s=wall,
                            msgs=forecast.total_messages * exchanges,
                            bytes=forecast.total_bytes * exchanges,
-                           collectives=iterations if topology.nbody else 0, write_ops=0,
-                           activations=iterations, units=units)
+                           collectives=iterations if topology.nbody else 0,
+                           write_ops=sum(outio.write_ops(layouts, [b.id for b in topology.blocks], m)
+                                         for _, m in targets),
+                           activations=iterations + len(targets), units=units)
     return CaseRunResult(fields=fields, forces=forces, counters=counters, wall_s=wall,
                          record=record, residual_norms=_fold_norms(norms_local, iterations),
                          force_history=[ForceCoefficients.from_stack(h) for h in hist_np])
@@ -532,7 +545,28 @@ def _history(dr, iterations):
     return dr.force_history_array(iterations).cpu().numpy()
 
 
-def _execute_single(spec, topology, partition, plan, iterations):
+def _output_targets(spec):
+    """(directory, WriteMode) pairs: out_dir with spec.io, then extra_outputs."""
+    from .outio import WriteMode
+    targets = []
+    if spec.out_dir is not None:
+        targets.append((spec.out_dir, WriteMode.BUFFERED if spec.io is None else WriteMode(spec.io)))
+    for out_dir, mode in spec.extra_outputs:
+        targets.append((out_dir, WriteMode(mode)))
+    return targets
+
+
+def _write_outputs(ranks, out):
+    """Every rank's records of every target, packed on its GPU (outio.py)."""
+    layouts, targets = out
+    t0 = time.perf_counter()
+    for out_dir, mode in targets:
+        for dr in ranks:
+            outio.write_output(dr, layouts, mode, out_dir)
+    return time.perf_counter() - t0
+
+
+def _execute_single(spec, topology, partition, plan, iterations, out=((), ())):
     """All blocks on this process's GPU, one engine, graph-replayed iterations."""
     import torch
     device = spec.device if spec.device is not None else torch.cuda.current_device()
@@ -551,6 +585,7 @@ def _execute_single(spec, topology, partition, plan, iterations):
         norms = dr.norm_history(iterations)
         torch.cuda.synchronize(dr.device)
         dr.timings.update(compute=t1 - t0, download=time.perf_counter() - t1)
+        dr.timings.update(output=_write_outputs([dr], out))
         LAST_TIMINGS.clear()
         LAST_TIMINGS.update(dr.timings)
     finally:
@@ -558,7 +593,7 @@ def _execute_single(spec, topology, partition, plan, iterations):
     return fields, hist, norms
 
 
-def _execute_distributed(spec, topology, partition, plan, iterations, dist, world):
+def _execute_distributed(spec, topology, partition, plan, iterations, dist, world, out=((), ())):
     """One rank per process/GPU; remote halos over NCCL inside the engine."""
     import torch
     rank = dist.get_rank()
@@ -582,13 +617,16 @@ def _execute_distributed(spec, topology, partition, plan, iterations, dist, worl
         dist.all_gather_object(allnorm, dr.norm_history(iterations))
         norms = {k: v for part in allnorm for k, v in part.items()}
         torch.cuda.synchronize(dr.device)
+        _write_outputs([dr], out)
+        if out[1]:
+            dist.barrier()
     finally:
         dr.close()
         native.load().hbgpu_comm_destroy(comm)
     return fields, hist, norms
 
 
-def _execute_loopback(spec, topology, partition, plan, iterations):
+def _execute_loopback(spec, topology, partition, plan, iterations, out=((), ())):
     """spec.ranks engines on this GPU, one per rank of the reference partition,
     stepped stage by stage; the remote halo payloads move between their send
     and receive buffers by device copies in place of NCCL.  This runs the
@@ -635,14 +673,15 @@ def _execute_loopback(spec, topology, partition, plan, iterations):
         if iterations > 0:
             stacked = torch.stack([dr.force_history_array(iterations).reshape(-1) for dr in ranks])
             count = stacked.shape[1]
-            out = torch.empty(count, dtype=torch.float64, device=stacked.device)
+            folded = torch.empty(count, dtype=torch.float64, device=stacked.device)
             if count:
-                native.check(lib.hbgpu_ordered_fold(_ptr(stacked), nr, count, _ptr(out), ranks[0].stream()),
+                native.check(lib.hbgpu_ordered_fold(_ptr(stacked), nr, count, _ptr(folded), ranks[0].stream()),
                              "hbgpu_ordered_fold")
-            hist = out.cpu().numpy().reshape(iterations, 3, spec.case.planes, spec.case.nbody)
+            hist = folded.cpu().numpy().reshape(iterations, 3, spec.case.planes, spec.case.nbody)
         else:
             hist = _history(ranks[0], 0)
         torch.cuda.synchronize(device)
+        _write_outputs(ranks, out)
     finally:
         for dr in ranks:
             dr.close()

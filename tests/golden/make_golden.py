@@ -14,6 +14,9 @@ Outputs (committed):
                      seeded random states, sub-ranges included
   host.json          reference partitions, cut plans, message forecasts,
                      case_text renderings and parse-error messages
+  outputs.json       (--outputs) sha256 / size / record layout of the
+                     restart and flowtec files the reference writes for a
+                     few runs, with their write_ops counters
 """
 
 from __future__ import annotations
@@ -286,7 +289,63 @@ def make_parse_errors():
     return out
 
 
+OUTPUT_RUNS = {
+    # name: (builder, iterations, ranks, io mode, seeded-workload key or None)
+    "tc-tiny-8": (tc_tiny, 8, 1, "buffered", None),
+    "tc-tiny-3-per-value-r2": (tc_tiny, 3, 2, "per-value", None),
+    "pair-reversed-6-r2": (reversed_pair, 6, 2, "buffered", None),
+    "self-cut-reversed-5": (reversed_self_cut_case, 5, 1, "buffered", None),
+    "C0-seeded-10": (lambda: mine.baseline_workload("C0").case, 10, 1, "buffered", "C0"),
+}
+
+
+def make_outputs():
+    """Reference-written restart/flowtec files: per-file sha256, size and the
+    record layout, plus the run's write_ops counter."""
+    import tempfile
+    from hbproxy.outio import WriteMode, compute_layout
+    out = {}
+    for name, (build, iters, ranks, io, wl_key) in OUTPUT_RUNS.items():
+        case = build()
+        initial = mine.baseline_workload(wl_key).initial if wl_key else None
+        saved = hbcore.initial_values
+        if initial is not None:
+            def hook(spec, planes, npde, n_lo, n_hi, j_lo, j_hi, initial=initial):
+                return initial(spec, planes, npde)[n_lo:n_hi, :, j_lo - 1:j_hi - 1, :]
+            hbcore.initial_values = hook
+        try:
+            with tempfile.TemporaryDirectory() as d:
+                res = run_case(RunSpec(case=case, ranks=ranks, iterations=iters, io=WriteMode(io),
+                                       out_dir=d))
+                files = {}
+                for fn in sorted(os.listdir(d)):
+                    if fn.endswith(".bin"):
+                        data = open(os.path.join(d, fn), "rb").read()
+                        files[fn] = {"sha256": hashlib.sha256(data).hexdigest(), "bytes": len(data)}
+        finally:
+            hbcore.initial_values = saved
+        topo = build_topology(case)
+        layouts = (compute_layout(topo, case.nharms, case.npde, "restart")
+                   + compute_layout(topo, case.nharms, case.npde, "flowtec"))
+        out[name] = {
+            "iterations": iters, "ranks": ranks, "io": io,
+            "input_hash": input_hash(case, initial),
+            "fingerprint": fingerprint(res.fields, res.forces),
+            "files": files,
+            "write_ops": res.record.write_ops, "activations": res.record.activations,
+            "layouts": {l.filename: {"kind": l.kind, "plane": l.plane, "total_bytes": l.total_bytes,
+                                     "records": [[r.block, r.plane, r.offset, r.nfloats]
+                                                 for r in l.records]} for l in layouts},
+        }
+        print(name, {k: v for k, v in out[name].items() if k not in ("layouts", "files")})
+    return out
+
+
 def main():
+    if "--outputs" in sys.argv:
+        with open(os.path.join(HERE, "outputs.json"), "w") as fh:
+            json.dump(make_outputs(), fh, indent=0, sort_keys=True)
+        return
     host = make_host()
     with open(os.path.join(HERE, "host.json"), "w") as fh:
         json.dump(host, fh, indent=0, sort_keys=True)
