@@ -16,8 +16,9 @@ reference's functions of the same names (outio.py:79-104, 185-206, 244-291).
 The writer differs in where the bytes come from: ``write_output`` packs each
 record's complete byte image on the GPU from the engine's result slot
 (hbgpu_pack_records, csrc/hb_io.cu), moves it to pinned host memory and
-writes each run of file-adjacent records with one positioned write, double
-buffered so the device packs chunk k+1 while the host writes chunk k.  The
+writes each run of file-adjacent records with one positioned write from a
+pool of host threads, so the device packs and copies chunk k+1 while the
+host writes chunks k, k-1, ...  The
 two reference write strategies (per-value, buffered) produce identical bytes
 there and here; ``write_ops`` reports the positioned-write count the chosen
 strategy defines (outio.py:221-241: 2 + nfloats or 3 per record), the
@@ -28,6 +29,7 @@ from __future__ import annotations
 
 import os
 import struct
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 from enum import Enum
 
@@ -38,7 +40,8 @@ from .exceptions import PlanError, WriteError
 
 DOUBLE_SIZE = 8
 MARKER_SIZE = 4
-CHUNK_BYTES = 256 << 20      # device staging per chunk (two chunks in flight)
+CHUNK_BYTES = 128 << 20      # device staging per chunk
+WRITE_SLOTS = 6              # chunks in flight (staging buffers = writer threads)
 
 
 class WriteMode(Enum):
@@ -187,11 +190,14 @@ def _chunks(records, limit):
         yield chunk
 
 
-def write_output(rank, layouts, mode, out_dir, chunk_bytes=CHUNK_BYTES):
+def write_output(rank, layouts, mode, out_dir, chunk_bytes=CHUNK_BYTES, slots=WRITE_SLOTS):
     """Write this rank's records of every layout from its device result slot.
 
-    The files must exist at their final size (create_output_files).  Returns
-    the write-op count of `mode` for the records written."""
+    Chunks of records are packed on the device into one of `slots` staging
+    buffers, copied to pinned host memory and written by a pool of host
+    threads (os.pwrite releases the GIL), so packing, PCIe and page-cache
+    writes of different chunks overlap.  The files must exist at their final
+    size (create_output_files).  Returns the write-op count of `mode`."""
     import torch
     lib = native.load()
     torch_dev = rank.device
@@ -209,22 +215,34 @@ def write_output(rank, layouts, mode, out_dir, chunk_bytes=CHUNK_BYTES):
         return 0
     cap = max(sum(r.total_bytes for r in c) for _, _, c in work)
     cap = (cap + 7) // 8 * 8
-    dev = [torch.empty(cap, dtype=torch.uint8, device=torch_dev) for _ in range(2)]
-    host = [torch.empty(cap, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
-    done = [torch.cuda.Event() for _ in range(2)]
+    nslot = max(1, min(slots, len(work)))
+    dev = [torch.empty(cap, dtype=torch.uint8, device=torch_dev) for _ in range(nslot)]
+    host = [torch.empty(cap, dtype=torch.uint8, pin_memory=True) for _ in range(nslot)]
+    done = [torch.cuda.Event() for _ in range(nslot)]
+    busy = [None] * nslot
     stream = torch.cuda.current_stream(torch_dev)
     slot = rank.slots[0]
     fds = {}
+    for layout in layouts:
+        path = os.path.join(out_dir, layout.filename)
+        try:
+            fds[path] = os.open(path, os.O_RDWR)
+        except OSError as exc:
+            for fd in fds.values():
+                os.close(fd)
+            raise WriteError(f"cannot open {path}: {exc}") from exc
+    pool = ThreadPoolExecutor(max_workers=nslot)
     try:
-        pending = None
         for k, (layout, kind, chunk) in enumerate(work):
-            s = k % 2
+            s = k % nslot
+            if busy[s] is not None:
+                busy[s].result()          # the slot's previous chunk is on disk
             table = np.zeros(len(chunk), dtype=native.OUT_RECORD_DTYPE)
             pos = 0
             for t, rec in enumerate(chunk):
                 table[t] = (local[rec.block], rec.plane, kind, 0, pos, xy_off[local[rec.block]])
                 pos += rec.total_bytes
-            t_table = torch.from_numpy(table.view(np.uint8).copy()).to(torch_dev, non_blocking=False)
+            t_table = torch.from_numpy(table.view(np.uint8).copy()).to(torch_dev)
             max_cells = max(spec_of[r.block].ni * spec_of[r.block].nj for r in chunk)
             native.check(lib.hbgpu_pack_records(slot.data_ptr(), rank.t_blocks.data_ptr(),
                                                 t_table.data_ptr(), len(chunk), max_cells,
@@ -232,26 +250,21 @@ def write_output(rank, layouts, mode, out_dir, chunk_bytes=CHUNK_BYTES):
                                                 stream.cuda_stream), "hbgpu_pack_records")
             host[s][:pos].copy_(dev[s][:pos], non_blocking=True)
             done[s].record(stream)
-            if pending is not None:
-                _write_chunk(*pending, fds, out_dir)
-            pending = (done[s], host[s], layout, chunk)
-        _write_chunk(*pending, fds, out_dir)
+            path = os.path.join(out_dir, layout.filename)
+            busy[s] = pool.submit(_write_chunk, done[s], host[s], chunk, fds[path], path)
+        for f in busy:
+            if f is not None:
+                f.result()
     finally:
+        pool.shutdown(wait=True)
         for fd in fds.values():
             os.close(fd)
     return write_ops(layouts, local, mode)
 
 
-def _write_chunk(event, host, layout, chunk, fds, out_dir):
-    """Positioned writes of the packed chunk, one per run of file-adjacent records."""
+def _write_chunk(event, host, chunk, fd, path):
+    """Positioned writes of one packed chunk, one per run of file-adjacent records."""
     event.synchronize()
-    path = os.path.join(out_dir, layout.filename)
-    if path not in fds:
-        try:
-            fds[path] = os.open(path, os.O_RDWR)
-        except OSError as exc:
-            raise WriteError(f"cannot open {path}: {exc}") from exc
-    fd = fds[path]
     buf = host.numpy()
     pos = 0
     k = 0
