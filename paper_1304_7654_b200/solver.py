@@ -27,13 +27,14 @@ import ctypes
 import math
 import time
 from dataclasses import dataclass, field
+from enum import Enum
 
 import numpy as np
 
 from . import hbop, native, outio
 from .cutplan import ExchangeStrategy, build_cut_plan, predicted_message_count
 from .devlayout import build_rank_layout
-from .exceptions import DivergenceError, ProtocolError
+from .exceptions import CollectiveError, DivergenceError, ProtocolError
 from .topology import build_topology, partition_blocks
 
 NO_BAD = (1 << 64) - 1
@@ -43,13 +44,30 @@ LAST_TIMINGS = {}
 LIN_BITS = 40
 
 
+class ReduceMode(Enum):
+    PER_BODY_PER_HARMONIC = "per-item"
+    SINGLE_BUFFER = "buffered"
+
+
 @dataclass(frozen=True)
 class ForceReduceStrategy:
-    """Kept for RunSpec compatibility (reduce.py:34-45); the device path always
-    uses the single-buffer packing with all three coefficients."""
+    """The reference's reduction strategy (reduce.py:27-45).  Both modes give
+    the same sums (the device folds every rank's force history in rank
+    order); the mode sets the collective-call counter (reduce.py:40-46).
+    functag 2 -- cm left unreduced -- is refused by run_case."""
 
-    mode: str = "buffered"
+    mode: object = ReduceMode.SINGLE_BUFFER
     functag: int = 3
+
+    def __post_init__(self):
+        object.__setattr__(self, "mode", ReduceMode(self.mode))
+        if self.functag not in (2, 3):
+            raise CollectiveError(f"functag must be 2 or 3, got {self.functag}")
+
+    def collective_calls(self, planes, nbody):
+        if nbody == 0:
+            return 0
+        return planes * nbody if self.mode is ReduceMode.PER_BODY_PER_HARMONIC else 1
 
 
 @dataclass
@@ -126,6 +144,8 @@ class RunRecord:
     write_ops: int
     activations: int
     units: int = 0
+    loop_s: float = 0.0          # device: prime + iteration loop wall time
+    gpus: int = 1
 
     @property
     def units_per_s(self):
@@ -481,6 +501,9 @@ def run_case(spec):
     partition = partition_blocks(topology, spec.ranks)
     plan = build_cut_plan(topology, partition, case.nharms, case.npde)
     iterations = case.iterations if spec.iterations is None else spec.iterations
+    if spec.reduce.functag != 3:
+        raise NotImplementedError("functag=2 (cm left as each rank's partial) is not supported: "
+                                  "the device path reduces cl, cd and cm")
     dist = _dist()
     world = dist.get_world_size() if dist is not None else 1
     if world > 1 and spec.ranks != world:
@@ -501,19 +524,20 @@ def run_case(spec):
     out = (layouts, targets)
     t0 = time.perf_counter()
     if world > 1:
-        fields, hist_np, norms_local = _execute_distributed(spec, topology, partition, plan,
-                                                            iterations, dist, world, out)
+        fields, hist_np, norms_local, loop_s = _execute_distributed(spec, topology, partition, plan,
+                                                                    iterations, dist, world, out)
     elif spec.ranks > 1 and spec.transport == "loopback":
-        fields, hist_np, norms_local = _execute_loopback(spec, topology, partition, plan, iterations, out)
+        fields, hist_np, norms_local, loop_s = _execute_loopback(spec, topology, partition, plan,
+                                                                 iterations, out)
     else:
         one = partition_blocks(topology, 1)
-        fields, hist_np, norms_local = _execute_single(
+        fields, hist_np, norms_local, loop_s = _execute_single(
             spec, topology, one, build_cut_plan(topology, one, case.nharms, case.npde), iterations, out)
     wall = time.perf_counter() - t0
 
     forces = (ForceCoefficients.from_stack(hist_np[-1]) if iterations > 0
               else ForceCoefficients.zeros(case.planes, case.nbody))
-    forecast = predicted_message_count(plan)
+    forecast = predicted_message_count(plan, spec.exchange)
     exchanges = 4 * iterations + 1
     counters = [{"rank": r, "msgs_sent": None, "bytes_sent": None} for r in range(spec.ranks)]
     record = None
@@ -523,10 +547,11 @@ def run_case(spec):
                            threads=spec.threads, iterations=iterations, wall_s=wall,
                            msgs=forecast.total_messages * exchanges,
                            bytes=forecast.total_bytes * exchanges,
-                           collectives=iterations if topology.nbody else 0,
+                           collectives=iterations * spec.reduce.collective_calls(case.planes, case.nbody),
                            write_ops=sum(outio.write_ops(layouts, [b.id for b in topology.blocks], m)
                                          for _, m in targets),
-                           activations=iterations + len(targets), units=units)
+                           activations=iterations + len(targets), units=units, loop_s=loop_s,
+                           gpus=world)
     return CaseRunResult(fields=fields, forces=forces, counters=counters, wall_s=wall,
                          record=record, residual_norms=_fold_norms(norms_local, iterations),
                          force_history=[ForceCoefficients.from_stack(h) for h in hist_np])
@@ -590,7 +615,7 @@ def _execute_single(spec, topology, partition, plan, iterations, out=((), ())):
         LAST_TIMINGS.update(dr.timings)
     finally:
         dr.close()
-    return fields, hist, norms
+    return fields, hist, norms, t1 - t0
 
 
 def _execute_distributed(spec, topology, partition, plan, iterations, dist, world, out=((), ())):
@@ -602,10 +627,13 @@ def _execute_distributed(spec, topology, partition, plan, iterations, dist, worl
     comm = make_comm(rank, world, device)
     dr = _new_rank(spec, topology, partition, plan, rank, device, comm, iterations)
     try:
+        torch.cuda.synchronize(dr.device)
+        t0 = time.perf_counter()
         dr.prime()
         if iterations > 0:
             dr.iterate(iterations, use_graph=spec.use_graph)
         torch.cuda.synchronize(dr.device)
+        loop_s = time.perf_counter() - t0
         divs = [None] * world
         dist.all_gather_object(divs, dr.divergence())
         divs = [d for d in divs if d is not None]
@@ -623,7 +651,7 @@ def _execute_distributed(spec, topology, partition, plan, iterations, dist, worl
     finally:
         dr.close()
         native.load().hbgpu_comm_destroy(comm)
-    return fields, hist, norms
+    return fields, hist, norms, loop_s
 
 
 def _execute_loopback(spec, topology, partition, plan, iterations, out=((), ())):
@@ -658,12 +686,15 @@ def _execute_loopback(spec, topology, partition, plan, iterations, out=((), ()))
                 for dr in ranks:
                     native.check(lib.hbgpu_engine_unpack(dr.engine, p, dr.stream()), "hbgpu_engine_unpack")
 
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
         phase(-1, True)
         for _ in range(iterations):
             for st in range(4):
                 phase(st, True)
             phase(4, False)
         torch.cuda.synchronize(device)
+        loop_s = time.perf_counter() - t0
         divs = [d for d in (dr.divergence() for dr in ranks) if d is not None]
         raise_divergence(min(divs, key=lambda d: d[:2]) if divs else None)
         fields, norms = {}, {}
@@ -685,7 +716,7 @@ def _execute_loopback(spec, topology, partition, plan, iterations, out=((), ()))
     finally:
         for dr in ranks:
             dr.close()
-    return fields, hist, norms
+    return fields, hist, norms, loop_s
 
 
 def _reduce_history(dr, hist, world):
