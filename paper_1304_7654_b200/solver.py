@@ -32,7 +32,7 @@ from enum import Enum
 import numpy as np
 
 from . import hbop, native, outio
-from .cutplan import ExchangeStrategy, build_cut_plan, predicted_message_count
+from .cutplan import ExchangeMode, ExchangeStrategy, build_cut_plan, predicted_message_count
 from .devlayout import build_rank_layout
 from .exceptions import CollectiveError, DivergenceError, ProtocolError
 from .topology import build_topology, partition_blocks
@@ -501,9 +501,11 @@ def run_case(spec):
     partition = partition_blocks(topology, spec.ranks)
     plan = build_cut_plan(topology, partition, case.nharms, case.npde)
     iterations = case.iterations if spec.iterations is None else spec.iterations
-    if spec.reduce.functag != 3:
-        raise NotImplementedError("functag=2 (cm left as each rank's partial) is not supported: "
-                                  "the device path reduces cl, cd and cm")
+    if spec.reduce.functag != 3 and spec.ranks > 1:
+        # reduce.py:79-96 leaves cm as each rank's own partial and the driver
+        # returns rank 0's; with one rank that is the full sum (supported)
+        raise NotImplementedError("functag=2 with ranks > 1 (cm left as rank 0's partial) is not "
+                                  "supported: the device path reduces cl, cd and cm")
     dist = _dist()
     world = dist.get_world_size() if dist is not None else 1
     if world > 1 and spec.ranks != world:
@@ -537,20 +539,18 @@ def run_case(spec):
 
     forces = (ForceCoefficients.from_stack(hist_np[-1]) if iterations > 0
               else ForceCoefficients.zeros(case.planes, case.nbody))
-    forecast = predicted_message_count(plan, spec.exchange)
-    exchanges = 4 * iterations + 1
-    counters = [{"rank": r, "msgs_sent": None, "bytes_sent": None} for r in range(spec.ranks)]
+    activations = iterations * (12 if _per_loop(spec.activation) else 1) + len(targets)
+    counters = rank_counters(plan, spec, partition, iterations, activations, layouts, targets)
     record = None
     if iterations >= 1:
         units = topology.total_cells() * case.planes * 4 * iterations
         record = RunRecord(case=case.name or "case", machine=spec.machine, ranks=spec.ranks,
                            threads=spec.threads, iterations=iterations, wall_s=wall,
-                           msgs=forecast.total_messages * exchanges,
-                           bytes=forecast.total_bytes * exchanges,
+                           msgs=sum(c.msgs_sent for c in counters),
+                           bytes=sum(c.bytes_sent for c in counters),
                            collectives=iterations * spec.reduce.collective_calls(case.planes, case.nbody),
-                           write_ops=sum(outio.write_ops(layouts, [b.id for b in topology.blocks], m)
-                                         for _, m in targets),
-                           activations=iterations + len(targets), units=units, loop_s=loop_s,
+                           write_ops=sum(c.write_ops for c in counters),
+                           activations=activations, units=units, loop_s=loop_s,
                            gpus=world)
     return CaseRunResult(fields=fields, forces=forces, counters=counters, wall_s=wall,
                          record=record, residual_norms=_fold_norms(norms_local, iterations),
@@ -568,6 +568,50 @@ def _history(dr, iterations):
     if iterations == 0:
         return np.zeros((0, 3, case.planes, case.nbody))
     return dr.force_history_array(iterations).cpu().numpy()
+
+
+@dataclass(frozen=True)
+class CounterSnapshot:
+    """Per-rank counters with the reference's fields (runtime.py:38-45)."""
+
+    msgs_sent: int
+    bytes_sent: int
+    msgs_received: int
+    collective_calls: int
+    write_ops: int
+    team_activations: int
+
+
+def _per_loop(activation):
+    return getattr(activation, "value", activation) == "per-loop"
+
+
+def rank_counters(plan, spec, partition, iterations, activations, layouts, targets):
+    """What each rank of the reference partition sends, receives, reduces and
+    writes under spec's strategies -- the reference's counters exactly
+    (exchange.py:172-188 message counts, reduce.py:40-46 collectives,
+    outio.py:221-241 write ops, hybrid.py:233-237 activations).  The device
+    moves the same bytes in one aggregated message per peer and stage."""
+    exchanges = 4 * iterations + 1
+    per_element = spec.exchange.mode is ExchangeMode.PER_ELEMENT
+    sent = [0] * spec.ranks
+    sent_bytes = [0] * spec.ranks
+    received = [0] * spec.ranks
+    for cut in plan.cuts:
+        if cut.local:
+            continue
+        msgs = 2 * cut.length if per_element else 1
+        for d in cut.directions:
+            sent[d.sender_rank] += msgs * exchanges
+            sent_bytes[d.sender_rank] += cut.length * cut.datasize * 8 * exchanges
+            received[d.recv_rank] += msgs * exchanges
+    calls = iterations * spec.reduce.collective_calls(spec.case.planes, spec.case.nbody)
+    out = []
+    for r in range(spec.ranks):
+        owned = partition.blocks_of(r)
+        ops = sum(outio.write_ops(layouts, owned, mode) for _, mode in targets)
+        out.append(CounterSnapshot(sent[r], sent_bytes[r], received[r], calls, ops, activations))
+    return out
 
 
 def _output_targets(spec):
