@@ -274,6 +274,10 @@ typedef struct hbgpu_engine_desc {
     int32_t *iter;                   /* device, 1 element */
     const hbgpu_halo_dir *prime_dirs;  int32_t nprime;  int32_t prime_max_len;
     const hbgpu_halo_dir *unpack_dirs; int32_t nunpack; int32_t unpack_max_len;
+    /* after every stage: forwarding of west / east face columns (local halo
+     * copies and remote packs); south / north rows are forwarded inside the
+     * stage kernel through the face-target pool                            */
+    const hbgpu_halo_dir *post_dirs;   int32_t npost;   int32_t post_max_len;
     const hbgpu_force_seg *segs;     int32_t nsegs;  /* device */
     double *force_hist;              /* device [max_iters*3*planes*nbody] */
     const hbgpu_peer_msg *sends;     int32_t nsends; /* HOST arrays */

@@ -216,6 +216,9 @@ int run_stage(hbgpu_engine *e, int st, cudaStream_t s) {
     a.norm_part = st == 0 ? d.norm_part : nullptr;
     int rc = hbgpu_stage(&a, s);
     if (!rc && st == 0) rc = hbgpu_norm_fold(d.blocks, d.nblocks, d.norm_part, d.sumsq, d.iter, s);
+    // west / east face columns: local halo copies and remote packs
+    if (!rc && d.npost > 0)
+        rc = hbgpu_halo(a.out, d.sendbuf, d.recvbuf, d.post_dirs, d.npost, d.post_max_len, d.planes, s);
     return rc;
 }
 
@@ -325,7 +328,7 @@ extern "C" int hbgpu_engine_unpack(hbgpu_engine *e, int32_t phase, void *stream)
 }
 
 extern "C" int hbgpu_engine_launches_per_iteration(const hbgpu_engine *e) {
-    int per_stage = 1 + ((e->d.comm && !e->recvs.empty() && e->d.nunpack > 0) ? 1 : 0);
+    int per_stage = 1 + (e->d.npost > 0 ? 1 : 0) + ((e->d.comm && !e->recvs.empty() && e->d.nunpack > 0) ? 1 : 0);
     return 4 * per_stage + 2;
 }
 

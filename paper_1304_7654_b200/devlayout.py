@@ -14,8 +14,10 @@ rank owns it fixes:
   block -- 64 columns x 4 pdes (tile_pdes 4) or 256 columns x 1 pde
   (tile_pdes 1, every block ni >= WIDE_MIN_NI); tile t of block b is strip
   t % tiles_i, row tile t / tiles_i;
-* the face-target pool (fused halo forwarding, see cutplan.py);
-* the standalone halo directions (priming exchange / pack / unpack);
+* the face-target pool (fused halo forwarding of south / north faces, see
+  cutplan.py);
+* the standalone halo directions (priming exchange / pack / unpack, and the
+  post-stage pass that forwards west / east faces);
 * the send / receive buffer segments, grouped per peer rank, one NCCL
   message per peer and stage;
 * the force segments in the reference's summation order (hbcore.py:369-381).
@@ -33,6 +35,7 @@ from .cutplan import rank_routes
 from .hbop import forcing_vectors, stencil_coefficients
 
 ROW_LEAD = native.ROW_LEAD
+ROW_FACES = ("south", "north")    # faces forwarded inside the stage kernel
 NPDE = native.NPDE
 WIDE_MIN_NI = 192         # blocks at least this wide use 256-column, 1-pde tiles
 BLOCK_ALIGN = 32          # elements (256 B)
@@ -91,6 +94,7 @@ class RankLayout:
     faces: np.ndarray
     prime_dirs: np.ndarray
     unpack_dirs: np.ndarray
+    post_dirs: np.ndarray           # column-face forwarding after every stage
     force_segs: np.ndarray
     sends: list = field(default_factory=list)     # (peer, offset, count)
     recvs: list = field(default_factory=list)
@@ -190,6 +194,7 @@ def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None,
                         sxy=sxy_parts, sxy_size=sxy_off, faces=np.zeros(0, native.FACE_TARGET_DTYPE),
                         prime_dirs=np.zeros(0, native.HALO_DIR_DTYPE),
                         unpack_dirs=np.zeros(0, native.HALO_DIR_DTYPE),
+                        post_dirs=np.zeros(0, native.HALO_DIR_DTYPE),
                         force_segs=np.zeros(0, native.FORCE_SEG_DTYPE))
     _build_routes(layout, topology, plan, rank)
     _build_force_segments(layout)
@@ -225,10 +230,15 @@ def _build_routes(layout, topology, plan, rank):
     send_off, layout.sends, layout.sendbuf_elems = segments(routes.sends, lambda d: d.recv_rank)
     recv_off, layout.recvs, layout.recvbuf_elems = segments(routes.recvs, lambda d: d.sender_rank)
 
-    # face-target pool: one entry per cell of every owned face that feeds a cut
+    # face-target pool: one entry per cell of every owned south / north face
+    # that feeds a cut -- the stage kernel forwards those rows as it writes
+    # them.  West / east (column) sources go through post_dirs instead: one
+    # strided copy pass after the stage, which costs far less than a
+    # single-lane scatter of P*4 values in every row of the boundary strips.
     face_base = {}
     size = 0
-    feeding = [(d, True) for d in routes.local] + [(d, False) for d in routes.sends]
+    feeding = [(d, True) for d in routes.local if d.src_face in ROW_FACES] + \
+              [(d, False) for d in routes.sends if d.src_face in ROW_FACES]
     for d, _ in feeding:
         key = (d.src_block, d.src_face)
         if key not in face_base:
@@ -272,6 +282,8 @@ def _build_routes(layout, topology, plan, rank):
     for k, d in enumerate(routes.sends):
         s_off, s_es, s_vs = slot_run(d.src_block, d.src_face, d.src_index(0), d.src_reversed, False)
         prime.append((s_off, s_es, s_vs, send_off[k], ds, 1, d.length, 0, 1, 0))
+    post = [row for row, d in zip(prime, list(routes.local) + list(routes.sends))
+            if d.src_face not in ROW_FACES]
     unpack = []
     for k, d in enumerate(routes.recvs):
         t_off, t_es, t_vs = slot_run(d.dst_block, d.dst_face, d.dst_index(0), d.dst_reversed, True)
@@ -279,6 +291,8 @@ def _build_routes(layout, topology, plan, rank):
     layout.prime_dirs = np.array(prime, dtype=native.HALO_DIR_DTYPE) if prime else \
         np.zeros(0, native.HALO_DIR_DTYPE)
     layout.unpack_dirs = np.array(unpack, dtype=native.HALO_DIR_DTYPE) if unpack else \
+        np.zeros(0, native.HALO_DIR_DTYPE)
+    layout.post_dirs = np.array(post, dtype=native.HALO_DIR_DTYPE) if post else \
         np.zeros(0, native.HALO_DIR_DTYPE)
     del planes
 

@@ -80,6 +80,7 @@ class EngineDesc(ctypes.Structure):
         ("norm_part", c_vp), ("sumsq", c_vp), ("status", c_vp), ("iter", c_vp),
         ("prime_dirs", c_vp), ("nprime", c_i32), ("prime_max_len", c_i32),
         ("unpack_dirs", c_vp), ("nunpack", c_i32), ("unpack_max_len", c_i32),
+        ("post_dirs", c_vp), ("npost", c_i32), ("post_max_len", c_i32),
         ("segs", c_vp), ("nsegs", c_i32),
         ("force_hist", c_vp),
         ("sends", ctypes.POINTER(PeerMsg)), ("nsends", c_i32),

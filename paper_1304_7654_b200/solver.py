@@ -214,6 +214,7 @@ class DeviceRank:
         self.t_faces = table(L.faces)
         self.t_prime = table(L.prime_dirs)
         self.t_unpack = table(L.unpack_dirs)
+        self.t_post = table(L.post_dirs)
         self.t_segs = table(L.force_segs)
         deriv = hbop.spectral_matrix(case.nharms, case.omega)
         self.dmat = np.ascontiguousarray(deriv.matrix)
@@ -308,6 +309,8 @@ class DeviceRank:
         d.prime_max_len = int(L.prime_dirs["length"].max()) if len(L.prime_dirs) else 0
         d.unpack_dirs, d.nunpack = self.t_unpack.data_ptr(), len(L.unpack_dirs)
         d.unpack_max_len = int(L.unpack_dirs["length"].max()) if len(L.unpack_dirs) else 0
+        d.post_dirs, d.npost = self.t_post.data_ptr(), len(L.post_dirs)
+        d.post_max_len = int(L.post_dirs["length"].max()) if len(L.post_dirs) else 0
         d.segs, d.nsegs = self.t_segs.data_ptr(), len(L.force_segs)
         d.force_hist = self.force_hist.data_ptr()
         self._sends = (native.PeerMsg * max(1, len(L.sends)))(

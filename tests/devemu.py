@@ -69,6 +69,7 @@ class RankEmulator:
         for b in self.L.blocks:
             self.view(out, b.id)[:, :, 1:b.nj + 1, 1:b.ni + 1] = new[b.id][:, :, 1:b.nj + 1, 1:b.ni + 1]
         self._forward(out, new)
+        self.halo(self.L.post_dirs, out)     # west / east columns (engine run_stage)
 
     def _forward(self, out, new):
         faces, tbl = self.L.faces, self.L.block_table
