@@ -413,7 +413,9 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
         cell_targets(a.faces, b, i, tl.j0, live, trow, tcol);
 
         // rows j0-1 and j0 -> registers; release row j0-1
-        double up[P], cur[P], dn[P];
+        // rows j-1, j, j+1 of this lane's column, rotated by the row step's
+        // argument order (the loop below is unrolled by 3: no register moves)
+        double ra[P], rb[P], rc3[P];
         {
             const RingPos c1 = advance<R>(cin);
             mbar_wait(full_in + cin.slot, cin.phase);
@@ -422,8 +424,8 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
             const double *r1 = ring + c1.slot * S::SLOT + in_off;
 #pragma unroll
             for (int m = 0; m < P; ++m) {
-                up[m] = r0[m * PT * G::BW];
-                cur[m] = r1[m * PT * G::BW];
+                ra[m] = r0[m * PT * G::BW];
+                rb[m] = r1[m * PT * G::BW];
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty_in + cin.slot);
@@ -431,7 +433,7 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
         }
         double nrm = 0.0;
 
-        for (int j = tl.j0; j <= tl.j1; ++j) {
+        auto row_step = [&](const int j, double(&up)[P], double(&cur)[P], double(&dn)[P]) {
             // prefetch the next row's halo targets (boundary cells only)
             FaceHit nrow, ncol;
             cell_targets(a.faces, b, i, j + 1, live && j < tl.j1, nrow, ncol);
@@ -551,17 +553,22 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
                         atomicMin(a.status + tl.bidx, divergence_key(gstage, lin));
                     }
             }
-#pragma unroll
-            for (int m = 0; m < P; ++m) {
-                up[m] = cur[m];
-                cur[m] = dn[m];
-            }
             trow = nrow;
             tcol = ncol;
             __syncwarp();
             if (lane == 0) mbar_arrive(empty_in + cin.slot);   // row j no longer read
             cin = nx;
             if (!FIRST) cq = advance<Q>(cq);
+        };
+        int j = tl.j0;
+        for (; j + 2 <= tl.j1; j += 3) {
+            row_step(j, ra, rb, rc3);
+            row_step(j + 1, rb, rc3, ra);
+            row_step(j + 2, rc3, ra, rb);
+        }
+        if (j <= tl.j1) {
+            row_step(j, ra, rb, rc3);
+            if (j + 1 <= tl.j1) row_step(j + 1, rb, rc3, ra);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty_in + cin.slot);   // row j1+1
