@@ -87,9 +87,12 @@ typedef struct hbgpu_block {
  *   ps <  0 : remote, send-buffer element off + n*4 + p (element-major,
  *             exchange.py:248-252).                                        */
 typedef struct hbgpu_face_target {
-    int64_t off;
+    int64_t off;         /* bit HBGPU_SECTOR_TARGET_BIT set (local targets):
+                            the cell's 32-byte sector holds no other cell of
+                            the block, so it may be written as a whole      */
     int64_t ps;
 } hbgpu_face_target;
+#define HBGPU_SECTOR_TARGET_BIT 62
 
 /* One halo copy direction for the standalone halo kernel (priming exchange,
  * unpack after a receive, exchange_halos).  Value v = n*4 + p of element e
@@ -274,9 +277,11 @@ typedef struct hbgpu_engine_desc {
     int32_t *iter;                   /* device, 1 element */
     const hbgpu_halo_dir *prime_dirs;  int32_t nprime;  int32_t prime_max_len;
     const hbgpu_halo_dir *unpack_dirs; int32_t nunpack; int32_t unpack_max_len;
-    /* after every stage: forwarding of west / east face columns (local halo
-     * copies and remote packs); south / north rows are forwarded inside the
-     * stage kernel through the face-target pool                            */
+    /* after the first stage: forwarding of west / east face columns (local
+     * halo copies and remote packs).  Inside the stage kernel the consumer
+     * warps forward south / north rows and, in the update stages, the TMA
+     * store warp forwards west / east columns from the staged row; both use
+     * the face-target pool                                                  */
     const hbgpu_halo_dir *post_dirs;   int32_t npost;   int32_t post_max_len;
     const hbgpu_force_seg *segs;     int32_t nsegs;  /* device */
     double *force_hist;              /* device [max_iters*3*planes*nbody] */

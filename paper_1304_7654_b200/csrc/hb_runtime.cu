@@ -216,8 +216,9 @@ int run_stage(hbgpu_engine *e, int st, cudaStream_t s) {
     a.norm_part = st == 0 ? d.norm_part : nullptr;
     int rc = hbgpu_stage(&a, s);
     if (!rc && st == 0) rc = hbgpu_norm_fold(d.blocks, d.nblocks, d.norm_part, d.sumsq, d.iter, s);
-    // west / east face columns: local halo copies and remote packs
-    if (!rc && d.npost > 0)
+    // first stage: west / east face columns, local halo copies and remote
+    // packs (the update stages forward them from their TMA store warp)
+    if (!rc && st == 0 && d.npost > 0)
         rc = hbgpu_halo(a.out, d.sendbuf, d.recvbuf, d.post_dirs, d.npost, d.post_max_len, d.planes, s);
     return rc;
 }
@@ -328,8 +329,8 @@ extern "C" int hbgpu_engine_unpack(hbgpu_engine *e, int32_t phase, void *stream)
 }
 
 extern "C" int hbgpu_engine_launches_per_iteration(const hbgpu_engine *e) {
-    int per_stage = 1 + (e->d.npost > 0 ? 1 : 0) + ((e->d.comm && !e->recvs.empty() && e->d.nunpack > 0) ? 1 : 0);
-    return 4 * per_stage + 2;
+    int per_stage = 1 + ((e->d.comm && !e->recvs.empty() && e->d.nunpack > 0) ? 1 : 0);
+    return 4 * per_stage + 2 + (e->d.npost > 0 ? 1 : 0);
 }
 
 static int iterate_on(hbgpu_engine *e, int32_t iterations, int32_t use_graph, cudaStream_t s);

@@ -214,10 +214,30 @@ __device__ __forceinline__ void cell_targets(const hbgpu_face_target *pool, cons
     else if (i == b.ni) tcol = load_target(pool, b.face_off[3], j - 1);
 }
 
+// the south/north face target of cell (i, j)
+__device__ __forceinline__ FaceHit row_target(const hbgpu_face_target *pool, const hbgpu_block &b, int i, int j,
+                                              bool live) {
+    if (!live) return FaceHit{0, 0};
+    if (j == 1) return load_target(pool, b.face_off[0], i - 1);
+    if (j == b.nj) return load_target(pool, b.face_off[1], i - 1);
+    return FaceHit{0, 0};
+}
+
 __device__ __forceinline__ void forward(const FaceHit &t, double *out, double *sendbuf, int n, int p,
                                         double v) {
+    constexpr int64_t SECTOR = (int64_t)1 << HBGPU_SECTOR_TARGET_BIT;
     if (t.ps > 0) {
-        out[t.off + (int64_t)(n * NPDE + p) * t.ps] = v;
+        double *dst = out + (t.off & ~SECTOR) + (int64_t)(n * NPDE + p) * t.ps;
+        if (t.off & SECTOR) {
+            // the whole 32-byte sector: the value in place, zeros in the lead /
+            // padding around it (no partial-sector fill in L2)
+            double2 *sec = reinterpret_cast<double2 *>((uintptr_t)dst & ~(uintptr_t)31);
+            const int pos = (int)(((uintptr_t)dst >> 3) & 3);
+            sec[0] = make_double2(pos == 0 ? v : 0.0, pos == 1 ? v : 0.0);
+            sec[1] = make_double2(pos == 2 ? v : 0.0, pos == 3 ? v : 0.0);
+        } else {
+            *dst = v;
+        }
     } else if (t.ps < 0) {
         sendbuf[t.off + n * NPDE + p] = v;
     }
@@ -354,23 +374,61 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
         // one TMA store per output row once all consumer threads have staged
         // it; the staging slot is handed back (to the q0 loads, or to the
         // consumers in the first stage) when the store has read it
-        if (lane != 0) return;
+        // The warp also forwards the strip's west / east face columns, cells
+        // i = 1 and i = ni, read back from the staged row: one lane per
+        // (plane, pde) value, off the consumers' critical path.
         RingPos ps{0, 0};
         for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
             const Tile tl = decode_tile<PT>(a, t);
             const CUtensorMap *mo = maps + (5 + a.out_slot) * a.nblocks + tl.bidx;
-            prefetch_tmap(mo);
+            if (lane == 0) prefetch_tmap(mo);
+            const hbgpu_block b = a.blocks[tl.bidx];
+            const int64_t west = tl.i0 == 1 ? b.face_off[2] : -1;
+            const int64_t east = tl.i0 + G::TCOLS > b.ni ? b.face_off[3] : -1;
+            constexpr int KV = (P * PT + 31) / 32;   // column values per lane
+            const int col_e = b.ni - tl.i0;
+            // targets are loaded a row ahead; values are read from the staged
+            // row into registers before the slot is handed back
+            FaceHit tw = load_target(a.faces, west, tl.j0 - 1), te = load_target(a.faces, east, tl.j0 - 1);
             for (int j = tl.j0; j <= tl.j1; ++j) {
                 mbar_wait(staged + ps.slot, ps.phase);
                 const double *src = FIRST ? oring + ps.slot * S::QSLOT : qring + ps.slot * S::QSLOT;
-                store_rows(mo, src, tl.i0 + LEAD, tl.pde0, j, inter);
-                bulk_commit();
-                bulk_wait_read_all();
-                mbar_arrive(FIRST ? out_free + ps.slot : empty_q + ps.slot);
+                if (lane == 0) {
+                    store_rows(mo, src, tl.i0 + LEAD, tl.pde0, j, inter);
+                    bulk_commit();
+                }
+                double vw[KV], ve[KV];
+#pragma unroll
+                for (int c = 0; c < KV; ++c) {   // value k = n * PT + pde within the tile
+                    const int k = lane + 32 * c;
+                    if (k < P * PT) {
+                        if (tw.ps != 0) vw[c] = src[k * G::TCOLS];
+                        if (te.ps != 0) ve[c] = src[k * G::TCOLS + col_e];
+                    }
+                }
+                const bool more = j < tl.j1;
+                const FaceHit nw = load_target(a.faces, more ? west : -1, j),
+                              ne = load_target(a.faces, more ? east : -1, j);
+                __syncwarp();
+                if (lane == 0) {
+                    bulk_wait_read_all();
+                    mbar_arrive(FIRST ? out_free + ps.slot : empty_q + ps.slot);
+                }
+#pragma unroll
+                for (int c = 0; c < KV; ++c) {
+                    const int k = lane + 32 * c;
+                    if (k < P * PT) {
+                        const int n = k / PT, pp = k - n * PT;
+                        if (tw.ps != 0) forward(tw, a.out, a.sendbuf, n, tl.pde0 + pp, vw[c]);
+                        if (te.ps != 0) forward(te, a.out, a.sendbuf, n, tl.pde0 + pp, ve[c]);
+                    }
+                }
+                tw = nw;
+                te = ne;
                 ps = advance<S::NS>(ps);
             }
         }
-        bulk_wait_all();
+        if (lane == 0) bulk_wait_all();
         return;
     }
 
@@ -409,8 +467,9 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
         double *const tail_out = a.out + b.base + (int64_t)p * b.ps + LEAD + i;
         const int64_t ps4 = b.ps * NPDE;
 
-        FaceHit trow, tcol;
-        cell_targets(a.faces, b, i, tl.j0, live, trow, tcol);
+        // south / north face rows are forwarded here; west / east columns by
+        // the store warp (update stages) or the engine's post pass (stage 1)
+        FaceHit trow = row_target(a.faces, b, i, tl.j0, live);
 
         // rows j0-1 and j0 -> registers; release row j0-1
         // rows j-1, j, j+1 of this lane's column, rotated by the row step's
@@ -435,8 +494,7 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
 
         auto row_step = [&](const int j, double(&up)[P], double(&cur)[P], double(&dn)[P]) {
             // prefetch the next row's halo targets (boundary cells only)
-            FaceHit nrow, ncol;
-            cell_targets(a.faces, b, i, j + 1, live && j < tl.j1, nrow, ncol);
+            const FaceHit nrow = row_target(a.faces, b, i, j + 1, live && j < tl.j1);
 
             const RingPos nx = advance<R>(cin);
             mbar_wait(full_in + nx.slot, nx.phase);
@@ -538,10 +596,6 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
 #pragma unroll
                 for (int n = 0; n < P; ++n) forward(trow, a.out, a.sendbuf, n, p, v[n]);
             }
-            if (tcol.ps != 0) {
-#pragma unroll
-                for (int n = 0; n < P; ++n) forward(tcol, a.out, a.sendbuf, n, p, v[n]);
-            }
             bool ok = true;
 #pragma unroll
             for (int n = 0; n < P; ++n) ok = ok && (MODE == 1 || finite_fp(v[n]));
@@ -554,7 +608,6 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
                     }
             }
             trow = nrow;
-            tcol = ncol;
             __syncwarp();
             if (lane == 0) mbar_arrive(empty_in + cin.slot);   // row j no longer read
             cin = nx;

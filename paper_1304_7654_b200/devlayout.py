@@ -35,7 +35,7 @@ from .cutplan import rank_routes
 from .hbop import forcing_vectors, stencil_coefficients
 
 ROW_LEAD = native.ROW_LEAD
-ROW_FACES = ("south", "north")    # faces forwarded inside the stage kernel
+SECTOR_TARGET = np.int64(1) << np.int64(62)   # face-target flag: whole-sector write allowed
 NPDE = native.NPDE
 WIDE_MIN_NI = 192         # blocks at least this wide use 256-column, 1-pde tiles
 BLOCK_ALIGN = 32          # elements (256 B)
@@ -230,15 +230,15 @@ def _build_routes(layout, topology, plan, rank):
     send_off, layout.sends, layout.sendbuf_elems = segments(routes.sends, lambda d: d.recv_rank)
     recv_off, layout.recvs, layout.recvbuf_elems = segments(routes.recvs, lambda d: d.sender_rank)
 
-    # face-target pool: one entry per cell of every owned south / north face
-    # that feeds a cut -- the stage kernel forwards those rows as it writes
-    # them.  West / east (column) sources go through post_dirs instead: one
-    # strided copy pass after the stage, which costs far less than a
-    # single-lane scatter of P*4 values in every row of the boundary strips.
+    # face-target pool: one entry per cell of every owned face that feeds a
+    # cut.  The stage kernel's consumer warps forward south / north rows as
+    # they compute them; west / east columns are forwarded by the TMA store
+    # warp from the staged output row (update stages) or, after the first
+    # stage, by one strided copy pass (post_dirs) -- a single-lane scatter of
+    # P*4 values in every row of the boundary strips would stall the tile.
     face_base = {}
     size = 0
-    feeding = [(d, True) for d in routes.local if d.src_face in ROW_FACES] + \
-              [(d, False) for d in routes.sends if d.src_face in ROW_FACES]
+    feeding = [(d, True) for d in routes.local] + [(d, False) for d in routes.sends]
     for d, _ in feeding:
         key = (d.src_block, d.src_face)
         if key not in face_base:
@@ -256,7 +256,14 @@ def _build_routes(layout, topology, plan, rank):
             lb = layout.local_index[d.dst_block]
             hj, hi = {"south": (0, kd), "north": (spec.nj + 1, kd), "west": (kd, 0),
                       "east": (kd, spec.ni + 1)}[d.dst_face]
-            faces["off"][fb + k - 1] = layout.base[lb] + hj * layout.rs[lb] + ROW_LEAD + hi
+            off = layout.base[lb] + hj * layout.rs[lb] + ROW_LEAD + hi
+            # a west halo cell is the last element of its 32-byte sector (the
+            # rest is row lead); an east one is the first when ni % 4 == 0 (the
+            # rest is row padding): such a target may be written as a whole
+            # sector, which spares L2 the partial-sector fill
+            if d.dst_face == "west" or (d.dst_face == "east" and spec.ni % 4 == 0):
+                off = off | SECTOR_TARGET
+            faces["off"][fb + k - 1] = off
             faces["ps"][fb + k - 1] = layout.ps[lb]
         else:
             faces["off"][fb + k - 1] = send_off[send_index[id(d)]] + e * ds
@@ -283,7 +290,7 @@ def _build_routes(layout, topology, plan, rank):
         s_off, s_es, s_vs = slot_run(d.src_block, d.src_face, d.src_index(0), d.src_reversed, False)
         prime.append((s_off, s_es, s_vs, send_off[k], ds, 1, d.length, 0, 1, 0))
     post = [row for row, d in zip(prime, list(routes.local) + list(routes.sends))
-            if d.src_face not in ROW_FACES]
+            if d.src_face in ("west", "east")]
     unpack = []
     for k, d in enumerate(routes.recvs):
         t_off, t_es, t_vs = slot_run(d.dst_block, d.dst_face, d.dst_index(0), d.dst_reversed, True)

@@ -68,18 +68,21 @@ class RankEmulator:
             new[b.id] = q
         for b in self.L.blocks:
             self.view(out, b.id)[:, :, 1:b.nj + 1, 1:b.ni + 1] = new[b.id][:, :, 1:b.nj + 1, 1:b.ni + 1]
-        self._forward(out, new)
-        self.halo(self.L.post_dirs, out)     # west / east columns (engine run_stage)
+        # south / north rows from the consumer warps; west / east columns from
+        # the store warp in the update stages, the post pass after stage 0
+        self._forward(out, new, columns=s > 0)
+        if s == 0:
+            self.halo(self.L.post_dirs, out)
 
-    def _forward(self, out, new):
+    def _forward(self, out, new, columns=True):
         faces, tbl = self.L.faces, self.L.block_table
         for k, b in enumerate(self.L.blocks):
             for face, fi in FACE_INDEX.items():
                 base = int(tbl["face_off"][k, fi])
-                if base < 0:
+                if base < 0 or (face in ("west", "east") and not columns):
                     continue
                 for c in range(b.face_extent(face)):
-                    off, ps = int(faces["off"][base + c]), int(faces["ps"][base + c])
+                    off, ps = int(faces["off"][base + c]) & ~(1 << 62), int(faces["ps"][base + c])
                     if ps == 0:
                         continue
                     j, i = {"south": (1, c + 1), "north": (b.nj, c + 1), "west": (c + 1, 1),
