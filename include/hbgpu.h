@@ -28,6 +28,8 @@ extern "C" {
 /* largest snapshot count of the library (forcing amplitudes travel as a
  * kernel parameter of HBGPU_MAX_P*4 doubles) */
 #define HBGPU_MAX_P 127
+/* largest snapshot count of the paired-stage kernel (shared-memory bound) */
+#define HBGPU_MAX_PAIR_P 9
 /* elements of the device row lead: cell i (0 = west halo) of row j sits at
  * row_base + HBGPU_ROW_LEAD + i, so interior cell i=1 -- and every stage
  * strip -- starts on a 64-byte DRAM access granule (rows are padded to a
@@ -158,6 +160,7 @@ typedef struct hbgpu_stage_args {
     const double *in;          /* slot read by the stencil (q_{s-1})       */
     const double *q0;          /* slot holding the iteration start (q_0)   */
     double *out;               /* slot written (q_s), may equal q0         */
+    const double *band;        /* pair != 0: the band slot (slot 2)        */
     double *sendbuf;           /* remote halo payloads (may be NULL)       */
     const hbgpu_block *blocks; /* device array [nblocks]                   */
     const int32_t *tile_block;  /* device array [total_tiles]: tile -> block */
@@ -180,14 +183,38 @@ typedef struct hbgpu_stage_args {
     int32_t tile_pdes;         /* pdes per tile: 4 (64-col strips) or 1
                                   (256-col strips)                          */
     int32_t out_slot;          /* which of the three slots `out` is (0..2) */
-    int32_t pad0;
+    int32_t pair;              /* 0: one stage.  1 / 2: two stages fused
+                                  (s, s+1) = (0, 1) / (2, 3): the first
+                                  stage's values at the tile perimeters come
+                                  from the band slot (hbgpu_band), slot 2  */
     double coef;               /* alpha_s * dtau                            */
+    double coef2;              /* alpha_{s+1} * dtau (pair != 0)            */
+    const struct hbgpu_band_seg *band_segs; /* hbgpu_band: device segments  */
+    int32_t nband_segs;
+    int32_t band_max_len;
     /* D row-major P x P with a +0.0 diagonal (hbcore.py:88-94); ap[n*4 + p]
      * = amp[n] (1 + p/4), zero except on planes 1 and 2 (hbcore.py:170-175):
      * the kernel adds those zero terms as exact signed zeros              */
     double D[HBGPU_MAX_TEMPLATED_P * HBGPU_MAX_TEMPLATED_P];
     double ap[HBGPU_MAX_P * HBGPU_NPDE];
 } hbgpu_stage_args;
+
+/* A run of tile-perimeter cells for hbgpu_band: `len` cells of block
+ * `block` from array cell (j, i) along a row (dir 0) or a column (dir 1). */
+typedef struct hbgpu_band_seg {
+    int32_t block;       /* local block index */
+    int32_t dir;
+    int32_t j, i;
+    int32_t len;
+    int32_t pad;
+} hbgpu_band_seg;
+
+/* One RK stage (args->stage, args->coef) at the listed cells only: the
+ * values the paired stage kernel (args->pair != 0) reads outside its tile.
+ * Writes them into args->out (the band slot) at their own cells and forwards
+ * cut-face cells into the band slot's halos / the send buffer, with the
+ * reference's rounding (hbcore.py:184-245) and divergence keys.            */
+int hbgpu_band(const hbgpu_stage_args *args, void *stream);
 
 /* one fused RK stage over every owned block: residual (hbcore.py:184-221),
  * update (hbcore.py:224-245), local halo forwarding and remote pack
@@ -207,9 +234,10 @@ int hbgpu_stage_prepare(int32_t planes);
  * strip-wide box over the block's sxy forcing table, sets 5..7 = strip-wide
  * store boxes over slot[0..2] whose column extent ends at cell ni (the
  * store clips the strip's columns past the block and never touches the
- * halo ring).  tile_pdes (4 or 1) fixes the strip geometry.
+ * halo ring), set 8 = strip-wide row box over slot[2] (the band slot), set
+ * 9 = one 64-byte column granule over slot[2] (a strip's edge columns).  tile_pdes (4 or 1) fixes the strip geometry.
  * out_bytes >= HBGPU_TMAP_SETS*nblocks*128.                                 */
-#define HBGPU_TMAP_SETS 8
+#define HBGPU_TMAP_SETS 10
 int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy,
                              const hbgpu_block *blocks_host,
                              int32_t nblocks, int32_t planes, int32_t tile_pdes,
@@ -283,6 +311,12 @@ typedef struct hbgpu_engine_desc {
      * store warp forwards west / east columns from the staged row; both use
      * the face-target pool                                                  */
     const hbgpu_halo_dir *post_dirs;   int32_t npost;   int32_t post_max_len;
+    /* fused != 0: each iteration runs band(0), pair(0,1), band(2), pair(2,3)
+     * and a full halo pass instead of four single stages; slot 2 holds the
+     * band values (hbgpu_band), band_segs lists the tile-perimeter cells   */
+    const hbgpu_band_seg *band_segs;   int32_t nband_segs; int32_t band_max_len;
+    int32_t fused;
+    int32_t pad1;
     const hbgpu_force_seg *segs;     int32_t nsegs;  /* device */
     double *force_hist;              /* device [max_iters*3*planes*nbody] */
     const hbgpu_peer_msg *sends;     int32_t nsends; /* HOST arrays */

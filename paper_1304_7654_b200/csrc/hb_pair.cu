@@ -1,0 +1,579 @@
+// hb_pair.cu -- two RK stages per pass.
+//
+// Stages 2-4 of the single-stage kernel are HBM-bound (they read q_{s-1} and
+// q_0 and write q_s: 96 B per unit) while their arithmetic would fit in far
+// less time.  Pairing stages (0, 1) and (2, 3) halves the traffic: a tile
+// computes the first stage's values v1 row by row and, one row behind, the
+// second stage's v2 from them, without v1 ever going to HBM.
+//
+// The catch is the stencil at the tile's edges: v2 at the first / last
+// column and row of a tile needs v1 just outside it -- in the neighbouring
+// strip or row tile (another CTA) or across a block face.  Those values come
+// from the band slot (slot 2): before each pair, hbgpu_band computes the
+// first stage at every tile-perimeter cell (about 1.6% of the cells at C4),
+// stores it there at the cell itself, and forwards cut-face cells into the
+// band slot's halo ring (and the send buffer for remote cuts).  Every value
+// is computed with the reference's per-point rounding wherever it is
+// computed, so the redundant copies are bitwise the tile's own.
+//
+//   iteration:  band(0)  pair(0,1) -> slot 1   band(2)  pair(2,3) -> slot 0
+//               (+ halo exchange after each, a full halo pass after the last)
+//
+// hbgpu_band (this file) is a plain kernel: one thread per (perimeter cell,
+// pde) computing all P snapshots.
+
+#include "hb_tma.cuh"
+
+#include <stdlib.h>
+#include <string.h>
+
+namespace hbgpu {
+
+// ---- band: the first stage of a pair at the tile-perimeter cells -----------------
+
+template <int P>
+__global__ void __launch_bounds__(128) band_kernel(const __grid_constant__ hbgpu_stage_args a) {
+    const hbgpu_band_seg sg = a.band_segs[blockIdx.y];
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= sg.len) return;
+    const int p = blockIdx.z;
+    const hbgpu_block b = a.blocks[sg.block];
+    const int j = sg.j + (sg.dir ? e : 0);
+    const int i = sg.i + (sg.dir ? 0 : e);
+    const int64_t ps4 = b.ps * NPDE;
+    const int64_t cell = b.base + (int64_t)p * b.ps + (int64_t)j * b.rs + LEAD + i;
+    const double *c = a.in + cell;
+    const bool first = a.stage == 0;
+    const double sv = a.sxy[b.sxy_off + (int64_t)(j - 1) * b.sxy_pitch + (i - 1)];
+    double cur[P];
+#pragma unroll
+    for (int m = 0; m < P; ++m) cur[m] = c[m * ps4];
+    FaceHit trow{0, 0}, tcol{0, 0};
+    if (j == 1) trow = load_target(a.faces, b.face_off[0], i - 1);
+    else if (j == b.nj) trow = load_target(a.faces, b.face_off[1], i - 1);
+    if (i == 1) tcol = load_target(a.faces, b.face_off[2], j - 1);
+    else if (i == b.ni) tcol = load_target(a.faces, b.face_off[3], j - 1);
+    const int gstage = (*a.iter) * 4 + a.stage + 1;
+#pragma unroll
+    for (int n = 0; n < P; ++n) {
+        const double *cn = c + n * ps4;
+        // hbcore.py:197-221: stencil, then m ascending (D[n][n] = +0 included
+        // as its exact 0*q product), then the forcing term
+        double o = stencil(cur[n], cn[-1], cn[1], cn[-b.rs], cn[b.rs], b.nu_h2, b.adv_2h);
+#pragma unroll
+        for (int m = 0; m < P; ++m) o = radd(o, rmul(a.D[n * P + m], cur[m]));
+        o = radd(o, rmul(a.ap[n * NPDE + p], sv));
+        const double base = first ? cur[n] : a.q0[cell + n * ps4];
+        const double v = rsub(base, rmul(a.coef, o));
+        a.out[cell + n * ps4] = v;
+        forward(trow, a.out, a.sendbuf, n, p, v);
+        forward(tcol, a.out, a.sendbuf, n, p, v);
+        if (nonfinite(v)) {
+            const long long lin = (((long long)(n * NPDE + p) * b.nj + (j - 1)) * b.ni) + (i - 1);
+            atomicMin(a.status + sg.block, divergence_key(gstage, lin));
+        }
+    }
+}
+
+template <int P>
+static int launch_band(const hbgpu_stage_args &a, cudaStream_t s) {
+    const dim3 grid((unsigned)((a.band_max_len + 127) / 128), (unsigned)a.nband_segs, NPDE);
+    band_kernel<P><<<grid, 128, 0, s>>>(a);
+    hbgpu_count_launch(1);
+    return hbgpu_check_launch("hbgpu_band");
+}
+
+// ---- the paired stage kernel ------------------------------------------------------
+//
+// Same CTA structure as stage_tma_kernel (hb_stage.cu): 8 consumer warps,
+// a TMA load warp, a TMA store warp; tiles of 256/PT columns x PT pdes x
+// tile_rows rows; lane = column.  Per row step r the consumers
+//   1. compute v1(r), the pair's first stage, from the stencil ring (rows
+//      r-1, r, r+1 of `in`, all read from shared memory);
+//   2. publish v1(r) in a 3-row shared ring and meet on a named barrier;
+//   3. compute v2(r-1), the second stage, from v1 rows r-2..r of their own
+//      column (registers) and v1(r-1) of the neighbouring columns (the
+//      shared ring, or -- at the strip's two edge columns -- the band slot's
+//      granules that ride on the stencil row's TMA transaction).
+// v1 above / below the tile (rows j0-1, j1+1) is read from the band slot.
+// Pass A (stages 0, 1) stores v2 with plain stores and forwards south/north
+// face rows; pass B (stages 2, 3) stages v2 in the q0 slot it replaces for
+// the TMA store warp and forwards nothing (a full halo pass follows).
+// Requires every block's ni to be a multiple of the strip width (all lanes
+// live); the engine falls back to single stages otherwise.
+
+template <int P, bool PB, int R, int Q, int PT>
+struct PairSmem {
+    using G = Geo<PT>;
+    static constexpr int BOXD = P * PT * G::BW;
+    static constexpr int REGION = (BOXD * 8 + 127) / 128 * 128 / 8;
+    static constexpr int EDGE = (P * PT * 8 * 8 + 127) / 128 * 128 / 8;   // {8 cols, PT, P} granule box
+    static constexpr int EDGE_W = G::NSPLIT * REGION;                     // band v1, column i0-1
+    static constexpr int EDGE_E = EDGE_W + EDGE;                          // band v1, column i0+TCOLS
+    static constexpr int SXY = EDGE_E + EDGE;
+    static constexpr int SLOT = SXY + G::TCOLS;
+    static constexpr int QSLOT = P * PT * G::TCOLS;
+    static constexpr int NQ = PB ? Q : 0;
+    static constexpr int NV = 3;                                          // v1 rows in flight
+    static constexpr size_t V1_OFF = ((size_t)R * SLOT + (size_t)NQ * QSLOT) * 8;
+    static constexpr size_t BAR_OFF = V1_OFF + (size_t)NV * QSLOT * 8;
+    static constexpr size_t BYTES = BAR_OFF + (size_t)(2 * R + 3 * NQ) * 8;
+    static_assert((SLOT * 8) % 128 == 0 && (QSLOT * 8) % 128 == 0, "TMA slots need 128-B alignment");
+};
+
+__device__ __forceinline__ void consumer_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(HBGPU_TILE_WARPS * 32) : "memory");
+}
+
+// o = residual, v = base - coef * o, with the stage kernel's operation order
+template <int P>
+__device__ __forceinline__ void stage_point(const double (&c)[P], const double (&w)[P], const double (&e)[P],
+                                            const double (&s)[P], const double (&nn)[P], const double (&dk)[P / 2 + 1],
+                                            const double (&ap)[P], double sv, double nu_h2, double adv_2h,
+                                            double coef, const double (&base)[P], double (&o)[P], double (&v)[P]) {
+#pragma unroll
+    for (int n = 0; n < P; ++n) o[n] = rmul(4.0, c[n]);
+#pragma unroll
+    for (int n = 0; n < P; ++n) o[n] = rsub(o[n], w[n]);
+#pragma unroll
+    for (int n = 0; n < P; ++n) o[n] = rsub(o[n], e[n]);
+#pragma unroll
+    for (int n = 0; n < P; ++n) o[n] = rsub(o[n], s[n]);
+#pragma unroll
+    for (int n = 0; n < P; ++n) o[n] = rsub(o[n], nn[n]);
+#pragma unroll
+    for (int n = 0; n < P; ++n) o[n] = rmul(o[n], nu_h2);
+#pragma unroll
+    for (int n = 0; n < P; ++n) o[n] = radd(o[n], rmul(rsub(e[n], w[n]), adv_2h));
+#pragma unroll
+    for (int m = 0; m < P; ++m) {
+        o[m] = radd(o[m], zero_times(c[m]));
+#pragma unroll
+        for (int k = 1; k <= P / 2; ++k) {
+            const double prod = rmul(dk[k], c[m]);
+            o[(m + k) % P] = radd(o[(m + k) % P], prod);
+            o[(m + P - k) % P] = rsub(o[(m + P - k) % P], prod);
+        }
+    }
+    const double sv0 = zero_times(sv);
+#pragma unroll
+    for (int n = 0; n < P; ++n) {
+        o[n] = radd(o[n], forced_plane(n) ? rmul(ap[n], sv) : sv0);
+        v[n] = rsub(base[n], rmul(coef, o[n]));
+    }
+}
+
+template <int P>
+__device__ __forceinline__ void record_nonfinite(const double (&v)[P], const hbgpu_stage_args &a, int bidx,
+                                                 const hbgpu_block &b, int p, int j, int i, int gstage) {
+    bool ok = true;
+#pragma unroll
+    for (int n = 0; n < P; ++n) ok = ok && finite_fp(v[n]);
+    if (!ok) {
+        for (int n = 0; n < P; ++n)
+            if (nonfinite(v[n])) {
+                const long long lin = (((long long)(n * NPDE + p) * b.nj + (j - 1)) * b.ni) + (i - 1);
+                atomicMin(a.status + bidx, divergence_key(gstage, lin));
+            }
+    }
+}
+
+template <int P, bool PB, int R, int Q, int PT>
+__global__ void __launch_bounds__(THREADS, 1) pair_tma_kernel(const __grid_constant__ hbgpu_stage_args a) {
+    using S = PairSmem<P, PB, R, Q, PT>;
+    using G = Geo<PT>;
+    static_assert(R >= 4 && (!PB || Q >= 3), "ring too short");
+    extern __shared__ __align__(1024) unsigned char smem[];
+    double *ring = reinterpret_cast<double *>(smem);
+    double *qring = ring + R * S::SLOT;
+    double *v1ring = reinterpret_cast<double *>(smem + S::V1_OFF);
+    uint64_t *full_in = reinterpret_cast<uint64_t *>(smem + S::BAR_OFF);
+    uint64_t *empty_in = full_in + R;
+    uint64_t *full_q = empty_in + R;
+    uint64_t *empty_q = full_q + S::NQ;   // q0 slot stored out and free (store warp)
+    uint64_t *staged = empty_q + S::NQ;   // v2 row written over it (consumers)
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < R; ++k) {
+            mbar_init(full_in + k, 1);
+            mbar_init(empty_in + k, CW);
+        }
+        for (int k = 0; k < S::NQ; ++k) {
+            mbar_init(full_q + k, 1);
+            mbar_init(empty_q + k, 1);
+            mbar_init(staged + k, CW * 32);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int ntile = a.total_tiles;
+    const CUtensorMap *maps = reinterpret_cast<const CUtensorMap *>(a.tmaps);
+    const bool inter = a.interleaved != 0;
+
+    if (warp == CW) {
+        // ------------------------------ producer ------------------------------
+        if (lane != 0) return;
+        constexpr uint32_t BYTES = S::BOXD * 8 * G::NSPLIT, QBYTES = S::QSLOT * 8, SBYTES = G::TCOLS * 8,
+                           EBYTES = P * PT * 8 * 8;
+        RingPos pin{0, 0}, pq{0, 0};
+        int issued_in = 0, issued_q = 0;
+        for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+            const Tile tl = decode_tile<PT>(a, t);
+            const CUtensorMap *min = maps + a.in_slot * a.nblocks + tl.bidx;
+            const CUtensorMap *mq = maps + 3 * a.nblocks + tl.bidx;
+            const CUtensorMap *ms = maps + 4 * a.nblocks + tl.bidx;
+            const CUtensorMap *me = maps + 9 * a.nblocks + tl.bidx;   // band slot, one granule
+            prefetch_tmap(min);
+            const int x = tl.i0 + LEAD - 2;
+            // entry of row `row`: the stencil row, sxy of row-1 (with_sxy) and
+            // the band values at the strip's two edge columns (with_edge)
+            auto put_in = [&](int row, bool with_sxy, bool with_edge) {
+                if (issued_in >= R) mbar_wait(empty_in + pin.slot, pin.phase ^ 1u);
+                else ++issued_in;
+                double *dst = ring + pin.slot * S::SLOT;
+                mbar_expect_tx(full_in + pin.slot, BYTES + (with_sxy ? SBYTES : 0) + (with_edge ? 2 * EBYTES : 0));
+#pragma unroll
+                for (int k = 0; k < G::NSPLIT; ++k)
+                    load_rows<PT>(dst + k * S::REGION, min, x + k * (G::TCOLS / G::NSPLIT), tl.pde0, row, inter,
+                                  full_in + pin.slot);
+                if (with_sxy) tma_load_2d(dst + S::SXY, ms, tl.i0 - 1, row - 2, full_in + pin.slot);
+                if (with_edge) {
+                    load_rows<PT>(dst + S::EDGE_W, me, tl.i0 + LEAD - 8, tl.pde0, row, inter, full_in + pin.slot);
+                    load_rows<PT>(dst + S::EDGE_E, me, tl.i0 + LEAD + G::TCOLS, tl.pde0, row, inter,
+                                  full_in + pin.slot);
+                }
+                pin = advance<R>(pin);
+            };
+            put_in(tl.j0 - 1, false, false);
+            put_in(tl.j0, false, true);
+            for (int j = tl.j0; j <= tl.j1; ++j) {
+                put_in(j + 1, true, j + 1 <= tl.j1);
+                if (PB) {
+                    if (issued_q >= Q) mbar_wait(empty_q + pq.slot, pq.phase ^ 1u);
+                    else ++issued_q;
+                    mbar_expect_tx(full_q + pq.slot, QBYTES);
+                    load_rows<PT>(qring + pq.slot * S::QSLOT, mq, x + 2, tl.pde0, j, inter, full_q + pq.slot);
+                    pq = advance<Q>(pq);
+                }
+            }
+        }
+        return;
+    }
+    if (warp == CW + 1) {
+        // ----------------------- store warp (pass B only) -----------------------
+        if (!PB || lane != 0) return;
+        RingPos ps{0, 0};
+        for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+            const Tile tl = decode_tile<PT>(a, t);
+            const CUtensorMap *mo = maps + (5 + a.out_slot) * a.nblocks + tl.bidx;
+            prefetch_tmap(mo);
+            for (int j = tl.j0; j <= tl.j1; ++j) {
+                mbar_wait(staged + ps.slot, ps.phase);
+                store_rows(mo, qring + ps.slot * S::QSLOT, tl.i0 + LEAD, tl.pde0, j, inter);
+                bulk_commit();
+                bulk_wait_read_all();
+                mbar_arrive(empty_q + ps.slot);
+                ps = advance<Q>(ps);
+            }
+        }
+        bulk_wait_all();
+        return;
+    }
+
+    // -------------------------------- consumers ---------------------------------
+    const int pp = warp % PT;
+    const int cw = warp / PT;
+    const int col0 = 32 * cw + lane;
+    const int in_off = (cw / G::CWPR) * S::REGION + pp * G::BW + 32 * (cw % G::CWPR) + lane + 2;
+    const int q_off = pp * G::TCOLS + col0;
+    // this lane's west / east v1 neighbour for the second stage: the shared v1
+    // row, or the band granule at the strip's edges (element 7 / 0 of it)
+    const bool west_edge = col0 == 0, east_edge = col0 == G::TCOLS - 1;
+    const int w_off = west_edge ? S::EDGE_W + pp * 8 + 7 : q_off - 1;      // + n * (PT*8 | PT*TCOLS)
+    const int e_off = east_edge ? S::EDGE_E + pp * 8 : q_off + 1;
+    const int w_nstride = west_edge ? PT * 8 : PT * G::TCOLS;
+    const int e_nstride = east_edge ? PT * 8 : PT * G::TCOLS;
+    const int gstage = (*a.iter) * 4 + a.stage + 1;   // first stage of the pair; +1 for the second
+    const double coef1 = a.coef, coef2 = a.coef2;
+    double dk[P / 2 + 1];
+#pragma unroll
+    for (int k = 1; k <= P / 2; ++k) dk[k] = a.D[k * P];
+    RingPos cin{0, 0}, cq{0, 0};
+    int ap_pde = -1;
+    double ap[P];
+    int vr = 0;   // v1 ring row of v1(r)
+    for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+        const Tile tl = decode_tile<PT>(a, t);
+        const int p = tl.pde0 + pp;
+        if (p != ap_pde) {
+#pragma unroll
+            for (int n = 0; n < P; ++n) ap[n] = a.ap[n * NPDE + p];
+            ap_pde = p;
+        }
+        const hbgpu_block b = a.blocks[tl.bidx];
+        const double nu_h2 = b.nu_h2, adv_2h = b.adv_2h;
+        const int i = tl.i0 + col0;
+        const int64_t ps4 = b.ps * NPDE;
+        const int64_t colbase = b.base + (int64_t)p * b.ps + LEAD + i;   // (n=0, p, j=0, i)
+        // v1 of row j0-1 (band slot: the neighbouring row tile's perimeter
+        // row, or the block's halo row)
+        double va[P], vb[P], vc[P];
+#pragma unroll
+        for (int n = 0; n < P; ++n) vb[n] = __ldg(a.band + colbase + n * ps4 + (int64_t)(tl.j0 - 1) * b.rs);
+        FaceHit trow = PB ? FaceHit{0, 0} : row_target(a.faces, b, i, tl.j0, true);
+        double nrm = 0.0;
+        double sv_prev = 0.0;
+        RingPos cprev{0, 0};   // stencil entry of row r-1
+        {
+            // row j0-1 entry: only its stencil row is used (as v1(j0)'s south)
+            cprev = cin;
+            cin = advance<R>(cin);
+        }
+        // one row step: v1(r) and, one row behind, v2(r-1)
+        auto row_step = [&](const int r, double(&pa)[P], double(&pb)[P], double(&pc)[P]) {
+            const RingPos nx = advance<R>(cin);
+            mbar_wait(full_in + cprev.slot, cprev.phase);
+            mbar_wait(full_in + cin.slot, cin.phase);
+            mbar_wait(full_in + nx.slot, nx.phase);
+            const double *ru = ring + cprev.slot * S::SLOT + in_off;
+            const double *rc = ring + cin.slot * S::SLOT + in_off;
+            const double *rn = ring + nx.slot * S::SLOT + in_off;
+            const double sv = ring[nx.slot * S::SLOT + S::SXY + col0];
+            const double *qv = nullptr;
+            if (PB) {
+                mbar_wait(full_q + cq.slot, cq.phase);
+                qv = qring + cq.slot * S::QSLOT + q_off;
+            }
+            double o[P], v[P];
+            {
+                double c[P], w[P], e[P], s[P], nn[P], base[P];
+#pragma unroll
+                for (int n = 0; n < P; ++n) {
+                    c[n] = rc[n * PT * G::BW];
+                    w[n] = rc[n * PT * G::BW - 1];
+                    e[n] = rc[n * PT * G::BW + 1];
+                    s[n] = ru[n * PT * G::BW];
+                    nn[n] = rn[n * PT * G::BW];
+                    base[n] = PB ? qv[n * PT * G::TCOLS] : c[n];
+                }
+                stage_point<P>(c, w, e, s, nn, dk, ap, sv, nu_h2, adv_2h, coef1, base, o, pc);
+            }
+            if (!PB) {
+#pragma unroll
+                for (int n = 0; n < P; ++n) nrm = __fma_rn(o[n], o[n], nrm);
+            }
+            record_nonfinite<P>(pc, a, tl.bidx, b, p, r, i, gstage);
+            double *vrow = v1ring + vr * S::QSLOT + q_off;
+#pragma unroll
+            for (int n = 0; n < P; ++n) vrow[n * PT * G::TCOLS] = pc[n];
+            consumer_sync();
+            if (r > tl.j0) {
+                // second stage at row r-1
+                const int vp = vr == 0 ? S::NV - 1 : vr - 1;   // v1 ring row of v1(r-1)
+                const double *vw = west_edge ? ring + cprev.slot * S::SLOT + w_off : v1ring + vp * S::QSLOT + w_off;
+                const double *ve = east_edge ? ring + cprev.slot * S::SLOT + e_off : v1ring + vp * S::QSLOT + e_off;
+                double w2[P], e2[P], base2[P];
+#pragma unroll
+                for (int n = 0; n < P; ++n) {
+                    w2[n] = vw[n * w_nstride];
+                    e2[n] = ve[n * e_nstride];
+                }
+                if (PB) {
+                    // q0 of row r-1: the previous q slot
+                    const RingPos cqp = cq.slot == 0 ? RingPos{Q - 1, cq.phase ^ 1u} : RingPos{cq.slot - 1, cq.phase};
+                    const double *qp = qring + cqp.slot * S::QSLOT + q_off;
+#pragma unroll
+                    for (int n = 0; n < P; ++n) base2[n] = qp[n * PT * G::TCOLS];
+                    stage_point<P>(pb, w2, e2, pa, pc, dk, ap, sv_prev, nu_h2, adv_2h, coef2, base2, o, v);
+                    double *stage_row = qring + cqp.slot * S::QSLOT + q_off;
+#pragma unroll
+                    for (int n = 0; n < P; ++n) stage_row[n * PT * G::TCOLS] = v[n];
+                    fence_proxy_async_smem();
+                    mbar_arrive(staged + cqp.slot);
+                } else {
+#pragma unroll
+                    for (int n = 0; n < P; ++n) base2[n] = ru[n * PT * G::BW];   // q0 = in, row r-1
+                    stage_point<P>(pb, w2, e2, pa, pc, dk, ap, sv_prev, nu_h2, adv_2h, coef2, base2, o, v);
+                    const int64_t row = (int64_t)(r - 1) * b.rs;
+#pragma unroll
+                    for (int n = 0; n < P; ++n) a.out[colbase + n * ps4 + row] = v[n];
+                    if (trow.ps != 0) {
+#pragma unroll
+                        for (int n = 0; n < P; ++n) forward(trow, a.out, a.sendbuf, n, p, v[n]);
+                    }
+                    trow = row_target(a.faces, b, i, r, true);
+                }
+                record_nonfinite<P>(v, a, tl.bidx, b, p, r - 1, i, gstage + 1);
+            }
+            sv_prev = sv;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty_in + cprev.slot);   // row r-1 no longer read
+            cprev = cin;
+            cin = nx;
+            if (PB) cq = advance<Q>(cq);
+            vr = vr == S::NV - 1 ? 0 : vr + 1;
+        };
+        // v1 window (pa, pb) = (v1(r-2), v1(r-1)) on entry of step r; pc <- v1(r)
+        int r = tl.j0;
+        for (; r + 2 <= tl.j1; r += 3) {
+            row_step(r, va, vb, vc);
+            row_step(r + 1, vb, vc, va);
+            row_step(r + 2, vc, va, vb);
+        }
+        // last second-stage row: v2(j1) from the window (A, B) = (v1(j1-1),
+        // v1(j1)) and v1(j1+1) from the band slot; cprev is the entry of row
+        // j1 (v1(j1)'s edge granules and, pass A, q0 row j1)
+        auto last_step = [&](double(&A)[P], double(&B)[P]) {
+            double vd[P];
+#pragma unroll
+            for (int n = 0; n < P; ++n) vd[n] = __ldg(a.band + colbase + n * ps4 + (int64_t)(tl.j1 + 1) * b.rs);
+            const int vp = vr == 0 ? S::NV - 1 : vr - 1;   // v1 ring row of v1(j1)
+            const double *vw = west_edge ? ring + cprev.slot * S::SLOT + w_off : v1ring + vp * S::QSLOT + w_off;
+            const double *ve = east_edge ? ring + cprev.slot * S::SLOT + e_off : v1ring + vp * S::QSLOT + e_off;
+            double w2[P], e2[P], base2[P], o[P], v[P];
+#pragma unroll
+            for (int n = 0; n < P; ++n) {
+                w2[n] = vw[n * w_nstride];
+                e2[n] = ve[n * e_nstride];
+            }
+            const double *ru = ring + cprev.slot * S::SLOT + in_off;
+            if (PB) {
+                const RingPos cqp = cq.slot == 0 ? RingPos{Q - 1, cq.phase ^ 1u} : RingPos{cq.slot - 1, cq.phase};
+                const double *qp = qring + cqp.slot * S::QSLOT + q_off;
+#pragma unroll
+                for (int n = 0; n < P; ++n) base2[n] = qp[n * PT * G::TCOLS];
+                stage_point<P>(B, w2, e2, A, vd, dk, ap, sv_prev, nu_h2, adv_2h, coef2, base2, o, v);
+                double *stage_row = qring + cqp.slot * S::QSLOT + q_off;
+#pragma unroll
+                for (int n = 0; n < P; ++n) stage_row[n * PT * G::TCOLS] = v[n];
+                fence_proxy_async_smem();
+                mbar_arrive(staged + cqp.slot);
+            } else {
+#pragma unroll
+                for (int n = 0; n < P; ++n) base2[n] = ru[n * PT * G::BW];
+                stage_point<P>(B, w2, e2, A, vd, dk, ap, sv_prev, nu_h2, adv_2h, coef2, base2, o, v);
+                const int64_t row = (int64_t)tl.j1 * b.rs;
+#pragma unroll
+                for (int n = 0; n < P; ++n) a.out[colbase + n * ps4 + row] = v[n];
+                if (trow.ps != 0) {
+#pragma unroll
+                    for (int n = 0; n < P; ++n) forward(trow, a.out, a.sendbuf, n, p, v[n]);
+                }
+            }
+            record_nonfinite<P>(v, a, tl.bidx, b, p, tl.j1, i, gstage + 1);
+        };
+        if (r > tl.j1) {
+            last_step(va, vb);
+        } else if (r == tl.j1) {
+            row_step(r, va, vb, vc);
+            last_step(vb, vc);
+        } else {
+            row_step(r, va, vb, vc);
+            row_step(r + 1, vb, vc, va);
+            last_step(vc, va);
+        }
+        // every consumer is past its reads of the v1 ring before the next
+        // tile's first row overwrites it
+        consumer_sync();
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(empty_in + cprev.slot);   // row j1
+            mbar_arrive(empty_in + cin.slot);     // row j1+1
+        }
+        cin = advance<R>(cin);
+        if (!PB && a.norm_part != nullptr) {
+            const double s = warp_sum(nrm);
+            if (lane == 0) a.norm_part[(int64_t)t * CW + warp] = s;
+        }
+    }
+}
+
+// ---- launch ---------------------------------------------------------------------
+
+struct PairLaunch {
+    void (*fn)(hbgpu_stage_args) = nullptr;
+    size_t smem = 0;
+    int grid = 0;
+    bool ready = false;
+};
+
+template <int P, bool PB, int R, int Q, int PT>
+static int prepare_pair(PairLaunch &L) {
+    if (L.ready) return HBGPU_OK;
+    L.fn = pair_tma_kernel<P, PB, R, Q, PT>;
+    L.smem = PairSmem<P, PB, R, Q, PT>::BYTES;
+    if (cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem) != cudaSuccess)
+        return hbgpu_check_launch("pair kernel smem attribute");
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.fn, THREADS, L.smem) != cudaSuccess || per_sm < 1)
+        return hbgpu_check_launch("pair kernel occupancy");
+    L.grid = sms * per_sm;
+    L.ready = true;
+    return HBGPU_OK;
+}
+
+template <int P, int PT>
+static int pair_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
+    static PairLaunch la, lb;
+    int rc = prepare_pair<P, false, 4, 3, PT>(la);
+    if (!rc) rc = prepare_pair<P, true, 4, 3, PT>(lb);
+    if (rc || prepare_only) return rc;
+    if (a.tmaps == nullptr || a.band == nullptr) {
+        hbgpu_set_error("hbgpu_stage (pair): args->tmaps and args->band are required");
+        return HBGPU_ERR_ARG;
+    }
+    PairLaunch &L = a.pair == 2 ? lb : la;
+    const int grid = min(L.grid, a.total_tiles);
+    L.fn<<<grid, THREADS, L.smem, s>>>(a);
+    hbgpu_count_launch(1);
+    return hbgpu_check_launch("hbgpu_stage (pair)");
+}
+
+template <int P>
+static int pair_p(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
+    return a.tile_pdes == 1 ? pair_cfg<P, 1>(a, s, prepare_only) : pair_cfg<P, 4>(a, s, prepare_only);
+}
+
+int pair_dispatch(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
+    switch (a.planes) {
+        case 1: return pair_p<1>(a, s, prepare_only);
+        case 3: return pair_p<3>(a, s, prepare_only);
+        case 5: return pair_p<5>(a, s, prepare_only);
+        case 7: return pair_p<7>(a, s, prepare_only);
+        case 9: return pair_p<9>(a, s, prepare_only);
+        default: break;
+    }
+    // the stencil ring, the v1 ring and the q0 ring of pass B fit the 227 KB
+    // of shared memory up to P = 9
+    hbgpu_set_error("paired stages need P <= %d, got %d", HBGPU_MAX_PAIR_P, a.planes);
+    return HBGPU_ERR_UNSUPPORTED;
+}
+
+}  // namespace hbgpu
+
+extern "C" int hbgpu_band(const hbgpu_stage_args *a, void *stream) {
+    using namespace hbgpu;
+    if (a == nullptr || a->nband_segs < 0 || a->nband_segs > 65535 || a->band_max_len < 0) {
+        hbgpu_set_error("hbgpu_band: bad arguments");
+        return HBGPU_ERR_ARG;
+    }
+    if (a->nband_segs == 0 || a->band_max_len == 0) return HBGPU_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (a->planes) {
+        case 1: return launch_band<1>(*a, s);
+        case 3: return launch_band<3>(*a, s);
+        case 5: return launch_band<5>(*a, s);
+        case 7: return launch_band<7>(*a, s);
+        case 9: return launch_band<9>(*a, s);
+        case 11: return launch_band<11>(*a, s);
+        case 13: return launch_band<13>(*a, s);
+        case 15: return launch_band<15>(*a, s);
+        case 17: return launch_band<17>(*a, s);
+        default: break;
+    }
+    hbgpu_set_error("hbgpu_band: P=%d is above the templated range (%d)", a->planes, HBGPU_MAX_TEMPLATED_P);
+    return HBGPU_ERR_UNSUPPORTED;
+}

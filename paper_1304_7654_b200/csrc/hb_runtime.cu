@@ -184,9 +184,74 @@ int exchange_remote(hbgpu_engine *e, double *slot, cudaStream_t s) {
     return hbgpu_halo(slot, d.sendbuf, d.recvbuf, d.unpack_dirs, d.nunpack, d.unpack_max_len, d.planes, s);
 }
 
+// fused (paired) schedule, per phase: (stencil slot, output slot)
+//   0: band(0)     A -> C (perimeter cells + halos)
+//   1: pair(0, 1)  A (+ band C) -> B
+//   2: band(2)     B, base A -> C
+//   3: pair(2, 3)  B, base A (+ band C) -> A, then a full halo pass on A
+constexpr int kInF[4] = {0, 0, 1, 1};
+constexpr int kOutF[4] = {2, 1, 2, 0};
+
+inline int out_slot(const hbgpu_engine_desc &d, int phase) { return d.fused ? kOutF[phase] : kOut[phase]; }
+
+void fill_args(const hbgpu_engine_desc &d, hbgpu_stage_args &a) {
+    memset(&a, 0, sizeof(a));
+    a.q0 = d.slot[0];
+    a.band = d.slot[2];
+    a.sendbuf = d.sendbuf;
+    a.blocks = d.blocks;
+    a.tile_block = d.tile_block;
+    a.sxy = d.sxy;
+    a.faces = d.faces;
+    a.status = d.status;
+    a.iter = d.iter;
+    a.dmat = d.dmat;
+    a.tmaps = d.tmaps;
+    a.nblocks = d.nblocks;
+    a.total_tiles = d.total_tiles;
+    a.planes = d.planes;
+    a.tile_rows = d.tile_rows;
+    a.interleaved = d.interleaved;
+    a.tile_pdes = d.tile_pdes;
+    a.band_segs = d.band_segs;
+    a.nband_segs = d.nband_segs;
+    a.band_max_len = d.band_max_len;
+    memcpy(a.D, d.D, sizeof(a.D));
+    memcpy(a.ap, d.ap, sizeof(a.ap));
+}
+
+// phase `ph` of the paired schedule (hb_pair.cu)
+int run_fused_phase(hbgpu_engine *e, int ph, cudaStream_t s) {
+    const hbgpu_engine_desc &d = e->d;
+    hbgpu_stage_args a;
+    fill_args(d, a);
+    const int st = ph < 2 ? 0 : 2;   // the first stage of the pair
+    a.in = d.slot[kInF[ph]];
+    a.in_slot = kInF[ph];
+    a.out = d.slot[kOutF[ph]];
+    a.out_slot = kOutF[ph];
+    a.stage = st;
+    a.coef = d.coef[st];
+    if (ph == 0 || ph == 2) return hbgpu_band(&a, s);
+    a.pair = ph == 1 ? 1 : 2;
+    a.coef2 = d.coef[st + 1];
+    a.norm_part = ph == 1 ? d.norm_part : nullptr;
+    int rc = hbgpu_stage(&a, s);
+    if (!rc && ph == 1) rc = hbgpu_norm_fold(d.blocks, d.nblocks, d.norm_part, d.sumsq, d.iter, s);
+    // pass A forwards south/north rows itself; west/east columns here
+    if (!rc && ph == 1 && d.npost > 0)
+        rc = hbgpu_halo(a.out, d.sendbuf, d.recvbuf, d.post_dirs, d.npost, d.post_max_len, d.planes, s);
+    // pass B writes q4 over q0, which other tiles still read as their base,
+    // so it forwards nothing: a full halo pass fills the new state's halos
+    if (!rc && ph == 3 && d.nprime > 0)
+        rc = hbgpu_halo(d.slot[0], d.sendbuf, d.recvbuf, d.prime_dirs, d.nprime, d.prime_max_len, d.planes, s);
+    return rc;
+}
+
 // the fused stage kernel of RK stage `st` (+ the norm fold after stage 0)
 int run_stage(hbgpu_engine *e, int st, cudaStream_t s) {
     const hbgpu_engine_desc &d = e->d;
+    if (d.fused) return run_fused_phase(e, st, s);
     hbgpu_stage_args a;
     memset(&a, 0, sizeof(a));
     a.q0 = d.slot[0];
@@ -227,7 +292,7 @@ int one_iteration(hbgpu_engine *e, cudaStream_t s) {
     const hbgpu_engine_desc &d = e->d;
     for (int st = 0; st < 4; ++st) {
         int rc = run_stage(e, st, s);
-        if (!rc) rc = exchange_remote(e, d.slot[kOut[st]], s);
+        if (!rc) rc = exchange_remote(e, d.slot[out_slot(d, st)], s);
         if (rc) return rc;
     }
     return hbgpu_forces(d.slot[0], d.segs, d.nsegs, d.planes, d.nbody, d.force_hist, d.iter, s);
@@ -323,13 +388,15 @@ extern "C" int hbgpu_engine_unpack(hbgpu_engine *e, int32_t phase, void *stream)
     int rc = enter(e, caller);
     if (rc) return rc;
     const hbgpu_engine_desc &d = e->d;
-    double *slot = phase < 0 ? d.slot[0] : d.slot[kOut[phase]];
+    double *slot = phase < 0 ? d.slot[0] : d.slot[out_slot(d, phase)];
     rc = hbgpu_halo(slot, d.sendbuf, d.recvbuf, d.unpack_dirs, d.nunpack, d.unpack_max_len, d.planes, e->work);
     return leave(e, caller, rc);
 }
 
 extern "C" int hbgpu_engine_launches_per_iteration(const hbgpu_engine *e) {
     int per_stage = 1 + ((e->d.comm && !e->recvs.empty() && e->d.nunpack > 0) ? 1 : 0);
+    if (e->d.fused)   // band, pair + norm fold (+ post), band, pair (+ halo pass), forces
+        return 4 * per_stage + 2 + (e->d.npost > 0 ? 1 : 0) + (e->d.nprime > 0 ? 1 : 0);
     return 4 * per_stage + 2 + (e->d.npost > 0 ? 1 : 0);
 }
 

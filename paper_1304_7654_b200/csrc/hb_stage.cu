@@ -604,6 +604,13 @@ static int dispatch(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only
         hbgpu_set_error("hbgpu_stage: tile_pdes must be 1 or 4, got %d", a.tile_pdes);
         return HBGPU_ERR_ARG;
     }
+    if (a.pair != 0) {
+        if (!prepare_only && !circulant_antisymmetric(a.D, a.planes)) {
+            hbgpu_set_error("hbgpu_stage: D must be the spectral matrix (+0.0 diagonal, D[m+k][m] == D[k][0] == -D[m-k][m])");
+            return HBGPU_ERR_ARG;
+        }
+        return pair_dispatch(a, s, prepare_only);
+    }
     if (!prepare_only && a.planes <= HBGPU_MAX_TEMPLATED_P && !circulant_antisymmetric(a.D, a.planes)) {
         hbgpu_set_error("hbgpu_stage: D must be the spectral matrix (+0.0 diagonal, D[m+k][m] == D[k][0] == -D[m-k][m])");
         return HBGPU_ERR_ARG;
@@ -665,7 +672,12 @@ extern "C" int hbgpu_stage_prepare(int32_t planes) {
     int rc = HBGPU_OK;
     for (int pt : {1, 4}) {
         a.tile_pdes = pt;
+        a.pair = 0;
         rc = rc ? rc : hbgpu::dispatch(a, nullptr, true);
+        if (planes <= HBGPU_MAX_PAIR_P) {
+            a.pair = 1;
+            rc = rc ? rc : hbgpu::dispatch(a, nullptr, true);
+        }
     }
     return rc;
 }
@@ -717,13 +729,15 @@ extern "C" int hbgpu_encode_tensor_maps(double *const slot[3], const double *sxy
                 // plane-major (cols, rows, pde, plane), interleaved (cols, pde,
                 // plane, rows); both land in smem as [plane][pde][cols]
                 const bool inter = b.rs > b.ps;
-                const cuuint32_t w = s < 3 ? bw : tcols;
+                // sets 8 / 9: strip-wide row box / one 8-column granule over the
+                // band slot (slot 2), read by the paired-stage kernel
+                const cuuint32_t w = s < 3 ? bw : s == 9 ? 8u : tcols;
                 const cuuint32_t npd = (cuuint32_t)tile_pdes;
                 // store extent: columns up to store_cols(ni), a 64-B boundary,
                 // so no store granule reaches the east halo cell (the kernel
                 // writes the <= 7 columns past it with plain stores)
-                const cuuint64_t cols = s >= 5 ? (cuuint64_t)(LEAD + 1 + store_cols(b.ni)) : (cuuint64_t)b.pitch;
-                const int slot_k = s < 3 ? s : s == 3 ? 0 : s - 5;
+                const cuuint64_t cols = (s >= 5 && s <= 7) ? (cuuint64_t)(LEAD + 1 + store_cols(b.ni)) : (cuuint64_t)b.pitch;
+                const int slot_k = s < 3 ? s : s == 3 ? 0 : s <= 7 ? s - 5 : 2;
                 cuuint64_t dims[4], strides[3];
                 cuuint32_t box[4];
                 if (inter) {

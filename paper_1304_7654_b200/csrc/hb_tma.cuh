@@ -205,4 +205,8 @@ __device__ __forceinline__ void store_rows(const void *map, const void *src, int
     else tma_store_4d(map, x, row, pde0, 0, src);
 }
 
+// hb_pair.cu: launch (or, prepare_only, just configure) the paired-stage
+// kernel for args.pair = 1 (stages 0, 1) or 2 (stages 2, 3)
+int pair_dispatch(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only);
+
 }  // namespace hbgpu

@@ -94,7 +94,7 @@ class RankLayout:
     faces: np.ndarray
     prime_dirs: np.ndarray
     unpack_dirs: np.ndarray
-    post_dirs: np.ndarray           # column-face forwarding after every stage
+    post_dirs: np.ndarray           # column-face forwarding after the first stage
     force_segs: np.ndarray
     sends: list = field(default_factory=list)     # (peer, offset, count)
     recvs: list = field(default_factory=list)
@@ -102,6 +102,9 @@ class RankLayout:
     recvbuf_elems: int = 0
     interleaved: bool = False
     tile_pdes: int = 4
+    band_segs: np.ndarray = None    # tile-perimeter cells (paired stages)
+    band_max_len: int = 0
+    fused: bool = False             # paired stages (hb_pair.cu)
 
     def elem(self, gid, n, p, j, i):
         """Slot element index of (n, p, j, i) -- array coordinates -- of block gid."""
@@ -134,7 +137,7 @@ def _halo_cell(spec, face, k):
 
 
 def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None,
-                      interleaved=None, tile_pdes=None):
+                      interleaved=None, tile_pdes=None, fused=None):
     """Device layout of one rank's blocks.
 
     interleaved=False: plane-major slots, (n, p) planes of (nj+2) x pitch;
@@ -198,7 +201,36 @@ def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None,
                         force_segs=np.zeros(0, native.FORCE_SEG_DTYPE))
     _build_routes(layout, topology, plan, rank)
     _build_force_segments(layout)
+    _build_band(layout, fused)
     return layout
+
+
+def fused_eligible(blocks, planes, tile_pdes):
+    """Paired stages need P <= MAX_PAIR_P (shared memory) and full strips
+    (every ni a multiple of the strip width, so every lane is live)."""
+    if os.environ.get("HBGPU_FUSED", "1") == "0":
+        return False
+    width = native.TILE_COLS[tile_pdes]
+    return planes <= native.MAX_PAIR_P and all(b.ni % width == 0 for b in blocks)
+
+
+def _build_band(layout, fused):
+    """Row and column runs covering every tile's perimeter cells: the first
+    and last row of each row tile and the first and last column of each
+    strip, over the whole block (hbgpu_band computes the first stage of a
+    pair there; the paired kernel reads it across tile edges)."""
+    eligible = fused_eligible(layout.blocks, layout.planes, layout.tile_pdes)
+    layout.fused = eligible if fused is None else (bool(fused) and eligible)
+    width = native.TILE_COLS[layout.tile_pdes]
+    segs = []
+    for k, b in enumerate(layout.blocks):
+        rows = sorted({r for j0 in range(1, b.nj + 1, layout.tile_rows)
+                       for r in (j0, min(j0 + layout.tile_rows - 1, b.nj))})
+        cols = sorted({c for i0 in range(1, b.ni + 1, width) for c in (i0, min(i0 + width - 1, b.ni))})
+        segs += [(k, 0, r, 1, b.ni, 0) for r in rows]
+        segs += [(k, 1, 1, c, b.nj, 0) for c in cols]
+    layout.band_segs = np.array(segs, dtype=native.BAND_SEG_DTYPE)
+    layout.band_max_len = max(max(b.ni, b.nj) for b in layout.blocks)
 
 
 def _face_stride(layout, gid, face):

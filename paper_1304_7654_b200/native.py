@@ -22,12 +22,13 @@ LIB_PATH = os.environ.get("HBGPU_LIB") or os.path.join(PKG_DIR, "libhbgpu.so")
 NPDE = 4
 MAX_TEMPLATED_P = 17
 MAX_P = 127
+MAX_PAIR_P = 9                # paired-stage kernel (HBGPU_MAX_PAIR_P)
 ROW_LEAD = 7
 STRIP = 64
 TILE_WARPS = 8                # consumer warps per stage tile
 TILE_COLS = {4: 64, 1: 256}   # tile_pdes -> interior columns per strip
 ABI_VERSION = 1
-TMAP_SETS = 8                  # tensor-map sets per block (hbgpu_encode_tensor_maps)
+TMAP_SETS = 10                 # tensor-map sets per block (hbgpu_encode_tensor_maps)
 
 c_i32, c_i64, c_f64, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
 
@@ -47,6 +48,9 @@ HALO_DIR_DTYPE = np.dtype([
     ("dst_off", "<i8"), ("dst_es", "<i8"), ("dst_vs", "<i8"),
     ("length", "<i4"), ("src_kind", "<i4"), ("dst_kind", "<i4"), ("pad", "<i4")], align=True)
 
+BAND_SEG_DTYPE = np.dtype([
+    ("block", "<i4"), ("dir", "<i4"), ("j", "<i4"), ("i", "<i4"), ("len", "<i4"), ("pad", "<i4")])
+
 OUT_RECORD_DTYPE = np.dtype([
     ("block", "<i4"), ("plane", "<i4"), ("kind", "<i4"), ("pad", "<i4"),
     ("dst", "<i8"), ("xy", "<i8")], align=True)
@@ -63,12 +67,13 @@ class PeerMsg(ctypes.Structure):
 
 class StageArgs(ctypes.Structure):
     _fields_ = [
-        ("in_", c_vp), ("q0", c_vp), ("out", c_vp), ("sendbuf", c_vp),
+        ("in_", c_vp), ("q0", c_vp), ("out", c_vp), ("band", c_vp), ("sendbuf", c_vp),
         ("blocks", c_vp), ("tile_block", c_vp), ("sxy", c_vp), ("faces", c_vp),
         ("norm_part", c_vp), ("status", c_vp), ("iter", c_vp), ("dmat", c_vp), ("tmaps", c_vp),
         ("nblocks", c_i32), ("total_tiles", c_i32), ("planes", c_i32), ("stage", c_i32),
         ("tile_rows", c_i32), ("in_slot", c_i32), ("interleaved", c_i32), ("tile_pdes", c_i32),
-        ("out_slot", c_i32), ("pad0", c_i32), ("coef", c_f64),
+        ("out_slot", c_i32), ("pair", c_i32), ("coef", c_f64), ("coef2", c_f64),
+        ("band_segs", c_vp), ("nband_segs", c_i32), ("band_max_len", c_i32),
         ("D", c_f64 * (MAX_TEMPLATED_P * MAX_TEMPLATED_P)),
         ("ap", c_f64 * (MAX_P * NPDE))]
 
@@ -81,6 +86,8 @@ class EngineDesc(ctypes.Structure):
         ("prime_dirs", c_vp), ("nprime", c_i32), ("prime_max_len", c_i32),
         ("unpack_dirs", c_vp), ("nunpack", c_i32), ("unpack_max_len", c_i32),
         ("post_dirs", c_vp), ("npost", c_i32), ("post_max_len", c_i32),
+        ("band_segs", c_vp), ("nband_segs", c_i32), ("band_max_len", c_i32),
+        ("fused", c_i32), ("pad1", c_i32),
         ("segs", c_vp), ("nsegs", c_i32),
         ("force_hist", c_vp),
         ("sends", ctypes.POINTER(PeerMsg)), ("nsends", c_i32),
@@ -99,6 +106,7 @@ SIGNATURES = {
     "hbgpu_update": (c_i32, [c_vp, c_vp, c_vp, c_f64, c_i32] + [c_i64] * 8 + [c_vp, c_vp]),
     "hbgpu_first_nonfinite": (c_i32, [c_vp] + [c_i64] * 4 + [c_vp, c_vp]),
     "hbgpu_stage": (c_i32, [ctypes.POINTER(StageArgs), c_vp]),
+    "hbgpu_band": (c_i32, [ctypes.POINTER(StageArgs), c_vp]),
     "hbgpu_stage_prepare": (c_i32, [c_i32]),
     "hbgpu_encode_tensor_maps": (c_i32, [c_vp * 3, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_i64]),
     "hbgpu_halo": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),

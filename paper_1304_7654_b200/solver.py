@@ -96,6 +96,9 @@ class RunSpec:
     # "loopback" runs one engine per rank on this GPU with device-copy
     # transport (exercises the multi-GPU halo path)
     transport: str = "fold"
+    # paired RK stages (hb_pair.cu): None = whenever eligible (P <= 17 and
+    # every block a whole number of strips wide), False = single stages
+    fused: bool | None = None
 
 
 @dataclass
@@ -176,7 +179,7 @@ class DeviceRank:
     """One rank's blocks resident on one GPU, plus its libhbgpu engine."""
 
     def __init__(self, case, topology, partition, plan, rank=0, device=None, comm=None,
-                 initial=None, tile_rows=None, max_iters=1, pinned_ic=None):
+                 initial=None, tile_rows=None, max_iters=1, pinned_ic=None, fused=None):
         import torch
         self.lib = native.require_cuda()
         self.torch = torch
@@ -187,7 +190,8 @@ class DeviceRank:
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         torch.cuda.set_device(self.device)
         t0 = time.perf_counter()
-        L = self.layout = build_rank_layout(topology, partition, plan, rank, case.planes, tile_rows)
+        L = self.layout = build_rank_layout(topology, partition, plan, rank, case.planes, tile_rows,
+                                            fused=fused)
         self.timings = {"layout": time.perf_counter() - t0}
         dev = self.device
         f64 = torch.float64
@@ -215,6 +219,7 @@ class DeviceRank:
         self.t_prime = table(L.prime_dirs)
         self.t_unpack = table(L.unpack_dirs)
         self.t_post = table(L.post_dirs)
+        self.t_band = table(L.band_segs)
         self.t_segs = table(L.force_segs)
         deriv = hbop.spectral_matrix(case.nharms, case.omega)
         self.dmat = np.ascontiguousarray(deriv.matrix)
@@ -311,6 +316,8 @@ class DeviceRank:
         d.unpack_max_len = int(L.unpack_dirs["length"].max()) if len(L.unpack_dirs) else 0
         d.post_dirs, d.npost = self.t_post.data_ptr(), len(L.post_dirs)
         d.post_max_len = int(L.post_dirs["length"].max()) if len(L.post_dirs) else 0
+        d.band_segs, d.nband_segs = self.t_band.data_ptr(), len(L.band_segs)
+        d.band_max_len, d.fused = int(L.band_max_len), int(L.fused)
         d.segs, d.nsegs = self.t_segs.data_ptr(), len(L.force_segs)
         d.force_hist = self.force_hist.data_ptr()
         self._sends = (native.PeerMsg * max(1, len(L.sends)))(
@@ -371,6 +378,31 @@ class DeviceRank:
     # slot rotation of the engine (hb_runtime.cu): stage s reads IN[s], writes OUT[s]
     STAGE_IN = (0, 1, 2, 1)
     STAGE_OUT = (1, 2, 1, 0)
+    # paired schedule, per phase: band(0), pair(0,1), band(2), pair(2,3)
+    PHASE_IN = (0, 0, 1, 1)
+    PHASE_OUT = (2, 1, 2, 0)
+
+    @property
+    def fused(self):
+        return bool(self.layout.fused)
+
+    def phase_args(self, phase):
+        """Arguments of phase `phase` of the paired schedule as the engine
+        issues them: phases 0 / 2 go to hbgpu_band, 1 / 3 to hbgpu_stage."""
+        a = self.stage_args(0 if phase < 2 else 2)
+        d = self._desc
+        a.in_ = self.slots[self.PHASE_IN[phase]].data_ptr()
+        a.out = self.slots[self.PHASE_OUT[phase]].data_ptr()
+        a.in_slot, a.out_slot = self.PHASE_IN[phase], self.PHASE_OUT[phase]
+        a.norm_part = d.norm_part if phase == 1 else None
+        if phase in (1, 3):
+            a.pair = 1 if phase == 1 else 2
+            a.coef2 = d.coef[(0 if phase == 1 else 2) + 1]
+        return a
+
+    def launch_band(self, args, stream=None):
+        s = stream if stream is not None else self.stream()
+        native.check(self.lib.hbgpu_band(ctypes.byref(args), s), "hbgpu_band")
 
     def stage_args(self, stage):
         """hbgpu_stage arguments of RK stage `stage` as the engine issues them."""
@@ -378,6 +410,8 @@ class DeviceRank:
         a.in_ = self.slots[self.STAGE_IN[stage]].data_ptr()
         a.q0 = self.slots[0].data_ptr()
         a.out = self.slots[self.STAGE_OUT[stage]].data_ptr()
+        a.band = self.slots[2].data_ptr()
+        a.band_segs, a.nband_segs, a.band_max_len = d.band_segs, d.nband_segs, d.band_max_len
         a.sendbuf, a.blocks, a.tile_block = d.sendbuf, d.blocks, d.tile_block
         a.sxy, a.faces, a.status, a.iter, a.dmat = d.sxy, d.faces, d.status, d.iter, d.dmat
         a.norm_part = d.norm_part if stage == 0 else None
@@ -563,7 +597,7 @@ def run_case(spec):
 def _new_rank(spec, topology, partition, plan, rank, device, comm, iterations):
     return DeviceRank(spec.case, topology, partition, plan, rank=rank, device=device, comm=comm,
                       initial=spec.initial, tile_rows=spec.tile_rows, max_iters=max(1, iterations),
-                      pinned_ic=spec.initial_state)
+                      pinned_ic=spec.initial_state, fused=spec.fused)
 
 
 def _history(dr, iterations):

@@ -146,3 +146,62 @@ def test_dtau_zero_is_identity(cuda):
     res = run_case(RunSpec(case=case, ranks=1, iterations=3))
     want = initial_values(case.blocks[0], 3, 4, 0, 3, 1, 5)
     assert np.array_equal(res.fields[0][:, :, 1:5, 1:5], want)
+
+
+# ---------------------------------------------------------------------------
+# paired stages (hb_pair.cu): every tile-perimeter path -- strip edges, row
+# tile edges, block faces across local / reversed / self / remote cuts
+# ---------------------------------------------------------------------------
+
+FUSED = {
+    # name: (builder, iterations, tile_rows, ranks, transport)
+    "lattice-256": (lambda: lattice_case(3, 2, 256, 40, 2, h=0.01, dtau=0.0002, nbody=2,
+                                         bodies=((0, "south", 0), (4, "north", 1))), 3, 16, 1, "fold"),
+    "lattice-256-rows1": (lambda: lattice_case(2, 2, 256, 7, 1, h=0.02, dtau=0.0005), 2, 1, 1, "fold"),
+    "lattice-256-ragged-rows": (lambda: lattice_case(2, 1, 512, 37, 4, h=0.01, dtau=0.0002, nbody=1,
+                                                     bodies=((1, "north", 0),)), 3, 10, 1, "fold"),
+    "pair-64-pt4": (lambda: pair_case(64, 30, 3, h=0.02, dtau=0.0005, reversed_cut=True, nbody=1,
+                                      bodies=((1, "north", 0),)), 3, 8, 1, "fold"),
+    "ring-128-pt4": (lambda: ring_case(3, 128, 20, 2, h=0.02, dtau=0.0005, nbody=1,
+                                       bodies=((2, "south", 0),)), 3, 7, 1, "fold"),
+    "self-cut-512": (lambda: CaseConfig(nharms=4, npde=4, iterations=3, dtau=0.0001, omega=0.12, nbody=1,
+                                        blocks=[BlockSpec(0, 512, 24, 0.0, 0.0, 0.01,
+                                                          body_faces=(("south", 0),))],
+                                        cuts=[CutSpec(CutSide(0, "east", 1, 24), CutSide(0, "west", 1, 24))]),
+                     3, 9, 1, "fold"),
+    "lattice-256-loopback4": (lambda: lattice_case(2, 2, 256, 24, 2, h=0.01, dtau=0.0002, nbody=1,
+                                                   bodies=((3, "north", 0),)), 3, 8, 4, "loopback"),
+    "C1-loopback2": (lambda: baseline_workload("C1").case, 2, None, 2, "loopback"),
+}
+
+
+@pytest.mark.parametrize("name", sorted(FUSED))
+def test_paired_stages_match_oracle_and_single_stages(name, cuda, oracle_mod):
+    from paper_1304_7654_b200 import build_topology, partition_blocks, build_cut_plan
+    from paper_1304_7654_b200.devlayout import build_rank_layout
+    build, iters, tile_rows, ranks, transport = FUSED[name]
+    case = build()
+    topo = build_topology(case)
+    part = partition_blocks(topo, 1)
+    lay = build_rank_layout(topo, part, build_cut_plan(topo, part, case.nharms, 4), 0, case.planes, tile_rows)
+    assert lay.fused, "case must take the paired-stage path"
+    initial = baseline_workload("C1").initial if name.startswith("C1") else None
+    got = run_case(RunSpec(case=case, ranks=ranks, iterations=iters, tile_rows=tile_rows, initial=initial,
+                           transport=transport, fused=True))
+    single = run_case(RunSpec(case=case, ranks=ranks, iterations=iters, tile_rows=tile_rows, initial=initial,
+                              transport=transport, fused=False))
+    want = oracle_mod.run(case, iters, initial=initial)
+    assert_parity(got, want, name)
+    assert got.field_bits_equal(single) and got.forces.equal_bits(single.forces)
+    np.testing.assert_allclose(got.residual_norms, single.residual_norms, rtol=1e-13)
+
+
+def test_paired_stages_divergence_location(cuda, oracle_mod):
+    """A blow-up inside a pair reports the reference's (stage, cell)."""
+    case = lattice_case(2, 1, 256, 12, 1, h=0.01, dtau=5.0)
+    with pytest.raises(oracle_mod.OracleDivergence) as want:
+        oracle_mod.run(case, 100)
+    with pytest.raises(DivergenceError) as got:
+        run_case(RunSpec(case=case, ranks=1, iterations=100, fused=True))
+    w, g = want.value, got.value
+    assert (g.block, g.i, g.j, g.p, g.n) == (w.block, w.i, w.j, w.p, w.n)
