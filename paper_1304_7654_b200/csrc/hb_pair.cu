@@ -31,15 +31,30 @@ namespace hbgpu {
 
 // ---- band: the first stage of a pair at the tile-perimeter cells -----------------
 
+// Segment kinds: dir 0 = a row run (threads along i), dir 1 = a column run
+// (threads along j), dir 2 = two adjacent columns i, i+1 (a strip boundary):
+// a 128-thread block takes 64 rows of both, so the two columns' overlapping
+// stencil sectors are fetched once into L1.
 template <int P>
 __global__ void __launch_bounds__(128) band_kernel(const __grid_constant__ hbgpu_stage_args a) {
     const hbgpu_band_seg sg = a.band_segs[blockIdx.y];
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    int e, di = 0;
+    if (sg.dir == 2) {
+        e = blockIdx.x * 64 + (threadIdx.x & 63);
+        di = threadIdx.x >> 6;
+    } else {
+        e = blockIdx.x * blockDim.x + threadIdx.x;
+    }
     if (e >= sg.len) return;
     const int p = blockIdx.z;
     const hbgpu_block b = a.blocks[sg.block];
     const int j = sg.j + (sg.dir ? e : 0);
-    const int i = sg.i + (sg.dir ? 0 : e);
+    const int i = sg.i + (sg.dir ? di : e);
+    // column runs skip the band rows (the row runs own those cells); then the
+    // rest of each column cell's 32-byte sector holds no band value, so the
+    // cell is stored as a whole sector (no partial-sector fill in L2)
+    const bool column = sg.dir != 0;
+    if (column && ((j - 1) % a.tile_rows == 0 || j % a.tile_rows == 0 || j == b.nj)) return;
     const int64_t ps4 = b.ps * NPDE;
     const int64_t cell = b.base + (int64_t)p * b.ps + (int64_t)j * b.rs + LEAD + i;
     const double *c = a.in + cell;
@@ -47,7 +62,7 @@ __global__ void __launch_bounds__(128) band_kernel(const __grid_constant__ hbgpu
     const double sv = a.sxy[b.sxy_off + (int64_t)(j - 1) * b.sxy_pitch + (i - 1)];
     double cur[P];
 #pragma unroll
-    for (int m = 0; m < P; ++m) cur[m] = c[m * ps4];
+    for (int m = 0; m < P; ++m) cur[m] = __ldg(c + m * ps4);
     FaceHit trow{0, 0}, tcol{0, 0};
     if (j == 1) trow = load_target(a.faces, b.face_off[0], i - 1);
     else if (j == b.nj) trow = load_target(a.faces, b.face_off[1], i - 1);
@@ -59,13 +74,22 @@ __global__ void __launch_bounds__(128) band_kernel(const __grid_constant__ hbgpu
         const double *cn = c + n * ps4;
         // hbcore.py:197-221: stencil, then m ascending (D[n][n] = +0 included
         // as its exact 0*q product), then the forcing term
-        double o = stencil(cur[n], cn[-1], cn[1], cn[-b.rs], cn[b.rs], b.nu_h2, b.adv_2h);
+        double o = stencil(cur[n], __ldg(cn - 1), __ldg(cn + 1), __ldg(cn - b.rs), __ldg(cn + b.rs), b.nu_h2,
+                           b.adv_2h);
 #pragma unroll
         for (int m = 0; m < P; ++m) o = radd(o, rmul(a.D[n * P + m], cur[m]));
         o = radd(o, rmul(a.ap[n * NPDE + p], sv));
-        const double base = first ? cur[n] : a.q0[cell + n * ps4];
+        const double base = first ? cur[n] : __ldg(a.q0 + cell + n * ps4);
         const double v = rsub(base, rmul(a.coef, o));
-        a.out[cell + n * ps4] = v;
+        double *dst = a.out + cell + n * ps4;
+        if (column) {
+            double2 *sec = reinterpret_cast<double2 *>((uintptr_t)dst & ~(uintptr_t)31);
+            const int pos = (int)(((uintptr_t)dst >> 3) & 3);
+            sec[0] = make_double2(pos == 0 ? v : 0.0, pos == 1 ? v : 0.0);
+            sec[1] = make_double2(pos == 2 ? v : 0.0, pos == 3 ? v : 0.0);
+        } else {
+            *dst = v;
+        }
         forward(trow, a.out, a.sendbuf, n, p, v);
         forward(tcol, a.out, a.sendbuf, n, p, v);
         if (nonfinite(v)) {
@@ -77,7 +101,8 @@ __global__ void __launch_bounds__(128) band_kernel(const __grid_constant__ hbgpu
 
 template <int P>
 static int launch_band(const hbgpu_stage_args &a, cudaStream_t s) {
-    const dim3 grid((unsigned)((a.band_max_len + 127) / 128), (unsigned)a.nband_segs, NPDE);
+    // dir-2 segments cover 64 rows per block, others 128 cells
+    const dim3 grid((unsigned)((a.band_max_len + 63) / 64), (unsigned)a.nband_segs, NPDE);
     band_kernel<P><<<grid, 128, 0, s>>>(a);
     hbgpu_count_launch(1);
     return hbgpu_check_launch("hbgpu_band");

@@ -228,7 +228,16 @@ def _build_band(layout, fused):
                        for r in (j0, min(j0 + layout.tile_rows - 1, b.nj))})
         cols = sorted({c for i0 in range(1, b.ni + 1, width) for c in (i0, min(i0 + width - 1, b.ni))})
         segs += [(k, 0, r, 1, b.ni, 0) for r in rows]
-        segs += [(k, 1, 1, c, b.nj, 0) for c in cols]
+        # adjacent columns (both sides of a strip boundary) go as one
+        # two-column run, whose stencil reads overlap
+        c = 0
+        while c < len(cols):
+            if c + 1 < len(cols) and cols[c + 1] == cols[c] + 1:
+                segs.append((k, 2, 1, cols[c], b.nj, 0))
+                c += 2
+            else:
+                segs.append((k, 1, 1, cols[c], b.nj, 0))
+                c += 1
     layout.band_segs = np.array(segs, dtype=native.BAND_SEG_DTYPE)
     layout.band_max_len = max(max(b.ni, b.nj) for b in layout.blocks)
 
