@@ -142,9 +142,11 @@ struct PairSmem {
     static constexpr int NV = 3;                                          // v1 rows in flight
     static constexpr size_t V1_OFF = ((size_t)R * SLOT + (size_t)NQ * QSLOT) * 8;
     static constexpr size_t BAR_OFF = V1_OFF + (size_t)NV * QSLOT * 8;
-    static constexpr size_t BYTES = BAR_OFF + (size_t)(2 * R + 3 * NQ) * 8;
+    static constexpr size_t BYTES = BAR_OFF + (size_t)(3 * R + 3 * NQ) * 8;
     static_assert((SLOT * 8) % 128 == 0 && (QSLOT * 8) % 128 == 0, "TMA slots need 128-B alignment");
 };
+
+constexpr int PAIR_THREADS = (CW + 3) * 32;   // + TMA load warp, TMA store warp, edge warp
 
 __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(HBGPU_TILE_WARPS * 32) : "memory");
@@ -204,7 +206,7 @@ __device__ __forceinline__ void record_nonfinite(const double (&v)[P], const hbg
 }
 
 template <int P, bool PB, int R, int Q, int PT>
-__global__ void __launch_bounds__(THREADS, 1) pair_tma_kernel(const __grid_constant__ hbgpu_stage_args a) {
+__global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_constant__ hbgpu_stage_args a) {
     using S = PairSmem<P, PB, R, Q, PT>;
     using G = Geo<PT>;
     static_assert(R >= 4 && (!PB || Q >= 3), "ring too short");
@@ -217,12 +219,14 @@ __global__ void __launch_bounds__(THREADS, 1) pair_tma_kernel(const __grid_const
     uint64_t *full_q = empty_in + R;
     uint64_t *empty_q = full_q + S::NQ;   // q0 slot stored out and free (store warp)
     uint64_t *staged = empty_q + S::NQ;   // v2 row written over it (consumers)
+    uint64_t *edge_ready = staged + S::NQ;   // per stencil slot: edge v1 written (edge warp)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int k = 0; k < R; ++k) {
             mbar_init(full_in + k, 1);
-            mbar_init(empty_in + k, CW);
+            mbar_init(empty_in + k, CW + 1);   // consumers + the edge warp
+            mbar_init(edge_ready + k, 1);
         }
         for (int k = 0; k < S::NQ; ++k) {
             mbar_init(full_q + k, 1);
@@ -251,23 +255,27 @@ __global__ void __launch_bounds__(THREADS, 1) pair_tma_kernel(const __grid_const
             const CUtensorMap *me = maps + 9 * a.nblocks + tl.bidx;   // band slot, one granule
             prefetch_tmap(min);
             const int x = tl.i0 + LEAD - 2;
+            const int west_face = tl.i0 == 1, east_face = tl.i0 + G::TCOLS > a.blocks[tl.bidx].ni;
             // entry of row `row`: the stencil row, sxy of row-1 (with_sxy) and
             // the band values at the strip's two edge columns (with_edge)
             auto put_in = [&](int row, bool with_sxy, bool with_edge) {
                 if (issued_in >= R) mbar_wait(empty_in + pin.slot, pin.phase ^ 1u);
                 else ++issued_in;
                 double *dst = ring + pin.slot * S::SLOT;
-                mbar_expect_tx(full_in + pin.slot, BYTES + (with_sxy ? SBYTES : 0) + (with_edge ? 2 * EBYTES : 0));
+                mbar_expect_tx(full_in + pin.slot, BYTES + (with_sxy ? SBYTES : 0) +
+                                                       (with_edge ? (west_face + east_face) * EBYTES : 0));
 #pragma unroll
                 for (int k = 0; k < G::NSPLIT; ++k)
                     load_rows<PT>(dst + k * S::REGION, min, x + k * (G::TCOLS / G::NSPLIT), tl.pde0, row, inter,
                                   full_in + pin.slot);
                 if (with_sxy) tma_load_2d(dst + S::SXY, ms, tl.i0 - 1, row - 2, full_in + pin.slot);
-                if (with_edge) {
+                // a strip edge on a block face reads the band slot's halo (TMA);
+                // an edge inside the block is computed by the edge warp
+                if (with_edge && west_face)
                     load_rows<PT>(dst + S::EDGE_W, me, tl.i0 + LEAD - 8, tl.pde0, row, inter, full_in + pin.slot);
+                if (with_edge && east_face)
                     load_rows<PT>(dst + S::EDGE_E, me, tl.i0 + LEAD + G::TCOLS, tl.pde0, row, inter,
                                   full_in + pin.slot);
-                }
                 pin = advance<R>(pin);
             };
             put_in(tl.j0 - 1, false, false);
@@ -303,6 +311,79 @@ __global__ void __launch_bounds__(THREADS, 1) pair_tma_kernel(const __grid_const
             }
         }
         bulk_wait_all();
+        return;
+    }
+
+    if (warp == CW + 2) {
+        // ------------------------------ edge warp ------------------------------
+        // v1 of the strip's two edge columns (i0-1, i0+TCOLS) where they lie
+        // inside the block: per row r, once rows r-1..r+1 are in the ring,
+        // lane k = (side, pde, plane n) accumulates plane n's residual in the
+        // reference order (hbcore.py:197-221: stencil, m ascending, forcing)
+        // from the stencil slots, and writes v1 into the slot's edge granule
+        // where the consumers' second stage reads it.
+        constexpr int NE = 2 * PT * P;
+        RingPos cin{0, 0};
+        for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+            const Tile tl = decode_tile<PT>(a, t);
+            const hbgpu_block b = a.blocks[tl.bidx];
+            const bool west_in = tl.i0 > 1, east_in = tl.i0 + G::TCOLS <= b.ni;
+            const int64_t ps4 = b.ps * NPDE;
+            RingPos cprev = cin;
+            cin = advance<R>(cin);
+            // every slot fill gets one edge_ready arrival (rows j0-1 and j1+1
+            // carry no edges) so the barrier's phase follows the fills; an
+            // arrival only once its fill has landed, or it could complete the
+            // next phase before the consumers waited on the previous one
+            mbar_wait(full_in + cprev.slot, cprev.phase);
+            if (lane == 0) mbar_arrive(edge_ready + cprev.slot);
+            for (int r = tl.j0; r <= tl.j1; ++r) {
+                const RingPos nx = advance<R>(cin);
+                mbar_wait(full_in + cprev.slot, cprev.phase);
+                mbar_wait(full_in + cin.slot, cin.phase);
+                mbar_wait(full_in + nx.slot, nx.phase);
+                if (west_in || east_in) {
+                    for (int k = lane; k < NE; k += 32) {
+                        const int side = k / (PT * P), pp = (k / P) % PT, n = k % P;
+                        if (side == 0 ? !west_in : !east_in) continue;
+                        // smem column of the edge cell inside the stencil box
+                        const int region = side == 0 ? 0 : G::NSPLIT - 1;
+                        const int idx = side == 0 ? 1 : G::TCOLS - region * (G::TCOLS / G::NSPLIT) + 2;
+                        const int off = region * S::REGION + pp * G::BW + idx;
+                        const double *rc = ring + cin.slot * S::SLOT + off;
+                        const double *ru = ring + cprev.slot * S::SLOT + off;
+                        const double *rn = ring + nx.slot * S::SLOT + off;
+                        const int ie = side == 0 ? tl.i0 - 1 : tl.i0 + G::TCOLS;
+                        const int p = tl.pde0 + pp;
+                        const double sv = __ldg(a.sxy + b.sxy_off + (int64_t)(r - 1) * b.sxy_pitch + (ie - 1));
+                        const int64_t cell = b.base + (int64_t)p * b.ps + (int64_t)r * b.rs + LEAD + ie;
+                        double o = stencil(rc[n * PT * G::BW], rc[n * PT * G::BW - 1], rc[n * PT * G::BW + 1],
+                                           ru[n * PT * G::BW], rn[n * PT * G::BW], b.nu_h2, b.adv_2h);
+#pragma unroll
+                        for (int m = 0; m < P; ++m) o = radd(o, rmul(a.D[n * P + m], rc[m * PT * G::BW]));
+                        o = radd(o, rmul(a.ap[n * NPDE + p], sv));
+                        const double base = PB ? __ldg(a.q0 + cell + n * ps4) : rc[n * PT * G::BW];
+                        const double v = rsub(base, rmul(a.coef, o));
+                        ring[cin.slot * S::SLOT + (side == 0 ? S::EDGE_W + (n * PT + pp) * 8 + 7
+                                                                : S::EDGE_E + (n * PT + pp) * 8)] = v;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(edge_ready + cin.slot);
+                    mbar_arrive(empty_in + cprev.slot);   // row r-1: read for the last time
+                }
+                cprev = cin;
+                cin = nx;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(edge_ready + cin.slot);   // row j1+1
+                mbar_arrive(empty_in + cprev.slot);   // row j1
+                mbar_arrive(empty_in + cin.slot);     // row j1+1
+            }
+            cin = advance<R>(cin);
+        }
         return;
     }
 
@@ -395,6 +476,7 @@ __global__ void __launch_bounds__(THREADS, 1) pair_tma_kernel(const __grid_const
             consumer_sync();
             if (r > tl.j0) {
                 // second stage at row r-1
+                mbar_wait(edge_ready + cprev.slot, cprev.phase);
                 const int vp = vr == 0 ? S::NV - 1 : vr - 1;   // v1 ring row of v1(r-1)
                 const double *vw = west_edge ? ring + cprev.slot * S::SLOT + w_off : v1ring + vp * S::QSLOT + w_off;
                 const double *ve = east_edge ? ring + cprev.slot * S::SLOT + e_off : v1ring + vp * S::QSLOT + e_off;
@@ -453,6 +535,7 @@ __global__ void __launch_bounds__(THREADS, 1) pair_tma_kernel(const __grid_const
             double vd[P];
 #pragma unroll
             for (int n = 0; n < P; ++n) vd[n] = __ldg(a.band + colbase + n * ps4 + (int64_t)(tl.j1 + 1) * b.rs);
+            mbar_wait(edge_ready + cprev.slot, cprev.phase);
             const int vp = vr == 0 ? S::NV - 1 : vr - 1;   // v1 ring row of v1(j1)
             const double *vw = west_edge ? ring + cprev.slot * S::SLOT + w_off : v1ring + vp * S::QSLOT + w_off;
             const double *ve = east_edge ? ring + cprev.slot * S::SLOT + e_off : v1ring + vp * S::QSLOT + e_off;
@@ -533,7 +616,8 @@ static int prepare_pair(PairLaunch &L) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.fn, THREADS, L.smem) != cudaSuccess || per_sm < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.fn, PAIR_THREADS, L.smem) != cudaSuccess ||
+        per_sm < 1)
         return hbgpu_check_launch("pair kernel occupancy");
     L.grid = sms * per_sm;
     L.ready = true;
@@ -552,7 +636,7 @@ static int pair_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only
     }
     PairLaunch &L = a.pair == 2 ? lb : la;
     const int grid = min(L.grid, a.total_tiles);
-    L.fn<<<grid, THREADS, L.smem, s>>>(a);
+    L.fn<<<grid, PAIR_THREADS, L.smem, s>>>(a);
     hbgpu_count_launch(1);
     return hbgpu_check_launch("hbgpu_stage (pair)");
 }

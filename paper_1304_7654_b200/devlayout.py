@@ -215,18 +215,20 @@ def fused_eligible(blocks, planes, tile_pdes):
 
 
 def _build_band(layout, fused):
-    """Row and column runs covering every tile's perimeter cells: the first
-    and last row of each row tile and the first and last column of each
-    strip, over the whole block (hbgpu_band computes the first stage of a
-    pair there; the paired kernel reads it across tile edges)."""
+    """Runs of cells where hbgpu_band computes the first stage of a pair:
+    the first and last row of every row tile (read across row-tile edges)
+    and the face columns that feed a cut (forwarded into the neighbours'
+    band halos, read across strip edges on block faces)."""
     eligible = fused_eligible(layout.blocks, layout.planes, layout.tile_pdes)
     layout.fused = eligible if fused is None else (bool(fused) and eligible)
-    width = native.TILE_COLS[layout.tile_pdes]
     segs = []
     for k, b in enumerate(layout.blocks):
         rows = sorted({r for j0 in range(1, b.nj + 1, layout.tile_rows)
                        for r in (j0, min(j0 + layout.tile_rows - 1, b.nj))})
-        cols = sorted({c for i0 in range(1, b.ni + 1, width) for c in (i0, min(i0 + width - 1, b.ni))})
+        # strip-edge columns inside a block are computed by the paired kernel's
+        # edge warp; the band covers the face columns that feed a cut
+        face = layout.block_table["face_off"][k]
+        cols = sorted({c for c, fi in ((1, 2), (b.ni, 3)) if face[fi] >= 0})
         segs += [(k, 0, r, 1, b.ni, 0) for r in rows]
         # adjacent columns (both sides of a strip boundary) go as one
         # two-column run, whose stencil reads overlap
