@@ -56,6 +56,93 @@ def parse():
     return ap.parse_args()
 
 
+def fp64_peak():
+    path = os.path.join(REPO, "profiles", "fp64_peak.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["dadd_ops_per_s"]) / 1e12, "measured (profiles/fp64_peak.json, DADD rate)"
+    except Exception:
+        return 18.5, "fallback (64 fp64 lanes/clk/SM x 148 SMs x 1.965 GHz)"
+
+
+def _time_launches(dr, launches, reps):
+    """Mean CUDA-event time (ms) of each launch, on the stream it runs on."""
+    import torch
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in launches] for _ in range(reps)]
+    launches[-1]()   # warm
+    torch.cuda.synchronize()
+    for r in range(reps):
+        for k, fn in enumerate(launches):
+            evs[r][k][0].record()
+            fn()
+            evs[r][k][1].record()
+    torch.cuda.synchronize()
+    return [sum(evs[r][k][0].elapsed_time(evs[r][k][1]) for r in range(reps)) / reps
+            for k in range(len(launches))]
+
+
+def roofline(dr, args, units_stage, step_ms_total, wl, world):
+    """Roofline of the dominant kernel.
+
+    Single stages: the stage kernel, HBM-bound, SURVEY.md §8d's 88 B/unit.
+    Paired stages (the default where eligible): the paired kernel does two
+    stages per launch and is co-limited by fp64 issue and HBM; it is reported
+    against the measured fp64 rate (the larger fraction), with its HBM
+    fraction for the fused schedule's own algorithmic traffic (pass A reads
+    q0 and writes q2, 64 B per cell-snapshot; pass B reads q2 and q0 and
+    writes q4, 96 B) and the fraction the unfused algorithm's 88 B/unit
+    would need at the achieved rate."""
+    P = wl.case.planes
+    flops_unit = 52 + 8 * P
+    peak, peak_src = peaks()
+    step_ms = step_ms_total / args.steps
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "stage_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            tj = json.load(fh)
+        if tj.get("workload") == wl.key and tj.get("n_gpus", 1) == world and \
+                bool(tj.get("fused")) == dr.fused:
+            traffic = tj.get("bytes_per_launch_avg")
+    if not dr.fused:
+        stage_args = [dr.stage_args(s) for s in range(4)]
+        t = _time_launches(dr, [lambda a=a: dr.launch_stage(a) for a in stage_args], args.kernel_reps)
+        algo = sum(ALGO_BYTES[s] for s in range(4)) * units_stage
+        achieved = algo / (sum(t) / 1e3) / 1e9
+        return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                "kernel": "hb_stage (fused residual + RK update + halo forward)",
+                "algorithmic_bytes_per_unit": {"stage0": 64, "stages1-3": 96, "avg": 88},
+                "units_per_launch": units_stage, "stage_ms": [round(x, 4) for x in t],
+                "share_of_step": round(sum(t) / step_ms, 4)}
+    phases = [dr.phase_args(k) for k in range(4)]
+    launch = [lambda a=phases[0]: dr.launch_band(a), lambda a=phases[1]: dr.launch_stage(a),
+              lambda a=phases[2]: dr.launch_band(a), lambda a=phases[3]: dr.launch_stage(a)]
+    t = _time_launches(dr, launch, args.kernel_reps)
+    pair_s = (t[1] + t[3]) / 1e3
+    units_pair = 2 * units_stage                      # unit-stages per paired launch
+    fp_peak, fp_src = fp64_peak()
+    tflops = flops_unit * 2 * units_pair / pair_s / 1e12
+    fused_bytes = (64 + 96) * units_stage             # passes A + B, per cell-snapshot
+    gbs = fused_bytes / pair_s / 1e9
+    return {"bound": "fp64", "achieved": round(tflops, 3), "peak": round(fp_peak, 3), "unit": "TFLOP/s",
+            "frac": round(tflops / fp_peak, 4), "traffic": traffic, "peak_source": fp_src,
+            "kernel": "hb_pair (two fused RK stages: residual + update + halo forward)",
+            "algorithmic_flops_per_unit": flops_unit,
+            "units_per_launch": units_pair,
+            "hbm": {"achieved": round(gbs, 1), "peak": peak, "unit": "GB/s", "frac": round(gbs / peak, 4),
+                    "peak_source": peak_src,
+                    "algorithmic_bytes": {"pass_A_per_cell_snapshot": 64, "pass_B_per_cell_snapshot": 96}},
+            # HBM fraction the single-stage algorithm (88 B/unit) would need
+            # to reach this step rate
+            "unfused_hbm_equivalent_frac": round(88 * 4 * units_stage / (step_ms / 1e3) / 1e9 / peak, 4),
+            "phase_ms": {"band0": round(t[0], 4), "pair01": round(t[1], 4), "band2": round(t[2], 4),
+                         "pair23": round(t[3], 4)},
+            "share_of_step": round((t[1] + t[3]) / step_ms, 4)}
+
+
 def peaks():
     path = os.path.join(REPO, "MEASURED_PEAKS.json")
     try:
@@ -280,42 +367,10 @@ def run_ours(args, wl):
         raise SystemExit(f"benchmark run diverged: {div}")
     value = total_units_iter * args.steps / (ms / 1e3)
 
-    # dominant kernel, timed alone on the launching stream: the 4 stage variants
+    # dominant kernel, timed alone on the launching stream
     my_units_stage = sum(b.cells() for b in mine) * case.planes
-    stage_args = [dr.stage_args(s) for s in range(4)]
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(4 * args.kernel_reps)]
-    dr.launch_stage(stage_args[1])  # warm
-    torch.cuda.synchronize()
-    k = 0
-    for _ in range(args.kernel_reps):
-        for s in range(4):
-            evs[k][0].record()
-            dr.launch_stage(stage_args[s])
-            evs[k][1].record()
-            k += 1
-    torch.cuda.synchronize()
-    stage_ms = [0.0] * 4
-    for k, (a, b) in enumerate(evs):
-        stage_ms[k % 4] += a.elapsed_time(b) / args.kernel_reps
-    algo = sum(ALGO_BYTES[s] for s in range(4)) * my_units_stage   # bytes per 4 launches
-    kernel_s = sum(stage_ms) / 1e3
-    achieved = algo / kernel_s / 1e9
-    peak, peak_src = peaks()
-    traffic = None
-    tpath = os.path.join(REPO, "profiles", "stage_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as fh:
-            tj = json.load(fh)
-        if tj.get("workload") == wl.key and tj.get("n_gpus", 1) == world:
-            traffic = tj.get("bytes_per_launch_avg")
-    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-            "kernel": "hb_stage (fused residual + RK update + halo forward)",
-            "algorithmic_bytes_per_unit": {"stage0": 64, "stages1-3": 96, "avg": 88},
-            "units_per_launch": my_units_stage,
-            "stage_ms": [round(x, 4) for x in stage_ms],
-            "share_of_step": round(sum(stage_ms) / (ms / args.steps), 4)}
+    roof = roofline(dr, args, my_units_stage, ms, wl, world)
+    tile_rows, fused = dr.layout.tile_rows, dr.fused
     dr.close()
     del dr
     torch.cuda.empty_cache()
@@ -355,7 +410,9 @@ def run_ours(args, wl):
                            "blocks": len(case.blocks), "cells": topo.total_cells(),
                            "planes": case.planes, "units_per_step": total_units_iter,
                            "parallelism": f"blocks/{world} gpu (LPT partition)",
-                           "tile_rows": stage_args[0].tile_rows,
+                           "tile_rows": tile_rows,
+                           "schedule": "paired RK stages (band + pair kernels)" if fused
+                                       else "single RK stages",
                            "l2": f"inputs larger than L2: {dr_slot_gb(case, mine):.1f} GB per state slot"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
                 "gpu_launches": int(launches)}
