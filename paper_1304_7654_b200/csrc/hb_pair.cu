@@ -438,9 +438,13 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
         }
         // one row step: v1(r) and, one row behind, v2(r-1)
         auto row_step = [&](const int r, double(&pa)[P], double(&pb)[P], double(&pc)[P]) {
+            // rows r-1 and r were waited for as earlier steps' rows r and r+1
+            // (the tile's first step waits for them here)
             const RingPos nx = advance<R>(cin);
-            mbar_wait(full_in + cprev.slot, cprev.phase);
-            mbar_wait(full_in + cin.slot, cin.phase);
+            if (r == tl.j0) {
+                mbar_wait(full_in + cprev.slot, cprev.phase);
+                mbar_wait(full_in + cin.slot, cin.phase);
+            }
             mbar_wait(full_in + nx.slot, nx.phase);
             const double *ru = ring + cprev.slot * S::SLOT + in_off;
             const double *rc = ring + cin.slot * S::SLOT + in_off;
@@ -624,11 +628,18 @@ static int prepare_pair(PairLaunch &L) {
     return HBGPU_OK;
 }
 
+#ifndef HBGPU_PAIR_R
+#define HBGPU_PAIR_R 4
+#endif
+#ifndef HBGPU_PAIR_Q
+#define HBGPU_PAIR_Q 4
+#endif
+
 template <int P, int PT>
 static int pair_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
     static PairLaunch la, lb;
-    int rc = prepare_pair<P, false, 4, 3, PT>(la);
-    if (!rc) rc = prepare_pair<P, true, 4, 3, PT>(lb);
+    int rc = prepare_pair<P, false, HBGPU_PAIR_R, HBGPU_PAIR_Q, PT>(la);
+    if (!rc) rc = prepare_pair<P, true, HBGPU_PAIR_R, HBGPU_PAIR_Q, PT>(lb);
     if (rc || prepare_only) return rc;
     if (a.tmaps == nullptr || a.band == nullptr) {
         hbgpu_set_error("hbgpu_stage (pair): args->tmaps and args->band are required");
