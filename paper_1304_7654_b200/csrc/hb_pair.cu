@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
             // entry of row `row`: the stencil row, sxy of row-1 (with_sxy) and
             // the band values at the strip's two edge columns (with_edge)
             auto put_in = [&](int row, bool with_sxy, bool with_edge) {
-                if (issued_in >= R) mbar_wait(empty_in + pin.slot, pin.phase ^ 1u);
+                if (issued_in >= R) mbar_wait_idle(empty_in + pin.slot, pin.phase ^ 1u);
                 else ++issued_in;
                 double *dst = ring + pin.slot * S::SLOT;
                 mbar_expect_tx(full_in + pin.slot, BYTES + (with_sxy ? SBYTES : 0) +
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
             for (int j = tl.j0; j <= tl.j1; ++j) {
                 put_in(j + 1, true, j + 1 <= tl.j1);
                 if (PB) {
-                    if (issued_q >= Q) mbar_wait(empty_q + pq.slot, pq.phase ^ 1u);
+                    if (issued_q >= Q) mbar_wait_idle(empty_q + pq.slot, pq.phase ^ 1u);
                     else ++issued_q;
                     mbar_expect_tx(full_q + pq.slot, QBYTES);
                     load_rows<PT>(qring + pq.slot * S::QSLOT, mq, x + 2, tl.pde0, j, inter, full_q + pq.slot);
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
             const CUtensorMap *mo = maps + (5 + a.out_slot) * a.nblocks + tl.bidx;
             prefetch_tmap(mo);
             for (int j = tl.j0; j <= tl.j1; ++j) {
-                mbar_wait(staged + ps.slot, ps.phase);
+                mbar_wait_idle(staged + ps.slot, ps.phase);
                 store_rows(mo, qring + ps.slot * S::QSLOT, tl.i0 + LEAD, tl.pde0, j, inter);
                 bulk_commit();
                 bulk_wait_read_all();
@@ -323,50 +323,86 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
         // from the stencil slots, and writes v1 into the slot's edge granule
         // where the consumers' second stage reads it.
         constexpr int NE = 2 * PT * P;
+        constexpr int KE = (NE + 31) / 32;   // (side, pde, plane) items per lane
+        // per item: its plane's D row and forcing amplitude (fixed), and the
+        // forcing / q0 values of the next row, loaded one row ahead
+        double drow[KE][P];
+        int side_k[KE], pp_k[KE], n_k[KE];
+#pragma unroll
+        for (int c = 0; c < KE; ++c) {
+            const int k = lane + 32 * c;
+            side_k[c] = k < NE ? k / (PT * P) : 2;
+            pp_k[c] = (k / P) % PT;
+            n_k[c] = k % P;
+#pragma unroll
+            for (int m = 0; m < P; ++m) drow[c][m] = k < NE ? a.D[n_k[c] * P + m] : 0.0;
+        }
         RingPos cin{0, 0};
         for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
             const Tile tl = decode_tile<PT>(a, t);
             const hbgpu_block b = a.blocks[tl.bidx];
             const bool west_in = tl.i0 > 1, east_in = tl.i0 + G::TCOLS <= b.ni;
             const int64_t ps4 = b.ps * NPDE;
+            bool act[KE];
+            int ie_k[KE];
+            double ap_k[KE], sv_n[KE], bs_n[KE];
+#pragma unroll
+            for (int c = 0; c < KE; ++c) {
+                act[c] = side_k[c] == 0 ? west_in : side_k[c] == 1 ? east_in : false;
+                ie_k[c] = side_k[c] == 0 ? tl.i0 - 1 : tl.i0 + G::TCOLS;
+                ap_k[c] = act[c] ? a.ap[n_k[c] * NPDE + tl.pde0 + pp_k[c]] : 0.0;
+            }
+            auto fetch = [&](int rr) {
+#pragma unroll
+                for (int c = 0; c < KE; ++c) {
+                    if (!act[c]) continue;
+                    sv_n[c] = __ldg(a.sxy + b.sxy_off + (int64_t)(rr - 1) * b.sxy_pitch + (ie_k[c] - 1));
+                    if (PB) {
+                        const int64_t cell = b.base + (int64_t)(tl.pde0 + pp_k[c]) * b.ps + (int64_t)rr * b.rs + LEAD +
+                                             ie_k[c];
+                        bs_n[c] = __ldg(a.q0 + cell + n_k[c] * ps4);
+                    }
+                }
+            };
+            fetch(tl.j0);
             RingPos cprev = cin;
             cin = advance<R>(cin);
             // every slot fill gets one edge_ready arrival (rows j0-1 and j1+1
             // carry no edges) so the barrier's phase follows the fills; an
             // arrival only once its fill has landed, or it could complete the
             // next phase before the consumers waited on the previous one
-            mbar_wait(full_in + cprev.slot, cprev.phase);
+            mbar_wait_idle(full_in + cprev.slot, cprev.phase);
             if (lane == 0) mbar_arrive(edge_ready + cprev.slot);
             for (int r = tl.j0; r <= tl.j1; ++r) {
-                const RingPos nx = advance<R>(cin);
-                mbar_wait(full_in + cprev.slot, cprev.phase);
-                mbar_wait(full_in + cin.slot, cin.phase);
-                mbar_wait(full_in + nx.slot, nx.phase);
-                if (west_in || east_in) {
-                    for (int k = lane; k < NE; k += 32) {
-                        const int side = k / (PT * P), pp = (k / P) % PT, n = k % P;
-                        if (side == 0 ? !west_in : !east_in) continue;
-                        // smem column of the edge cell inside the stencil box
-                        const int region = side == 0 ? 0 : G::NSPLIT - 1;
-                        const int idx = side == 0 ? 1 : G::TCOLS - region * (G::TCOLS / G::NSPLIT) + 2;
-                        const int off = region * S::REGION + pp * G::BW + idx;
-                        const double *rc = ring + cin.slot * S::SLOT + off;
-                        const double *ru = ring + cprev.slot * S::SLOT + off;
-                        const double *rn = ring + nx.slot * S::SLOT + off;
-                        const int ie = side == 0 ? tl.i0 - 1 : tl.i0 + G::TCOLS;
-                        const int p = tl.pde0 + pp;
-                        const double sv = __ldg(a.sxy + b.sxy_off + (int64_t)(r - 1) * b.sxy_pitch + (ie - 1));
-                        const int64_t cell = b.base + (int64_t)p * b.ps + (int64_t)r * b.rs + LEAD + ie;
-                        double o = stencil(rc[n * PT * G::BW], rc[n * PT * G::BW - 1], rc[n * PT * G::BW + 1],
-                                           ru[n * PT * G::BW], rn[n * PT * G::BW], b.nu_h2, b.adv_2h);
+                double sv_c[KE], bs_c[KE];
 #pragma unroll
-                        for (int m = 0; m < P; ++m) o = radd(o, rmul(a.D[n * P + m], rc[m * PT * G::BW]));
-                        o = radd(o, rmul(a.ap[n * NPDE + p], sv));
-                        const double base = PB ? __ldg(a.q0 + cell + n * ps4) : rc[n * PT * G::BW];
-                        const double v = rsub(base, rmul(a.coef, o));
-                        ring[cin.slot * S::SLOT + (side == 0 ? S::EDGE_W + (n * PT + pp) * 8 + 7
-                                                                : S::EDGE_E + (n * PT + pp) * 8)] = v;
-                    }
+                for (int c = 0; c < KE; ++c) {
+                    sv_c[c] = sv_n[c];
+                    bs_c[c] = bs_n[c];
+                }
+                if (r < tl.j1) fetch(r + 1);
+                const RingPos nx = advance<R>(cin);
+                mbar_wait_idle(full_in + nx.slot, nx.phase);   // rows r-1, r: waited for already
+#pragma unroll
+                for (int c = 0; c < KE; ++c) {
+                    if (!act[c]) continue;
+                    const int side = side_k[c], pp = pp_k[c], n = n_k[c];
+                    // smem column of the edge cell inside the stencil box
+                    const int region = side == 0 ? 0 : G::NSPLIT - 1;
+                    const int idx = side == 0 ? 1 : G::TCOLS - region * (G::TCOLS / G::NSPLIT) + 2;
+                    const int off = region * S::REGION + pp * G::BW + idx;
+                    const double *rc = ring + cin.slot * S::SLOT + off;
+                    const double *ru = ring + cprev.slot * S::SLOT + off;
+                    const double *rn = ring + nx.slot * S::SLOT + off;
+                    double o = stencil(rc[n * PT * G::BW], rc[n * PT * G::BW - 1], rc[n * PT * G::BW + 1],
+                                       ru[n * PT * G::BW], rn[n * PT * G::BW], b.nu_h2, b.adv_2h);
+#pragma unroll
+                    for (int m = 0; m < P; ++m) o = radd(o, rmul(drow[c][m], rc[m * PT * G::BW]));
+                    o = radd(o, rmul(ap_k[c], sv_c[c]));
+                    const double base = PB ? bs_c[c] : rc[n * PT * G::BW];
+                    const double v = rsub(base, rmul(a.coef, o));
+                    ring[cin.slot * S::SLOT + (side == 0 ? S::EDGE_W + (n * PT + pp) * 8 + 7
+                                                            : S::EDGE_E + (n * PT + pp) * 8)] = v;
                 }
                 __syncwarp();
                 if (lane == 0) {
@@ -628,6 +664,11 @@ static int prepare_pair(PairLaunch &L) {
     return HBGPU_OK;
 }
 
+// ring depths: pass A has no q0 ring, so its stencil ring can go one deeper
+// (two rows of look-ahead); pass B fits R = 4 with a 4-deep q0 ring
+#ifndef HBGPU_PAIR_RA
+#define HBGPU_PAIR_RA 5
+#endif
 #ifndef HBGPU_PAIR_R
 #define HBGPU_PAIR_R 4
 #endif
@@ -638,7 +679,7 @@ static int prepare_pair(PairLaunch &L) {
 template <int P, int PT>
 static int pair_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
     static PairLaunch la, lb;
-    int rc = prepare_pair<P, false, HBGPU_PAIR_R, HBGPU_PAIR_Q, PT>(la);
+    int rc = prepare_pair<P, false, HBGPU_PAIR_RA, HBGPU_PAIR_Q, PT>(la);
     if (!rc) rc = prepare_pair<P, true, HBGPU_PAIR_R, HBGPU_PAIR_Q, PT>(lb);
     if (rc || prepare_only) return rc;
     if (a.tmaps == nullptr || a.band == nullptr) {

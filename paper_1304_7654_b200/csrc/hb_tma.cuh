@@ -37,6 +37,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
             : "memory");
     } while (!done);
 }
+// The same wait for the helper warps (TMA load / store, edge): the thread
+// asks to be suspended until the phase completes (up to the hint, in ns)
+// instead of re-polling, so a producer running rows ahead does not take
+// issue slots from the consumer warps sharing its scheduler.
+__device__ __forceinline__ void mbar_wait_idle(uint64_t *b, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(saddr(b)), "r"(parity), "n"(1000000)
+            : "memory");
+    } while (!done);
+}
 __device__ __forceinline__ void tma_load_4d(void *dst, const void *map, int c0, int c1, int c2, int c3,
                                             uint64_t *bar) {
     asm volatile(

@@ -205,3 +205,11 @@ def test_paired_stages_divergence_location(cuda, oracle_mod):
         run_case(RunSpec(case=case, ranks=1, iterations=100, fused=True))
     w, g = want.value, got.value
     assert (g.block, g.i, g.j, g.p, g.n) == (w.block, w.i, w.j, w.p, w.n)
+
+
+def test_paired_graph_and_eager_identical(cuda):
+    case = lattice_case(2, 2, 256, 20, 2, h=0.01, dtau=0.0002, nbody=1, bodies=((1, "north", 0),))
+    a = run_case(RunSpec(case=case, ranks=1, iterations=3, tile_rows=8, use_graph=True, fused=True))
+    b = run_case(RunSpec(case=case, ranks=1, iterations=3, tile_rows=8, use_graph=False, fused=True))
+    assert a.field_bits_equal(b) and a.forces.equal_bits(b.forces)
+    np.testing.assert_allclose(a.residual_norms, b.residual_norms, rtol=1e-13)
