@@ -1,4 +1,4 @@
-"""Summarise an `ncu --set full` capture of the stage-kernel launches.
+"""Summarise an `ncu --set full` capture of the stage- or pair-kernel launches.
 
     python profiles/summarize_ncu.py REPORT.ncu-rep OUT.json [--traffic profiles/stage_traffic.json]
 
@@ -52,8 +52,9 @@ def main():
     launches = []
     for r in data:
         name = r[hdr.index("Kernel Name")]
-        if "stage_tma_kernel" not in name:
+        if "stage_tma_kernel" not in name and "pair_tma_kernel" not in name:
             continue
+        pair = "pair_tma_kernel" in name
         e = {"kernel": name}
         for k in KEYS:
             if k in hdr:
@@ -62,12 +63,19 @@ def main():
             k = f"smsp__average_warps_issue_stalled_{s}_per_issue_active.ratio"
             if k in hdr:
                 e["stall_" + s] = _num(r[hdr.index(k)], "")
-        first = "9, 1," in name or "(bool)1" in name
-        algo = (64 if first else 96) * units_per_launch
+        second = "(bool)1" in name or "9, 1," in name    # FIRST (stage kernel) / PB (pair kernel)
+        if pair:
+            # pass A reads q0 and writes q2, pass B reads q2 and q0 and writes q4
+            algo = (96 if second else 64) * units_per_launch
+            e["algorithmic_flops"] = 2 * (52 + 8 * case.planes) * units_per_launch
+        else:
+            algo = (64 if second else 96) * units_per_launch
         dram = e["dram__bytes_read.sum"] + e["dram__bytes_write.sum"]
         t = e["gpu__time_duration.sum"]
         e.update(algorithmic_bytes=algo, dram_bytes=dram, dram_over_algorithmic=round(dram / algo, 4),
                  dram_TBps=round(dram / t / 1e12, 3), algorithmic_TBps=round(algo / t / 1e12, 3))
+        if pair:
+            e["algorithmic_TFLOPs"] = round(e["algorithmic_flops"] / t / 1e12, 3)
         launches.append(e)
     with open(out, "w") as fh:
         json.dump({"report": rep, "workload": "C4", "units_per_launch": units_per_launch,
@@ -77,6 +85,7 @@ def main():
         algo = sum(l["algorithmic_bytes"] for l in launches) / len(launches)
         with open(traffic, "w") as fh:
             json.dump({"workload": "C4", "n_gpus": 1, "kernel": launches[0]["kernel"],
+                       "fused": any("pair_tma_kernel" in l["kernel"] for l in launches),
                        "bytes_per_launch_avg": int(avg), "algorithmic_bytes_per_launch_avg": int(algo),
                        "source": f"{out}: mean over the {len(launches)} RK-stage launches of one iteration "
                                  "of dram__bytes_read.sum + dram__bytes_write.sum (ncu --set full)"},
