@@ -57,11 +57,6 @@ namespace hbgpu {
 #define HBGPU_FIRST_STAGING 0
 #endif
 constexpr int NOUT = HBGPU_FIRST_STAGING;
-// measurement builds only (wrong results): bit 0 drops the sxy loads, bit 1
-// loads the stencil row as one aligned strip-wide box, bit 2 drops the q0 loads
-#ifndef HBGPU_EXP
-#define HBGPU_EXP 0
-#endif
 
 template <int P, bool FIRST, int R, int Q, int PT>
 struct Smem {
@@ -134,21 +129,14 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
             // stencil rows; the entry of row r also carries sxy row r-1, the
             // forcing of the row computed while r is the "north" row
             auto put_in = [&](int row, bool with_sxy) {
-                if (issued_in >= R) mbar_wait(empty_in + pin.slot, pin.phase ^ 1u);
+                if (issued_in >= R) mbar_wait_idle(empty_in + pin.slot, pin.phase ^ 1u);
                 else ++issued_in;
                 double *dst = ring + pin.slot * S::SLOT;
-                if (HBGPU_EXP & 1) with_sxy = false;
-                if (HBGPU_EXP & 2) {   // measurement: one aligned strip-wide box
-                    mbar_expect_tx(full_in + pin.slot, with_sxy ? QBYTES / P / PT * P * PT + SBYTES : QBYTES);
-                    load_rows<PT>(dst, maps + (5 + a.in_slot) * a.nblocks + tl.bidx, x + 2, tl.pde0, row, inter,
-                                  full_in + pin.slot);
-                } else {
-                    mbar_expect_tx(full_in + pin.slot, with_sxy ? BYTES + SBYTES : BYTES);
+                mbar_expect_tx(full_in + pin.slot, with_sxy ? BYTES + SBYTES : BYTES);
 #pragma unroll
-                    for (int k = 0; k < G::NSPLIT; ++k)
-                        load_rows<PT>(dst + k * S::REGION, min, x + k * (G::TCOLS / G::NSPLIT), tl.pde0, row,
-                                      inter, full_in + pin.slot);
-                }
+                for (int k = 0; k < G::NSPLIT; ++k)
+                    load_rows<PT>(dst + k * S::REGION, min, x + k * (G::TCOLS / G::NSPLIT), tl.pde0, row, inter,
+                                  full_in + pin.slot);
                 if (with_sxy) tma_load_2d(dst + S::SXY, ms, tl.i0 - 1, row - 2, full_in + pin.slot);
                 pin = advance<R>(pin);
             };
@@ -157,14 +145,10 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
             for (int j = tl.j0; j <= tl.j1; ++j) {
                 put_in(j + 1, true);
                 if (!FIRST) {
-                    if (issued_q >= Q) mbar_wait(empty_q + pq.slot, pq.phase ^ 1u);
+                    if (issued_q >= Q) mbar_wait_idle(empty_q + pq.slot, pq.phase ^ 1u);
                     else ++issued_q;
-                    if (HBGPU_EXP & 4) {   // measurement: no q0 traffic
-                        mbar_arrive(full_q + pq.slot);
-                    } else {
-                        mbar_expect_tx(full_q + pq.slot, QBYTES);
-                        load_rows<PT>(qring + pq.slot * S::QSLOT, mq, x + 2, tl.pde0, j, inter, full_q + pq.slot);
-                    }
+                    mbar_expect_tx(full_q + pq.slot, QBYTES);
+                    load_rows<PT>(qring + pq.slot * S::QSLOT, mq, x + 2, tl.pde0, j, inter, full_q + pq.slot);
                     pq = advance<Q>(pq);
                 }
             }
