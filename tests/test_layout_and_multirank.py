@@ -178,3 +178,34 @@ def test_peer_messages_pair_up():
                 match = [c for p, _, c in lay[peer].recvs if p == r]
                 assert match == [count]
             assert lay[r].sendbuf_elems == sum(c for _, _, c in lay[r].sends)
+
+
+def test_paired_schedule_eligibility_and_band_segments():
+    """Paired stages need P <= 9 and every block a whole number of strips;
+    the band covers the first / last row of every row tile and the face
+    columns that feed a cut (paired-kernel edge warp covers the rest)."""
+    from paper_1304_7654_b200.devlayout import fused_eligible
+    from paper_1304_7654_b200 import baseline_workload
+    for key in ("C0", "C1", "C2", "C3", "C4"):
+        case = baseline_workload(key).case
+        topo = build_topology(case)
+        part = partition_blocks(topo, 1)
+        L = build_rank_layout(topo, part, build_cut_plan(topo, part, case.nharms, 4), 0, case.planes)
+        assert L.fused, key
+    case = lattice_case(2, 2, 45, 19, 3, h=0.02, dtau=0.0005)          # ragged strips
+    topo = build_topology(case)
+    assert not fused_eligible(topo.blocks, case.planes, 4)
+    assert not fused_eligible(build_topology(lattice_case(2, 1, 256, 8, 5, h=0.02, dtau=0.0005)).blocks, 11, 1)
+    case = lattice_case(3, 2, 256, 40, 2, h=0.01, dtau=0.0002)
+    topo = build_topology(case)
+    part = partition_blocks(topo, 1)
+    L = build_rank_layout(topo, part, build_cut_plan(topo, part, 2, 4), 0, case.planes, tile_rows=16)
+    segs = L.band_segs
+    for k, b in enumerate(L.blocks):
+        rows = sorted(int(s["j"]) for s in segs if s["block"] == k and s["dir"] == 0)
+        want = sorted({r for j0 in range(1, b.nj + 1, 16) for r in (j0, min(j0 + 15, b.nj))})
+        assert rows == want
+        cols = sorted(int(s["i"]) for s in segs if s["block"] == k and s["dir"] != 0)
+        face = L.block_table["face_off"][k]
+        assert cols == sorted(c for c, fi in ((1, 2), (b.ni, 3)) if face[fi] >= 0)
+        assert all(int(s["len"]) == (b.ni if s["dir"] == 0 else b.nj) for s in segs if s["block"] == k)
