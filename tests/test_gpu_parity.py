@@ -172,6 +172,12 @@ FUSED = {
     "lattice-256-loopback4": (lambda: lattice_case(2, 2, 256, 24, 2, h=0.01, dtau=0.0002, nbody=1,
                                                    bodies=((3, "north", 0),)), 3, 8, 4, "loopback"),
     "C1-loopback2": (lambda: baseline_workload("C1").case, 2, None, 2, "loopback"),
+    "nj1-p1": (lambda: CaseConfig(nharms=0, npde=4, iterations=4, dtau=0.001, omega=1.0, nbody=1,
+                                  blocks=[BlockSpec(0, 512, 1, 0.0, 0.0, 0.01, body_faces=(("north", 0),))],
+                                  cuts=[CutSpec(CutSide(0, "east", 1, 1), CutSide(0, "west", 1, 1))]),
+               4, None, 1, "fold"),
+    "nj2-stacked": (lambda: stacked_pair_case(256, 2, 1, h=0.01, dtau=0.0002, nbody=1,
+                                              bodies=((1, "north", 0),)), 3, 1, 1, "fold"),
 }
 
 
