@@ -69,4 +69,9 @@ def test_sm100a_cubin_present():
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", native.LIB_PATH], capture_output=True, text=True).stdout
     assert "UTMALDG" in sass          # tensor TMA loads in the stage kernel
+    assert "UTMASTG" in sass          # tensor TMA stores (update stages, pass B)
     assert "SYNCS" in sass            # mbarrier pipeline
+    assert "pair_tma_kernel" in sass and "band_kernel" in sass   # paired-stage schedule
+    # no fused multiply-adds in the reference-rounded arithmetic: the only
+    # DFMAs are the residual-norm partials (P per row of the first stage)
+    assert sass.count("DMUL") > sass.count("DFMA")
