@@ -193,10 +193,13 @@ __device__ __forceinline__ void stage_point(const double (&c)[P], const double (
 template <int P>
 __device__ __forceinline__ void record_nonfinite(const double (&v)[P], const hbgpu_stage_args &a, int bidx,
                                                  const hbgpu_block &b, int p, int j, int i, int gstage) {
-    bool ok = true;
+    // on the integer pipe (the fp64 pipe is this kernel's binding resource):
+    // a value is non-finite iff its exponent field is all ones, and the
+    // largest masked exponent of the P values is all ones iff any one is
+    unsigned ex = 0;
 #pragma unroll
-    for (int n = 0; n < P; ++n) ok = ok && finite_fp(v[n]);
-    if (!ok) {
+    for (int n = 0; n < P; ++n) ex = max(ex, (unsigned)__double2hiint(v[n]) & 0x7ff00000u);
+    if (ex == 0x7ff00000u) {
         for (int n = 0; n < P; ++n)
             if (nonfinite(v[n])) {
                 const long long lin = (((long long)(n * NPDE + p) * b.nj + (j - 1)) * b.ni) + (i - 1);
