@@ -348,6 +348,10 @@ def run_ours(args, wl):
     dr = DeviceRank(case, topo, part, plan, rank=rank, device=local, comm=comm,
                     tile_rows=args.tile_rows, max_iters=args.warmup + args.steps + 1, pinned_ic=ic)
     dr.prime()
+    if world > 1:
+        # one eager iteration first, so every NCCL send/recv of the iteration
+        # has run (connections set up) before the graph capture records them
+        dr.iterate(1, use_graph=False)
     dr.iterate(args.warmup, use_graph=True)
     torch.cuda.synchronize()
     l0 = native.launch_count()

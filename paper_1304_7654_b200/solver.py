@@ -712,7 +712,12 @@ def _execute_distributed(spec, topology, partition, plan, iterations, dist, worl
         t0 = time.perf_counter()
         dr.prime()
         if iterations > 0:
-            dr.iterate(iterations, use_graph=spec.use_graph)
+            # the first iteration eagerly: NCCL sets up its peer connections
+            # outside the graph capture that records the rest
+            first = 1 if spec.use_graph and iterations > 1 else 0
+            if first:
+                dr.iterate(first, use_graph=False)
+            dr.iterate(iterations - first, use_graph=spec.use_graph)
         torch.cuda.synchronize(dr.device)
         loop_s = time.perf_counter() - t0
         divs = [None] * world
