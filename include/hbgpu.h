@@ -192,6 +192,12 @@ typedef struct hbgpu_stage_args {
     const struct hbgpu_band_seg *band_segs; /* hbgpu_band: device segments  */
     int32_t nband_segs;
     int32_t band_max_len;
+    /* pair != 0: device [total_tiles * tile_rows * 2 * tile_pdes * planes].
+     * Pass A (pair 1) saves q0 at each tile's strip-edge columns inside the
+     * block; pass B (pair 2), which overwrites q0 in place, reads them back
+     * from here: by then the neighbouring strip's CTA may have replaced q0
+     * at those columns                                                      */
+    double *edge_q0;
     /* D row-major P x P with a +0.0 diagonal (hbcore.py:88-94); ap[n*4 + p]
      * = amp[n] (1 + p/4), zero except on planes 1 and 2 (hbcore.py:170-175):
      * the kernel adds those zero terms as exact signed zeros              */
@@ -317,6 +323,7 @@ typedef struct hbgpu_engine_desc {
     const hbgpu_band_seg *band_segs;   int32_t nband_segs; int32_t band_max_len;
     int32_t fused;
     int32_t pad1;
+    double *edge_q0;                 /* fused: device, see hbgpu_stage_args */
     const hbgpu_force_seg *segs;     int32_t nsegs;  /* device */
     double *force_hist;              /* device [max_iters*3*planes*nbody] */
     const hbgpu_peer_msg *sends;     int32_t nsends; /* HOST arrays */

@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
             const Tile tl = decode_tile<PT>(a, t);
             const hbgpu_block b = a.blocks[tl.bidx];
             const bool west_in = tl.i0 > 1, east_in = tl.i0 + G::TCOLS <= b.ni;
-            const int64_t ps4 = b.ps * NPDE;
+            const int64_t erow = (int64_t)t * a.tile_rows;   // this tile's rows in edge_q0
             bool act[KE];
             int ie_k[KE];
             double ap_k[KE], sv_n[KE], bs_n[KE];
@@ -360,11 +360,10 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
                 for (int c = 0; c < KE; ++c) {
                     if (!act[c]) continue;
                     sv_n[c] = __ldg(a.sxy + b.sxy_off + (int64_t)(rr - 1) * b.sxy_pitch + (ie_k[c] - 1));
-                    if (PB) {
-                        const int64_t cell = b.base + (int64_t)(tl.pde0 + pp_k[c]) * b.ps + (int64_t)rr * b.rs + LEAD +
-                                             ie_k[c];
-                        bs_n[c] = __ldg(a.q0 + cell + n_k[c] * ps4);
-                    }
+                    // q0 at the edge cell: pass B overwrites q0 in place, and the
+                    // edge column belongs to the neighbouring strip, whose CTA
+                    // may already have replaced it -- read pass A's copy
+                    if (PB) bs_n[c] = __ldg(a.edge_q0 + (erow + rr - tl.j0) * NE + lane + 32 * c);
                 }
             };
             fetch(tl.j0);
@@ -403,6 +402,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
                     for (int m = 0; m < P; ++m) o = radd(o, rmul(drow[c][m], rc[m * PT * G::BW]));
                     o = radd(o, rmul(ap_k[c], sv_c[c]));
                     const double base = PB ? bs_c[c] : rc[n * PT * G::BW];
+                    if (!PB) a.edge_q0[(erow + r - tl.j0) * NE + lane + 32 * c] = base;   // q0 (pass A: in)
                     const double v = rsub(base, rmul(a.coef, o));
                     ring[cin.slot * S::SLOT + (side == 0 ? S::EDGE_W + (n * PT + pp) * 8 + 7
                                                             : S::EDGE_E + (n * PT + pp) * 8)] = v;
@@ -685,8 +685,8 @@ static int pair_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only
     int rc = prepare_pair<P, false, HBGPU_PAIR_RA, HBGPU_PAIR_Q, PT>(la);
     if (!rc) rc = prepare_pair<P, true, HBGPU_PAIR_R, HBGPU_PAIR_Q, PT>(lb);
     if (rc || prepare_only) return rc;
-    if (a.tmaps == nullptr || a.band == nullptr) {
-        hbgpu_set_error("hbgpu_stage (pair): args->tmaps and args->band are required");
+    if (a.tmaps == nullptr || a.band == nullptr || a.edge_q0 == nullptr) {
+        hbgpu_set_error("hbgpu_stage (pair): args->tmaps, args->band and args->edge_q0 are required");
         return HBGPU_ERR_ARG;
     }
     PairLaunch &L = a.pair == 2 ? lb : la;

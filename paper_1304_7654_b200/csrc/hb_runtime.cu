@@ -216,6 +216,7 @@ void fill_args(const hbgpu_engine_desc &d, hbgpu_stage_args &a) {
     a.band_segs = d.band_segs;
     a.nband_segs = d.nband_segs;
     a.band_max_len = d.band_max_len;
+    a.edge_q0 = d.edge_q0;
     memcpy(a.D, d.D, sizeof(a.D));
     memcpy(a.ap, d.ap, sizeof(a.ap));
 }
@@ -303,6 +304,10 @@ int one_iteration(hbgpu_engine *e, cudaStream_t s) {
 extern "C" int hbgpu_engine_create(const hbgpu_engine_desc *desc, hbgpu_engine **out) {
     if (desc == nullptr || out == nullptr || desc->planes < 1 || desc->nblocks < 1) {
         hbgpu_set_error("hbgpu_engine_create: bad descriptor");
+        return HBGPU_ERR_ARG;
+    }
+    if (desc->fused && desc->edge_q0 == nullptr) {
+        hbgpu_set_error("hbgpu_engine_create: fused schedule needs edge_q0");
         return HBGPU_ERR_ARG;
     }
     int prc = hbgpu_stage_prepare(desc->planes);

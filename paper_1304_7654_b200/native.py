@@ -74,6 +74,7 @@ class StageArgs(ctypes.Structure):
         ("tile_rows", c_i32), ("in_slot", c_i32), ("interleaved", c_i32), ("tile_pdes", c_i32),
         ("out_slot", c_i32), ("pair", c_i32), ("coef", c_f64), ("coef2", c_f64),
         ("band_segs", c_vp), ("nband_segs", c_i32), ("band_max_len", c_i32),
+        ("edge_q0", c_vp),
         ("D", c_f64 * (MAX_TEMPLATED_P * MAX_TEMPLATED_P)),
         ("ap", c_f64 * (MAX_P * NPDE))]
 
@@ -87,7 +88,7 @@ class EngineDesc(ctypes.Structure):
         ("unpack_dirs", c_vp), ("nunpack", c_i32), ("unpack_max_len", c_i32),
         ("post_dirs", c_vp), ("npost", c_i32), ("post_max_len", c_i32),
         ("band_segs", c_vp), ("nband_segs", c_i32), ("band_max_len", c_i32),
-        ("fused", c_i32), ("pad1", c_i32),
+        ("fused", c_i32), ("pad1", c_i32), ("edge_q0", c_vp),
         ("segs", c_vp), ("nsegs", c_i32),
         ("force_hist", c_vp),
         ("sends", ctypes.POINTER(PeerMsg)), ("nsends", c_i32),

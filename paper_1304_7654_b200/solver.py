@@ -228,6 +228,10 @@ class DeviceRank:
         nb = len(L.blocks)
         self.max_iters = max(1, max_iters)
         self.norm_part = torch.zeros(L.total_tiles * native.TILE_WARPS, dtype=f64, device=dev)
+        # paired schedule: q0 at every tile's two edge columns, saved by pass A
+        # for pass B (which overwrites q0 in place); hbgpu_stage_args.edge_q0
+        self.edge_q0 = torch.zeros(L.total_tiles * L.tile_rows * 2 * L.tile_pdes * case.planes
+                                   if L.fused else 1, dtype=f64, device=dev)
         self.sumsq = torch.zeros(self.max_iters * nb, dtype=f64, device=dev)
         self.status = torch.full((nb,), -1, dtype=torch.int64, device=dev)
         self.iter = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -318,6 +322,7 @@ class DeviceRank:
         d.post_max_len = int(L.post_dirs["length"].max()) if len(L.post_dirs) else 0
         d.band_segs, d.nband_segs = self.t_band.data_ptr(), len(L.band_segs)
         d.band_max_len, d.fused = int(L.band_max_len), int(L.fused)
+        d.edge_q0 = self.edge_q0.data_ptr()
         d.segs, d.nsegs = self.t_segs.data_ptr(), len(L.force_segs)
         d.force_hist = self.force_hist.data_ptr()
         self._sends = (native.PeerMsg * max(1, len(L.sends)))(
@@ -412,6 +417,7 @@ class DeviceRank:
         a.out = self.slots[self.STAGE_OUT[stage]].data_ptr()
         a.band = self.slots[2].data_ptr()
         a.band_segs, a.nband_segs, a.band_max_len = d.band_segs, d.nband_segs, d.band_max_len
+        a.edge_q0 = d.edge_q0
         a.sendbuf, a.blocks, a.tile_block = d.sendbuf, d.blocks, d.tile_block
         a.sxy, a.faces, a.status, a.iter, a.dmat = d.sxy, d.faces, d.status, d.iter, d.dmat
         a.norm_part = d.norm_part if stage == 0 else None
