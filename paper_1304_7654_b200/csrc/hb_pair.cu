@@ -32,9 +32,9 @@ namespace hbgpu {
 // ---- band: the first stage of a pair at the tile-perimeter cells -----------------
 
 // Segment kinds: dir 0 = a row run (threads along i), dir 1 = a column run
-// (threads along j), dir 2 = two adjacent columns i, i+1 (a strip boundary):
-// a 128-thread block takes 64 rows of both, so the two columns' overlapping
-// stencil sectors are fetched once into L1.
+// (threads along j), dir 2 = two adjacent columns i, i+1 (both face columns
+// of a block 2 cells wide): a 128-thread block takes 64 rows of both, so the
+// two columns' overlapping stencil sectors are fetched once into L1.
 template <int P>
 __global__ void __launch_bounds__(128) band_kernel(const __grid_constant__ hbgpu_stage_args a) {
     const hbgpu_band_seg sg = a.band_segs[blockIdx.y];

@@ -230,7 +230,7 @@ def _build_band(layout, fused):
         face = layout.block_table["face_off"][k]
         cols = sorted({c for c, fi in ((1, 2), (b.ni, 3)) if face[fi] >= 0})
         segs += [(k, 0, r, 1, b.ni, 0) for r in rows]
-        # adjacent columns (both sides of a strip boundary) go as one
+        # two adjacent face columns (a block 2 cells wide) go as one
         # two-column run, whose stencil reads overlap
         c = 0
         while c < len(cols):
