@@ -110,9 +110,10 @@ static int launch_band(const hbgpu_stage_args &a, cudaStream_t s) {
 
 // ---- the paired stage kernel ------------------------------------------------------
 //
-// Same CTA structure as stage_tma_kernel (hb_stage.cu): 8 consumer warps,
-// a TMA load warp, a TMA store warp; tiles of 256/PT columns x PT pdes x
-// tile_rows rows; lane = column.  Per row step r the consumers
+// CTA structure as stage_tma_kernel (hb_stage.cu) -- 8 consumer warps, a
+// TMA load warp, a TMA store warp -- plus an edge warp (v1 at the strip's
+// edge columns); tiles of 256/PT columns x PT pdes x tile_rows rows;
+// lane = column.  Per row step r the consumers
 //   1. compute v1(r), the pair's first stage, from the stencil ring (rows
 //      r-1, r, r+1 of `in`, all read from shared memory);
 //   2. publish v1(r) in a 3-row shared ring and meet on a named barrier;
