@@ -385,7 +385,12 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
                 }
                 if (r < tl.j1) fetch(r + 1);
                 const RingPos nx = advance<R>(cin);
-                mbar_wait_idle(full_in + nx.slot, nx.phase);   // rows r-1, r: waited for already
+                // row r-1 was waited for at the tile start or as the previous
+                // step's row r; row r as the previous step's row r+1, except at
+                // the tile's first row: the ring's fills complete in any order,
+                // so row j0+1 having landed says nothing about row j0
+                if (r == tl.j0) mbar_wait_idle(full_in + cin.slot, cin.phase);
+                mbar_wait_idle(full_in + nx.slot, nx.phase);
 #pragma unroll
                 for (int c = 0; c < KE; ++c) {
                     if (!act[c]) continue;
