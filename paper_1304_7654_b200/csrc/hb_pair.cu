@@ -413,6 +413,9 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
                     ring[cin.slot * S::SLOT + (side == 0 ? S::EDGE_W + (n * PT + pp) * 8 + 7
                                                             : S::EDGE_E + (n * PT + pp) * 8)] = v;
                 }
+                // a later fill of this slot may TMA a face granule over the
+                // same words: order these generic-proxy writes before it
+                fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(edge_ready + cin.slot);
