@@ -699,7 +699,7 @@ static int pair_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only
         return HBGPU_ERR_ARG;
     }
     PairLaunch &L = a.pair == 2 ? lb : la;
-    const int grid = min(L.grid, a.total_tiles);
+    const int grid = persistent_grid(L.grid, a.total_tiles);
     L.fn<<<grid, PAIR_THREADS, L.smem, s>>>(a);
     hbgpu_count_launch(1);
     return hbgpu_check_launch("hbgpu_stage (pair)");

@@ -480,6 +480,15 @@ __global__ void __launch_bounds__(CW * 32) stage_kernel_generic(const __grid_con
 
 // ---- launch -------------------------------------------------------------------
 
+int persistent_grid(int resident, int tiles) {
+    int grid = min(resident, tiles);
+    if (const char *cap = getenv("HBGPU_GRID_LIMIT")) {
+        const int c = atoi(cap);
+        if (c > 0) grid = min(grid, c);
+    }
+    return max(grid, 1);
+}
+
 struct Launch {
     void (*fn)(hbgpu_stage_args) = nullptr;
     size_t smem = 0;
@@ -539,7 +548,7 @@ static int launch_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_on
         return HBGPU_ERR_ARG;
     }
     Launch &L = a.stage == 0 ? first : rest;
-    const int grid = min(L.grid, a.total_tiles);
+    const int grid = persistent_grid(L.grid, a.total_tiles);
     L.fn<<<grid, THREADS, L.smem, s>>>(a);
     hbgpu_count_launch(1);
     return hbgpu_check_launch("hbgpu_stage");

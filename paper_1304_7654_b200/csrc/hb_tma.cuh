@@ -219,6 +219,12 @@ __device__ __forceinline__ void store_rows(const void *map, const void *src, int
     else tma_store_4d(map, x, row, pde0, 0, src);
 }
 
+// Persistent grid of a stage / pair launch: min(resident CTAs, tiles),
+// further capped by HBGPU_GRID_LIMIT when set (a test knob: with a few CTAs
+// each one walks many tiles, which exercises the rings' tile-to-tile hand-
+// over and lets strips drift apart as they do at full size).
+int persistent_grid(int resident, int tiles);
+
 // hb_pair.cu: launch (or, prepare_only, just configure) the paired-stage
 // kernel for args.pair = 1 (stages 0, 1) or 2 (stages 2, 3)
 int pair_dispatch(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only);

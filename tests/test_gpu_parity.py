@@ -219,3 +219,36 @@ def test_paired_graph_and_eager_identical(cuda):
     b = run_case(RunSpec(case=case, ranks=1, iterations=3, tile_rows=8, use_graph=False, fused=True))
     assert a.field_bits_equal(b) and a.forces.equal_bits(b.forces)
     np.testing.assert_allclose(a.residual_norms, b.residual_norms, rtol=1e-13)
+
+
+MANY_TILES = {
+    # 4 blocks x 2 strips x 4 pdes x 5 row tiles = 160 tiles
+    "lattice-512": (lambda: lattice_case(2, 2, 512, 40, 2, h=0.01, dtau=0.0002, nbody=1,
+                                         bodies=((3, "north", 0),)), 3, 8),
+    # 64-column strips x 4 pdes (PT = 4), reversed cut
+    "pair-64-pt4": (lambda: pair_case(64, 30, 3, h=0.02, dtau=0.0005, reversed_cut=True, nbody=1,
+                                      bodies=((1, "north", 0),)), 3, 4),
+    # self-cut: a block's own strips feed each other's halos
+    "self-cut-768": (lambda: CaseConfig(nharms=4, npde=4, iterations=3, dtau=0.0001, omega=0.12, nbody=1,
+                                        blocks=[BlockSpec(0, 768, 23, 0.0, 0.0, 0.01,
+                                                          body_faces=(("south", 0),))],
+                                        cuts=[CutSpec(CutSide(0, "east", 1, 23), CutSide(0, "west", 1, 23))]),
+                     3, 5),
+}
+
+
+@pytest.mark.parametrize("limit", [1, 3])
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("name", sorted(MANY_TILES))
+def test_many_tiles_per_cta_match_oracle(name, fused, limit, cuda, oracle_mod, monkeypatch):
+    """With HBGPU_GRID_LIMIT CTAs every CTA walks many tiles, as at full size
+    (C4: 4096 tiles on 148 CTAs), and the strips of one row tile are not
+    processed together (limit 1: strictly one after another).  This covers
+    the rings' hand-over from tile to tile and the in-place pass B, where a
+    strip must not read q0 at its neighbour's edge column from HBM."""
+    monkeypatch.setenv("HBGPU_GRID_LIMIT", str(limit))
+    build, iters, tile_rows = MANY_TILES[name]
+    case = build()
+    got = run_case(RunSpec(case=case, ranks=1, iterations=iters, tile_rows=tile_rows, fused=fused))
+    want = oracle_mod.run(case, iters)
+    assert_parity(got, want, f"{name} fused={fused} limit={limit}")
