@@ -25,6 +25,7 @@ rank owns it fixes:
 
 from __future__ import annotations
 
+import functools
 import os
 from dataclasses import dataclass, field
 
@@ -39,7 +40,8 @@ SECTOR_TARGET = np.int64(1) << np.int64(62)   # face-target flag: whole-sector w
 NPDE = native.NPDE
 WIDE_MIN_NI = 192         # blocks at least this wide use 256-column, 1-pde tiles
 BLOCK_ALIGN = 32          # elements (256 B)
-TARGET_TILES = 148 * 8    # ~8 tiles per persistent CTA (148 SMs x 1 CTA)
+GRID_CTAS = 148           # persistent CTAs of the stage / pair kernels (B200: 1 per SM)
+TILE_OVERHEAD_ROWS = 4    # a tile's cost beyond its rows: 2 halo rows, ring fill, band rows
 MAX_TILE_ROWS = 256
 MIN_TILE_ROWS = 8
 SLOT_TAIL = 64            # elements of zero padding after the last block
@@ -65,14 +67,42 @@ def tiles_per_row(blocks, tile_pdes):
     return {b.id: -(-b.ni // native.TILE_COLS[tile_pdes]) * (NPDE // tile_pdes) for b in blocks}
 
 
-def choose_tile_rows(blocks, tile_pdes=4):
-    """Rows per tile: long tiles amortise the two halo rows each tile re-reads;
-    enough tiles keep every persistent CTA of the stage kernel busy."""
+def round_robin_makespan(blocks, tile_pdes, tile_rows, ctas=GRID_CTAS):
+    """Largest per-CTA load when the persistent kernels walk the tiles round
+    robin (tile t on CTA t mod ctas, tiles in decode_tile order), a tile
+    costing its rows plus TILE_OVERHEAD_ROWS."""
     per_row = tiles_per_row(blocks, tile_pdes)
-    rows = sum(per_row[b.id] * b.nj for b in blocks)
-    tj = rows // TARGET_TILES
-    tj = max(MIN_TILE_ROWS, min(MAX_TILE_ROWS, tj))
-    return tj
+    return _makespan(tuple((per_row[b.id], b.nj) for b in blocks), tile_rows, ctas)
+
+
+@functools.lru_cache(maxsize=4096)
+def _makespan(shape, tile_rows, ctas):
+    costs = []
+    for per_row, nj in shape:
+        rows = np.minimum(tile_rows, nj - np.arange(0, nj, tile_rows)) + TILE_OVERHEAD_ROWS
+        costs.append(np.repeat(rows, per_row))
+    costs = np.concatenate(costs)
+    costs = np.concatenate([costs, np.zeros((-len(costs)) % ctas)])
+    return float(costs.reshape(-1, ctas).sum(axis=0).max())
+
+
+def choose_tile_rows(blocks, tile_pdes=4, ctas=GRID_CTAS):
+    """Rows per tile with the smallest round-robin makespan over the
+    persistent CTAs, among ceil(nj / k) of the tallest block clipped to
+    [MIN_TILE_ROWS, MAX_TILE_ROWS]; ties go to the longer tile.  Long tiles
+    amortise the two halo rows each tile re-reads (and, paired, the band
+    rows); the makespan avoids a last wave that leaves most CTAs idle, e.g.
+    8 blocks of 1024 rows take 128-row tiles (1024 tiles: 7 per CTA) rather
+    than 110-row ones (1280 tiles: 8.6 per CTA)."""
+    nj = max(b.nj for b in blocks)
+    cands = sorted({min(MAX_TILE_ROWS, max(MIN_TILE_ROWS, -(-nj // k))) for k in range(1, nj + 1)},
+                   reverse=True)
+    best = None
+    for tj in cands:
+        load = round_robin_makespan(blocks, tile_pdes, tj, ctas)
+        if best is None or load < best[0]:
+            best = (load, tj)
+    return best[1]
 
 
 @dataclass
