@@ -42,7 +42,7 @@ WIDE_MIN_NI = 192         # blocks at least this wide use 256-column, 1-pde tile
 BLOCK_ALIGN = 32          # elements (256 B)
 GRID_CTAS = 148           # persistent CTAs of the stage / pair kernels (B200: 1 per SM)
 TILE_OVERHEAD_ROWS = 4    # a tile's cost beyond its rows: 2 halo rows, ring fill, band rows
-MAX_TILE_ROWS = 256
+MAX_TILE_ROWS = 1024
 MIN_TILE_ROWS = 8
 SLOT_TAIL = 64            # elements of zero padding after the last block
 # slot layout default: row-interleaved (row j of every (n, p) plane contiguous)
