@@ -242,7 +242,7 @@ MANY_TILES = {
 @pytest.mark.parametrize("name", sorted(MANY_TILES))
 def test_many_tiles_per_cta_match_oracle(name, fused, limit, cuda, oracle_mod, monkeypatch):
     """With HBGPU_GRID_LIMIT CTAs every CTA walks many tiles, as at full size
-    (C4: 4096 tiles on 148 CTAs), and the strips of one row tile are not
+    (C4: 1024 tiles on 148 CTAs), and the strips of one row tile are not
     processed together (limit 1: strictly one after another).  This covers
     the rings' hand-over from tile to tile and the in-place pass B, where a
     strip must not read q0 at its neighbour's edge column from HBM."""
