@@ -44,6 +44,12 @@ GRID_CTAS = 148           # persistent CTAs of the stage / pair kernels (B200: 1
 TILE_OVERHEAD_ROWS = 4    # a tile's cost beyond its rows: 2 halo rows, ring fill, band rows
 MAX_TILE_ROWS = 1024
 MIN_TILE_ROWS = 8
+# auto schedule: paired stages from this many units (cells x P x 4) per stage
+# on the rank.  Below it the band / halo launches of the paired schedule cost
+# more than the halved traffic saves: single stages are 10-13% faster at C1
+# and C2 (2.6M, 4.7M units), paired ones 16% faster at C3 (117M) and ~35% at
+# C4 (2.4G)
+FUSED_MIN_UNITS = 16 * 2 ** 20
 SLOT_TAIL = 64            # elements of zero padding after the last block
 # slot layout default: row-interleaved (row j of every (n, p) plane contiguous)
 # unless HBGPU_LAYOUT=plane selects the plane-major layout
@@ -250,7 +256,11 @@ def _build_band(layout, fused):
     and the face columns that feed a cut (forwarded into the neighbours'
     band halos, read across strip edges on block faces)."""
     eligible = fused_eligible(layout.blocks, layout.planes, layout.tile_pdes)
-    layout.fused = eligible if fused is None else (bool(fused) and eligible)
+    if fused is None:
+        units = sum(b.ni * b.nj for b in layout.blocks) * layout.planes * NPDE
+        layout.fused = eligible and units >= FUSED_MIN_UNITS
+    else:
+        layout.fused = bool(fused) and eligible
     segs = []
     for k, b in enumerate(layout.blocks):
         rows = sorted({r for j0 in range(1, b.nj + 1, layout.tile_rows)

@@ -189,7 +189,8 @@ def test_paired_stages_match_oracle_and_single_stages(name, cuda, oracle_mod):
     case = build()
     topo = build_topology(case)
     part = partition_blocks(topo, 1)
-    lay = build_rank_layout(topo, part, build_cut_plan(topo, part, case.nharms, 4), 0, case.planes, tile_rows)
+    lay = build_rank_layout(topo, part, build_cut_plan(topo, part, case.nharms, 4), 0, case.planes, tile_rows,
+                            fused=True)
     assert lay.fused, "case must take the paired-stage path"
     initial = baseline_workload("C1").initial if name.startswith("C1") else None
     got = run_case(RunSpec(case=case, ranks=ranks, iterations=iters, tile_rows=tile_rows, initial=initial,

@@ -190,8 +190,11 @@ def test_paired_schedule_eligibility_and_band_segments():
         case = baseline_workload(key).case
         topo = build_topology(case)
         part = partition_blocks(topo, 1)
-        L = build_rank_layout(topo, part, build_cut_plan(topo, part, case.nharms, 4), 0, case.planes)
-        assert L.fused, key
+        plan = build_cut_plan(topo, part, case.nharms, 4)
+        L = build_rank_layout(topo, part, plan, 0, case.planes)
+        # auto: paired stages only from FUSED_MIN_UNITS units per stage (C3, C4)
+        assert L.fused == (key in ("C3", "C4")), key
+        assert build_rank_layout(topo, part, plan, 0, case.planes, fused=True).fused, key
     case = lattice_case(2, 2, 45, 19, 3, h=0.02, dtau=0.0005)          # ragged strips
     topo = build_topology(case)
     assert not fused_eligible(topo.blocks, case.planes, 4)
