@@ -7,7 +7,9 @@
   - the paired-stage schedule (band + pair kernels: the bench's path)
     against the single-stage schedule. These are two independent kernel
     paths, each pinned to the oracle at small sizes in test_gpu_parity.py.
-    Fields must agree bitwise after one iteration, compared on the device.
+    Fields must agree bitwise after three iterations (one eager, two graph
+    replays), compared on the device.  (A 50-iteration run, BASELINE's count,
+    agreed bitwise as well; it is left out of the suite for time.)
   - dtau = 0 leaves the state unchanged (hbcore.py:240, q = q0 - 0*R).
     The check is a device-side comparison of all 19.4 GB.
 """
@@ -36,7 +38,7 @@ def _pinned_ic(wl, blocks):
         return dict(ex.map(one, blocks))
 
 
-def _c4_rank(wl, ic, fused, case=None):
+def _c4_rank(wl, ic, fused, case=None, max_iters=2):
     from paper_1304_7654_b200.cutplan import build_cut_plan
     from paper_1304_7654_b200.solver import DeviceRank
     from paper_1304_7654_b200.topology import build_topology, partition_blocks
@@ -44,7 +46,7 @@ def _c4_rank(wl, ic, fused, case=None):
     topo = build_topology(case)
     part = partition_blocks(topo, 1)
     plan = build_cut_plan(topo, part, case.nharms, case.npde)
-    return DeviceRank(case, topo, part, plan, rank=0, device=0, pinned_ic=ic, max_iters=2, fused=fused)
+    return DeviceRank(case, topo, part, plan, rank=0, device=0, pinned_ic=ic, max_iters=max_iters, fused=fused)
 
 
 def _need_hbm(gb):
@@ -72,10 +74,11 @@ def test_c4_full_size_paired_equals_single_stages(cuda):
     ranks = []
     try:
         for fused in (True, False):
-            dr = _c4_rank(wl, ic, fused)
+            dr = _c4_rank(wl, ic, fused, max_iters=3)
             assert dr.fused == fused
             dr.prime()
-            dr.iterate(1, use_graph=True)
+            dr.iterate(1, use_graph=False)
+            dr.iterate(2, use_graph=True)
             torch.cuda.synchronize()
             assert dr.divergence() is None
             ranks.append(dr)
@@ -84,9 +87,9 @@ def test_c4_full_size_paired_equals_single_stages(cuda):
             a = paired.block_view(paired.slots[0], b.id)
             s = single.block_view(single.slots[0], b.id)
             assert torch.equal(a, s), f"C4 block {b.id}: paired and single-stage fields differ"
-            # the state moved (one iteration is not a no-op)
+            # the state moved (the iterations are not a no-op)
             assert not torch.equal(a[:, :, 1:-1, 1:-1], ic[b.id].to(a.device))
-        np.testing.assert_allclose(paired.sumsq[:64].cpu().numpy(), single.sumsq[:64].cpu().numpy(),
+        np.testing.assert_allclose(paired.sumsq[:3 * 64].cpu().numpy(), single.sumsq[:3 * 64].cpu().numpy(),
                                    rtol=1e-12, atol=0)
     finally:
         for dr in ranks:
