@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--kernel-reps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-iters", type=int, default=1)
+    ap.add_argument("--cpu-sample-iters", type=int, default=10)
     ap.add_argument("--zero-ic", action="store_true",
                     help="development only: zero initial state (skips the seeded IC build)")
     return ap.parse_args()
