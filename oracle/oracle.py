@@ -73,6 +73,9 @@ def lib():
         L.oracle_stage_many.argtypes = [ctypes.c_int, dp, dp, dp, dp, dp, dp, dp, dp, dp,
                                         lg, lg, ctypes.c_double, ctypes.c_int, ctypes.c_int, dp]
         L.oracle_stage_many.restype = ctypes.c_int
+        L.oracle_stage_lean.argtypes = [ctypes.c_int, dp, dp, dp, dp, dp, dp, dp, dp, dp,
+                                        lg, lg, ctypes.c_double, ctypes.c_int, ctypes.c_int, dp, dp]
+        L.oracle_stage_lean.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -313,12 +316,93 @@ class OracleSolver:
         return sum(s.ni * s.nj for s in self.blocks) * self.planes * 4
 
 
+class LeanOracleSolver(OracleSolver):
+    """The same run loop holding only q and q0 per block (BASELINE C3/C4 at
+    full size: C4 needs 38.8 GB instead of the reference's 77.5 GB).  The
+    stage is oracle_stage_lean (hb_oracle.c): forcing formed on the fly as
+    (amp[n] pfac[p]) * sxy -- bitwise forcing_values() -- and a 2-row residual
+    scratch per (block, pde).  Norms: per-block compensated sums of R**2,
+    combined with math.fsum (rtol 1e-12 against the fsum definition)."""
+
+    def __init__(self, case, initial=None, nthreads=None, record_norms=True,
+                 record_forces=False):
+        self.case = case
+        self.planes = planes = 2 * case.nharms + 1
+        self.npde = npde = case.npde
+        self.blocks = blocks = sorted(case.blocks, key=lambda s: s.id)
+        self.nthreads = nthreads or max(1, len(os.sched_getaffinity(0)))
+        self.dmat = np.ascontiguousarray(spectral_matrix(case.nharms, case.omega))
+        amp = np.zeros(planes)
+        if planes > 1:
+            amp[1] = 0.8
+        if planes > 2:
+            amp[2] = -0.5
+        pfac = 1.0 + 0.25 * np.arange(npde, dtype=np.float64)
+        self.ap = np.ascontiguousarray(amp[:, None] * pfac[None, :])   # (planes, npde)
+        self.qs, self.q0s, self.sxys = {}, {}, {}
+        for s in blocks:
+            self.qs[s.id] = np.zeros((planes, npde, s.nj + 2, s.ni + 2))
+            self.q0s[s.id] = np.zeros_like(self.qs[s.id])
+            xc, yc = cell_centres(s)
+            self.sxys[s.id] = np.ascontiguousarray(
+                np.sin(TWO_PI * xc)[None, :] * np.sin(TWO_PI * yc)[:, None])
+            ic = initial(s, planes, npde) if initial is not None else initial_values(s, planes, npde)
+            self.qs[s.id][:, :, 1:s.nj + 1, 1:s.ni + 1] = ic
+        self.alpha_dtau = [a * case.dtau for a in RK_ALPHAS]
+        arr = lambda vals, t: np.array(vals, dtype=t)  # noqa: E731
+        self._q = arr([_ptr(self.qs[s.id]) for s in blocks], np.uintp)
+        self._q0 = arr([_ptr(self.q0s[s.id]) for s in blocks], np.uintp)
+        self._sxy = arr([_ptr(self.sxys[s.id]) for s in blocks], np.uintp)
+        self._ni = arr([s.ni for s in blocks], np.int64)
+        self._nj = arr([s.nj for s in blocks], np.int64)
+        self._nu = arr([NU / (s.h * s.h) for s in blocks], np.float64)
+        self._adv = arr([ADVECTION / (2.0 * s.h) for s in blocks], np.float64)
+        self._sumsq = np.zeros(len(blocks))
+        self._bad = np.zeros(len(blocks), dtype=np.int32)
+        self.record_norms, self.record_forces = record_norms, record_forces
+        self.result = OracleResult(fields=self.qs, forces=np.zeros((3, planes, case.nbody)))
+        self.done = 0
+
+    def iterate(self, iterations):
+        L = lib()
+        nb = len(self.blocks)
+        for _ in range(iterations):
+            for stage in range(4):
+                want_norm = stage == 0 and self.record_norms
+                bad = L.oracle_stage_lean(nb, _ptr(self._q), _ptr(self._q0), _ptr(self._sxy),
+                                          _ptr(self._ni), _ptr(self._nj), _ptr(self._nu),
+                                          _ptr(self._adv), _ptr(self.dmat), _ptr(self.ap),
+                                          self.planes, self.npde, self.alpha_dtau[stage],
+                                          int(stage == 0), self.nthreads,
+                                          _ptr(self._sumsq) if want_norm else None,
+                                          _ptr(self._bad))
+                if want_norm:
+                    try:
+                        self.result.norms.append(math.sqrt(math.fsum(self._sumsq.tolist())))
+                    except (OverflowError, ValueError):
+                        self.result.norms.append(math.inf)
+                if bad:
+                    for k, s in enumerate(self.blocks):
+                        if self._bad[k]:
+                            raise OracleDivergence(self.done, stage, s.id,
+                                                   *divergence_location(self.qs[s.id]))
+                exchange(self.qs, self.case.cuts)
+            forces = compute_forces(self.qs, self.blocks, self.planes, self.case.nbody)
+            self.result.forces = forces
+            if self.record_forces:
+                self.result.force_history.append(forces.copy())
+            self.done += 1
+        return self.result
+
+
 def run(case, iterations=None, initial=None, nthreads=None, record_norms=True,
-        record_forces=False):
-    """Single-rank restatement of driver.run_case: prime, iterate, return fields/forces."""
+        record_forces=False, lean=False):
+    """Single-rank restatement of driver.run_case: prime, iterate, return fields/forces.
+    lean=True holds only q and q0 (LeanOracleSolver)."""
     import time
     iterations = case.iterations if iterations is None else iterations
-    solver = OracleSolver(case, initial, nthreads, record_norms, record_forces)
+    cls = LeanOracleSolver if lean else OracleSolver
+    solver = cls(case, initial, nthreads, record_norms, record_forces)
     t0 = time.perf_counter()
     solver.prime()
     result = solver.iterate(iterations)

@@ -169,3 +169,43 @@ def test_oracle_ordered_sum_is_rank_ordered(oracle_mod):
     acc = oracle_mod.ordered_sum(bufs)
     want = (bufs[0] + bufs[1]) + bufs[2]
     assert np.array_equal(acc, want)
+
+
+@pytest.mark.parametrize("name", sorted(RUNS))
+def test_lean_oracle_matches_reference_fingerprint(name, oracle_mod):
+    """The memory-lean driver (q and q0 only, forcing on the fly, 2-row
+    residual scratch; used for C3/C4 at full size) reproduces the reference's
+    own fingerprints bit for bit."""
+    build, wl = RUNS[name]
+    case = build()
+    initial = baseline_workload(wl).initial if wl else None
+    _host_matches(name, case, initial)
+    res = oracle_mod.run(case, FPS[name]["iterations"], initial=initial, record_norms=False, lean=True)
+    assert oracle_mod.fingerprint(res.fields, res.forces) == FPS[name]["fingerprint"]
+
+
+@pytest.mark.parametrize("name,iters", [("tc1-mini-20", 20), ("self-cut-5", 5), ("C0-seeded-10", 10)])
+def test_lean_oracle_equals_full_oracle(name, iters, oracle_mod):
+    """Same fields bitwise and the same per-iteration norms (rtol 1e-13: the
+    lean driver sums R**2 per block with a compensated accumulator, the full
+    one with math.fsum) on any host, fixtures or not."""
+    build, wl = RUNS[name]
+    case = build()
+    initial = baseline_workload(wl).initial if wl else None
+    full = oracle_mod.run(case, iters, initial=initial)
+    lean = oracle_mod.run(case, iters, initial=initial, lean=True)
+    for b in full.fields:
+        assert np.array_equal(full.fields[b], lean.fields[b]), f"block {b}"
+    assert np.array_equal(full.forces, lean.forces)
+    np.testing.assert_allclose(lean.norms, full.norms, rtol=1e-13, atol=0)
+
+
+def test_lean_oracle_divergence_like_full(oracle_mod):
+    case = pair_case(8, 6, 1, h=0.25, dtau=50.0, nbody=0)
+    errs = []
+    for lean in (False, True):
+        with pytest.raises(oracle_mod.OracleDivergence) as ei:
+            oracle_mod.run(case, 100, lean=lean)
+        e = ei.value
+        errs.append((e.iteration, e.stage, e.block, e.i, e.j, e.p, e.n))
+    assert errs[0] == errs[1]
