@@ -20,7 +20,7 @@
 extern "C" {
 #endif
 
-#define HBGPU_ABI_VERSION 1
+#define HBGPU_ABI_VERSION 2
 #define HBGPU_NPDE 4
 /* largest snapshot count handled by the register-window stage kernels;
  * larger P runs the generic kernel */
@@ -96,6 +96,19 @@ typedef struct hbgpu_face_target {
 } hbgpu_face_target;
 #define HBGPU_SECTOR_TARGET_BIT 62
 
+/* Divergence status keys (hbgpu_stage_args.status, one per block, reset to
+ * all-ones; kernels atomicMin into them):
+ *   (gstage << 40) | lin        a non-finite value at global stage gstage
+ *                               (iteration*4 + stage + 1), lin = the
+ *                               lexicographic (n, p, j-1, i-1) interior
+ *                               index (hbcore.py:279-284)
+ *   ... | HBGPU_HAZARD_BIT      a finite value of magnitude >= 2^1022 (the
+ *                               paired kernel's exact rewrites need
+ *                               |q| < 2^1022; the host then repeats the
+ *                               run on the strict single-stage kernels)   */
+#define HBGPU_STATUS_LIN_BITS 40
+#define HBGPU_HAZARD_BIT (1ull << 39)
+
 /* One halo copy direction for the standalone halo kernel (priming exchange,
  * unpack after a receive, exchange_halos).  Value v = n*4 + p of element e
  * moves from src_base[src_off + e*src_es + v*src_vs] to
@@ -166,7 +179,8 @@ typedef struct hbgpu_stage_args {
     const int32_t *tile_block;  /* device array [total_tiles]: tile -> block */
     const double *sxy;         /* device forcing tables                    */
     const hbgpu_face_target *faces; /* device face-target pool             */
-    double *norm_part;         /* device [total_tiles] (stage 0) or NULL    */
+    double *norm_part;         /* device [total_tiles * HBGPU_TILE_WARPS]
+                                  (stage 0) or NULL                         */
     unsigned long long *status;/* device [nblocks] divergence keys         */
     const int32_t *iter;       /* device iteration counter                 */
     const double *dmat;        /* device P*P (generic kernel only)         */
@@ -255,15 +269,29 @@ int hbgpu_halo(double *slot, double *sendbuf, const double *recvbuf,
                int32_t planes, void *stream);
 
 /* per-block sums of the stage-0 norm partials -> sumsq[iter*nblocks + b] */
+/* hazard key at gstage 0 for every block whose region of `slot` holds a
+ * finite value of magnitude >= 2^1022 (the engine runs it before the
+ * priming exchange of a paired-schedule run)                               */
+int hbgpu_hazard_scan(const double *slot, const hbgpu_block *blocks, int32_t nblocks,
+                      int32_t planes, unsigned long long *status, void *stream);
+
+/* per-iteration residual norms: norms[it] = sqrt(sum over b ascending of
+ * sumsq[it * nblocks + b]), one strict left-to-right fold per iteration
+ * (the host fold of SURVEY.md §8 a14, bitwise)                             */
+int hbgpu_norm_totals(const double *sumsq, int32_t iters, int32_t nblocks, double *norms,
+                      void *stream);
+
 int hbgpu_norm_fold(const hbgpu_block *blocks, int32_t nblocks,
                     const double *norm_part, double *sumsq,
-                    const int32_t *iter, void *stream);
+                    const int32_t *iter, int32_t max_iters, void *stream);
 
 /* per-rank force partials (hbcore.py:359-382) into
- * hist[iter][k][n][body] (k = cl, cd, cm), then iter += 1               */
+ * hist[iter][k][n][body] (k = cl, cd, cm), then iter += 1.  `max_iters` is
+ * hist's capacity in iterations (and sumsq's in hbgpu_norm_fold): a device
+ * counter at or past it writes nothing.                                  */
 int hbgpu_forces(const double *slot, const hbgpu_force_seg *segs,
                  int32_t nsegs, int32_t planes, int32_t nbody, double *hist,
-                 int32_t *iter, void *stream);
+                 int32_t *iter, int32_t max_iters, void *stream);
 
 /* rank-ordered sum (runtime.py:290-294): out[k] = in[0][k] + in[1][k] + ...
  * over `nranks` stacked buffers of `count` doubles                        */
@@ -305,7 +333,7 @@ typedef struct hbgpu_engine_desc {
     const double *sxy;               /* device */
     const hbgpu_face_target *faces;  /* device */
     const double *dmat;              /* device */
-    double *norm_part;               /* device [total_tiles] */
+    double *norm_part;               /* device [total_tiles * HBGPU_TILE_WARPS] */
     double *sumsq;                   /* device [max_iters * nblocks] */
     unsigned long long *status;      /* device [nblocks] */
     int32_t *iter;                   /* device, 1 element */
@@ -347,9 +375,17 @@ int hbgpu_engine_create(const hbgpu_engine_desc *desc, hbgpu_engine **out);
 /* priming halo exchange of slot A (driver.py:129) */
 int hbgpu_engine_prime(hbgpu_engine *eng, void *stream);
 /* `iterations` full iterations: 4 x (stage [+ NCCL + unpack]), norm fold,
- * forces.  use_graph != 0 replays a CUDA graph of one iteration.          */
+ * forces.  use_graph != 0 replays a CUDA graph of one iteration.  The
+ * engine counts the iterations it has issued (iterate and step phase 4)
+ * and refuses (HBGPU_ERR_ARG, nothing launched) a call that would take the
+ * count past desc.max_iters, the capacity of sumsq and force_hist.        */
 int hbgpu_engine_iterate(hbgpu_engine *eng, int32_t iterations, int32_t use_graph,
                          void *stream);
+/* iterations issued since create / the last rewind */
+int hbgpu_engine_iterations_done(const hbgpu_engine *eng);
+/* start the history over: issued count = 0, and on `stream` the device
+ * iteration counter = 0 and every status key = all-ones (no divergence)  */
+int hbgpu_engine_rewind(hbgpu_engine *eng, void *stream);
 /* The same schedule split at its exchange points, for a caller that moves
  * the remote halo payloads itself (several ranks' engines in one process):
  * phase -1 = priming halo moves of slot A (local copies + pack), 0..3 = the
@@ -370,6 +406,20 @@ int hbgpu_comm_init(const unsigned char id[128], int32_t nranks, int32_t rank,
 int hbgpu_comm_allgather(void *comm, const double *send, double *recv,
                          int64_t count, void *stream);
 int hbgpu_comm_destroy(void *comm);
+/* all-reduce of `count` elements: HBGPU_REDUCE_SUM_F64 (doubles, sum) or
+ * HBGPU_REDUCE_MIN_U64 (status keys, unsigned min)                        */
+#define HBGPU_REDUCE_SUM_F64 0
+#define HBGPU_REDUCE_MIN_U64 1
+int hbgpu_comm_allreduce(void *comm, const void *send, void *recv, int64_t count,
+                         int32_t op, void *stream);
+/* HBGPU_OK while the communicator is healthy (or has work in progress);
+ * HBGPU_ERR_NCCL with the message when ncclCommGetAsyncError reports an
+ * error (a peer failed, a network error).  Poll it while waiting.         */
+int hbgpu_comm_async_error(void *comm);
+/* ncclCommAbort: frees the communicator and aborts its uncompleted
+ * operations, so a rank that failed (or timed out) does not leave its
+ * peers blocked in a collective (runtime.py:133-144 aborts the fabric).   */
+int hbgpu_comm_abort(void *comm);
 
 /* ---- misc ---------------------------------------------------------------- */
 /* sizeof / offsetof of the ABI structs, for binding checks:

@@ -186,5 +186,5 @@ def compute_forces(field, topology):
     hist = torch.zeros(3 * P * nbody, dtype=torch.float64, device=dev)
     it = torch.zeros(1, dtype=torch.int32, device=dev)
     native.check(native.load().hbgpu_forces(_vp(field.pool), _vp(t_segs), len(segs), P, nbody, _vp(hist),
-                                            _vp(it), _stream()), "hbgpu_forces")
+                                            _vp(it), 1, _stream()), "hbgpu_forces")
     return ForceCoefficients.from_stack(hist.cpu().numpy().reshape(3, P, nbody))

@@ -23,13 +23,35 @@ __global__ void halo_kernel(double *slot, double *sendbuf, const double *recvbuf
     dst[d.dst_off + e * d.dst_es + v * d.dst_vs] = src[d.src_off + e * d.src_es + v * d.src_vs];
 }
 
+// ---- hazard scan ----------------------------------------------------------------
+
+// Any finite value of magnitude >= 2^1022 in a block's region of `slot` sets
+// the block's hazard key at gstage 0 (before the first stage): the paired
+// kernel's DFMA 4c - w matches the reference only below that (hb_pair.cu
+// stage_point).  Regions are 256-B aligned and a multiple of 8 elements.
+__global__ void hazard_scan_kernel(const double *slot, const hbgpu_block *blocks, int planes,
+                                   unsigned long long *status) {
+    const hbgpu_block b = blocks[blockIdx.y];
+    const int64_t n2 = (int64_t)planes * NPDE * (b.nj + 2) * b.pitch / 2;
+    const double2 *p = reinterpret_cast<const double2 *>(slot + b.base);
+    unsigned ex = 0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n2; k += (int64_t)gridDim.x * blockDim.x) {
+        const double2 v = p[k];
+        const unsigned e0 = (unsigned)__double2hiint(v.x) & 0x7ff00000u, e1 = (unsigned)__double2hiint(v.y) & 0x7ff00000u;
+        if (e0 >= HAZARD_EXP && e0 != 0x7ff00000u) ex = 1;
+        if (e1 >= HAZARD_EXP && e1 != 0x7ff00000u) ex = 1;
+    }
+    if (__any_sync(0xffffffffu, ex != 0) && (threadIdx.x & 31) == 0) atomicMin(status + blockIdx.y, hazard_key(0, 0));
+}
+
 // ---- residual norm ----------------------------------------------------------
 
 // per block: sequential sum of its (tile, consumer warp) partials in tile order
+// (sumsq holds max_iters rows: an iteration counter at or past it writes nothing)
 __global__ void norm_fold_kernel(const hbgpu_block *blocks, int nblocks, const double *part,
-                                 double *sumsq, const int32_t *iter) {
+                                 double *sumsq, const int32_t *iter, int max_iters) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nblocks) return;
+    if (b >= nblocks || *iter >= max_iters || *iter < 0) return;
     const hbgpu_block &blk = blocks[b];
     double s = 0.0;
     // one partial per (tile, pde), tiles of a block contiguous
@@ -38,15 +60,28 @@ __global__ void norm_fold_kernel(const hbgpu_block *blocks, int nblocks, const d
     sumsq[(int64_t)(*iter) * nblocks + b] = s;
 }
 
+// one thread per iteration: the rank-global per-block sums of R^2 (columns in
+// ascending global block id) folded left to right, then the correctly
+// rounded square root -- bitwise the host's math.sqrt(sum(...)) fold
+__global__ void norm_totals_kernel(const double *sumsq, int iters, int nblocks, double *norms) {
+    const int it = blockIdx.x * blockDim.x + threadIdx.x;
+    if (it >= iters) return;
+    double s = 0.0;
+    for (int b = 0; b < nblocks; ++b) s = radd(s, sumsq[(int64_t)it * nblocks + b]);
+    norms[it] = __dsqrt_rn(s);
+}
+
 // ---- forces (hbcore.py:359-382) --------------------------------------------
 
 // one thread per (coefficient k, plane n, body): a strict left-to-right fold
 // of h*q over the body's face segments in reference order.  Then one thread
 // advances the device iteration counter (this is the iteration's last kernel).
+// hist holds max_iters rows; an iteration counter at or past it writes no
+// history (the engine refuses to issue such iterations in the first place).
 __global__ void forces_kernel(const double *slot, const hbgpu_force_seg *segs, int nsegs,
-                              int planes, int nbody, double *hist, int32_t *iter) {
+                              int planes, int nbody, double *hist, int32_t *iter, int max_iters) {
     const int it = *iter;
-    const int total = 3 * planes * nbody;
+    const int total = (it >= 0 && it < max_iters) ? 3 * planes * nbody : 0;
     for (int t = threadIdx.x; t < total; t += blockDim.x) {
         const int body = t % nbody;
         const int n = (t / nbody) % planes;
@@ -176,19 +211,41 @@ extern "C" int hbgpu_halo(double *slot, double *sendbuf, const double *recvbuf,
     return hbgpu_check_launch("hbgpu_halo");
 }
 
+extern "C" int hbgpu_hazard_scan(const double *slot, const hbgpu_block *blocks, int32_t nblocks, int32_t planes,
+                                 unsigned long long *status, void *stream) {
+    if (nblocks <= 0) return HBGPU_OK;
+    if (nblocks > 65535) {
+        hbgpu_set_error("hbgpu_hazard_scan: %d blocks exceed one grid row per block", nblocks);
+        return HBGPU_ERR_ARG;
+    }
+    hazard_scan_kernel<<<dim3(64, (unsigned)nblocks), 256, 0, (cudaStream_t)stream>>>(slot, blocks, planes, status);
+    hbgpu_count_launch(1);
+    return hbgpu_check_launch("hbgpu_hazard_scan");
+}
+
+extern "C" int hbgpu_norm_totals(const double *sumsq, int32_t iters, int32_t nblocks, double *norms,
+                                 void *stream) {
+    if (iters <= 0) return HBGPU_OK;
+    norm_totals_kernel<<<(iters + 127) / 128, 128, 0, (cudaStream_t)stream>>>(sumsq, iters, nblocks, norms);
+    hbgpu_count_launch(1);
+    return hbgpu_check_launch("hbgpu_norm_totals");
+}
+
 extern "C" int hbgpu_norm_fold(const hbgpu_block *blocks, int32_t nblocks, const double *norm_part,
-                               double *sumsq, const int32_t *iter, void *stream) {
+                               double *sumsq, const int32_t *iter, int32_t max_iters, void *stream) {
     norm_fold_kernel<<<(nblocks + 127) / 128, 128, 0, (cudaStream_t)stream>>>(blocks, nblocks, norm_part,
-                                                                            sumsq, iter);
+                                                                            sumsq, iter, max_iters);
     hbgpu_count_launch(1);
     return hbgpu_check_launch("hbgpu_norm_fold");
 }
 
 extern "C" int hbgpu_forces(const double *slot, const hbgpu_force_seg *segs, int32_t nsegs,
-                            int32_t planes, int32_t nbody, double *hist, int32_t *iter, void *stream) {
+                            int32_t planes, int32_t nbody, double *hist, int32_t *iter, int32_t max_iters,
+                            void *stream) {
     int threads = 3 * planes * nbody;
     threads = threads < 32 ? 32 : (threads > 1024 ? 1024 : ((threads + 31) / 32) * 32);
-    forces_kernel<<<1, threads, 0, (cudaStream_t)stream>>>(slot, segs, nsegs, planes, nbody, hist, iter);
+    forces_kernel<<<1, threads, 0, (cudaStream_t)stream>>>(slot, segs, nsegs, planes, nbody, hist, iter,
+                                                           max_iters);
     hbgpu_count_launch(1);
     return hbgpu_check_launch("hbgpu_forces");
 }

@@ -42,6 +42,16 @@ __device__ __forceinline__ unsigned long long divergence_key(int gstage, long lo
     return ((unsigned long long)(unsigned)gstage << 40) | (unsigned long long)lin;
 }
 
+// Hazard key: a finite value of magnitude >= 2^1022 written at `gstage`
+// (HBGPU_HAZARD_BIT set; the lin bits stay below it).  It sorts after every
+// divergence key of the same stage and before those of later stages: the
+// stages after it may have used the paired kernel's DFMA 4c - w on an
+// overflowing 4c, so the host repeats the run on the strict kernels.
+constexpr unsigned HAZARD_EXP = 0x7fd00000u;   // high-word exponent field of 2^1022
+__device__ __forceinline__ unsigned long long hazard_key(int gstage, long long lin) {
+    return divergence_key(gstage, lin) | HBGPU_HAZARD_BIT;
+}
+
 __device__ __forceinline__ bool nonfinite(double v) { return !isfinite(v); }
 
 // rmul(+0.0, x) for finite x: a zero carrying x's sign bit, built on the

@@ -50,11 +50,16 @@ __global__ void __launch_bounds__(128) band_kernel(const __grid_constant__ hbgpu
     const hbgpu_block b = a.blocks[sg.block];
     const int j = sg.j + (sg.dir ? e : 0);
     const int i = sg.i + (sg.dir ? di : e);
-    // column runs skip the band rows (the row runs own those cells); then the
-    // rest of each column cell's 32-byte sector holds no band value, so the
-    // cell is stored as a whole sector (no partial-sector fill in L2)
+    // column runs skip the band rows (the row runs own those cells)
     const bool column = sg.dir != 0;
     if (column && ((j - 1) % a.tile_rows == 0 || j % a.tile_rows == 0 || j == b.nj)) return;
+    // A single face column's cell is then stored as a whole 32-byte sector
+    // (no partial-sector fill in L2) when the rest of its sector holds no
+    // value anyone reads: cell 1's sector is cells 1..4 (LEAD + 1 = 8), cell
+    // ni's is cells ni-3..ni when ni % 4 == 0 -- not the east halo cell ni+1,
+    // which a neighbour forwards into -- and with ni >= 8 neither holds the
+    // other face column.  Otherwise (and for two-column runs) plain stores.
+    const bool sector_store = sg.dir == 1 && b.ni % 4 == 0 && b.ni >= 8;
     const int64_t ps4 = b.ps * NPDE;
     const int64_t cell = b.base + (int64_t)p * b.ps + (int64_t)j * b.rs + LEAD + i;
     const double *c = a.in + cell;
@@ -88,7 +93,7 @@ __global__ void __launch_bounds__(128) band_kernel(const __grid_constant__ hbgpu
         o = radd(o, rmul(a.ap[n * NPDE + p], sv));
         const double v = rsub(bq[n], rmul(a.coef, o));
         double *dst = a.out + cell + n * ps4;
-        if (column) {
+        if (sector_store) {
             double2 *sec = reinterpret_cast<double2 *>((uintptr_t)dst & ~(uintptr_t)31);
             const int pos = (int)(((uintptr_t)dst >> 3) & 3);
             sec[0] = make_double2(pos == 0 ? v : 0.0, pos == 1 ? v : 0.0);
@@ -159,16 +164,32 @@ __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(HBGPU_TILE_WARPS * 32) : "memory");
 }
 
-// o = residual, v = base - coef * o, with the stage kernel's operation order
+// o = residual, v = base - coef * o: the reference's per-point rounding
+// sequence (hbcore.py:197-221, 240) with two exact rewrites that the paired
+// schedule's eligibility guarantees (devlayout.fused_eligible: nu_h2 >= 1)
+// and the hazard keys police (record_nonfinite):
+//
+// 1. t = 4c - w as one DFMA.  4c is exact (a power-of-two scaling) unless it
+//    overflows, i.e. unless |c| >= 2^1022, so round(4c - w) == the
+//    reference's round(round(4c) - w).  Every value this library writes is
+//    checked: one of magnitude >= 2^1022 records a hazard key, and the run
+//    is repeated on the strict single-stage kernels (solver.run_case), so a
+//    result that depended on an overflowing 4c is never returned.
+//
+// 2. The signed-zero terms -- D[n][n]*q[n] (D[n][n] = +0) and the forcing of
+//    the unforced planes (amplitude +0) -- are dropped.  Adding +-0 to o
+//    changes o only when o == -0, and o is never -0 here: with nu_h2 >= 1,
+//    t*nu_h2 is -0 only if t is (no underflow to zero), t is -0 only if
+//    4c == -0 and w, e, s, n are all +0, and then (e - w)*adv_2h is +0, so
+//    t*nu_h2 + u is not -0; a round-to-nearest sum is -0 only when both
+//    addends are, so no later partial sum is -0 either.
 template <int P>
 __device__ __forceinline__ void stage_point(const double (&c)[P], const double (&w)[P], const double (&e)[P],
                                             const double (&s)[P], const double (&nn)[P], const double (&dk)[P / 2 + 1],
                                             const double (&ap)[P], double sv, double nu_h2, double adv_2h,
                                             double coef, const double (&base)[P], double (&o)[P], double (&v)[P]) {
 #pragma unroll
-    for (int n = 0; n < P; ++n) o[n] = rmul(4.0, c[n]);
-#pragma unroll
-    for (int n = 0; n < P; ++n) o[n] = rsub(o[n], w[n]);
+    for (int n = 0; n < P; ++n) o[n] = __fma_rn(4.0, c[n], -w[n]);
 #pragma unroll
     for (int n = 0; n < P; ++n) o[n] = rsub(o[n], e[n]);
 #pragma unroll
@@ -181,7 +202,6 @@ __device__ __forceinline__ void stage_point(const double (&c)[P], const double (
     for (int n = 0; n < P; ++n) o[n] = radd(o[n], rmul(rsub(e[n], w[n]), adv_2h));
 #pragma unroll
     for (int m = 0; m < P; ++m) {
-        o[m] = radd(o[m], zero_times(c[m]));
 #pragma unroll
         for (int k = 1; k <= P / 2; ++k) {
             const double prod = rmul(dk[k], c[m]);
@@ -189,10 +209,9 @@ __device__ __forceinline__ void stage_point(const double (&c)[P], const double (
             o[(m + P - k) % P] = rsub(o[(m + P - k) % P], prod);
         }
     }
-    const double sv0 = zero_times(sv);
 #pragma unroll
     for (int n = 0; n < P; ++n) {
-        o[n] = radd(o[n], forced_plane(n) ? rmul(ap[n], sv) : sv0);
+        if (forced_plane(n)) o[n] = radd(o[n], rmul(ap[n], sv));
         v[n] = rsub(base[n], rmul(coef, o[n]));
     }
 }
@@ -201,17 +220,20 @@ template <int P>
 __device__ __forceinline__ void record_nonfinite(const double (&v)[P], const hbgpu_stage_args &a, int bidx,
                                                  const hbgpu_block &b, int p, int j, int i, int gstage) {
     // on the integer pipe (the fp64 pipe is this kernel's binding resource):
-    // a value is non-finite iff its exponent field is all ones, and the
-    // largest masked exponent of the P values is all ones iff any one is
+    // the largest masked exponent field of the P values is >= 0x7fd iff one
+    // of them is non-finite (0x7ff: a divergence key) or has magnitude
+    // >= 2^1022 (a hazard key: stage_point's DFMA 4c - w would not be the
+    // reference's rounding for it in the next stage)
     unsigned ex = 0;
 #pragma unroll
     for (int n = 0; n < P; ++n) ex = max(ex, (unsigned)__double2hiint(v[n]) & 0x7ff00000u);
-    if (ex == 0x7ff00000u) {
-        for (int n = 0; n < P; ++n)
-            if (nonfinite(v[n])) {
-                const long long lin = (((long long)(n * NPDE + p) * b.nj + (j - 1)) * b.ni) + (i - 1);
-                atomicMin(a.status + bidx, divergence_key(gstage, lin));
-            }
+    if (ex >= HAZARD_EXP) {
+        for (int n = 0; n < P; ++n) {
+            const unsigned e = (unsigned)__double2hiint(v[n]) & 0x7ff00000u;
+            if (e < HAZARD_EXP) continue;
+            const long long lin = (((long long)(n * NPDE + p) * b.nj + (j - 1)) * b.ni) + (i - 1);
+            atomicMin(a.status + bidx, e == 0x7ff00000u ? divergence_key(gstage, lin) : hazard_key(gstage, lin));
+        }
     }
 }
 
@@ -473,6 +495,10 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
         }
         const hbgpu_block b = a.blocks[tl.bidx];
         const double nu_h2 = b.nu_h2, adv_2h = b.adv_2h;
+        // stage_point's dropped signed zeros need nu_h2 >= 1 (the engine only
+        // pairs such blocks; a C-ABI caller that does not gets a hazard key,
+        // i.e. "repeat on the strict kernels")
+        if (warp == 0 && lane == 0 && !(nu_h2 >= 1.0)) atomicMin(a.status + tl.bidx, hazard_key(gstage, 0));
         const int i = tl.i0 + col0;
         const int64_t ps4 = b.ps * NPDE;
         const int64_t colbase = b.base + (int64_t)p * b.ps + LEAD + i;   // (n=0, p, j=0, i)
@@ -696,7 +722,11 @@ static int prepare_pair(PairLaunch &L) {
 
 template <int P, int PT>
 static int pair_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
-    static PairLaunch la, lb;
+    // the smem attribute and the occupancy grid are per device
+    static PairLaunch la_d[HB_MAX_DEVICES], lb_d[HB_MAX_DEVICES];
+    const int dev = current_device();
+    if (dev < 0) return HBGPU_ERR_CUDA;
+    PairLaunch &la = la_d[dev], &lb = lb_d[dev];
     int rc = prepare_pair<P, false, HBGPU_PAIR_RA, HBGPU_PAIR_Q, PT>(la);
     if (!rc) rc = prepare_pair<P, true, HBGPU_PAIR_R, HBGPU_PAIR_Q, PT>(lb);
     if (rc || prepare_only) return rc;

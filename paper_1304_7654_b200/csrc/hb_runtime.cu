@@ -67,6 +67,10 @@ struct NcclApi {
     ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -94,6 +98,9 @@ bool load_nccl() {
     HB_SYM(Send, "ncclSend");
     HB_SYM(Recv, "ncclRecv");
     HB_SYM(AllGather, "ncclAllGather");
+    HB_SYM(AllReduce, "ncclAllReduce");
+    HB_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
+    HB_SYM(CommAbort, "ncclCommAbort");
     HB_SYM(GetErrorString, "ncclGetErrorString");
 #undef HB_SYM
     g_nccl.loaded = true;
@@ -138,6 +145,44 @@ extern "C" int hbgpu_comm_allgather(void *comm, const double *send, double *recv
     return HBGPU_OK;
 }
 
+extern "C" int hbgpu_comm_allreduce(void *comm, const void *send, void *recv, int64_t count, int32_t op,
+                                    void *stream) {
+    if (!load_nccl()) return HBGPU_ERR_NCCL;
+    ncclDataType_t t;
+    ncclRedOp_t o;
+    if (op == HBGPU_REDUCE_SUM_F64) {
+        t = ncclFloat64;
+        o = ncclSum;
+    } else if (op == HBGPU_REDUCE_MIN_U64) {
+        t = ncclUint64;
+        o = ncclMin;
+    } else {
+        hbgpu_set_error("hbgpu_comm_allreduce: unknown op %d", op);
+        return HBGPU_ERR_ARG;
+    }
+    ncclResult_t r = g_nccl.AllReduce(send, recv, (size_t)count, t, o, (ncclComm_t)comm, (cudaStream_t)stream);
+    if (r != ncclSuccess) return nccl_fail("ncclAllReduce", r);
+    return HBGPU_OK;
+}
+
+extern "C" int hbgpu_comm_async_error(void *comm) {
+    if (comm == nullptr) return HBGPU_OK;
+    if (!load_nccl()) return HBGPU_ERR_NCCL;
+    ncclResult_t err = ncclSuccess;
+    ncclResult_t r = g_nccl.CommGetAsyncError((ncclComm_t)comm, &err);
+    if (r != ncclSuccess) return nccl_fail("ncclCommGetAsyncError", r);
+    if (err != ncclSuccess && err != ncclInProgress) return nccl_fail("NCCL asynchronous error", err);
+    return HBGPU_OK;
+}
+
+extern "C" int hbgpu_comm_abort(void *comm) {
+    if (comm == nullptr) return HBGPU_OK;
+    if (!load_nccl()) return HBGPU_ERR_NCCL;
+    ncclResult_t r = g_nccl.CommAbort((ncclComm_t)comm);
+    if (r != ncclSuccess) return nccl_fail("ncclCommAbort", r);
+    return HBGPU_OK;
+}
+
 extern "C" int hbgpu_comm_destroy(void *comm) {
     if (comm == nullptr) return HBGPU_OK;
     if (!load_nccl()) return HBGPU_ERR_NCCL;
@@ -155,6 +200,7 @@ struct hbgpu_engine {
     std::vector<hbgpu_peer_msg> sends, recvs;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
+    int32_t done = 0;   // iterations issued (rows of sumsq / force_hist used)
 };
 
 namespace {
@@ -238,7 +284,7 @@ int run_fused_phase(hbgpu_engine *e, int ph, cudaStream_t s) {
     a.coef2 = d.coef[st + 1];
     a.norm_part = ph == 1 ? d.norm_part : nullptr;
     int rc = hbgpu_stage(&a, s);
-    if (!rc && ph == 1) rc = hbgpu_norm_fold(d.blocks, d.nblocks, d.norm_part, d.sumsq, d.iter, s);
+    if (!rc && ph == 1) rc = hbgpu_norm_fold(d.blocks, d.nblocks, d.norm_part, d.sumsq, d.iter, d.max_iters, s);
     // pass A forwards south/north rows itself; west/east columns here
     if (!rc && ph == 1 && d.npost > 0)
         rc = hbgpu_halo(a.out, d.sendbuf, d.recvbuf, d.post_dirs, d.npost, d.post_max_len, d.planes, s);
@@ -281,7 +327,7 @@ int run_stage(hbgpu_engine *e, int st, cudaStream_t s) {
     a.coef = d.coef[st];
     a.norm_part = st == 0 ? d.norm_part : nullptr;
     int rc = hbgpu_stage(&a, s);
-    if (!rc && st == 0) rc = hbgpu_norm_fold(d.blocks, d.nblocks, d.norm_part, d.sumsq, d.iter, s);
+    if (!rc && st == 0) rc = hbgpu_norm_fold(d.blocks, d.nblocks, d.norm_part, d.sumsq, d.iter, d.max_iters, s);
     // first stage: west / east face columns, local halo copies and remote
     // packs (the update stages forward them from their TMA store warp)
     if (!rc && st == 0 && d.npost > 0)
@@ -296,7 +342,18 @@ int one_iteration(hbgpu_engine *e, cudaStream_t s) {
         if (!rc) rc = exchange_remote(e, d.slot[out_slot(d, st)], s);
         if (rc) return rc;
     }
-    return hbgpu_forces(d.slot[0], d.segs, d.nsegs, d.planes, d.nbody, d.force_hist, d.iter, s);
+    return hbgpu_forces(d.slot[0], d.segs, d.nsegs, d.planes, d.nbody, d.force_hist, d.iter, d.max_iters, s);
+}
+
+// the sumsq / force_hist rows the next `n` iterations would use exist
+int check_capacity(const hbgpu_engine *e, int64_t n, const char *who) {
+    if (n < 0 || (int64_t)e->done + n > (int64_t)e->d.max_iters) {
+        hbgpu_set_error("%s: %lld more iteration(s) after %d would exceed max_iters = %d (the capacity of "
+                        "sumsq and force_hist); rewind or create the engine with a larger max_iters",
+                        who, (long long)n, e->done, e->d.max_iters);
+        return HBGPU_ERR_ARG;
+    }
+    return HBGPU_OK;
 }
 
 }  // namespace
@@ -352,7 +409,11 @@ extern "C" int hbgpu_engine_prime(hbgpu_engine *e, void *stream) {
     int rc = enter(e, caller);
     if (rc) return rc;
     const hbgpu_engine_desc &d = e->d;
-    rc = hbgpu_halo(d.slot[0], d.sendbuf, d.recvbuf, d.prime_dirs, d.nprime, d.prime_max_len, d.planes, e->work);
+    // the paired kernel's exact rewrites need |q| < 2^1022 in its inputs
+    if (d.fused) rc = hbgpu_hazard_scan(d.slot[0], d.blocks, d.nblocks, d.planes, d.status, e->work);
+    if (!rc)
+        rc = hbgpu_halo(d.slot[0], d.sendbuf, d.recvbuf, d.prime_dirs, d.nprime, d.prime_max_len, d.planes,
+                        e->work);
     if (!rc) rc = exchange_remote(e, d.slot[0], e->work);
     return leave(e, caller, rc);
 }
@@ -370,13 +431,20 @@ extern "C" int hbgpu_engine_step(hbgpu_engine *e, int32_t phase, void *stream) {
     int rc = enter(e, caller);
     if (rc) return rc;
     const hbgpu_engine_desc &d = e->d;
-    if (phase == -1)
-        rc = hbgpu_halo(d.slot[0], d.sendbuf, d.recvbuf, d.prime_dirs, d.nprime, d.prime_max_len, d.planes,
-                        e->work);
+    if (phase == -1) {
+        if (d.fused) rc = hbgpu_hazard_scan(d.slot[0], d.blocks, d.nblocks, d.planes, d.status, e->work);
+        if (!rc)
+            rc = hbgpu_halo(d.slot[0], d.sendbuf, d.recvbuf, d.prime_dirs, d.nprime, d.prime_max_len, d.planes,
+                            e->work);
+    }
     else if (phase >= 0 && phase < 4)
         rc = run_stage(e, phase, e->work);
-    else if (phase == 4)
-        rc = hbgpu_forces(d.slot[0], d.segs, d.nsegs, d.planes, d.nbody, d.force_hist, d.iter, e->work);
+    else if (phase == 4) {
+        rc = check_capacity(e, 1, "hbgpu_engine_step");
+        if (!rc) rc = hbgpu_forces(d.slot[0], d.segs, d.nsegs, d.planes, d.nbody, d.force_hist, d.iter,
+                                   d.max_iters, e->work);
+        if (!rc) ++e->done;
+    }
     else {
         hbgpu_set_error("hbgpu_engine_step: bad phase %d", phase);
         rc = HBGPU_ERR_ARG;
@@ -408,10 +476,35 @@ extern "C" int hbgpu_engine_launches_per_iteration(const hbgpu_engine *e) {
 static int iterate_on(hbgpu_engine *e, int32_t iterations, int32_t use_graph, cudaStream_t s);
 
 extern "C" int hbgpu_engine_iterate(hbgpu_engine *e, int32_t iterations, int32_t use_graph, void *stream) {
+    if (e == nullptr) {
+        hbgpu_set_error("hbgpu_engine_iterate: null engine");
+        return HBGPU_ERR_ARG;
+    }
+    int rc = check_capacity(e, iterations, "hbgpu_engine_iterate");
+    if (rc) return rc;
+    cudaStream_t caller = (cudaStream_t)stream;
+    rc = enter(e, caller);
+    if (rc) return rc;
+    rc = iterate_on(e, iterations, use_graph, e->work);
+    if (!rc) e->done += iterations;
+    return leave(e, caller, rc);
+}
+
+extern "C" int hbgpu_engine_iterations_done(const hbgpu_engine *e) { return e ? e->done : 0; }
+
+extern "C" int hbgpu_engine_rewind(hbgpu_engine *e, void *stream) {
+    if (e == nullptr) {
+        hbgpu_set_error("hbgpu_engine_rewind: null engine");
+        return HBGPU_ERR_ARG;
+    }
     cudaStream_t caller = (cudaStream_t)stream;
     int rc = enter(e, caller);
     if (rc) return rc;
-    rc = iterate_on(e, iterations, use_graph, e->work);
+    if (cudaMemsetAsync(e->d.iter, 0, sizeof(int32_t), e->work) != cudaSuccess ||
+        cudaMemsetAsync(e->d.status, 0xff, sizeof(unsigned long long) * (size_t)e->d.nblocks, e->work) !=
+            cudaSuccess)
+        rc = hbgpu_check_launch("hbgpu_engine_rewind");
+    if (!rc) e->done = 0;
     return leave(e, caller, rc);
 }
 

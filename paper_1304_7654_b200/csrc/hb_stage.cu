@@ -480,6 +480,15 @@ __global__ void __launch_bounds__(CW * 32) stage_kernel_generic(const __grid_con
 
 // ---- launch -------------------------------------------------------------------
 
+int current_device() {
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= HB_MAX_DEVICES) {
+        hbgpu_set_error("hbgpu: current device %d unusable (limit %d devices)", dev, HB_MAX_DEVICES);
+        return -1;
+    }
+    return dev;
+}
+
 int persistent_grid(int resident, int tiles) {
     int grid = min(resident, tiles);
     if (const char *cap = getenv("HBGPU_GRID_LIMIT")) {
@@ -539,7 +548,11 @@ template <> struct Depth<17> { static constexpr int R = 4, RF = 5, Q = 2; };
 template <int P, int PT, int MODE>
 static int launch_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
     using D = Depth<P>;
-    static Launch first, rest;
+    // the smem attribute and the occupancy grid are per device
+    static Launch first_d[HB_MAX_DEVICES], rest_d[HB_MAX_DEVICES];
+    const int dev = current_device();
+    if (dev < 0) return HBGPU_ERR_CUDA;
+    Launch &first = first_d[dev], &rest = rest_d[dev];
     int rc = prepare<P, true, D::RF, D::Q, PT, MODE>(first);
     if (!rc) rc = prepare<P, false, D::R, D::Q, PT, MODE>(rest);
     if (rc || prepare_only) return rc;
@@ -554,20 +567,15 @@ static int launch_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_on
     return hbgpu_check_launch("hbgpu_stage");
 }
 
-// HBGPU_NOMATH=1 (measurements only, P = 9): the same pipeline and traffic
-// with the arithmetic replaced by a copy of q0
-static bool nomath() {
-    const char *env = getenv("HBGPU_NOMATH");
-    return env != nullptr && atoi(env) == 1;
-}
-
 template <int P>
 static int launch_p(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only) {
-    if constexpr (P == 9) {
-        static const bool nm = nomath();
-        if (nm) return a.tile_pdes == 1 ? launch_cfg<P, 1, 1>(a, s, prepare_only)
-                                        : launch_cfg<P, 4, 1>(a, s, prepare_only);
-    }
+#ifdef HBGPU_MEASURE_NOMATH
+    // measurement builds only (-DHBGPU_MEASURE_NOMATH, never the shipped
+    // library): P = 9 with the arithmetic replaced by a copy of q0, the
+    // same pipeline and traffic
+    if constexpr (P == 9)
+        return a.tile_pdes == 1 ? launch_cfg<P, 1, 1>(a, s, prepare_only) : launch_cfg<P, 4, 1>(a, s, prepare_only);
+#endif
     return a.tile_pdes == 1 ? launch_cfg<P, 1, 0>(a, s, prepare_only) : launch_cfg<P, 4, 0>(a, s, prepare_only);
 }
 

@@ -225,6 +225,11 @@ __device__ __forceinline__ void store_rows(const void *map, const void *src, int
 // over and lets strips drift apart as they do at full size).
 int persistent_grid(int resident, int tiles);
 
+// launch configurations (smem attribute, occupancy grid) are cached per
+// device ordinal; current_device() is the cache index, -1 on error
+constexpr int HB_MAX_DEVICES = 64;
+int current_device();
+
 // hb_pair.cu: launch (or, prepare_only, just configure) the paired-stage
 // kernel for args.pair = 1 (stages 0, 1) or 2 (stages 2, 3)
 int pair_dispatch(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only);

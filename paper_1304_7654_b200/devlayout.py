@@ -50,6 +50,7 @@ MIN_TILE_ROWS = 8
 # and C2 (2.6M, 4.7M units), paired ones 16% faster at C3 (117M) and ~35% at
 # C4 (2.4G)
 FUSED_MIN_UNITS = 16 * 2 ** 20
+MAX_BAND_SEGS = 65535
 SLOT_TAIL = 64            # elements of zero padding after the last block
 # slot layout default: row-interleaved (row j of every (n, p) plane contiguous)
 # unless HBGPU_LAYOUT=plane selects the plane-major layout
@@ -242,12 +243,16 @@ def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None,
 
 
 def fused_eligible(blocks, planes, tile_pdes):
-    """Paired stages need P <= MAX_PAIR_P (shared memory) and full strips
-    (every ni a multiple of the strip width, so every lane is live)."""
+    """Paired stages need P <= MAX_PAIR_P (shared memory), full strips
+    (every ni a multiple of the strip width, so every lane is live), and
+    nu/h^2 >= 1 in every block: the paired kernel drops the reference's
+    signed-zero terms, which is exact only when t*nu_h2 cannot underflow to
+    zero (hb_pair.cu stage_point)."""
     if os.environ.get("HBGPU_FUSED", "1") == "0":
         return False
     width = native.TILE_COLS[tile_pdes]
-    return planes <= native.MAX_PAIR_P and all(b.ni % width == 0 for b in blocks)
+    return (planes <= native.MAX_PAIR_P and all(b.ni % width == 0 for b in blocks)
+            and all(stencil_coefficients(b.h)[0] >= 1.0 for b in blocks))
 
 
 def _build_band(layout, fused):
@@ -256,6 +261,10 @@ def _build_band(layout, fused):
     and the face columns that feed a cut (forwarded into the neighbours'
     band halos, read across strip edges on block faces)."""
     eligible = fused_eligible(layout.blocks, layout.planes, layout.tile_pdes)
+    # hbgpu_band takes one segment per grid row (gridDim.y <= 65535)
+    nsegs = sum(len({r for j0 in range(1, b.nj + 1, layout.tile_rows)
+                     for r in (j0, min(j0 + layout.tile_rows - 1, b.nj))}) + 2 for b in layout.blocks)
+    eligible = eligible and nsegs <= MAX_BAND_SEGS
     if fused is None:
         units = sum(b.ni * b.nj for b in layout.blocks) * layout.planes * NPDE
         layout.fused = eligible and units >= FUSED_MIN_UNITS

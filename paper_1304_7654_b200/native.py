@@ -27,7 +27,11 @@ ROW_LEAD = 7
 STRIP = 64
 TILE_WARPS = 8                # consumer warps per stage tile
 TILE_COLS = {4: 64, 1: 256}   # tile_pdes -> interior columns per strip
-ABI_VERSION = 1
+ABI_VERSION = 2
+# status keys (include/hbgpu.h): (gstage << STATUS_LIN_BITS) | lin, HAZARD_BIT for |v| >= 2^1022
+STATUS_LIN_BITS = 40
+HAZARD_BIT = 1 << 39
+REDUCE_SUM_F64, REDUCE_MIN_U64 = 0, 1
 TMAP_SETS = 10                 # tensor-map sets per block (hbgpu_encode_tensor_maps)
 
 c_i32, c_i64, c_f64, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
@@ -111,14 +115,17 @@ SIGNATURES = {
     "hbgpu_stage_prepare": (c_i32, [c_i32]),
     "hbgpu_encode_tensor_maps": (c_i32, [c_vp * 3, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_i64]),
     "hbgpu_halo": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
-    "hbgpu_norm_fold": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
-    "hbgpu_forces": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp]),
+    "hbgpu_hazard_scan": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp]),
+    "hbgpu_norm_fold": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp]),
+    "hbgpu_forces": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_i32, c_vp]),
     "hbgpu_ordered_fold": (c_i32, [c_vp, c_i32, c_i64, c_vp, c_vp]),
     "hbgpu_pack_records": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "hbgpu_engine_create": (c_i32, [ctypes.POINTER(EngineDesc), ctypes.POINTER(c_vp)]),
     "hbgpu_engine_prime": (c_i32, [c_vp, c_vp]),
     "hbgpu_engine_iterate": (c_i32, [c_vp, c_i32, c_i32, c_vp]),
     "hbgpu_engine_launches_per_iteration": (c_i32, [c_vp]),
+    "hbgpu_engine_iterations_done": (c_i32, [c_vp]),
+    "hbgpu_engine_rewind": (c_i32, [c_vp, c_vp]),
     "hbgpu_engine_step": (c_i32, [c_vp, c_i32, c_vp]),
     "hbgpu_engine_unpack": (c_i32, [c_vp, c_i32, c_vp]),
     "hbgpu_engine_destroy": (c_i32, [c_vp]),
@@ -126,6 +133,10 @@ SIGNATURES = {
     "hbgpu_comm_init": (c_i32, [ctypes.c_char_p, c_i32, c_i32, c_i32, ctypes.POINTER(c_vp)]),
     "hbgpu_comm_allgather": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp]),
     "hbgpu_comm_destroy": (c_i32, [c_vp]),
+    "hbgpu_comm_allreduce": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp]),
+    "hbgpu_comm_async_error": (c_i32, [c_vp]),
+    "hbgpu_comm_abort": (c_i32, [c_vp]),
+    "hbgpu_norm_totals": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_vp]),
     "hbgpu_abi_version": (c_i32, []),
     "hbgpu_last_error": (ctypes.c_char_p, []),
     "hbgpu_launch_count": (ctypes.c_uint64, []),

@@ -34,14 +34,31 @@ import numpy as np
 from . import hbop, native, outio
 from .cutplan import ExchangeMode, ExchangeStrategy, build_cut_plan, predicted_message_count
 from .devlayout import build_rank_layout
-from .exceptions import CollectiveError, DivergenceError, ProtocolError
+from .exceptions import CollectiveError, DivergenceError, ProtocolError, RankFailure, RunAborted
 from .topology import build_topology, partition_blocks
 
 NO_BAD = (1 << 64) - 1
 # phase wall times (s) of the last single-GPU run_case: layout, alloc,
 # upload, engine, compute, download
 LAST_TIMINGS = {}
-LIN_BITS = 40
+# the last single-GPU run_case: iterations the engine issued before the loop
+# ended (early on divergence) and whether it ran the paired schedule
+LAST_RUN = {}
+LIN_BITS = native.STATUS_LIN_BITS
+HAZARD_BIT = native.HAZARD_BIT
+# status polling: about this many units of work between two looks at the
+# device divergence keys (~25 ms at C4 rates), at most POLL_MAX iterations
+POLL_UNITS = 1 << 31
+POLL_MAX = 64
+# run_case calls repeated on the strict kernels (StrictRerun), process-wide
+STRICT_RERUNS = [0]
+
+
+class StrictRerun(Exception):
+    """A paired-schedule run met a value of magnitude >= 2^1022 (a hazard
+    key, include/hbgpu.h): the paired kernel's exact rewrites do not hold
+    for the stages after it, so run_case repeats the run on the strict
+    single-stage kernels.  Never escapes run_case."""
 
 
 class ReduceMode(Enum):
@@ -436,8 +453,12 @@ class DeviceRank:
         native.check(self.lib.hbgpu_stage(ctypes.byref(args), s), "hbgpu_stage")
 
     def reset_counters(self):
-        self.iter.zero_()
-        self.status.fill_(-1)
+        """Start the iteration history over (device counter, status keys and
+        the engine's issued-iteration count)."""
+        native.check(self.lib.hbgpu_engine_rewind(self.engine, self.stream()), "hbgpu_engine_rewind")
+
+    def iterations_done(self):
+        return int(self.lib.hbgpu_engine_iterations_done(self.engine))
 
     def close(self):
         if getattr(self, "engine", None):
@@ -452,27 +473,17 @@ class DeviceRank:
 
     # -- results ---------------------------------------------------------------
 
-    def divergence(self):
-        """(gstage, gid, i, j, p, n) of this rank's first non-finite value, or None."""
-        keys = self.status.cpu().numpy().view(np.uint64)
-        best = None
-        for lb, key in enumerate(keys):
-            key = int(key)
-            if key == NO_BAD:
-                continue
-            gstage, lin = key >> LIN_BITS, key & ((1 << LIN_BITS) - 1)
-            b = self.layout.blocks[lb]
-            cand = (gstage, b.id, lin)
-            if best is None or cand[:2] < best[:2]:
-                best = cand
-        if best is None:
-            return None
-        gstage, gid, lin = best
-        b = self.layout.blocks[self.layout.local_index[gid]]
-        i = lin % b.ni
-        j = (lin // b.ni) % b.nj
-        np_ = lin // (b.ni * b.nj)
-        return gstage, gid, i + 1, j + 1, np_ % 4, np_ // 4
+    def divergence(self, keys=None):
+        """(gstage, hazard, gid, i, j, p, n) of this rank's first event, or None.
+
+        The first event is the earliest global stage; at one stage a
+        non-finite value (hazard False, the reference's DivergenceError at
+        that stage) outranks a hazard key, and blocks go in ascending id.
+        hazard True means a value of magnitude >= 2^1022 was written at that
+        stage (or was present at the start, gstage 0): see StrictRerun."""
+        if keys is None:
+            keys = self.status.cpu().numpy()
+        return decode_status(np.asarray(keys).view(np.uint64), self.layout)
 
     def norm_history(self, iterations):
         nb = len(self.layout.blocks)
@@ -512,21 +523,141 @@ def make_comm(rank, world, device):
     return comm
 
 
-def _fold_norms(per_block, iterations):
-    """sqrt of the sum over global blocks in ascending id of each block's R^2 sum."""
-    norms = []
-    for it in range(iterations):
-        total = 0.0
-        for gid in sorted(per_block):
-            total += float(per_block[gid][it])
-        norms.append(math.sqrt(total))
-    return norms
+def _global_sumsq(ranks, nblocks, iterations):
+    """(iterations, nblocks) tensor: every given rank's per-block sums of R^2
+    in the column of its global block id, zeros elsewhere."""
+    torch = ranks[0].torch
+    g = torch.zeros((iterations, nblocks), dtype=torch.float64, device=ranks[0].device)
+    for dr in ranks:
+        nb = len(dr.layout.blocks)
+        gids = torch.tensor([b.id for b in dr.layout.blocks], dtype=torch.long, device=g.device)
+        g[:, gids] = dr.sumsq[:iterations * nb].view(iterations, nb).to(g.device)
+    return g
+
+
+def _norm_totals(gsumsq, iterations, stream):
+    """Per-iteration residual norms on the device (hbgpu_norm_totals): sqrt of
+    the left-to-right sum over global blocks in ascending id."""
+    torch = __import__("torch")
+    if iterations == 0:
+        return []
+    nblocks = gsumsq.shape[1]
+    out = torch.empty(iterations, dtype=torch.float64, device=gsumsq.device)
+    native.check(native.load().hbgpu_norm_totals(_ptr(gsumsq.contiguous()), iterations, nblocks, _ptr(out),
+                                                 stream), "hbgpu_norm_totals")
+    return out.cpu().tolist()
+
+
+class GlobalBlocks:
+    """decode_status's view of all blocks of the topology (multi-GPU: the
+    job-wide status keys are indexed by global block id)."""
+
+    def __init__(self, topology):
+        self.blocks = sorted(topology.blocks, key=lambda b: b.id)
+        self.local_index = {b.id: k for k, b in enumerate(self.blocks)}
+
+
+def decode_status(keys, layout):
+    """Decode a rank's per-block status keys (include/hbgpu.h) into its first
+    event (gstage, hazard, gid, i, j, p, n), or None."""
+    best = None
+    for lb, key in enumerate(keys):
+        key = int(key)
+        if key == NO_BAD:
+            continue
+        gstage, hazard = key >> LIN_BITS, bool(key & HAZARD_BIT)
+        lin = key & (HAZARD_BIT - 1)
+        b = layout.blocks[lb]
+        cand = (gstage, hazard, b.id, lin)
+        if best is None or cand[:3] < best[:3]:
+            best = cand
+    if best is None:
+        return None
+    gstage, hazard, gid, lin = best
+    b = layout.blocks[layout.local_index[gid]]
+    i = lin % b.ni
+    j = (lin // b.ni) % b.nj
+    np_ = lin // (b.ni * b.nj)
+    return gstage, hazard, gid, i + 1, j + 1, np_ % 4, np_ // 4
+
+
+def first_event(events):
+    """The earliest of several ranks' first events (None if there is none)."""
+    events = [e for e in events if e is not None]
+    return min(events, key=lambda e: e[:3]) if events else None
 
 
 def raise_divergence(div):
-    if div is not None:
-        _, gid, i, j, p, n = div
-        raise DivergenceError(gid, i, j, p, n)
+    """DivergenceError with the reference's fields (errors.py:28-29), or
+    StrictRerun for a hazard key."""
+    if div is None:
+        return
+    _, hazard, gid, i, j, p, n = div
+    if hazard:
+        raise StrictRerun(f"value of magnitude >= 2^1022 at global stage {div[0]} (block {gid})")
+    raise DivergenceError(gid, i, j, p, n)
+
+
+def poll_interval(topology, planes, iterations):
+    units = max(1, topology.total_cells() * planes * 4)
+    return max(1, min(POLL_MAX, iterations, POLL_UNITS // units))
+
+
+class StatusPoller:
+    """Iterates a DeviceRank in chunks and looks at its divergence keys
+    between them, so a diverging run stops within about one chunk of the
+    failing stage (the reference raises at the stage itself, hbcore.py:
+    273-276) instead of finishing the loop on NaNs.
+
+    After each chunk the keys go to pinned host memory by an async copy on
+    the compute stream; the host reads the PREVIOUS chunk's copy while the
+    current one runs, so the device never waits for the host.  `reduce`,
+    when given, turns the local keys into the job-wide ones (multi-GPU:
+    every rank must stop at the same chunk or NCCL would hang)."""
+
+    def __init__(self, dr, chunk, reduce=None, wait=None):
+        import torch
+        self.torch = torch
+        self.dr, self.chunk, self.reduce = dr, max(1, int(chunk)), reduce
+        self.wait = wait or (lambda ev: ev.synchronize())
+        self.host = [None, None]
+        self.events = [torch.cuda.Event(), torch.cuda.Event()]
+        self.k = 0
+        self.pending = None
+
+    def _snapshot(self):
+        src = self.dr.status if self.reduce is None else self.reduce(self.dr.status)
+        if self.host[self.k] is None:
+            self.host[self.k] = self.torch.empty(src.numel(), dtype=self.torch.int64, pin_memory=True)
+        buf = self.host[self.k]
+        buf.copy_(src, non_blocking=True)
+        self.events[self.k].record()
+        slot, self.k = self.k, 1 - self.k
+        return slot
+
+    def _check(self, slot):
+        self.wait(self.events[slot])
+        keys = self.host[slot].numpy()
+        return None if np.all(keys == -1) else keys
+
+    def run(self, iterations, use_graph):
+        """Returns the keys of the first chunk that saw an event, else None."""
+        done = 0
+        while done < iterations:
+            k = min(self.chunk, iterations - done)
+            self.dr.iterate(k, use_graph=use_graph)
+            done += k
+            slot = self._snapshot()
+            if self.pending is not None:
+                keys = self._check(self.pending)
+                if keys is not None:
+                    return keys
+            self.pending = slot
+        if self.pending is not None:
+            keys = self._check(self.pending)
+            self.pending = None
+            return keys
+        return None
 
 
 def run_case(spec):
@@ -568,16 +699,33 @@ def run_case(spec):
             dist.barrier()
     out = (layouts, targets)
     t0 = time.perf_counter()
-    if world > 1:
-        fields, hist_np, norms_local, loop_s = _execute_distributed(spec, topology, partition, plan,
-                                                                    iterations, dist, world, out)
-    elif spec.ranks > 1 and spec.transport == "loopback":
-        fields, hist_np, norms_local, loop_s = _execute_loopback(spec, topology, partition, plan,
-                                                                 iterations, out)
-    else:
+
+    def execute(sp):
+        if world > 1:
+            return _execute_distributed(sp, topology, partition, plan, iterations, dist, world, out)
+        if sp.ranks > 1 and sp.transport == "loopback":
+            return _execute_loopback(sp, topology, partition, plan, iterations, out)
         one = partition_blocks(topology, 1)
-        fields, hist_np, norms_local, loop_s = _execute_single(
-            spec, topology, one, build_cut_plan(topology, one, case.nharms, case.npde), iterations, out)
+        return _execute_single(sp, topology, one, build_cut_plan(topology, one, case.nharms, case.npde),
+                               iterations, out)
+
+    try:
+        try:
+            fields, hist_np, norms, loop_s = execute(spec)
+        except StrictRerun:
+            STRICT_RERUNS[0] += 1
+            # a value of magnitude >= 2^1022 appeared on the paired schedule:
+            # repeat the whole run on the strict single-stage kernels (every
+            # rank takes this branch: the first event is agreed job-wide)
+            import dataclasses
+            fields, hist_np, norms, loop_s = execute(dataclasses.replace(spec, fused=False))
+    except DivergenceError as err:
+        # the reference's spawn_ranks wraps every rank error in a RankFailure
+        # naming the failing rank (runtime.py:359-364), so run_case raises
+        # RankFailure(rank, DivergenceError) at any rank count
+        # (tests/test_driver_cli.py:30-36); the rank is the owner of the
+        # diverging block in the reference partition
+        raise RankFailure(partition.rank_of(err.block), err) from err
     wall = time.perf_counter() - t0
 
     forces = (ForceCoefficients.from_stack(hist_np[-1]) if iterations > 0
@@ -596,7 +744,7 @@ def run_case(spec):
                            activations=activations, units=units, loop_s=loop_s,
                            gpus=world)
     return CaseRunResult(fields=fields, forces=forces, counters=counters, wall_s=wall,
-                         record=record, residual_norms=_fold_norms(norms_local, iterations),
+                         record=record, residual_norms=norms,
                          force_history=[ForceCoefficients.from_stack(h) for h in hist_np])
 
 
@@ -688,13 +836,15 @@ def _execute_single(spec, topology, partition, plan, iterations, out=((), ())):
         t0 = time.perf_counter()
         dr.prime()
         if iterations > 0:
-            dr.iterate(iterations, use_graph=spec.use_graph)
+            StatusPoller(dr, poll_interval(topology, spec.case.planes, iterations)).run(iterations, spec.use_graph)
         torch.cuda.synchronize(dr.device)
         t1 = time.perf_counter()
+        LAST_RUN.clear()
+        LAST_RUN.update(iterations_issued=dr.iterations_done(), fused=dr.fused)
         raise_divergence(dr.divergence())
         fields = dr.fields(0, pinned_out=spec.output)
         hist = _history(dr, iterations)
-        norms = dr.norm_history(iterations)
+        norms = _norm_totals(_global_sumsq([dr], len(topology.blocks), iterations), iterations, dr.stream())
         torch.cuda.synchronize(dr.device)
         dr.timings.update(compute=t1 - t0, download=time.perf_counter() - t1)
         dr.timings.update(output=_write_outputs([dr], out))
@@ -706,44 +856,183 @@ def _execute_single(spec, topology, partition, plan, iterations, out=((), ())):
 
 
 def _execute_distributed(spec, topology, partition, plan, iterations, dist, world, out=((), ())):
-    """One rank per process/GPU; remote halos over NCCL inside the engine."""
+    """One rank per process/GPU; remote halos over NCCL inside the engine.
+
+    Every job-level exchange after setup goes through the engine's NCCL
+    communicator -- the divergence consensus (MIN all-reduce of the status
+    keys), the norm sums (SUM all-reduce, then the device fold) and the force
+    history (all-gather + rank-ordered fold) -- and every wait on it runs
+    under a CommGuard: NCCL async errors, a peer's failure notice and a
+    timeout abort the communicator and raise, instead of leaving ranks
+    blocked (the reference aborts its fabric: runtime.py:133-144, 345-364)."""
     import torch
     rank = dist.get_rank()
     device = spec.device if spec.device is not None else rank % torch.cuda.device_count()
     torch.cuda.set_device(device)
     comm = make_comm(rank, world, device)
-    dr = _new_rank(spec, topology, partition, plan, rank, device, comm, iterations)
+    guard = CommGuard(comm, rank, _store(dist))
+    dr = None
     try:
-        torch.cuda.synchronize(dr.device)
-        t0 = time.perf_counter()
-        dr.prime()
-        if iterations > 0:
-            # the first iteration eagerly: NCCL sets up its peer connections
-            # outside the graph capture that records the rest
-            first = 1 if spec.use_graph and iterations > 1 else 0
-            if first:
-                dr.iterate(first, use_graph=False)
-            dr.iterate(iterations - first, use_graph=spec.use_graph)
-        torch.cuda.synchronize(dr.device)
-        loop_s = time.perf_counter() - t0
-        divs = [None] * world
-        dist.all_gather_object(divs, dr.divergence())
-        divs = [d for d in divs if d is not None]
-        raise_divergence(min(divs, key=lambda d: d[:2]) if divs else None)
-        fields = dr.fields(0, pinned_out=spec.output)
-        hist = dr.force_history_array(iterations)
-        hist = _reduce_history(dr, hist, world).cpu().numpy() if iterations > 0 else _history(dr, 0)
-        allnorm = [None] * world
-        dist.all_gather_object(allnorm, dr.norm_history(iterations))
-        norms = {k: v for part in allnorm for k, v in part.items()}
-        torch.cuda.synchronize(dr.device)
-        _write_outputs([dr], out)
-        if out[1]:
-            dist.barrier()
+        try:
+            dr = _new_rank(spec, topology, partition, plan, rank, device, comm, iterations)
+            gblocks = GlobalBlocks(topology)
+            torch.cuda.synchronize(dr.device)
+            t0 = time.perf_counter()
+            dr.prime()
+            job_keys = _job_keys(dr, gblocks, comm)
+            if iterations > 0:
+                # the first iteration eagerly: NCCL sets up its peer connections
+                # outside the graph capture that records the rest
+                first = 1 if spec.use_graph and iterations > 1 else 0
+                if first:
+                    dr.iterate(first, use_graph=False)
+                chunk = poll_interval(topology, spec.case.planes, iterations)
+                StatusPoller(dr, chunk, reduce=job_keys, wait=guard.wait).run(iterations - first,
+                                                                              spec.use_graph)
+            keys = job_keys(dr.status)
+            guard.sync()
+            loop_s = time.perf_counter() - t0
+            raise_divergence(decode_status(keys.cpu().numpy().view(np.uint64), gblocks))
+            fields = dr.fields(0, pinned_out=spec.output)
+            if iterations > 0:
+                hist = _reduce_history(dr, dr.force_history_array(iterations), world)
+                gs = _global_sumsq([dr], len(gblocks.blocks), iterations)
+                native.check(dr.lib.hbgpu_comm_allreduce(comm, _ptr(gs), _ptr(gs), gs.numel(),
+                                                         native.REDUCE_SUM_F64, dr.stream()),
+                             "hbgpu_comm_allreduce")
+                guard.sync()
+                norms = _norm_totals(gs, iterations, dr.stream())
+                hist = hist.cpu().numpy()
+            else:
+                hist, norms = _history(dr, 0), []
+            guard.sync()
+            _write_outputs([dr], out)
+            if out[1]:
+                dist.barrier()
+        except (DivergenceError, StrictRerun, RankFailure):
+            raise
+        except BaseException as exc:   # noqa: BLE001 - this rank failed: tell the peers
+            guard.notify_failure()
+            if isinstance(exc, (CollectiveError, RunAborted)):
+                raise
+            raise RankFailure(rank, exc) from exc
     finally:
-        dr.close()
-        native.load().hbgpu_comm_destroy(comm)
+        if dr is not None:
+            dr.close()
+        if not guard.aborted:
+            native.load().hbgpu_comm_destroy(comm)
     return fields, hist, norms, loop_s
+
+
+def _store(dist):
+    try:
+        return dist.distributed_c10d._get_default_store()
+    except Exception:
+        return None
+
+
+def _job_keys(dr, gblocks, comm):
+    """Status keys -> the job-wide per-block keys (one per global block,
+    all-ones where nothing happened): scatter into a global array, MIN
+    all-reduce (unsigned) over the engine's communicator."""
+    torch = dr.torch
+    gids = torch.tensor([b.id for b in dr.layout.blocks], dtype=torch.long, device=dr.device)
+    buf = torch.full((len(gblocks.blocks),), -1, dtype=torch.int64, device=dr.device)
+
+    def reduce(status):
+        buf.fill_(-1)
+        buf[gids] = status
+        native.check(dr.lib.hbgpu_comm_allreduce(comm, _ptr(buf), _ptr(buf), buf.numel(), native.REDUCE_MIN_U64,
+                                                 dr.stream()), "hbgpu_comm_allreduce")
+        return buf
+
+    return reduce
+
+
+class CommGuard:
+    """Bounded waits for a multi-GPU run.
+
+    wait(event) returns once the event completed.  While waiting it polls
+    (1) the communicator's asynchronous error state, (2) the job's failure
+    notice (a key in torch.distributed's store, written by the first rank
+    that fails) and (3) a deadline, TIMEOUT seconds as the reference's
+    runtime.py:29.  Any of them aborts the NCCL communicator (its pending
+    operations fail, so this rank's stream drains) and raises: CollectiveError
+    for an NCCL error or a timeout, RankFailure(failed_rank, RunAborted) when
+    a peer reported its failure.  notify_failure() is the failing rank's
+    side: post the notice (first writer wins), abort the communicator."""
+
+    TIMEOUT = 120.0
+    KEY = "hbgpu/failed_rank"
+    POLL_S = 50e-6
+
+    def __init__(self, comm, rank, store, timeout=None, async_error=None, abort=None):
+        self.comm, self.rank, self.store = comm, rank, store
+        self.timeout = self.TIMEOUT if timeout is None else timeout
+        self._async_error = async_error or self._nccl_async_error
+        self._abort = abort or self._nccl_abort
+        self.aborted = False
+
+    def _nccl_async_error(self):
+        lib = native.load()
+        if lib.hbgpu_comm_async_error(self.comm) != 0:
+            return lib.hbgpu_last_error().decode(errors="replace")
+        return None
+
+    def _nccl_abort(self):
+        native.load().hbgpu_comm_abort(self.comm)
+
+    def abort(self):
+        if not self.aborted:
+            self.aborted = True
+            self._abort()
+
+    def failed_peer(self):
+        if self.store is None:
+            return None
+        try:
+            if self.store.check([self.KEY]):
+                return int(self.store.get(self.KEY))
+        except Exception:
+            return None
+        return None
+
+    def notify_failure(self):
+        if self.store is not None:
+            try:
+                self.store.compare_set(self.KEY, "", str(self.rank))
+            except Exception:
+                pass
+        self.abort()
+
+    def check(self):
+        msg = self._async_error()
+        if msg is not None:
+            self.abort()
+            raise CollectiveError(f"rank {self.rank}: {msg}")
+        peer = self.failed_peer()
+        if peer is not None and peer != self.rank:
+            self.abort()
+            raise RankFailure(peer, RunAborted(f"rank {self.rank} aborted: rank {peer} failed"))
+
+    def wait(self, event):
+        deadline = time.monotonic() + self.timeout
+        while not event.query():
+            self.check()
+            if time.monotonic() > deadline:
+                self.abort()
+                raise CollectiveError(f"rank {self.rank}: device work did not complete within "
+                                      f"{self.timeout:.0f} s (a peer stopped?)")
+            time.sleep(self.POLL_S)
+        self.check()
+
+    def sync(self):
+        """wait() for everything issued so far on torch's current stream (the
+        engine joins its work back onto it; the collectives run on it)."""
+        import torch
+        ev = torch.cuda.Event()
+        ev.record()
+        self.wait(ev)
 
 
 def _execute_loopback(spec, topology, partition, plan, iterations, out=((), ())):
@@ -781,18 +1070,21 @@ def _execute_loopback(spec, topology, partition, plan, iterations, out=((), ()))
         torch.cuda.synchronize(device)
         t0 = time.perf_counter()
         phase(-1, True)
-        for _ in range(iterations):
+        chunk = poll_interval(topology, spec.case.planes, max(1, iterations))
+        for it in range(iterations):
             for st in range(4):
                 phase(st, True)
             phase(4, False)
+            if (it + 1) % chunk == 0 and first_event(dr.divergence() for dr in ranks) is not None:
+                break
         torch.cuda.synchronize(device)
         loop_s = time.perf_counter() - t0
-        divs = [d for d in (dr.divergence() for dr in ranks) if d is not None]
-        raise_divergence(min(divs, key=lambda d: d[:2]) if divs else None)
-        fields, norms = {}, {}
+        raise_divergence(first_event(dr.divergence() for dr in ranks))
+        fields = {}
         for dr in ranks:
             fields.update(dr.fields(0, pinned_out=spec.output))
-            norms.update(dr.norm_history(iterations))
+        norms = _norm_totals(_global_sumsq(ranks, len(topology.blocks), iterations), iterations,
+                             ranks[0].stream())
         if iterations > 0:
             stacked = torch.stack([dr.force_history_array(iterations).reshape(-1) for dr in ranks])
             count = stacked.shape[1]

@@ -10,7 +10,7 @@ Bar: bitwise for fields and forces; residual norms within 1e-12 relative
 import numpy as np
 import pytest
 
-from paper_1304_7654_b200 import (BlockSpec, CaseConfig, CutSide, CutSpec, DivergenceError,
+from paper_1304_7654_b200 import (BlockSpec, CaseConfig, CutSide, CutSpec, DivergenceError, RankFailure,
                                   RunSpec, baseline_workload, lattice_case, pair_case,
                                   ring_case, run_case, stacked_pair_case, tc1_mini, tc2_mini,
                                   tc_tiny)
@@ -134,9 +134,9 @@ def test_divergence_reports_reference_location(cuda, oracle_mod):
     case = pair_case(8, 6, 1, h=0.25, dtau=50.0, nbody=0)
     with pytest.raises(oracle_mod.OracleDivergence) as want:
         oracle_mod.run(case, 100)
-    with pytest.raises(DivergenceError) as got:
+    with pytest.raises(RankFailure) as got:
         run_case(RunSpec(case=case, ranks=1, iterations=100))
-    w, g = want.value, got.value
+    w, g = want.value, got.value.cause
     assert (g.block, g.i, g.j, g.p, g.n) == (w.block, w.i, w.j, w.p, w.n)
 
 
@@ -208,9 +208,9 @@ def test_paired_stages_divergence_location(cuda, oracle_mod):
     case = lattice_case(2, 1, 256, 12, 1, h=0.01, dtau=5.0)
     with pytest.raises(oracle_mod.OracleDivergence) as want:
         oracle_mod.run(case, 100)
-    with pytest.raises(DivergenceError) as got:
+    with pytest.raises(RankFailure) as got:
         run_case(RunSpec(case=case, ranks=1, iterations=100, fused=True))
-    w, g = want.value, got.value
+    w, g = want.value, got.value.cause
     assert (g.block, g.i, g.j, g.p, g.n) == (w.block, w.i, w.j, w.p, w.n)
 
 
@@ -253,3 +253,144 @@ def test_many_tiles_per_cta_match_oracle(name, fused, limit, cuda, oracle_mod, m
     got = run_case(RunSpec(case=case, ranks=1, iterations=iters, tile_rows=tile_rows, fused=fused))
     want = oracle_mod.run(case, iters)
     assert_parity(got, want, f"{name} fused={fused} limit={limit}")
+
+
+# ---------------------------------------------------------------------------
+# run control: early divergence stop, iteration capacity, hazard -> strict rerun
+# ---------------------------------------------------------------------------
+
+def test_divergence_stops_the_loop_early(cuda, oracle_mod):
+    """A 500-iteration run that diverges in its first iterations stops
+    within one polling chunk (the reference raises at the failing stage,
+    hbcore.py:273-276) and reports the reference's location."""
+    from paper_1304_7654_b200 import solver
+    case = lattice_case(2, 1, 256, 12, 1, h=0.01, dtau=5.0)
+    with pytest.raises(oracle_mod.OracleDivergence) as want:
+        oracle_mod.run(case, 500)
+    with pytest.raises(RankFailure) as got:
+        run_case(RunSpec(case=case, ranks=1, iterations=500))
+    w, g = want.value, got.value.cause
+    assert (g.block, g.i, g.j, g.p, g.n) == (w.block, w.i, w.j, w.p, w.n)
+    chunk = solver.POLL_MAX
+    assert solver.LAST_RUN["iterations_issued"] <= w.iteration + 1 + 2 * chunk < 500
+
+
+def test_engine_refuses_iterations_past_max_iters(cuda):
+    """sumsq and force_hist hold max_iters rows: the engine refuses to issue
+    more iterations (include/hbgpu.h hbgpu_engine_iterate) until rewound."""
+    from paper_1304_7654_b200.solver import DeviceRank
+    from paper_1304_7654_b200 import build_topology, partition_blocks, build_cut_plan
+    case = tc_tiny()
+    topo = build_topology(case)
+    part = partition_blocks(topo, 1)
+    dr = DeviceRank(case, topo, part, build_cut_plan(topo, part, case.nharms, 4), max_iters=2)
+    try:
+        dr.prime()
+        dr.iterate(2)
+        assert dr.iterations_done() == 2
+        with pytest.raises(RuntimeError, match="max_iters"):
+            dr.iterate(1)
+        with pytest.raises(RuntimeError, match="max_iters"):
+            dr.iterate(1, use_graph=False)
+        dr.reset_counters()
+        assert dr.iterations_done() == 0
+        dr.iterate(2, use_graph=False)
+        import torch
+        torch.cuda.synchronize()
+        assert int(dr.iter.item()) == 2
+    finally:
+        dr.close()
+
+
+@pytest.mark.parametrize("scale", [1.5, 1.0])
+def test_huge_initial_value_reruns_strict_and_matches_oracle(scale, cuda, oracle_mod):
+    """The paired kernel's DFMA 4c - w is the reference's rounding only for
+    |c| < 2^1022.  A state holding a larger finite value sets a hazard key
+    (engine prime scan / stage outputs) and run_case repeats the run on the
+    strict single-stage kernels, so the outcome is the reference's: here
+    the divergence the overflowing 4c causes, at the reference's cell."""
+    from paper_1304_7654_b200 import solver
+    case = lattice_case(2, 1, 256, 12, 1, h=0.01, dtau=0.0002)
+    big = scale * 2.0 ** 1022
+
+    def initial(spec, planes, npde):
+        ic = oracle_mod.initial_values(spec, planes, npde)
+        if spec.id == 1:
+            ic[1, 2, 5, 17] = big
+            ic[1, 2, 5, 16] = 2.9 * big   # 4c - w stays finite in one rounding
+        return ic
+
+    before = solver.STRICT_RERUNS[0]
+    try:
+        want = oracle_mod.run(case, 3, initial=initial)
+        want_err = None
+    except oracle_mod.OracleDivergence as e:
+        want_err = e
+    if want_err is None:
+        got = run_case(RunSpec(case=case, ranks=1, iterations=3, initial=initial, fused=True))
+        assert_parity(got, want, "huge")
+    else:
+        with pytest.raises(RankFailure) as got:
+            run_case(RunSpec(case=case, ranks=1, iterations=3, initial=initial, fused=True))
+        g = got.value.cause
+        assert (g.block, g.i, g.j, g.p, g.n) == (want_err.block, want_err.i, want_err.j, want_err.p,
+                                                 want_err.n)
+    assert solver.STRICT_RERUNS[0] == before + 1
+
+
+def test_stage_output_hazard_is_recorded(cuda, oracle_mod):
+    """In-kernel hazard keys.  One cell of q = 2^1021 (below the prime
+    scan's 2^1022) with coef = dtau/4 = 1 and nu_h2 = 1.25: stage 1 is
+    exact and finite everywhere, but writes -2^1023 at that cell (and
+    1.875 * 2^1022 east of it).  Stage 2's 4c then overflows -- in the
+    reference a DivergenceError at stage 2, which the paired kernel's DFMA
+    4c - w would only match by luck.  The paired kernel must flag the stage-1
+    outputs of magnitude >= 2^1022 (hazard key, global stage 1) so that
+    run_case repeats the run on the strict kernels, whose outcome is the
+    reference's."""
+    import torch
+    from paper_1304_7654_b200 import solver
+    from paper_1304_7654_b200.solver import DeviceRank
+    from paper_1304_7654_b200 import build_topology, partition_blocks, build_cut_plan
+    case = lattice_case(2, 1, 256, 12, 1, h=0.2, dtau=4.0)
+
+    def initial(spec, planes, npde):
+        ic = oracle_mod.initial_values(spec, planes, npde)
+        if spec.id == 1:
+            ic[0, 0, 5, 100] = 2.0 ** 1021
+        return ic
+
+    with pytest.raises(oracle_mod.OracleDivergence) as want:
+        oracle_mod.run(case, 1, initial=initial)
+    w = want.value
+    assert (w.iteration, w.stage) == (0, 1)
+    topo = build_topology(case)
+    part = partition_blocks(topo, 1)
+    dr = DeviceRank(case, topo, part, build_cut_plan(topo, part, case.nharms, 4), initial=initial,
+                    tile_rows=12, max_iters=1, fused=True)
+    try:
+        assert dr.fused
+        dr.prime()
+        dr.iterate(1, use_graph=False)
+        torch.cuda.synchronize()
+        assert dr.divergence() == (1, True, 1, 101, 6, 0, 0)
+    finally:
+        dr.close()
+    before = solver.STRICT_RERUNS[0]
+    with pytest.raises(RankFailure) as got:
+        run_case(RunSpec(case=case, ranks=1, iterations=1, initial=initial, fused=True))
+    g = got.value.cause
+    assert (g.block, g.i, g.j, g.p, g.n) == (w.block, w.i, w.j, w.p, w.n)
+    assert solver.STRICT_RERUNS[0] == before + 1
+
+
+def test_run_diverges_with_rank_in_error(cuda):
+    """The reference's run_case wraps a rank's DivergenceError in a
+    RankFailure naming the rank (runtime.py:359-364; its
+    tests/test_driver_cli.py:30-36 asserts exactly this)."""
+    case = pair_case(4, 4, 1, h=0.25, dtau=50.0)
+    for ranks in (1, 2):
+        with pytest.raises(RankFailure) as err:
+            run_case(RunSpec(case=case, ranks=ranks, iterations=50))
+        assert isinstance(err.value.cause, DivergenceError)
+        assert err.value.rank in range(ranks)
