@@ -119,8 +119,12 @@ typedef struct hbgpu_halo_dir {
     int64_t dst_off, dst_es, dst_vs;
     int32_t length;
     int32_t src_kind, dst_kind;
-    int32_t pad;
+    int32_t flags;       /* HBGPU_HALO_SECTOR_DST: every destination cell's
+                            32-byte sector holds no other live value (a
+                            west halo column; an east one when ni % 4 == 0),
+                            so it is written as a whole sector            */
 } hbgpu_halo_dir;
+#define HBGPU_HALO_SECTOR_DST 1
 
 /* Force-integration segment: one (block, face) body face, in reference
  * order (blocks ascending, body_faces order; hbcore.py:369-381).          */
@@ -212,6 +216,13 @@ typedef struct hbgpu_stage_args {
      * from here: by then the neighbouring strip's CTA may have replaced q0
      * at those columns                                                      */
     double *edge_q0;
+    /* tiles this launch processes: tile_order[k] (identity when NULL) for k
+     * in [tile_lo, tile_hi), tile_hi <= 0 meaning total_tiles.  The engine
+     * splits a multi-GPU stage into its boundary tiles (whose faces feed a
+     * remote cut) and the interior tiles that overlap the NCCL exchange.  */
+    const int32_t *tile_order;
+    int32_t tile_lo;
+    int32_t tile_hi;
     /* D row-major P x P with a +0.0 diagonal (hbcore.py:88-94); ap[n*4 + p]
      * = amp[n] (1 + p/4), zero except on planes 1 and 2 (hbcore.py:170-175):
      * the kernel adds those zero terms as exact signed zeros              */
@@ -352,6 +363,12 @@ typedef struct hbgpu_engine_desc {
     int32_t fused;
     int32_t pad1;
     double *edge_q0;                 /* fused: device, see hbgpu_stage_args */
+    /* multi-GPU overlap (used when comm != NULL and the rank sends): device
+     * tile permutation with the nbound_tiles boundary tiles first;
+     * prime_dirs / post_dirs start with prime_remote / post_remote remote
+     * packs (dst_kind 1), followed by the local copies                    */
+    const int32_t *tile_order;
+    int32_t nbound_tiles, prime_remote, post_remote, pad2;
     const hbgpu_force_seg *segs;     int32_t nsegs;  /* device */
     double *force_hist;              /* device [max_iters*3*planes*nbody] */
     const hbgpu_peer_msg *sends;     int32_t nsends; /* HOST arrays */
@@ -394,6 +411,14 @@ int hbgpu_engine_rewind(hbgpu_engine *eng, void *stream);
  * scatters the receive buffer into the slot that phase wrote.            */
 int hbgpu_engine_step(hbgpu_engine *eng, int32_t phase, void *stream);
 int hbgpu_engine_unpack(hbgpu_engine *eng, int32_t phase, void *stream);
+/* phase 0..3 (a pass phase: single stages, or the paired schedule's 1 and
+ * 3) in the two parts the multi-GPU engine overlaps with its exchange:
+ * part 0 = the boundary tiles (desc.tile_order[0, nbound_tiles)) and the
+ * remote packs -- after it the send buffer is complete; part 1 = the
+ * interior tiles, the norm fold (first stage) and the local halo copies.
+ * A caller that moves the payloads itself runs part 0, its transfer
+ * (concurrently with part 1 if it likes), part 1, then unpack.            */
+int hbgpu_engine_step_split(hbgpu_engine *eng, int32_t phase, int32_t part, void *stream);
 /* kernels this engine launches per iteration (for launch accounting) */
 int hbgpu_engine_launches_per_iteration(const hbgpu_engine *eng);
 int hbgpu_engine_destroy(hbgpu_engine *eng);

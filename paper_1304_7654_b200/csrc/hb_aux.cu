@@ -11,16 +11,43 @@ namespace hbgpu {
 
 // ---- halo moves (exchange.py:195-202, 248-261) ------------------------------
 
-__global__ void halo_kernel(double *slot, double *sendbuf, const double *recvbuf,
-                            const hbgpu_halo_dir *dirs, int nv) {
+// One thread per (direction, element, slice of the 4P values).  Consecutive
+// threads take consecutive elements, so a row face (element stride 1) moves
+// as coalesced 256-byte warp accesses; a column face is one cell per row,
+// and its slot-halo destination is written as the cell's whole 32-byte
+// sector (HBGPU_HALO_SECTOR_DST: the rest of the sector is row lead or
+// padding) so L2 never fills a partial sector.  Each thread keeps up to 8
+// loads in flight.
+constexpr int HALO_THREADS = 128;
+constexpr int HALO_VCHUNK = 8;
+
+__global__ void __launch_bounds__(HALO_THREADS) halo_kernel(double *slot, double *sendbuf, const double *recvbuf,
+                                                            const hbgpu_halo_dir *dirs, int nv) {
     const hbgpu_halo_dir d = dirs[blockIdx.y];
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (int64_t)d.length * nv) return;
-    const int64_t e = idx / nv;
-    const int64_t v = idx - e * nv;
-    const double *src = d.src_kind == 0 ? slot : (d.src_kind == 1 ? sendbuf : recvbuf);
-    double *dst = d.dst_kind == 0 ? slot : sendbuf;
-    dst[d.dst_off + e * d.dst_es + v * d.dst_vs] = src[d.src_off + e * d.src_es + v * d.src_vs];
+    const int64_t e = (int64_t)blockIdx.x * HALO_THREADS + threadIdx.x;
+    if (e >= d.length) return;
+    const int v0 = blockIdx.z * HALO_VCHUNK;
+    const int nvk = min(HALO_VCHUNK, nv - v0);
+    const double *src = (d.src_kind == 0 ? slot : (d.src_kind == 1 ? sendbuf : recvbuf)) + d.src_off + e * d.src_es;
+    double *dst = (d.dst_kind == 0 ? slot : sendbuf) + d.dst_off + e * d.dst_es;
+    double val[HALO_VCHUNK];
+#pragma unroll
+    for (int k = 0; k < HALO_VCHUNK; ++k)
+        if (k < nvk) val[k] = src[(int64_t)(v0 + k) * d.src_vs];
+    const bool sector = (d.flags & HBGPU_HALO_SECTOR_DST) != 0 && d.dst_kind == 0;
+#pragma unroll
+    for (int k = 0; k < HALO_VCHUNK; ++k) {
+        if (k >= nvk) break;
+        double *t = dst + (int64_t)(v0 + k) * d.dst_vs;
+        if (sector) {
+            double2 *sec = reinterpret_cast<double2 *>((uintptr_t)t & ~(uintptr_t)31);
+            const int pos = (int)(((uintptr_t)t >> 3) & 3);
+            sec[0] = make_double2(pos == 0 ? val[k] : 0.0, pos == 1 ? val[k] : 0.0);
+            sec[1] = make_double2(pos == 2 ? val[k] : 0.0, pos == 3 ? val[k] : 0.0);
+        } else {
+            *t = val[k];
+        }
+    }
 }
 
 // ---- hazard scan ----------------------------------------------------------------
@@ -205,8 +232,9 @@ extern "C" int hbgpu_halo(double *slot, double *sendbuf, const double *recvbuf,
                           int32_t planes, void *stream) {
     if (ndirs <= 0 || max_len <= 0) return HBGPU_OK;
     const int nv = planes * NPDE;
-    dim3 grid((unsigned)(((int64_t)max_len * nv + 127) / 128), (unsigned)ndirs);
-    halo_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(slot, sendbuf, recvbuf, dirs, nv);
+    dim3 grid((unsigned)((max_len + HALO_THREADS - 1) / HALO_THREADS), (unsigned)ndirs,
+              (unsigned)((nv + HALO_VCHUNK - 1) / HALO_VCHUNK));
+    halo_kernel<<<grid, HALO_THREADS, 0, (cudaStream_t)stream>>>(slot, sendbuf, recvbuf, dirs, nv);
     hbgpu_count_launch(1);
     return hbgpu_check_launch("hbgpu_halo");
 }

@@ -158,7 +158,31 @@ struct PairSmem {
     static_assert((SLOT * 8) % 128 == 0 && (QSLOT * 8) % 128 == 0, "TMA slots need 128-B alignment");
 };
 
-constexpr int PAIR_THREADS = (CW + 3) * 32;   // + TMA load warp, TMA store warp, edge warp
+// Three warpgroups: the 8 consumer warps (two groups) and a helper group of
+// the TMA load warp, the TMA store warp, the edge warp and one idle warp.
+// The helpers need few registers: after the launch (168 per thread) the
+// helper group gives registers back (setmaxnreg.dec) and the consumer groups
+// take them (setmaxnreg.inc), so the consumers can hold two register row
+// windows (the input rows r-1..r+1 and v1 rows r-2..r) without spilling.
+constexpr int PAIR_THREADS = (CW + 4) * 32;
+static_assert(CW == 8, "two consumer warpgroups + one helper warpgroup");
+// per tile geometry: the PT = 4 edge warp carries 3 (side, pde, plane)
+// items per lane and needs more registers.  Budget: 256 * (consumer - 168)
+// <= 128 * (168 - helper) + (65536 - 384 * 168).
+template <int PT> struct PairRegs {
+    static constexpr int HELPER = PT == 1 ? 64 : 80;
+    static constexpr int CONSUMER = PT == 1 ? 216 : 208;
+    static_assert(256 * (CONSUMER - 168) <= 128 * (168 - HELPER) + (65536 - PAIR_THREADS * 168), "regs");
+};
+
+template <int PT>
+__device__ __forceinline__ void helper_regs() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PairRegs<PT>::HELPER));
+}
+template <int PT>
+__device__ __forceinline__ void consumer_regs() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(PairRegs<PT>::CONSUMER));
+}
 
 __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(HBGPU_TILE_WARPS * 32) : "memory");
@@ -268,9 +292,13 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
         fence_mbar_init();
     }
     __syncthreads();
-    const int ntile = a.total_tiles;
+    const int ntile = tile_end(a);
     const CUtensorMap *maps = reinterpret_cast<const CUtensorMap *>(a.tmaps);
     const bool inter = a.interleaved != 0;
+    if (warp >= CW) {
+        helper_regs<PT>();
+        if (warp == CW + 3) return;   // the helper group's fourth warp
+    }
 
     if (warp == CW) {
         // ------------------------------ producer ------------------------------
@@ -279,7 +307,8 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
                            EBYTES = P * PT * 8 * 8;
         RingPos pin{0, 0}, pq{0, 0};
         int issued_in = 0, issued_q = 0;
-        for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+        for (int k = a.tile_lo + blockIdx.x; k < ntile; k += gridDim.x) {
+            const int t = tile_at(a, k);
             const Tile tl = decode_tile<PT>(a, t);
             const CUtensorMap *min = maps + a.in_slot * a.nblocks + tl.bidx;
             const CUtensorMap *mq = maps + 3 * a.nblocks + tl.bidx;
@@ -329,7 +358,8 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
         // ----------------------- store warp (pass B only) -----------------------
         if (!PB || lane != 0) return;
         RingPos ps{0, 0};
-        for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+        for (int k = a.tile_lo + blockIdx.x; k < ntile; k += gridDim.x) {
+            const int t = tile_at(a, k);
             const Tile tl = decode_tile<PT>(a, t);
             const CUtensorMap *mo = maps + (5 + a.out_slot) * a.nblocks + tl.bidx;
             prefetch_tmap(mo);
@@ -370,7 +400,8 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
             for (int m = 0; m < P; ++m) drow[c][m] = k < NE ? a.D[n_k[c] * P + m] : 0.0;
         }
         RingPos cin{0, 0};
-        for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+        for (int k = a.tile_lo + blockIdx.x; k < ntile; k += gridDim.x) {
+            const int t = tile_at(a, k);
             const Tile tl = decode_tile<PT>(a, t);
             const hbgpu_block b = a.blocks[tl.bidx];
             const bool west_in = tl.i0 > 1, east_in = tl.i0 + G::TCOLS <= b.ni;
@@ -464,6 +495,8 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
     }
 
     // -------------------------------- consumers ---------------------------------
+    // (every helper warp has returned above: this region runs at CONSUMER_REGS)
+    consumer_regs<PT>();
     const int pp = warp % PT;
     const int cw = warp / PT;
     const int col0 = 32 * cw + lane;
@@ -485,7 +518,8 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
     int ap_pde = -1;
     double ap[P];
     int vr = 0;   // v1 ring row of v1(r)
-    for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+    for (int k = a.tile_lo + blockIdx.x; k < ntile; k += gridDim.x) {
+            const int t = tile_at(a, k);
         const Tile tl = decode_tile<PT>(a, t);
         const int p = tl.pde0 + pp;
         if (p != ap_pde) {
@@ -511,22 +545,32 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
         double nrm = 0.0;
         double sv_prev = 0.0;
         RingPos cprev{0, 0};   // stencil entry of row r-1
+        // input window: this lane's column of `in` at rows r-1, r, r+1 stays
+        // in registers, so a row step loads only the new row's centre and
+        // the current row's west / east neighbours from the ring
+        double xa[P], xb[P], xc[P];
         {
             // row j0-1 entry: only its stencil row is used (as v1(j0)'s south)
             cprev = cin;
             cin = advance<R>(cin);
-        }
-        // one row step: v1(r) and, one row behind, v2(r-1)
-        auto row_step = [&](const int r, double(&pa)[P], double(&pb)[P], double(&pc)[P]) {
-            // rows r-1 and r were waited for as earlier steps' rows r and r+1
-            // (the tile's first step waits for them here)
-            const RingPos nx = advance<R>(cin);
-            if (r == tl.j0) {
-                mbar_wait(full_in + cprev.slot, cprev.phase);
-                mbar_wait(full_in + cin.slot, cin.phase);
-            }
-            mbar_wait(full_in + nx.slot, nx.phase);
+            mbar_wait(full_in + cprev.slot, cprev.phase);
+            mbar_wait(full_in + cin.slot, cin.phase);
             const double *ru = ring + cprev.slot * S::SLOT + in_off;
+            const double *rc = ring + cin.slot * S::SLOT + in_off;
+#pragma unroll
+            for (int n = 0; n < P; ++n) {
+                xa[n] = ru[n * PT * G::BW];
+                xb[n] = rc[n * PT * G::BW];
+            }
+        }
+        // one row step: v1(r) and, one row behind, v2(r-1).  Input window on
+        // entry: ia = in(r-1), ib = in(r); ic <- in(r+1)
+        auto row_step = [&](const int r, double(&pa)[P], double(&pb)[P], double(&pc)[P], double(&ia)[P],
+                            double(&ib)[P], double(&ic)[P]) {
+            // rows r-1 and r were waited for as earlier steps' rows r and r+1
+            // (the tile's first step: before the first step)
+            const RingPos nx = advance<R>(cin);
+            mbar_wait(full_in + nx.slot, nx.phase);
             const double *rc = ring + cin.slot * S::SLOT + in_off;
             const double *rn = ring + nx.slot * S::SLOT + in_off;
             const double sv = ring[nx.slot * S::SLOT + S::SXY + col0];
@@ -537,17 +581,15 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
             }
             double o[P], v[P];
             {
-                double c[P], w[P], e[P], s[P], nn[P], base[P];
+                double w[P], e[P], base[P];
 #pragma unroll
                 for (int n = 0; n < P; ++n) {
-                    c[n] = rc[n * PT * G::BW];
+                    ic[n] = rn[n * PT * G::BW];
                     w[n] = rc[n * PT * G::BW - 1];
                     e[n] = rc[n * PT * G::BW + 1];
-                    s[n] = ru[n * PT * G::BW];
-                    nn[n] = rn[n * PT * G::BW];
-                    base[n] = PB ? qv[n * PT * G::TCOLS] : c[n];
+                    base[n] = PB ? qv[n * PT * G::TCOLS] : ib[n];
                 }
-                stage_point<P>(c, w, e, s, nn, dk, ap, sv, nu_h2, adv_2h, coef1, base, o, pc);
+                stage_point<P>(ib, w, e, ia, ic, dk, ap, sv, nu_h2, adv_2h, coef1, base, o, pc);
             }
             if (!PB) {
 #pragma unroll
@@ -584,7 +626,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
                     mbar_arrive(staged + cqp.slot);
                 } else {
 #pragma unroll
-                    for (int n = 0; n < P; ++n) base2[n] = ru[n * PT * G::BW];   // q0 = in, row r-1
+                    for (int n = 0; n < P; ++n) base2[n] = ia[n];   // q0 = in, row r-1
                     stage_point<P>(pb, w2, e2, pa, pc, dk, ap, sv_prev, nu_h2, adv_2h, coef2, base2, o, v);
                     const int64_t row = (int64_t)(r - 1) * b.rs;
 #pragma unroll
@@ -608,14 +650,14 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
         // v1 window (pa, pb) = (v1(r-2), v1(r-1)) on entry of step r; pc <- v1(r)
         int r = tl.j0;
         for (; r + 2 <= tl.j1; r += 3) {
-            row_step(r, va, vb, vc);
-            row_step(r + 1, vb, vc, va);
-            row_step(r + 2, vc, va, vb);
+            row_step(r, va, vb, vc, xa, xb, xc);
+            row_step(r + 1, vb, vc, va, xb, xc, xa);
+            row_step(r + 2, vc, va, vb, xc, xa, xb);
         }
         // last second-stage row: v2(j1) from the window (A, B) = (v1(j1-1),
         // v1(j1)) and v1(j1+1) from the band slot; cprev is the entry of row
-        // j1 (v1(j1)'s edge granules and, pass A, q0 row j1)
-        auto last_step = [&](double(&A)[P], double(&B)[P]) {
+        // j1 (v1(j1)'s edge granules); X = in(j1) (pass A: q0 row j1)
+        auto last_step = [&](double(&A)[P], double(&B)[P], double(&X)[P]) {
             double vd[P];
 #pragma unroll
             for (int n = 0; n < P; ++n) vd[n] = __ldg(a.band + colbase + n * ps4 + (int64_t)(tl.j1 + 1) * b.rs);
@@ -629,7 +671,6 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
                 w2[n] = vw[n * w_nstride];
                 e2[n] = ve[n * e_nstride];
             }
-            const double *ru = ring + cprev.slot * S::SLOT + in_off;
             if (PB) {
                 const RingPos cqp = cq.slot == 0 ? RingPos{Q - 1, cq.phase ^ 1u} : RingPos{cq.slot - 1, cq.phase};
                 const double *qp = qring + cqp.slot * S::QSLOT + q_off;
@@ -643,7 +684,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
                 mbar_arrive(staged + cqp.slot);
             } else {
 #pragma unroll
-                for (int n = 0; n < P; ++n) base2[n] = ru[n * PT * G::BW];
+                for (int n = 0; n < P; ++n) base2[n] = X[n];
                 stage_point<P>(B, w2, e2, A, vd, dk, ap, sv_prev, nu_h2, adv_2h, coef2, base2, o, v);
                 const int64_t row = (int64_t)tl.j1 * b.rs;
 #pragma unroll
@@ -656,14 +697,14 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
             record_nonfinite<P>(v, a, tl.bidx, b, p, tl.j1, i, gstage + 1);
         };
         if (r > tl.j1) {
-            last_step(va, vb);
+            last_step(va, vb, xa);
         } else if (r == tl.j1) {
-            row_step(r, va, vb, vc);
-            last_step(vb, vc);
+            row_step(r, va, vb, vc, xa, xb, xc);
+            last_step(vb, vc, xb);
         } else {
-            row_step(r, va, vb, vc);
-            row_step(r + 1, vb, vc, va);
-            last_step(vc, va);
+            row_step(r, va, vb, vc, xa, xb, xc);
+            row_step(r + 1, vb, vc, va, xb, xc, xa);
+            last_step(vc, va, xc);
         }
         // every consumer is past its reads of the v1 ring before the next
         // tile's first row overwrites it
@@ -735,7 +776,7 @@ static int pair_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only
         return HBGPU_ERR_ARG;
     }
     PairLaunch &L = a.pair == 2 ? lb : la;
-    const int grid = persistent_grid(L.grid, a.total_tiles);
+    const int grid = persistent_grid(L.grid, tile_end(a) - a.tile_lo);
     L.fn<<<grid, PAIR_THREADS, L.smem, s>>>(a);
     hbgpu_count_launch(1);
     return hbgpu_check_launch("hbgpu_stage (pair)");

@@ -201,6 +201,11 @@ struct hbgpu_engine {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     int32_t done = 0;   // iterations issued (rows of sumsq / force_hist used)
+    // multi-GPU overlap: boundary tiles -> remote pack -> NCCL on `comm_s`
+    // while the interior tiles run on the work stream (run_split)
+    bool split = false;
+    cudaStream_t comm_s = nullptr;
+    cudaEvent_t ev_pack = nullptr, ev_comm = nullptr;
 };
 
 namespace {
@@ -209,6 +214,27 @@ namespace {
 //   stage 0: A -> B, stage 1: B -> C, stage 2: C -> B, stage 3: B -> A (in place on q0)
 constexpr int kIn[4] = {0, 1, 2, 1};
 constexpr int kOut[4] = {1, 2, 1, 0};
+
+// one grouped NCCL send/recv of every peer segment (exchange.py:307-316:
+// one aggregated message per direction, here per peer) on stream s
+int nccl_group(hbgpu_engine *e, cudaStream_t s) {
+    const hbgpu_engine_desc &d = e->d;
+    if (!load_nccl()) return HBGPU_ERR_NCCL;
+    ncclComm_t comm = (ncclComm_t)d.comm;
+    ncclResult_t r = g_nccl.GroupStart();
+    if (r != ncclSuccess) return nccl_fail("ncclGroupStart", r);
+    for (const auto &m : e->sends) {
+        r = g_nccl.Send(d.sendbuf + m.offset, (size_t)m.count, ncclFloat64, m.peer, comm, s);
+        if (r != ncclSuccess) return nccl_fail("ncclSend", r);
+    }
+    for (const auto &m : e->recvs) {
+        r = g_nccl.Recv(d.recvbuf + m.offset, (size_t)m.count, ncclFloat64, m.peer, comm, s);
+        if (r != ncclSuccess) return nccl_fail("ncclRecv", r);
+    }
+    r = g_nccl.GroupEnd();
+    if (r != ncclSuccess) return nccl_fail("ncclGroupEnd", r);
+    return HBGPU_OK;
+}
 
 int exchange_remote(hbgpu_engine *e, double *slot, cudaStream_t s) {
     const hbgpu_engine_desc &d = e->d;
@@ -267,10 +293,8 @@ void fill_args(const hbgpu_engine_desc &d, hbgpu_stage_args &a) {
     memcpy(a.ap, d.ap, sizeof(a.ap));
 }
 
-// phase `ph` of the paired schedule (hb_pair.cu)
-int run_fused_phase(hbgpu_engine *e, int ph, cudaStream_t s) {
-    const hbgpu_engine_desc &d = e->d;
-    hbgpu_stage_args a;
+// arguments of phase `ph` of the paired schedule (hb_pair.cu)
+void fused_args(const hbgpu_engine_desc &d, int ph, hbgpu_stage_args &a) {
     fill_args(d, a);
     const int st = ph < 2 ? 0 : 2;   // the first stage of the pair
     a.in = d.slot[kInF[ph]];
@@ -279,67 +303,137 @@ int run_fused_phase(hbgpu_engine *e, int ph, cudaStream_t s) {
     a.out_slot = kOutF[ph];
     a.stage = st;
     a.coef = d.coef[st];
-    if (ph == 0 || ph == 2) return hbgpu_band(&a, s);
-    a.pair = ph == 1 ? 1 : 2;
-    a.coef2 = d.coef[st + 1];
-    a.norm_part = ph == 1 ? d.norm_part : nullptr;
-    int rc = hbgpu_stage(&a, s);
-    if (!rc && ph == 1) rc = hbgpu_norm_fold(d.blocks, d.nblocks, d.norm_part, d.sumsq, d.iter, d.max_iters, s);
-    // pass A forwards south/north rows itself; west/east columns here
-    if (!rc && ph == 1 && d.npost > 0)
-        rc = hbgpu_halo(a.out, d.sendbuf, d.recvbuf, d.post_dirs, d.npost, d.post_max_len, d.planes, s);
-    // pass B writes q4 over q0, which other tiles still read as their base,
-    // so it forwards nothing: a full halo pass fills the new state's halos
-    if (!rc && ph == 3 && d.nprime > 0)
-        rc = hbgpu_halo(d.slot[0], d.sendbuf, d.recvbuf, d.prime_dirs, d.nprime, d.prime_max_len, d.planes, s);
-    return rc;
+    if (ph == 1 || ph == 3) {
+        a.pair = ph == 1 ? 1 : 2;
+        a.coef2 = d.coef[st + 1];
+        a.norm_part = ph == 1 ? d.norm_part : nullptr;
+    }
 }
 
-// the fused stage kernel of RK stage `st` (+ the norm fold after stage 0)
-int run_stage(hbgpu_engine *e, int st, cudaStream_t s) {
-    const hbgpu_engine_desc &d = e->d;
-    if (d.fused) return run_fused_phase(e, st, s);
-    hbgpu_stage_args a;
-    memset(&a, 0, sizeof(a));
-    a.q0 = d.slot[0];
-    a.sendbuf = d.sendbuf;
-    a.blocks = d.blocks;
-    a.tile_block = d.tile_block;
-    a.sxy = d.sxy;
-    a.faces = d.faces;
-    a.status = d.status;
-    a.iter = d.iter;
-    a.dmat = d.dmat;
-    a.tmaps = d.tmaps;
-    a.nblocks = d.nblocks;
-    a.total_tiles = d.total_tiles;
-    a.planes = d.planes;
-    a.tile_rows = d.tile_rows;
-    memcpy(a.D, d.D, sizeof(a.D));
-    memcpy(a.ap, d.ap, sizeof(a.ap));
+// arguments of single RK stage `st` (hb_stage.cu)
+void single_args(const hbgpu_engine_desc &d, int st, hbgpu_stage_args &a) {
+    fill_args(d, a);
+    a.band = nullptr;
+    a.band_segs = nullptr;
+    a.nband_segs = 0;
+    a.band_max_len = 0;
+    a.edge_q0 = nullptr;
     a.in = d.slot[kIn[st]];
     a.out = d.slot[kOut[st]];
     a.stage = st;
     a.in_slot = kIn[st];
     a.out_slot = kOut[st];
-    a.interleaved = d.interleaved;
-    a.tile_pdes = d.tile_pdes;
     a.coef = d.coef[st];
     a.norm_part = st == 0 ? d.norm_part : nullptr;
+}
+
+// The halo moves that follow a stage kernel, split in the remote packs
+// (the first `remote` of `dirs`, dst_kind 1) and the local copies:
+//   single stage 0 and pass A: west / east face columns (post_dirs);
+//   pass B: the full halo pass (prime_dirs), pass B forwarding nothing
+//   itself because it writes q4 over q0, which other tiles still read.
+struct PostMoves {
+    const hbgpu_halo_dir *dirs = nullptr;
+    int32_t n = 0, remote = 0, max_len = 0;
+};
+
+PostMoves post_moves(const hbgpu_engine_desc &d, int st) {
+    PostMoves m;
+    if (d.fused ? st == 1 : st == 0) {
+        m.dirs = d.post_dirs;
+        m.n = d.npost;
+        m.remote = d.post_remote;
+        m.max_len = d.post_max_len;
+    } else if (d.fused && st == 3) {
+        m.dirs = d.prime_dirs;
+        m.n = d.nprime;
+        m.remote = d.prime_remote;
+        m.max_len = d.prime_max_len;
+    }
+    return m;
+}
+
+int halo_moves(const hbgpu_engine_desc &d, double *slot, const hbgpu_halo_dir *dirs, int32_t n, int32_t max_len,
+               cudaStream_t s) {
+    if (n <= 0) return HBGPU_OK;
+    return hbgpu_halo(slot, d.sendbuf, d.recvbuf, dirs, n, max_len, d.planes, s);
+}
+
+// stage / phase `st` (+ the norm fold after the first stage, + its halo moves)
+int run_stage(hbgpu_engine *e, int st, cudaStream_t s) {
+    const hbgpu_engine_desc &d = e->d;
+    hbgpu_stage_args a;
+    if (d.fused) fused_args(d, st, a);
+    else single_args(d, st, a);
+    if (d.fused && (st == 0 || st == 2)) return hbgpu_band(&a, s);
     int rc = hbgpu_stage(&a, s);
-    if (!rc && st == 0) rc = hbgpu_norm_fold(d.blocks, d.nblocks, d.norm_part, d.sumsq, d.iter, d.max_iters, s);
-    // first stage: west / east face columns, local halo copies and remote
-    // packs (the update stages forward them from their TMA store warp)
-    if (!rc && st == 0 && d.npost > 0)
-        rc = hbgpu_halo(a.out, d.sendbuf, d.recvbuf, d.post_dirs, d.npost, d.post_max_len, d.planes, s);
+    if (!rc && a.norm_part != nullptr)
+        rc = hbgpu_norm_fold(d.blocks, d.nblocks, d.norm_part, d.sumsq, d.iter, d.max_iters, s);
+    const PostMoves m = post_moves(d, st);
+    if (!rc) rc = halo_moves(d, a.out, m.dirs, m.n, m.max_len, s);
     return rc;
 }
+
+// The same stage with its remote exchange overlapped (multi-GPU):
+//   work:   boundary tiles -> remote packs -> [ev_pack] -> interior tiles ->
+//           norm fold -> local halo copies -> wait [ev_comm] -> unpack
+//   comm_s: wait [ev_pack] -> ncclGroupStart / Send / Recv / End -> [ev_comm]
+// Boundary tiles hold every cell this rank sends (devlayout tile_order), so
+// the send buffer is complete at ev_pack; interior tiles neither write a
+// sent cell nor read a received halo, so they may run under the transfer;
+// the unpack writes the received halos once both are done.  Band phases
+// (all perimeter work) exchange after the kernel as before.
+int split_part(hbgpu_engine *e, int st, int part, cudaStream_t s) {
+    const hbgpu_engine_desc &d = e->d;
+    hbgpu_stage_args a;
+    if (d.fused) fused_args(d, st, a);
+    else single_args(d, st, a);
+    const PostMoves m = post_moves(d, st);
+    a.tile_order = d.tile_order;
+    if (part == 0) {   // boundary tiles, then the remote packs
+        a.tile_lo = 0;
+        a.tile_hi = d.nbound_tiles;
+        int rc = hbgpu_stage(&a, s);
+        if (!rc) rc = halo_moves(d, a.out, m.dirs, m.remote, m.max_len, s);
+        return rc;
+    }
+    // interior tiles, the norm fold (first stage), the local halo copies
+    a.tile_lo = d.nbound_tiles;
+    a.tile_hi = d.total_tiles;
+    int rc = hbgpu_stage(&a, s);
+    if (!rc && a.norm_part != nullptr)
+        rc = hbgpu_norm_fold(d.blocks, d.nblocks, d.norm_part, d.sumsq, d.iter, d.max_iters, s);
+    if (!rc) rc = halo_moves(d, a.out, m.dirs + m.remote, m.n - m.remote, m.max_len, s);
+    return rc;
+}
+
+int run_split(hbgpu_engine *e, int st, cudaStream_t s) {
+    const hbgpu_engine_desc &d = e->d;
+    int rc = split_part(e, st, 0, s);
+    if (!rc && (cudaEventRecord(e->ev_pack, s) != cudaSuccess ||
+                cudaStreamWaitEvent(e->comm_s, e->ev_pack, 0) != cudaSuccess))
+        rc = hbgpu_check_launch("run_split fork");
+    if (!rc) rc = nccl_group(e, e->comm_s);
+    if (!rc && cudaEventRecord(e->ev_comm, e->comm_s) != cudaSuccess) rc = hbgpu_check_launch("run_split record");
+    if (!rc) rc = split_part(e, st, 1, s);
+    if (!rc && cudaStreamWaitEvent(s, e->ev_comm, 0) != cudaSuccess) rc = hbgpu_check_launch("run_split join");
+    if (!rc) rc = halo_moves(d, d.slot[out_slot(d, st)], d.unpack_dirs, d.nunpack, d.unpack_max_len, s);
+    return rc;
+}
+
+// a pass (stage kernel) phase, as opposed to a band phase
+inline bool pass_phase(const hbgpu_engine_desc &d, int st) { return !d.fused || st == 1 || st == 3; }
 
 int one_iteration(hbgpu_engine *e, cudaStream_t s) {
     const hbgpu_engine_desc &d = e->d;
     for (int st = 0; st < 4; ++st) {
-        int rc = run_stage(e, st, s);
-        if (!rc) rc = exchange_remote(e, d.slot[out_slot(d, st)], s);
+        int rc;
+        if (e->split && pass_phase(d, st)) {
+            rc = run_split(e, st, s);
+        } else {
+            rc = run_stage(e, st, s);
+            if (!rc) rc = exchange_remote(e, d.slot[out_slot(d, st)], s);
+        }
         if (rc) return rc;
     }
     return hbgpu_forces(d.slot[0], d.segs, d.nsegs, d.planes, d.nbody, d.force_hist, d.iter, d.max_iters, s);
@@ -379,6 +473,17 @@ extern "C" int hbgpu_engine_create(const hbgpu_engine_desc *desc, hbgpu_engine *
         cudaEventCreateWithFlags(&e->ev_in, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&e->ev_out, cudaEventDisableTiming) != cudaSuccess) {
         int rc = hbgpu_check_launch("hbgpu_engine_create");
+        hbgpu_engine_destroy(e);
+        return rc ? rc : HBGPU_ERR_CUDA;
+    }
+    // overlap the remote exchange of every pass with its interior tiles when
+    // this rank sends and has a boundary/interior tile split to use
+    e->split = desc->comm != nullptr && !e->sends.empty() && desc->tile_order != nullptr &&
+               desc->nbound_tiles > 0 && desc->nbound_tiles < desc->total_tiles;
+    if (e->split && (cudaStreamCreateWithFlags(&e->comm_s, cudaStreamNonBlocking) != cudaSuccess ||
+                     cudaEventCreateWithFlags(&e->ev_pack, cudaEventDisableTiming) != cudaSuccess ||
+                     cudaEventCreateWithFlags(&e->ev_comm, cudaEventDisableTiming) != cudaSuccess)) {
+        int rc = hbgpu_check_launch("hbgpu_engine_create (comm stream)");
         hbgpu_engine_destroy(e);
         return rc ? rc : HBGPU_ERR_CUDA;
     }
@@ -452,6 +557,20 @@ extern "C" int hbgpu_engine_step(hbgpu_engine *e, int32_t phase, void *stream) {
     return leave(e, caller, rc);
 }
 
+extern "C" int hbgpu_engine_step_split(hbgpu_engine *e, int32_t phase, int32_t part, void *stream) {
+    const hbgpu_engine_desc &d = e->d;
+    if (phase < 0 || phase > 3 || part < 0 || part > 1 || !pass_phase(d, phase) || d.tile_order == nullptr) {
+        hbgpu_set_error("hbgpu_engine_step_split: phase %d part %d is not a split pass phase (or no tile_order)",
+                        phase, part);
+        return HBGPU_ERR_ARG;
+    }
+    cudaStream_t caller = (cudaStream_t)stream;
+    int rc = enter(e, caller);
+    if (rc) return rc;
+    rc = split_part(e, phase, part, e->work);
+    return leave(e, caller, rc);
+}
+
 extern "C" int hbgpu_engine_unpack(hbgpu_engine *e, int32_t phase, void *stream) {
     cudaStream_t caller = (cudaStream_t)stream;
     if (phase < -1 || phase > 3) {
@@ -467,10 +586,19 @@ extern "C" int hbgpu_engine_unpack(hbgpu_engine *e, int32_t phase, void *stream)
 }
 
 extern "C" int hbgpu_engine_launches_per_iteration(const hbgpu_engine *e) {
-    int per_stage = 1 + ((e->d.comm && !e->recvs.empty() && e->d.nunpack > 0) ? 1 : 0);
-    if (e->d.fused)   // band, pair + norm fold (+ post), band, pair (+ halo pass), forces
-        return 4 * per_stage + 2 + (e->d.npost > 0 ? 1 : 0) + (e->d.nprime > 0 ? 1 : 0);
-    return 4 * per_stage + 2 + (e->d.npost > 0 ? 1 : 0);
+    const hbgpu_engine_desc &d = e->d;
+    const bool remote = d.comm != nullptr && !e->recvs.empty() && d.nunpack > 0;
+    int n = 1;   // forces
+    for (int st = 0; st < 4; ++st) {
+        const PostMoves m = post_moves(d, st);
+        const bool fold = d.fused ? st == 1 : st == 0;
+        if (e->split && pass_phase(d, st)) {
+            n += 2 + (fold ? 1 : 0) + (m.remote > 0 ? 1 : 0) + (m.n - m.remote > 0 ? 1 : 0) + (remote ? 1 : 0);
+        } else {
+            n += 1 + (pass_phase(d, st) && fold ? 1 : 0) + (m.n > 0 ? 1 : 0) + (remote ? 1 : 0);
+        }
+    }
+    return n;
 }
 
 static int iterate_on(hbgpu_engine *e, int32_t iterations, int32_t use_graph, cudaStream_t s);
@@ -566,6 +694,12 @@ extern "C" int hbgpu_engine_destroy(hbgpu_engine *e) {
     }
     if (e->ev_in) cudaEventDestroy(e->ev_in);
     if (e->ev_out) cudaEventDestroy(e->ev_out);
+    if (e->comm_s) {
+        cudaStreamSynchronize(e->comm_s);
+        cudaStreamDestroy(e->comm_s);
+    }
+    if (e->ev_pack) cudaEventDestroy(e->ev_pack);
+    if (e->ev_comm) cudaEventDestroy(e->ev_comm);
     delete e;
     return HBGPU_OK;
 }

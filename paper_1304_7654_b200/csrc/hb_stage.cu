@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
         fence_mbar_init();
     }
     __syncthreads();
-    const int ntile = a.total_tiles;
+    const int ntile = tile_end(a);
     const CUtensorMap *maps = reinterpret_cast<const CUtensorMap *>(a.tmaps);
     const bool inter = a.interleaved != 0;
 
@@ -119,7 +119,8 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
         constexpr uint32_t BYTES = S::BOXD * 8 * G::NSPLIT, QBYTES = S::QSLOT * 8, SBYTES = G::TCOLS * 8;
         RingPos pin{0, 0}, pq{0, 0};
         int issued_in = 0, issued_q = 0;   // saturate at the ring size
-        for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+        for (int k = a.tile_lo + blockIdx.x; k < ntile; k += gridDim.x) {
+            const int t = tile_at(a, k);
             const Tile tl = decode_tile<PT>(a, t);
             const CUtensorMap *min = maps + a.in_slot * a.nblocks + tl.bidx;
             const CUtensorMap *mq = maps + 3 * a.nblocks + tl.bidx;   // q0: slot 0, strip box
@@ -166,7 +167,8 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
         // i = 1 and i = ni, read back from the staged row: one lane per
         // (plane, pde) value, off the consumers' critical path.
         RingPos ps{0, 0};
-        for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+        for (int k = a.tile_lo + blockIdx.x; k < ntile; k += gridDim.x) {
+            const int t = tile_at(a, k);
             const Tile tl = decode_tile<PT>(a, t);
             const CUtensorMap *mo = maps + (5 + a.out_slot) * a.nblocks + tl.bidx;
             if (lane == 0) prefetch_tmap(mo);
@@ -236,7 +238,8 @@ __global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_cons
     double dk[P / 2 + 1];   // dk[k] = D[m+k][m] for every m (circulant)
 #pragma unroll
     for (int k = 1; k <= P / 2; ++k) dk[k] = a.D[k * P];
-    for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+    for (int k = a.tile_lo + blockIdx.x; k < ntile; k += gridDim.x) {
+            const int t = tile_at(a, k);
         const Tile tl = decode_tile<PT>(a, t);
         const int p = tl.pde0 + pp;
         if (p != ap_pde) {
@@ -434,7 +437,7 @@ __global__ void __launch_bounds__(CW * 32) stage_kernel_generic(const __grid_con
     const double *D = sh;
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int t = blockIdx.x;
+    const int t = tile_at(a, a.tile_lo + blockIdx.x);
     const Tile tl = decode_tile<PT>(a, t);
     const int p = tl.pde0 + warp % PT;
     const hbgpu_block &b = a.blocks[tl.bidx];
@@ -561,7 +564,7 @@ static int launch_cfg(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_on
         return HBGPU_ERR_ARG;
     }
     Launch &L = a.stage == 0 ? first : rest;
-    const int grid = persistent_grid(L.grid, a.total_tiles);
+    const int grid = persistent_grid(L.grid, tile_end(a) - a.tile_lo);
     L.fn<<<grid, THREADS, L.smem, s>>>(a);
     hbgpu_count_launch(1);
     return hbgpu_check_launch("hbgpu_stage");
@@ -638,7 +641,8 @@ static int dispatch(const hbgpu_stage_args &a, cudaStream_t s, bool prepare_only
         hbgpu_set_error("hbgpu_stage: P=%d needs args->dmat", a.planes);
         return HBGPU_ERR_ARG;
     }
-    kern<<<a.total_tiles, CW * 32, sm, s>>>(a);
+    if (tile_end(a) <= a.tile_lo) return HBGPU_OK;
+    kern<<<tile_end(a) - a.tile_lo, CW * 32, sm, s>>>(a);
     hbgpu_count_launch(1);
     return hbgpu_check_launch("hbgpu_stage");
 }
@@ -689,6 +693,12 @@ extern "C" int hbgpu_stage(const hbgpu_stage_args *args, void *stream) {
         hbgpu_set_error("hbgpu_stage: bad arguments");
         return HBGPU_ERR_ARG;
     }
+    const int end = hbgpu::tile_end(*args);
+    if (args->tile_lo < 0 || end > args->total_tiles || args->tile_lo > end) {
+        hbgpu_set_error("hbgpu_stage: tile range [%d, %d) outside [0, %d)", args->tile_lo, end, args->total_tiles);
+        return HBGPU_ERR_ARG;
+    }
+    if (end == args->tile_lo) return HBGPU_OK;   // an empty part of a split stage
     return hbgpu::dispatch(*args, (cudaStream_t)stream, false);
 }
 

@@ -129,6 +129,16 @@ __device__ __forceinline__ Tile decode_tile(const hbgpu_stage_args &a, int t) {
     return T;
 }
 
+// the launch's tile range (hbgpu_stage_args.tile_order / tile_lo / tile_hi):
+// persistent CTAs walk k = tile_lo + blockIdx.x, += gridDim.x, below
+// tile_end(a), processing tile tile_at(a, k)
+__host__ __device__ __forceinline__ int tile_end(const hbgpu_stage_args &a) {
+    return a.tile_hi > 0 ? a.tile_hi : a.total_tiles;
+}
+__device__ __forceinline__ int tile_at(const hbgpu_stage_args &a, int k) {
+    return a.tile_order != nullptr ? a.tile_order[k] : k;
+}
+
 struct FaceHit {
     int64_t off;
     int64_t ps;

@@ -139,6 +139,13 @@ class RankLayout:
     recvbuf_elems: int = 0
     interleaved: bool = False
     tile_pdes: int = 4
+    # multi-GPU overlap: tiles holding a cell of a face that feeds a remote
+    # cut come first in tile_order (nbound of them); prime_dirs / post_dirs
+    # list their remote packs (dst_kind 1) first (prime_remote / post_remote)
+    tile_order: np.ndarray = None
+    nbound: int = 0
+    prime_remote: int = 0
+    post_remote: int = 0
     band_segs: np.ndarray = None    # tile-perimeter cells (paired stages)
     band_max_len: int = 0
     fused: bool = False             # paired stages (hb_pair.cu)
@@ -239,7 +246,58 @@ def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None,
     _build_routes(layout, topology, plan, rank)
     _build_force_segments(layout)
     _build_band(layout, fused)
+    _build_tile_order(layout, topology, plan, rank)
     return layout
+
+
+def tile_box(layout, t):
+    """(local block, first column, last column, first row, last row) of tile t
+    (the decode_tile of hb_tma.cuh)."""
+    k = int(layout.tile_block[t])
+    b = layout.blocks[k]
+    row = layout.block_table[k]
+    local = t - int(row["tile_begin"])
+    tiles_i = int(row["tiles_i"])
+    width = native.TILE_COLS[layout.tile_pdes]
+    i0 = (local % tiles_i) * width + 1
+    rest = local // tiles_i
+    j0 = (rest // (NPDE // layout.tile_pdes)) * layout.tile_rows + 1
+    return k, i0, min(i0 + width - 1, b.ni), j0, min(j0 + layout.tile_rows - 1, b.nj)
+
+
+def _build_tile_order(layout, topology, plan, rank):
+    """Boundary tiles first: a tile is a boundary tile when it holds a cell
+    of a face range that feeds a remote cut, i.e. a value this rank sends.
+    The engine runs those tiles, packs the send buffer and starts the NCCL
+    exchange on its communication stream, and only then runs the interior
+    tiles, which overlap the transfer (hb_runtime.cu run_split).  Both lists
+    keep the natural (block, row tile, strip) order."""
+    sends = rank_routes(plan, rank).sends
+    faces = {}
+    for d in sends:
+        faces.setdefault(layout.local_index[d.src_block], []).append((d.src_face, d.src_lo, d.src_hi))
+    bound, inner = [], []
+    for t in range(layout.total_tiles):
+        k, i0, i1, j0, j1 = tile_box(layout, t)
+        b = layout.blocks[k]
+        hit = False
+        for face, lo, hi in faces.get(k, ()):
+            if face == "south" and j0 == 1 or face == "north" and j1 == b.nj:
+                hit = hit or (i0 <= hi and lo <= i1)
+            elif face == "west" and i0 == 1 or face == "east" and i1 == b.ni:
+                hit = hit or (j0 <= hi and lo <= j1)
+        (bound if hit else inner).append(t)
+    layout.tile_order = np.asarray(bound + inner, dtype=np.int32)
+    layout.nbound = len(bound)
+
+    # remote packs first, so the engine can issue them right after the
+    # boundary tiles and the local copies after the interior ones
+    def remote_first(dirs):
+        remote = dirs["dst_kind"] == 1
+        return np.concatenate([dirs[remote], dirs[~remote]]), int(remote.sum())
+
+    layout.prime_dirs, layout.prime_remote = remote_first(layout.prime_dirs)
+    layout.post_dirs, layout.post_remote = remote_first(layout.post_dirs)
 
 
 def fused_eligible(blocks, planes, tile_pdes):
@@ -373,11 +431,16 @@ def _build_routes(layout, topology, plan, rank):
         return layout.elem(gid, 0, 0, j, i), (-step if reversed_ else step), \
             layout.ps[layout.local_index[gid]]
 
+    def sector_dst(gid, face):
+        # a west halo cell is the last of its 32-byte sector (the rest is row
+        # lead), an east one the first when ni % 4 == 0 (the rest padding)
+        return native.HALO_SECTOR_DST if face == "west" or (face == "east" and blocks[gid].ni % 4 == 0) else 0
+
     prime = []
     for d in routes.local:
         s_off, s_es, s_vs = slot_run(d.src_block, d.src_face, d.src_index(0), d.src_reversed, False)
         t_off, t_es, t_vs = slot_run(d.dst_block, d.dst_face, d.dst_index(0), d.dst_reversed, True)
-        prime.append((s_off, s_es, s_vs, t_off, t_es, t_vs, d.length, 0, 0, 0))
+        prime.append((s_off, s_es, s_vs, t_off, t_es, t_vs, d.length, 0, 0, sector_dst(d.dst_block, d.dst_face)))
     for k, d in enumerate(routes.sends):
         s_off, s_es, s_vs = slot_run(d.src_block, d.src_face, d.src_index(0), d.src_reversed, False)
         prime.append((s_off, s_es, s_vs, send_off[k], ds, 1, d.length, 0, 1, 0))
@@ -386,7 +449,7 @@ def _build_routes(layout, topology, plan, rank):
     unpack = []
     for k, d in enumerate(routes.recvs):
         t_off, t_es, t_vs = slot_run(d.dst_block, d.dst_face, d.dst_index(0), d.dst_reversed, True)
-        unpack.append((recv_off[k], ds, 1, t_off, t_es, t_vs, d.length, 2, 0, 0))
+        unpack.append((recv_off[k], ds, 1, t_off, t_es, t_vs, d.length, 2, 0, sector_dst(d.dst_block, d.dst_face)))
     layout.prime_dirs = np.array(prime, dtype=native.HALO_DIR_DTYPE) if prime else \
         np.zeros(0, native.HALO_DIR_DTYPE)
     layout.unpack_dirs = np.array(unpack, dtype=native.HALO_DIR_DTYPE) if unpack else \

@@ -50,7 +50,8 @@ FACE_TARGET_DTYPE = np.dtype([("off", "<i8"), ("ps", "<i8")], align=True)
 HALO_DIR_DTYPE = np.dtype([
     ("src_off", "<i8"), ("src_es", "<i8"), ("src_vs", "<i8"),
     ("dst_off", "<i8"), ("dst_es", "<i8"), ("dst_vs", "<i8"),
-    ("length", "<i4"), ("src_kind", "<i4"), ("dst_kind", "<i4"), ("pad", "<i4")], align=True)
+    ("length", "<i4"), ("src_kind", "<i4"), ("dst_kind", "<i4"), ("flags", "<i4")], align=True)
+HALO_SECTOR_DST = 1
 
 BAND_SEG_DTYPE = np.dtype([
     ("block", "<i4"), ("dir", "<i4"), ("j", "<i4"), ("i", "<i4"), ("len", "<i4"), ("pad", "<i4")])
@@ -79,6 +80,7 @@ class StageArgs(ctypes.Structure):
         ("out_slot", c_i32), ("pair", c_i32), ("coef", c_f64), ("coef2", c_f64),
         ("band_segs", c_vp), ("nband_segs", c_i32), ("band_max_len", c_i32),
         ("edge_q0", c_vp),
+        ("tile_order", c_vp), ("tile_lo", c_i32), ("tile_hi", c_i32),
         ("D", c_f64 * (MAX_TEMPLATED_P * MAX_TEMPLATED_P)),
         ("ap", c_f64 * (MAX_P * NPDE))]
 
@@ -93,6 +95,8 @@ class EngineDesc(ctypes.Structure):
         ("post_dirs", c_vp), ("npost", c_i32), ("post_max_len", c_i32),
         ("band_segs", c_vp), ("nband_segs", c_i32), ("band_max_len", c_i32),
         ("fused", c_i32), ("pad1", c_i32), ("edge_q0", c_vp),
+        ("tile_order", c_vp), ("nbound_tiles", c_i32), ("prime_remote", c_i32), ("post_remote", c_i32),
+        ("pad2", c_i32),
         ("segs", c_vp), ("nsegs", c_i32),
         ("force_hist", c_vp),
         ("sends", ctypes.POINTER(PeerMsg)), ("nsends", c_i32),
@@ -128,6 +132,7 @@ SIGNATURES = {
     "hbgpu_engine_rewind": (c_i32, [c_vp, c_vp]),
     "hbgpu_engine_step": (c_i32, [c_vp, c_i32, c_vp]),
     "hbgpu_engine_unpack": (c_i32, [c_vp, c_i32, c_vp]),
+    "hbgpu_engine_step_split": (c_i32, [c_vp, c_i32, c_i32, c_vp]),
     "hbgpu_engine_destroy": (c_i32, [c_vp]),
     "hbgpu_comm_unique_id": (c_i32, [ctypes.c_char_p]),
     "hbgpu_comm_init": (c_i32, [ctypes.c_char_p, c_i32, c_i32, c_i32, ctypes.POINTER(c_vp)]),

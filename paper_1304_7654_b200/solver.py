@@ -111,7 +111,8 @@ class RunSpec:
     device: int | None = None
     # single process, ranks > 1: "fold" runs all blocks in one engine;
     # "loopback" runs one engine per rank on this GPU with device-copy
-    # transport (exercises the multi-GPU halo path)
+    # transport (exercises the multi-GPU halo path); "loopback-split" does
+    # so with the overlapped boundary / interior schedule of the NCCL engine
     transport: str = "fold"
     # paired RK stages (hb_pair.cu): None = whenever eligible (P <= 17 and
     # every block a whole number of strips wide), False = single stages
@@ -322,6 +323,7 @@ class DeviceRank:
         self.t_tmaps = self.torch.frombuffer(bytearray(host), dtype=self.torch.uint8).to(self.device)
 
     def _make_engine(self):
+        torch = self.torch
         L = self.layout
         d = native.EngineDesc()
         for k in range(3):
@@ -340,6 +342,10 @@ class DeviceRank:
         d.band_segs, d.nband_segs = self.t_band.data_ptr(), len(L.band_segs)
         d.band_max_len, d.fused = int(L.band_max_len), int(L.fused)
         d.edge_q0 = self.edge_q0.data_ptr()
+        # multi-GPU overlap: boundary tiles first, remote packs first
+        self.t_order = torch.from_numpy(np.ascontiguousarray(L.tile_order, dtype=np.int32)).to(self.device)
+        d.tile_order = self.t_order.data_ptr()
+        d.nbound_tiles, d.prime_remote, d.post_remote = int(L.nbound), int(L.prime_remote), int(L.post_remote)
         d.segs, d.nsegs = self.t_segs.data_ptr(), len(L.force_segs)
         d.force_hist = self.force_hist.data_ptr()
         self._sends = (native.PeerMsg * max(1, len(L.sends)))(
@@ -703,7 +709,7 @@ def run_case(spec):
     def execute(sp):
         if world > 1:
             return _execute_distributed(sp, topology, partition, plan, iterations, dist, world, out)
-        if sp.ranks > 1 and sp.transport == "loopback":
+        if sp.ranks > 1 and sp.transport in ("loopback", "loopback-split"):
             return _execute_loopback(sp, topology, partition, plan, iterations, out)
         one = partition_blocks(topology, 1)
         return _execute_single(sp, topology, one, build_cut_plan(topology, one, case.nharms, case.npde),
@@ -1060,6 +1066,28 @@ def _execute_loopback(spec, topology, partition, plan, iterations, out=((), ()))
                     ranks[peer].recvbuf[roff:roff + cnt].copy_(dr.sendbuf[off:off + cnt])
 
         def phase(p, exchange):
+            if split and 0 <= p < 4 and (not ranks[0].fused or p in (1, 3)):
+                # the multi-GPU engine's overlapped schedule (hb_runtime.cu
+                # run_split): boundary tiles + remote packs, then the payload
+                # transfer on a side stream concurrently with the interior
+                # tiles, then the unpack once both are done
+                for dr in ranks:
+                    native.check(lib.hbgpu_engine_step_split(dr.engine, p, 0, dr.stream()),
+                                 "hbgpu_engine_step_split")
+                fork = torch.cuda.Event()
+                fork.record()
+                with torch.cuda.stream(side):
+                    side.wait_event(fork)
+                    transport()
+                join = torch.cuda.Event()
+                join.record(side)
+                for dr in ranks:
+                    native.check(lib.hbgpu_engine_step_split(dr.engine, p, 1, dr.stream()),
+                                 "hbgpu_engine_step_split")
+                torch.cuda.current_stream().wait_event(join)
+                for dr in ranks:
+                    native.check(lib.hbgpu_engine_unpack(dr.engine, p, dr.stream()), "hbgpu_engine_unpack")
+                return
             for dr in ranks:
                 native.check(lib.hbgpu_engine_step(dr.engine, p, dr.stream()), "hbgpu_engine_step")
             if exchange:
@@ -1067,6 +1095,10 @@ def _execute_loopback(spec, topology, partition, plan, iterations, out=((), ()))
                 for dr in ranks:
                     native.check(lib.hbgpu_engine_unpack(dr.engine, p, dr.stream()), "hbgpu_engine_unpack")
 
+        # spec.transport "loopback-split": every pass phase as the overlapped
+        # boundary / transfer + interior / unpack schedule of the NCCL engine
+        split = spec.transport == "loopback-split"
+        side = torch.cuda.Stream(device)
         torch.cuda.synchronize(device)
         t0 = time.perf_counter()
         phase(-1, True)

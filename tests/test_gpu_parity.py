@@ -116,15 +116,19 @@ LOOPBACK = {
 }
 
 
+@pytest.mark.parametrize("transport", ["loopback", "loopback-split"])
 @pytest.mark.parametrize("name", sorted(LOOPBACK))
-def test_loopback_multirank_matches_oracle(name, cuda, oracle_mod):
+def test_loopback_multirank_matches_oracle(name, transport, cuda, oracle_mod):
     """Several ranks' engines on one GPU: remote cuts go through the fused
     pack, per-peer segments and unpack of the multi-GPU path, with device
-    copies standing in for NCCL; the force history is folded in rank order."""
+    copies standing in for NCCL; the force history is folded in rank order.
+    "loopback-split" runs every pass as the NCCL engine's overlapped
+    schedule: boundary tiles + remote packs, then the transfer on a side
+    stream concurrently with the interior tiles, then the unpack."""
     build, ranks, iters = LOOPBACK[name]
     case = build()
     initial = baseline_workload("C1").initial if name.startswith("C1") else None
-    got = run_case(RunSpec(case=case, ranks=ranks, iterations=iters, transport="loopback",
+    got = run_case(RunSpec(case=case, ranks=ranks, iterations=iters, transport=transport,
                            initial=initial))
     want = oracle_mod.run(case, iters, initial=initial)
     assert_parity(got, want, name)
@@ -171,6 +175,10 @@ FUSED = {
                      3, 9, 1, "fold"),
     "lattice-256-loopback4": (lambda: lattice_case(2, 2, 256, 24, 2, h=0.01, dtau=0.0002, nbody=1,
                                                    bodies=((3, "north", 0),)), 3, 8, 4, "loopback"),
+    "lattice-256-split4": (lambda: lattice_case(2, 2, 256, 24, 2, h=0.01, dtau=0.0002, nbody=1,
+                                                bodies=((3, "north", 0),)), 3, 8, 4, "loopback-split"),
+    "lattice-3x2-split2": (lambda: lattice_case(3, 2, 256, 40, 4, h=0.01, dtau=0.0002, nbody=1,
+                                                bodies=((4, "north", 0),)), 2, 8, 2, "loopback-split"),
     "C1-loopback2": (lambda: baseline_workload("C1").case, 2, None, 2, "loopback"),
     "nj1-p1": (lambda: CaseConfig(nharms=0, npde=4, iterations=4, dtau=0.001, omega=1.0, nbody=1,
                                   blocks=[BlockSpec(0, 512, 1, 0.0, 0.0, 0.01, body_faces=(("north", 0),))],
