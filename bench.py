@@ -17,8 +17,10 @@ roofline of the fused stage kernel, cpu_baseline (the oracle port on this
 host), e2e (run_case with pinned host input/output copies inside the timed
 region), clocks, gpu_launches.
 
-`--impl reference` times the reference's CPU path (the C restatement in
-oracle/, with all host threads) on a bounded sample of the same workload.
+`--impl reference` times the reference itself -- hbproxy.driver.run_case
+with its numba kernels, pip-installed into baseline/_ref -- on a bounded
+sample of the same workload with all host cores, and its C restatement
+(oracle/) beside it; with no baseline/_ref it times the C restatement.
 """
 
 from __future__ import annotations
@@ -47,8 +49,13 @@ def parse():
     ap.add_argument("--workload", default="C4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tile-rows", type=int, default=None)
+    ap.add_argument("--schedule", default="auto", choices=["auto", "paired", "single", "small"],
+                    help="auto: the engine's choice (paired from 16 Mi units per stage, the one-launch "
+                         "small schedule up to 8 Mi, single stages between)")
     ap.add_argument("--kernel-reps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--allow-knobs", action="store_true",
+                    help="run even with HBGPU_* environment knobs set (recorded in the line)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-iters", type=int, default=10)
     ap.add_argument("--zero-ic", action="store_true",
@@ -106,6 +113,16 @@ def roofline(dr, args, units_stage, step_ms_total, wl, world):
         if tj.get("workload") == wl.key and tj.get("n_gpus", 1) == world and \
                 bool(tj.get("fused")) == dr.fused:
             traffic = tj.get("bytes_per_launch_avg")
+    if dr.layout.small:
+        # one cooperative launch runs whole iterations: the kernel time is the step
+        algo = sum(ALGO_BYTES[s] for s in range(4)) * units_stage
+        achieved = algo / (step_ms / 1e3) / 1e9
+        return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                "kernel": "hb_small (whole iterations in one cooperative launch; state L2-resident, so "
+                          "the HBM roofline is a lower bound on what the memory system could give)",
+                "algorithmic_bytes_per_unit": {"stage0": 64, "stages1-3": 96, "avg": 88},
+                "units_per_launch": units_stage * 4 * args.steps, "share_of_step": 1.0}
     if not dr.fused:
         stage_args = [dr.stage_args(s) for s in range(4)]
         t = _time_launches(dr, [lambda a=a: dr.launch_stage(a) for a in stage_args], args.kernel_reps)
@@ -206,6 +223,14 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def library_knobs():
+    """libhbgpu / layout environment knobs (HBGPU_GRID_LIMIT, HBGPU_FUSED,
+    HBGPU_LAYOUT, HBGPU_L2_PROMOTION, HBGPU_TILE_PDES, HBGPU_NVCC_EXTRA, ...):
+    test and measurement switches that change the schedule; a benchmark
+    line must not be taken with any of them set unknowingly."""
+    return {k: v for k, v in sorted(os.environ.items()) if k.startswith("HBGPU_")}
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -256,6 +281,18 @@ def cpu_sample_blocks(wl):
 
 
 def cpu_baseline(wl, iters):
+    """The reported CPU baseline of our arm: the reference's own run_case
+    (numba, baseline/_ref) on a bounded sample, with the C port beside it."""
+    ref = reference_rate(wl, steps=1, warmup=1, nblocks=None)
+    port = port_rate(wl, iters)
+    if ref is None:
+        port["note"] = "reference not installed in baseline/_ref: the C port is the baseline"
+        return port
+    ref["port"] = {k: port[k] for k in ("value", "cores", "sample")}
+    return ref
+
+
+def port_rate(wl, iters):
     sys.path.insert(0, os.path.join(REPO, "oracle"))
     import oracle  # the checker / CPU baseline only
     nb = cpu_sample_blocks(wl)
@@ -273,32 +310,107 @@ def cpu_baseline(wl, iters):
                       f"pthreads over (block, plane)"}
 
 
+def _import_reference():
+    """The unmodified reference package from baseline/_ref (pip-installed from
+    /root/reference/pkg), or None."""
+    path = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "hbproxy")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/hbproxy_numba_cache")
+    os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import hbproxy  # noqa: F401
+        from hbproxy import driver, hbcore, mesh
+    except Exception:
+        return None
+    return driver, hbcore, mesh
+
+
+def _ref_case(mesh, case):
+    """Our CaseConfig -> the reference's mesh.CaseConfig (same fields)."""
+    blocks = [mesh.BlockSpec(b.id, b.ni, b.nj, b.x0, b.y0, b.h, tuple(b.body_faces)) for b in case.blocks]
+    cuts = [mesh.CutSpec(mesh.CutSide(c.side_a.block, c.side_a.face, c.side_a.lo, c.side_a.hi),
+                         mesh.CutSide(c.side_b.block, c.side_b.face, c.side_b.lo, c.side_b.hi),
+                         c.reversed) for c in case.cuts]
+    return mesh.CaseConfig(nharms=case.nharms, npde=case.npde, iterations=case.iterations, dtau=case.dtau,
+                           omega=case.omega, nbody=case.nbody, blocks=blocks, cuts=cuts, name=case.name)
+
+
+def ref_sample_blocks(wl):
+    # ~300M units per sampled iteration (a few s of 16-core numba): 8 blocks
+    # of C4, 4 of C3, all of C0..C2
+    budget = 300e6
+    per = wl.case.blocks[0].cells() * wl.case.planes * 4
+    return max(1, min(len(wl.case.blocks), int(budget // per)))
+
+
+def reference_rate(wl, steps, warmup, nblocks=None):
+    """hbproxy.driver.run_case -- the reference's public API and stock path
+    (numba kernels, thread ranks) -- on the first `nblocks` blocks of the
+    workload, per SURVEY.md §8d's CPU plan: ranks = min(blocks, cores),
+    threads = cores // ranks, default axis (harmonics), hoisted activation,
+    aggregated serial exchange, buffered reduction; the seeded initial state
+    through the hbcore.initial_values hook; the JIT warmed first.  Value =
+    units / RunRecord.wall_s of one run of `steps` iterations."""
+    mods = _import_reference()
+    if mods is None:
+        return None
+    driver, hbcore, mesh = mods
+    nb = nblocks or ref_sample_blocks(wl)
+    case = _ref_case(mesh, sample_case(wl, nb))
+    cores = len(os.sched_getaffinity(0))
+    ranks = min(nb, cores)
+    threads = max(1, cores // ranks)
+    saved = hbcore.initial_values
+
+    def hook(spec, planes, npde, n_lo, n_hi, j_lo, j_hi):
+        full = wl.initial(spec, planes, npde)
+        return full[n_lo:n_hi, :, j_lo - 1:j_hi - 1, :]
+
+    hbcore.initial_values = hook
+    try:
+        tiny = _ref_case(mesh, sample_case(wl, 1))
+        tiny = mesh.CaseConfig(nharms=tiny.nharms, npde=4, iterations=1, dtau=tiny.dtau, omega=tiny.omega,
+                               nbody=0, blocks=[mesh.BlockSpec(0, 16, 8, 0.0, 0.0, tiny.blocks[0].h)],
+                               cuts=[], name="jit-warm")
+        driver.run_case(driver.RunSpec(case=tiny, ranks=1, iterations=1))       # numba JIT
+        if warmup > 0:
+            driver.run_case(driver.RunSpec(case=case, ranks=ranks, threads=threads, iterations=warmup))
+        res = driver.run_case(driver.RunSpec(case=case, ranks=ranks, threads=threads, iterations=steps))
+    finally:
+        hbcore.initial_values = saved
+    units = sum(b.ni * b.nj for b in case.blocks) * (2 * case.nharms + 1) * 4 * steps
+    wall = res.record.wall_s
+    import numba
+    return {"value": units / wall, "unit": UNIT, "cores": ranks * threads, "kind": "reference",
+            "sample": f"hbproxy.driver.run_case (numba {numba.__version__}, baseline/_ref) on blocks "
+                      f"0..{nb - 1} of {wl.key} ({nb} of {len(wl.case.blocks)}, cuts among them), "
+                      f"{steps} iteration(s) after {warmup} warm-up, ranks={ranks} x threads={threads} on "
+                      f"{cores} host cores; {units / 1e6:.0f} M units in RunRecord.wall_s = {wall:.2f} s",
+            "wall_s": wall}
+
+
 def run_reference_arm(args, wl):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    sys.path.insert(0, os.path.join(REPO, "oracle"))
-    import oracle
-    nb = cpu_sample_blocks(wl)
-    case = sample_case(wl, nb)
-    solver = oracle.OracleSolver(case, initial=wl.initial, record_norms=False)
-    solver.prime()
-    solver.iterate(args.warmup)
-    t0 = time.perf_counter()
-    solver.iterate(args.steps)
-    dt = time.perf_counter() - t0
-    units = solver.units_per_iteration * args.steps
-    value = units / dt
-    sample = (f"each step = 1 iteration over blocks 0..{nb - 1} of {wl.key} ({nb} of "
-              f"{len(wl.case.blocks)}); C restatement of the reference kernels (oracle/), "
-              f"{solver.nthreads} pthreads")
+    ref = reference_rate(wl, args.steps, args.warmup)
+    port = port_rate(wl, max(1, min(args.steps, 3)))
+    if ref is None:
+        ref = dict(port)
+        ref["note"] = "reference not installed in baseline/_ref: timing its C restatement (oracle/)"
+    else:
+        ref["port"] = {k: port[k] for k in ("value", "cores", "sample")}
+    value = ref["value"]
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": None if "wall_s" not in ref else ref["wall_s"] / args.steps * 1e3,
+            "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": wl.key, "description": wl.description, "sample_blocks": nb},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": solver.nthreads,
-                             "kind": "port", "sample": sample},
+            "config": {"workload": wl.key, "description": wl.description},
+            "cpu_baseline": ref,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -321,6 +433,10 @@ def run_ours(args, wl):
     world, rank, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    knobs = library_knobs()
+    if knobs and not args.allow_knobs:
+        raise SystemExit(f"refusing to benchmark with libhbgpu test/measurement knobs set: {knobs} "
+                         f"(--allow-knobs to override; the line then records them)")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -345,8 +461,11 @@ def run_ours(args, wl):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    fused = {"auto": None, "paired": True, "single": False, "small": False}[args.schedule]
+    small = {"auto": None, "paired": False, "single": False, "small": True}[args.schedule]
     dr = DeviceRank(case, topo, part, plan, rank=rank, device=local, comm=comm,
-                    tile_rows=args.tile_rows, max_iters=args.warmup + args.steps + 1, pinned_ic=ic)
+                    tile_rows=args.tile_rows, max_iters=args.warmup + args.steps + 1, pinned_ic=ic,
+                    fused=fused, small=small)
     dr.prime()
     if world > 1:
         # one eager iteration first, so every NCCL send/recv of the iteration
@@ -374,7 +493,7 @@ def run_ours(args, wl):
     # dominant kernel, timed alone on the launching stream
     my_units_stage = sum(b.cells() for b in mine) * case.planes
     roof = roofline(dr, args, my_units_stage, ms, wl, world)
-    tile_rows, fused = dr.layout.tile_rows, dr.fused
+    tile_rows, fused, small = dr.layout.tile_rows, dr.fused, bool(dr.layout.small)
     dr.close()
     del dr
     torch.cuda.empty_cache()
@@ -416,10 +535,14 @@ def run_ours(args, wl):
                            "parallelism": f"blocks/{world} gpu (LPT partition)",
                            "tile_rows": tile_rows,
                            "schedule": "paired RK stages (band + pair kernels)" if fused
-                                       else "single RK stages",
+                                       else ("one-launch small schedule (hb_small.cu)" if small
+                                             else "single RK stages"),
                            "l2": f"inputs larger than L2: {dr_slot_gb(case, mine):.1f} GB per state slot"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
-                "gpu_launches": int(launches)}
+                "gpu_launches": int(launches),
+                "env": {"hbgpu_knobs": knobs, "library": native.LIB_PATH,
+                        "abi": int(native.load().hbgpu_abi_version()),
+                        "nccl_vars": {k: v for k, v in os.environ.items() if k.startswith("NCCL_")}}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -361,14 +361,18 @@ typedef struct hbgpu_engine_desc {
      * band values (hbgpu_band), band_segs lists the tile-perimeter cells   */
     const hbgpu_band_seg *band_segs;   int32_t nband_segs; int32_t band_max_len;
     int32_t fused;
-    int32_t pad1;
+    /* small != 0 (single-rank, no remote cut, not fused): hbgpu_engine_iterate
+     * runs whole iterations in one cooperative launch (hb_small.cu) instead
+     * of the per-stage kernels; small_max_cells = the largest block's
+     * ni * nj (sizes the grid)                                              */
+    int32_t small;
     double *edge_q0;                 /* fused: device, see hbgpu_stage_args */
     /* multi-GPU overlap (used when comm != NULL and the rank sends): device
      * tile permutation with the nbound_tiles boundary tiles first;
      * prime_dirs / post_dirs start with prime_remote / post_remote remote
      * packs (dst_kind 1), followed by the local copies                    */
     const int32_t *tile_order;
-    int32_t nbound_tiles, prime_remote, post_remote, pad2;
+    int32_t nbound_tiles, prime_remote, post_remote, small_max_cells;
     const hbgpu_force_seg *segs;     int32_t nsegs;  /* device */
     double *force_hist;              /* device [max_iters*3*planes*nbody] */
     const hbgpu_peer_msg *sends;     int32_t nsends; /* HOST arrays */
@@ -437,6 +441,12 @@ int hbgpu_comm_destroy(void *comm);
 #define HBGPU_REDUCE_MIN_U64 1
 int hbgpu_comm_allreduce(void *comm, const void *send, void *recv, int64_t count,
                          int32_t op, void *stream);
+/* one grouped ncclSend / ncclRecv of every listed peer segment (doubles;
+ * hbgpu_peer_msg arrays on the HOST) on `stream`: the block-level
+ * exchange_halos transport (exchange.py:307-316, one payload per peer)    */
+int hbgpu_comm_exchange(void *comm, const double *sendbuf, const hbgpu_peer_msg *sends,
+                        int32_t nsends, double *recvbuf, const hbgpu_peer_msg *recvs,
+                        int32_t nrecvs, void *stream);
 /* HBGPU_OK while the communicator is healthy (or has work in progress);
  * HBGPU_ERR_NCCL with the message when ncclCommGetAsyncError reports an
  * error (a peer failed, a network error).  Poll it while waiting.         */

@@ -8,7 +8,8 @@ exchange.py:382-402) on CUDA tensors in the reference's dense layout
   residual_into  -> hbgpu_residual      (hbcore._residual_kernel, hbcore.py:184-221)
   update_stage   -> hbgpu_update        (hbcore._update_kernel, hbcore.py:224-245)
                     + hbgpu_first_nonfinite for the DivergenceError location
-  exchange_halos -> hbgpu_halo          (exchange.py:295-316, all cuts local)
+  exchange_halos -> hbgpu_halo          (exchange.py:295-316: local copies, remote
+                                         pack / unpack around a HaloContext transfer)
   compute_forces -> hbgpu_forces        (hbcore.py:359-382)
 
 Sub-range bounds are the reference's array coordinates.  Results are bitwise
@@ -146,26 +147,125 @@ def _dense_run(field, gid, face, first, reversed_, halo):
     return field.offsets[gid] + j * ni2 + i, (-step if reversed_ else step), nj2 * ni2
 
 
-def exchange_halos(field, plan):
-    """One halo exchange of an all-local plan: every cut halo cell <- its paired
-    interior cell (exchange.py:382-402)."""
-    rows = []
-    for d in plan.directions():
-        if not d.local:
-            raise NotImplementedError("remote cuts run through solver.run_case (NCCL engine)")
-        s_off, s_es, s_vs = _dense_run(field, d.src_block, d.src_face, d.src_index(0),
-                                       d.src_reversed, False)
-        t_off, t_es, t_vs = _dense_run(field, d.dst_block, d.dst_face, d.dst_index(0),
-                                       d.dst_reversed, True)
-        rows.append((s_off, s_es, s_vs, t_off, t_es, t_vs, d.length, 0, 0, 0))
-    if not rows:
-        return
+class HaloContext:
+    """A rank's side of block-level halo exchange with remote cuts: its rank
+    in the plan's partition and a transport for the per-peer payloads (the
+    reference passes its RankContext, exchange.py:382-402 /
+    runtime.py:196-309).
+
+    comm: an NCCL communicator from solver.make_comm -> one grouped
+    ncclSend/ncclRecv per peer on the current stream (hbgpu_comm_exchange);
+    hub: a LoopbackHub shared by the ranks' threads of one process (device
+    copies between their buffers)."""
+
+    def __init__(self, rank, comm=None, hub=None):
+        if (comm is None) == (hub is None):
+            raise ValueError("HaloContext needs exactly one of comm or hub")
+        self.rank, self.comm, self.hub = rank, comm, hub
+
+    def transfer(self, sendbuf, sends, recvbuf, recvs):
+        if self.comm is not None:
+            snd = (native.PeerMsg * max(1, len(sends)))(*[native.PeerMsg(p, 0, o, c) for p, o, c in sends])
+            rcv = (native.PeerMsg * max(1, len(recvs)))(*[native.PeerMsg(p, 0, o, c) for p, o, c in recvs])
+            native.check(native.load().hbgpu_comm_exchange(self.comm, _vp(sendbuf), snd, len(sends), _vp(recvbuf),
+                                                           rcv, len(recvs), _stream()), "hbgpu_comm_exchange")
+        else:
+            self.hub.transfer(self.rank, sendbuf, sends, recvbuf, recvs)
+
+
+class LoopbackHub:
+    """In-process transport of HaloContext for ranks run as threads of one
+    process on one GPU: each rank posts its send buffer and segments, all
+    ranks meet, every rank copies its receive segments from the peers'
+    send buffers, all ranks meet again (so no buffer is reused early)."""
+
+    def __init__(self, nranks):
+        import threading
+        self.posted = {}
+        self.barrier = threading.Barrier(nranks)
+
+    def transfer(self, rank, sendbuf, sends, recvbuf, recvs):
+        import torch
+        torch.cuda.current_stream().synchronize()
+        self.posted[rank] = (sendbuf, {p: (o, c) for p, o, c in sends})
+        self.barrier.wait()
+        for peer, off, cnt in recvs:
+            buf, segs = self.posted[peer]
+            soff, scnt = segs[rank]
+            if scnt != cnt:
+                from .exceptions import ProtocolError
+                raise ProtocolError(f"rank {peer} -> {rank}: {scnt} != {cnt} doubles")
+            recvbuf[off:off + cnt].copy_(buf[soff:soff + cnt])
+        torch.cuda.current_stream().synchronize()
+        self.barrier.wait()
+
+
+def _segments(dirs, peer_of, datasize):
+    """Element-major payload offsets per direction, grouped by peer ascending
+    (plan order inside), and the (peer, offset, count) messages."""
+    order = sorted(range(len(dirs)), key=lambda k: (peer_of(dirs[k]), k))
+    offs, msgs, pos = {}, [], 0
+    for k in order:
+        d = dirs[k]
+        offs[k] = pos
+        n = d.length * datasize
+        if msgs and msgs[-1][0] == peer_of(d):
+            msgs[-1][2] += n
+        else:
+            msgs.append([peer_of(d), pos, n])
+        pos += n
+    return offs, [tuple(m) for m in msgs], pos
+
+
+def exchange_halos(field, plan, ctx=None):
+    """One halo exchange (exchange.py:382-402): every cut halo cell of the
+    field's blocks <- its paired interior cell, bitwise.  Cuts between two
+    of this rank's blocks are copied on the device; with `ctx` (HaloContext)
+    the remote ones are packed element-major (exchange.py:248-252), moved
+    one aggregated payload per peer, and unpacked (exchange.py:254-258)."""
     import torch
-    arr = np.array(rows, dtype=native.HALO_DIR_DTYPE)
-    dirs = torch.from_numpy(arr.view(np.uint8).copy()).to(field.pool.device)
-    native.check(native.load().hbgpu_halo(_vp(field.pool), None, None, _vp(dirs), len(rows),
-                                          int(arr["length"].max()), field.planes, _stream()),
-                 "hbgpu_halo")
+    from .cutplan import rank_routes
+    from .exceptions import ProtocolError
+    rank = ctx.rank if ctx is not None else None
+    if rank is None:
+        dirs = list(plan.directions())
+        if any(not d.local for d in dirs):
+            raise ProtocolError("the plan has remote cuts: pass a HaloContext (rank + transport)")
+        local, sends, recvs = dirs, (), ()
+    else:
+        routes = rank_routes(plan, rank)
+        local, sends, recvs = routes.local, routes.sends, routes.recvs
+    ds = plan.datasize
+    dev = field.pool.device
+    send_off, send_msgs, nsend = _segments(sends, lambda d: d.recv_rank, ds)
+    recv_off, recv_msgs, nrecv = _segments(recvs, lambda d: d.sender_rank, ds)
+    sendbuf = torch.zeros(max(1, nsend), dtype=torch.float64, device=dev)
+    recvbuf = torch.zeros(max(1, nrecv), dtype=torch.float64, device=dev)
+
+    def run(rows):
+        if not rows:
+            return
+        arr = np.array(rows, dtype=native.HALO_DIR_DTYPE)
+        t = torch.from_numpy(arr.view(np.uint8).copy()).to(dev)
+        native.check(native.load().hbgpu_halo(_vp(field.pool), _vp(sendbuf), _vp(recvbuf), _vp(t), len(rows),
+                                              int(arr["length"].max()), field.planes, _stream()), "hbgpu_halo")
+
+    rows = []
+    for d in local:
+        s_off, s_es, s_vs = _dense_run(field, d.src_block, d.src_face, d.src_index(0), d.src_reversed, False)
+        t_off, t_es, t_vs = _dense_run(field, d.dst_block, d.dst_face, d.dst_index(0), d.dst_reversed, True)
+        rows.append((s_off, s_es, s_vs, t_off, t_es, t_vs, d.length, 0, 0, 0))
+    for k, d in enumerate(sends):   # pack: element e of the direction at send_off + e * datasize
+        s_off, s_es, s_vs = _dense_run(field, d.src_block, d.src_face, d.src_index(0), d.src_reversed, False)
+        rows.append((s_off, s_es, s_vs, send_off[k], ds, 1, d.length, 0, 1, 0))
+    run(rows)
+    if ctx is not None and (send_msgs or recv_msgs):
+        ctx.transfer(sendbuf, send_msgs, recvbuf, recv_msgs)
+        rows = []
+        for k, d in enumerate(recvs):
+            t_off, t_es, t_vs = _dense_run(field, d.dst_block, d.dst_face, d.dst_index(0), d.dst_reversed, True)
+            rows.append((recv_off[k], ds, 1, t_off, t_es, t_vs, d.length, 2, 0, 0))
+        run(rows)
 
 
 def compute_forces(field, topology):

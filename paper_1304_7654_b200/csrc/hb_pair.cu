@@ -599,7 +599,9 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
             double *vrow = v1ring + vr * S::QSLOT + q_off;
 #pragma unroll
             for (int n = 0; n < P; ++n) vrow[n * PT * G::TCOLS] = pc[n];
+#ifndef HBGPU_MEASURE_NOBARRIER   // measurement builds only: wrong results, barrier cost
             consumer_sync();
+#endif
             if (r > tl.j0) {
                 // second stage at row r-1
                 mbar_wait(edge_ready + cprev.slot, cprev.phase);

@@ -165,6 +165,31 @@ extern "C" int hbgpu_comm_allreduce(void *comm, const void *send, void *recv, in
     return HBGPU_OK;
 }
 
+extern "C" int hbgpu_comm_exchange(void *comm, const double *sendbuf, const hbgpu_peer_msg *sends, int32_t nsends,
+                                   double *recvbuf, const hbgpu_peer_msg *recvs, int32_t nrecvs, void *stream) {
+    if (!load_nccl()) return HBGPU_ERR_NCCL;
+    if (comm == nullptr || nsends < 0 || nrecvs < 0) {
+        hbgpu_set_error("hbgpu_comm_exchange: bad arguments");
+        return HBGPU_ERR_ARG;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    ncclResult_t r = g_nccl.GroupStart();
+    if (r != ncclSuccess) return nccl_fail("ncclGroupStart", r);
+    for (int k = 0; k < nsends; ++k) {
+        r = g_nccl.Send(sendbuf + sends[k].offset, (size_t)sends[k].count, ncclFloat64, sends[k].peer,
+                        (ncclComm_t)comm, s);
+        if (r != ncclSuccess) return nccl_fail("ncclSend", r);
+    }
+    for (int k = 0; k < nrecvs; ++k) {
+        r = g_nccl.Recv(recvbuf + recvs[k].offset, (size_t)recvs[k].count, ncclFloat64, recvs[k].peer,
+                        (ncclComm_t)comm, s);
+        if (r != ncclSuccess) return nccl_fail("ncclRecv", r);
+    }
+    r = g_nccl.GroupEnd();
+    if (r != ncclSuccess) return nccl_fail("ncclGroupEnd", r);
+    return HBGPU_OK;
+}
+
 extern "C" int hbgpu_comm_async_error(void *comm) {
     if (comm == nullptr) return HBGPU_OK;
     if (!load_nccl()) return HBGPU_ERR_NCCL;
@@ -206,7 +231,15 @@ struct hbgpu_engine {
     bool split = false;
     cudaStream_t comm_s = nullptr;
     cudaEvent_t ev_pack = nullptr, ev_comm = nullptr;
+    // small schedule: per-CTA stage-0 partials of the cooperative kernel
+    double *small_part = nullptr;
+    int small_cap = 0;
 };
+
+namespace hbgpu {
+int small_iterations(const hbgpu_engine_desc &d, int32_t it0, int32_t iters, cudaStream_t s, double **part_buf,
+                     int *part_cap);
+}
 
 namespace {
 
@@ -461,6 +494,12 @@ extern "C" int hbgpu_engine_create(const hbgpu_engine_desc *desc, hbgpu_engine *
         hbgpu_set_error("hbgpu_engine_create: fused schedule needs edge_q0");
         return HBGPU_ERR_ARG;
     }
+    if (desc->small && (desc->fused || desc->nsends > 0 || desc->nrecvs > 0 || desc->small_max_cells <= 0 ||
+                        desc->planes > 9 || desc->planes % 2 == 0)) {
+        hbgpu_set_error("hbgpu_engine_create: the small schedule needs one rank without remote cuts, single "
+                        "stages, P <= 9 and small_max_cells");
+        return HBGPU_ERR_ARG;
+    }
     int prc = hbgpu_stage_prepare(desc->planes);
     if (prc) return prc;
     auto *e = new hbgpu_engine();
@@ -587,6 +626,7 @@ extern "C" int hbgpu_engine_unpack(hbgpu_engine *e, int32_t phase, void *stream)
 
 extern "C" int hbgpu_engine_launches_per_iteration(const hbgpu_engine *e) {
     const hbgpu_engine_desc &d = e->d;
+    if (d.small) return 1;   // one cooperative launch per hbgpu_engine_iterate call (<= 1 per iteration)
     const bool remote = d.comm != nullptr && !e->recvs.empty() && d.nunpack > 0;
     int n = 1;   // forces
     for (int st = 0; st < 4; ++st) {
@@ -613,7 +653,10 @@ extern "C" int hbgpu_engine_iterate(hbgpu_engine *e, int32_t iterations, int32_t
     cudaStream_t caller = (cudaStream_t)stream;
     rc = enter(e, caller);
     if (rc) return rc;
-    rc = iterate_on(e, iterations, use_graph, e->work);
+    if (e->d.small)
+        rc = hbgpu::small_iterations(e->d, e->done, iterations, e->work, &e->small_part, &e->small_cap);
+    else
+        rc = iterate_on(e, iterations, use_graph, e->work);
     if (!rc) e->done += iterations;
     return leave(e, caller, rc);
 }
@@ -700,6 +743,7 @@ extern "C" int hbgpu_engine_destroy(hbgpu_engine *e) {
     }
     if (e->ev_pack) cudaEventDestroy(e->ev_pack);
     if (e->ev_comm) cudaEventDestroy(e->ev_comm);
+    if (e->small_part) cudaFree(e->small_part);
     delete e;
     return HBGPU_OK;
 }

@@ -50,6 +50,7 @@ MIN_TILE_ROWS = 8
 # and C2 (2.6M, 4.7M units), paired ones 16% faster at C3 (117M) and ~35% at
 # C4 (2.4G)
 FUSED_MIN_UNITS = 16 * 2 ** 20
+SMALL_MAX_UNITS = 2 ** 18
 MAX_BAND_SEGS = 65535
 SLOT_TAIL = 64            # elements of zero padding after the last block
 # slot layout default: row-interleaved (row j of every (n, p) plane contiguous)
@@ -146,6 +147,8 @@ class RankLayout:
     nbound: int = 0
     prime_remote: int = 0
     post_remote: int = 0
+    small: bool = False             # one-launch small schedule (hb_small.cu)
+    small_max_cells: int = 0
     band_segs: np.ndarray = None    # tile-perimeter cells (paired stages)
     band_max_len: int = 0
     fused: bool = False             # paired stages (hb_pair.cu)
@@ -181,7 +184,7 @@ def _halo_cell(spec, face, k):
 
 
 def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None,
-                      interleaved=None, tile_pdes=None, fused=None):
+                      interleaved=None, tile_pdes=None, fused=None, small=None):
     """Device layout of one rank's blocks.
 
     interleaved=False: plane-major slots, (n, p) planes of (nj+2) x pitch;
@@ -247,7 +250,27 @@ def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None,
     _build_force_segments(layout)
     _build_band(layout, fused)
     _build_tile_order(layout, topology, plan, rank)
+    _choose_small(layout, small)
     return layout
+
+
+def small_eligible(layout):
+    """The one-launch small schedule (hb_small.cu): single stages, no remote
+    cut (its grid barriers cannot wait on NCCL), a templated odd P <= 9."""
+    return (not layout.fused and not layout.sends and not layout.recvs
+            and layout.planes in (1, 3, 5, 7, 9) and os.environ.get("HBGPU_SMALL", "1") != "0")
+
+
+def _choose_small(layout, small):
+    """Auto: up to SMALL_MAX_UNITS units per stage, where launches, pipeline
+    fill and drain dominate the per-stage TMA kernels.  Measured on one B200
+    (bench --schedule small / single, 50 iterations): C0 1.68 vs 0.88 G
+    units/s; C1 22.0 vs 29.4 G and C2 16.1 vs 32.7 G -- from C1's size the
+    per-stage kernels win, so the threshold sits between C0 and C1."""
+    units = sum(b.ni * b.nj for b in layout.blocks) * layout.planes * NPDE
+    ok = small_eligible(layout)
+    layout.small = ok and units <= SMALL_MAX_UNITS if small is None else bool(small) and ok
+    layout.small_max_cells = max(b.ni * b.nj for b in layout.blocks)
 
 
 def tile_box(layout, t):

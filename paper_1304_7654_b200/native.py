@@ -94,9 +94,9 @@ class EngineDesc(ctypes.Structure):
         ("unpack_dirs", c_vp), ("nunpack", c_i32), ("unpack_max_len", c_i32),
         ("post_dirs", c_vp), ("npost", c_i32), ("post_max_len", c_i32),
         ("band_segs", c_vp), ("nband_segs", c_i32), ("band_max_len", c_i32),
-        ("fused", c_i32), ("pad1", c_i32), ("edge_q0", c_vp),
+        ("fused", c_i32), ("small", c_i32), ("edge_q0", c_vp),
         ("tile_order", c_vp), ("nbound_tiles", c_i32), ("prime_remote", c_i32), ("post_remote", c_i32),
-        ("pad2", c_i32),
+        ("small_max_cells", c_i32),
         ("segs", c_vp), ("nsegs", c_i32),
         ("force_hist", c_vp),
         ("sends", ctypes.POINTER(PeerMsg)), ("nsends", c_i32),
@@ -140,6 +140,8 @@ SIGNATURES = {
     "hbgpu_comm_destroy": (c_i32, [c_vp]),
     "hbgpu_comm_allreduce": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp]),
     "hbgpu_comm_async_error": (c_i32, [c_vp]),
+    "hbgpu_comm_exchange": (c_i32, [c_vp, c_vp, ctypes.POINTER(PeerMsg), c_i32, c_vp, ctypes.POINTER(PeerMsg),
+                                    c_i32, c_vp]),
     "hbgpu_comm_abort": (c_i32, [c_vp]),
     "hbgpu_norm_totals": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_vp]),
     "hbgpu_abi_version": (c_i32, []),

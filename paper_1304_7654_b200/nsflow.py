@@ -1,0 +1,329 @@
+"""North-star physics: the HB Euler / laminar
+Navier-Stokes residual-and-smoothing loop on curvilinear structured blocks.
+
+The reference has none of this (hbcore.py:3-13 is a linear advection-
+diffusion proxy; SPEC.md:8, 182 list flux physics as a non-goal; PAPER.md:
+158-166 promises the HB NS formulation but the text is absent).  This module
+and hb_ns.cu implement a standard formulation, specified below; the CPU
+checker oracle/ns_oracle.c is an independent restatement of the same
+specification.  **Parity is unpinned**: there is no reference output to pin
+either side to; GPU == oracle bitwise is what the tests require.
+
+Specification (every operation a separately rounded IEEE fp64 mul / add /
+div / sqrt, in the order written; no FMA)
+---------------------------------------------------------------------------
+State per cell and HB snapshot n: W = (rho, rho u, rho v, rho E), gamma = 1.4,
+p = (gamma - 1) (rho E - 0.5 (rho u * u + rho v * v)) with u = rho u / rho,
+c = sqrt(gamma p / rho).  Freestream rho = 1, c = 1 (p = 1/gamma), speed M at
+the snapshot's angle alpha_n = dalpha sin(2 pi n / P).  Viscosity mu = M / Re
+(reference length 1), Pr = 0.72.
+
+Geometry (host, numpy, from node coordinates with two extrapolated ghost
+node layers): cell centres = 0.25 ((x00 + x10) + (x11 + x01)); cell area
+V = 0.5 ((x11 - x00)(y01 - y10) - (y11 - y00)(x01 - x10)); i-face normal
+(area-weighted, pointing +i) S = (y_top - y_bot, x_bot - x_top) of the face
+from node (i, j-1) to (i, j); j-face S = (y_left - y_right, x_right - x_left)
+of the face from node (i-1, j) to (i, j).  Rigidly moving meshes (C2's
+pitching airfoil) carry per-snapshot normals and the face grid flux
+G = x_t Sx + y_t Sy.
+
+Face flux (i or j face between cells L and R, with LL, RR the next cells
+out along the same index; S, G the face metrics):
+  convective   Fc = 0.5 (F(W_L) + F(W_R)),  F(W) = W (u.S - G) + p (0, Sx, Sy, u.S)
+  JST          lambda_X = |u_X.S - G| + c_X |S|,  lambda = 0.5 (lambda_L + lambda_R)
+               nu_X = |p_{X+1} - 2 p_X + p_{X-1}| / (p_{X+1} + 2 p_X + p_{X-1})
+               eps2 = K2 lambda max(nu_L, nu_R),  eps4 = max(0, K4 lambda - eps2)
+               D = eps2 (W_R - W_L) - eps4 (((W_RR - 3 W_R) + 3 W_L) - W_LL)
+  viscous (NS) face gradients of u, v and e = p / ((gamma-1) rho) on the
+               "diamond": d/dxi = phi_R - phi_L, d/deta = 0.25 ((phi_L+ + phi_R+)
+               - (phi_L- + phi_R-)) from the cells beside L and R across the
+               face's tangential index; x/y derivatives through the Jacobian of
+               the cell centres; tau and q = -(mu gamma / Pr) grad e;
+               Fv = (0, tau_xx Sx + tau_xy Sy, tau_xy Sx + tau_yy Sy,
+                     (u_f tau_xx + v_f tau_xy - q_x) Sx + (u_f tau_xy + v_f tau_yy - q_y) Sy)
+  face flux    Ff = (Fc - D) - Fv
+Residual  R = ((Ff_{i+1/2} - Ff_{i-1/2}) + Ff_{j+1/2}) - Ff_{j-1/2}
+              + V sum_{m ascending} D[n][m] W_m            (HB source)
+Local time step (from the iteration's start state, all snapshots):
+  dt = min_n CFL V / (((lambda_i + lambda_j) + lambda_v) + omega N_H V),
+  lambda_i = 0.5 (lambda(S_{i-1/2}) + lambda(S_{i+1/2})) with the cell's own
+  state, lambda_v = (2 gamma mu / (Pr rho)) (|S_i|^2 + |S_j|^2) / V (NS only).
+4-stage RK (alphas 1/4, 1/3, 1/2, 1):  W^(s) = W^0 - (alpha_s dt / V) R(W^(s-1)).
+Boundaries (two halo layers, filled before every residual): far-field =
+freestream of the snapshot; no-slip wall = (rho, -rho u, -rho v, rho E) of the
+mirrored interior cell; slip wall = the interior state with its velocity
+(relative to the wall) reflected about the face normal; cuts = the paired
+interior layers; corner halos = the i-halo cell of the nearest interior row.
+Residual norm: sqrt(sum over blocks, snapshots, cells of R_rho^2) of stage 1.
+Forces: per snapshot, cl / cd = sum over wall faces (blocks ascending, face
+order) of p S rotated into the snapshot's lift / drag axes.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+GAMMA = 1.4
+PR = 0.72
+K2 = 0.5
+K4 = 1.0 / 64.0
+CFL = 1.5
+NG = 2            # halo layers
+
+# face kinds (per block side: south, north, west, east)
+FARFIELD, NOSLIP, SLIP, CUT = 0, 1, 2, 3
+SIDES = ("south", "north", "west", "east")
+
+
+@dataclass
+class NSBlock:
+    id: int
+    ni: int
+    nj: int
+    # node coordinates, shape (P_geo, nj+1+2NG, ni+1+2NG): snapshot-major when
+    # the mesh moves (P_geo = P), else P_geo = 1
+    x: np.ndarray
+    y: np.ndarray
+    kinds: tuple = (FARFIELD, FARFIELD, FARFIELD, FARFIELD)
+    # grid velocity field (per snapshot) as functions of node position, or None
+    xt: np.ndarray | None = None
+    yt: np.ndarray | None = None
+
+
+@dataclass
+class NSCut:
+    """side_a of block a (face, 1-based range lo..hi) <-> side_b of block b."""
+    a: int
+    face_a: str
+    b: int
+    face_b: str
+    lo: int
+    hi: int
+
+
+@dataclass
+class NSCase:
+    name: str
+    nharms: int
+    mach: float
+    dalpha_deg: float
+    reynolds: float | None          # None: Euler
+    omega: float
+    blocks: list
+    cuts: list = field(default_factory=list)
+    iterations: int = 100
+    cfl: float = CFL
+
+    @property
+    def planes(self):
+        return 2 * self.nharms + 1
+
+    @property
+    def mu(self):
+        return 0.0 if self.reynolds is None else self.mach / self.reynolds
+
+
+# ---------------------------------------------------------------------------
+# meshes (BASELINE.json configs, physics versions)
+# ---------------------------------------------------------------------------
+
+def _extend(X):
+    """Two ghost node layers on every side by linear extrapolation."""
+    for _ in range(NG):
+        X = np.concatenate([2 * X[:, :1] - X[:, 1:2], X, 2 * X[:, -1:] - X[:, -2:-1]], axis=1)
+        X = np.concatenate([2 * X[:1] - X[1:2], X, 2 * X[-1:] - X[-2:-1]], axis=0)
+    return X
+
+
+def sinusoidal_mesh(ni, nj, x0=0.0, y0=0.0, lx=1.0, ly=None, amp=0.05):
+    """The unit square (or its [x0, x0+lx] x [y0, y0+ly] piece) mapped by
+    x += amp sin(2 pi y), y += amp sin(2 pi x) (configs 0 and 4)."""
+    ly = lx * nj / ni if ly is None else ly
+    X, Y = np.meshgrid(x0 + lx * np.arange(ni + 1) / ni, y0 + ly * np.arange(nj + 1) / nj)
+    x = X + amp * np.sin(2 * np.pi * Y)
+    y = Y + amp * np.sin(2 * np.pi * X)
+    return _extend(x)[None], _extend(y)[None]
+
+
+def tanh_mesh(ni, nj, x0, y0, lx, ly, beta=2.0, ytot=None, yoff=0.0):
+    """Rectangle piece whose y coordinate is clustered toward the bottom wall
+    y = 0 by tanh stretching (configs 1 and 3): y = H (1 + tanh(beta (eta -
+    1)) / tanh(beta)) over the whole height H, eta uniform."""
+    ytot = ly if ytot is None else ytot
+    eta = (yoff + ly * np.arange(nj + 1) / nj) / ytot
+    yy = ytot * (1.0 + np.tanh(beta * (eta - 1.0)) / np.tanh(beta))
+    xx = x0 + lx * np.arange(ni + 1) / ni
+    X, Y = np.meshgrid(xx, yy)
+    return _extend(X)[None], _extend(Y)[None]
+
+
+def naca0012(t):
+    """Half-thickness of NACA 0012 (closed trailing edge) at chord station t."""
+    return 0.6 * (0.2969 * np.sqrt(t) - 0.1260 * t - 0.3516 * t ** 2 + 0.2843 * t ** 3 - 0.1036 * t ** 4)
+
+
+def ogrid_mesh(ni, nj, radius=20.0, stretch=1.02, planes=1, pitch_deg=0.0, k=0.1, mach=0.6):
+    """O-grid around NACA 0012 (config 2): i runs around the airfoil
+    (periodic, a self-cut), j outward with geometric radial spacing (ratio
+    `stretch`) to a circle of `radius` chords about mid-chord.  With
+    pitch_deg > 0 the whole mesh rotates rigidly about the quarter chord,
+    alpha(t) = pitch sin(omega t), omega = 2 k M (chord 1); snapshot n sits
+    at t_n = 2 pi n / (P omega); node velocities are returned as xt, yt."""
+    th = 2 * np.pi * np.arange(ni + 1) / ni
+    t = 0.5 * (1.0 + np.cos(th))                       # TE -> LE -> TE
+    xs = t
+    ys = np.where(np.sin(th) >= 0, 1.0, -1.0) * naca0012(t)
+    xo = 0.5 + radius * np.cos(th)
+    yo = radius * np.sin(th)
+    g = stretch ** np.arange(nj + 1)
+    s = (g - 1.0) / (g[-1] - 1.0)                      # 0 at the wall, 1 outside
+    x = xs[None, :] + s[:, None] * (xo - xs)[None, :]
+    y = ys[None, :] + s[:, None] * (yo - ys)[None, :]
+    x, y = _extend(x), _extend(y)
+    if pitch_deg == 0.0:
+        return x[None], y[None], None, None
+    omega = 2.0 * k * mach
+    xs_, ys_, xt_, yt_ = [], [], [], []
+    for n in range(planes):
+        tn = 2 * np.pi * n / (planes * omega)
+        a = math.radians(pitch_deg) * math.sin(omega * tn)
+        ad = math.radians(pitch_deg) * omega * math.cos(omega * tn)
+        ca, sa = math.cos(-a), math.sin(-a)           # nose-up pitch: clockwise rotation
+        dx, dy = x - 0.25, y
+        xr = 0.25 + ca * dx - sa * dy
+        yr = sa * dx + ca * dy
+        xs_.append(xr)
+        ys_.append(yr)
+        # d/dt of the rotation: omega_z = -ad about (0.25, 0)
+        xt_.append(ad * (yr - 0.0))
+        yt_.append(-ad * (xr - 0.25))
+    return np.stack(xs_), np.stack(ys_), np.stack(xt_), np.stack(yt_)
+
+
+def ns_workload(key, iterations=None, scale=1):
+    """BASELINE.json configs with their physics.  `scale`
+    divides the cell counts (tests run small versions of the same setups)."""
+    key = key.upper()
+    if key == "C0":
+        ni, nj = 64 // scale, 32 // scale
+        x, y = sinusoidal_mesh(ni, nj, ly=0.5)
+        case = NSCase("C0-euler", 1, 0.5, 1.0, None, 1.0, [NSBlock(0, ni, nj, x, y)], iterations=100)
+    elif key in ("C1", "C3"):
+        nbx, nby = (2, 2) if key == "C1" else (4, 2)
+        ni, nj = ((256, 128) if key == "C1" else (1024, 512))
+        ni, nj = ni // scale, nj // scale
+        mach, re, nh = (0.3, 1e4, 2) if key == "C1" else (0.4, 1e5, 3)
+        lx, ly = 1.0, 0.5
+        blocks = []
+        for r in range(nby):
+            for c in range(nbx):
+                x, y = tanh_mesh(ni, nj, c * lx, 0.0, lx, ly, ytot=nby * ly, yoff=r * ly)
+                kinds = [FARFIELD] * 4
+                if r == 0:
+                    kinds[0] = NOSLIP
+                if r > 0:
+                    kinds[0] = CUT
+                if r < nby - 1:
+                    kinds[1] = CUT
+                if c > 0:
+                    kinds[2] = CUT
+                if c < nbx - 1:
+                    kinds[3] = CUT
+                blocks.append(NSBlock(r * nbx + c, ni, nj, x, y, tuple(kinds)))
+        cuts = [NSCut(r * nbx + c, "east", r * nbx + c + 1, "west", 1, nj)
+                for r in range(nby) for c in range(nbx - 1)]
+        cuts += [NSCut(r * nbx + c, "north", (r + 1) * nbx + c, "south", 1, ni)
+                 for r in range(nby - 1) for c in range(nbx)]
+        case = NSCase(f"{key}-ns", nh, mach, 0.0, re, 1.0, blocks, cuts,
+                      iterations=200 if key == "C1" else 200)
+    elif key == "C2":
+        ni, nj = 512 // scale, 256 // scale
+        P = 9
+        x, y, xt, yt = ogrid_mesh(ni, nj, planes=P, pitch_deg=5.0, mach=0.6)
+        blk = NSBlock(0, ni, nj, x, y, (SLIP, FARFIELD, CUT, CUT), xt, yt)
+        case = NSCase("C2-euler-pitching", 4, 0.6, 0.0, None, 2 * 0.1 * 0.6, [blk],
+                      [NSCut(0, "east", 0, "west", 1, nj)], iterations=500)
+    elif key == "C4":
+        ni = nj = 1024 // scale
+        blocks = []
+        for r in range(8):
+            for c in range(8):
+                x, y = sinusoidal_mesh(ni, nj, x0=c / 8, y0=r / 8, lx=1 / 8, ly=1 / 8)
+                kinds = [FARFIELD if r == 0 else CUT, FARFIELD if r == 7 else CUT,
+                         FARFIELD if c == 0 else CUT, FARFIELD if c == 7 else CUT]
+                blocks.append(NSBlock(r * 8 + c, ni, nj, x, y, tuple(kinds)))
+        cuts = [NSCut(r * 8 + c, "east", r * 8 + c + 1, "west", 1, nj) for r in range(8) for c in range(7)]
+        cuts += [NSCut(r * 8 + c, "north", (r + 1) * 8 + c, "south", 1, ni) for r in range(7) for c in range(8)]
+        case = NSCase("C4-euler", 4, 0.5, 2.0, None, 1.0, blocks, cuts, iterations=50)
+    else:
+        raise KeyError(key)
+    if iterations is not None:
+        case.iterations = iterations
+    return case
+
+
+# ---------------------------------------------------------------------------
+# geometry (the specification's formulas, numpy element-wise: each op one
+# IEEE rounding, the written order)
+# ---------------------------------------------------------------------------
+
+def metrics(block):
+    """Cell centres (incl. ghosts), areas, face normals: arrays over the
+    extended index range.  Shapes (Pg = 1 or P):
+      xc, yc   (Pg, nj+2NG, ni+2NG)      cell (j, i) at [j+NG-1, i+NG-1]
+      vol      (Pg, nj+2NG, ni+2NG)
+      six, siy (Pg, nj+2NG, ni+2NG+1)    i-face between cells i and i+1
+      sjx, sjy (Pg, nj+2NG+1, ni+2NG)    j-face between cells j and j+1
+    """
+    x, y = block.x, block.y
+    x00, x10, x11, x01 = x[:, :-1, :-1], x[:, :-1, 1:], x[:, 1:, 1:], x[:, 1:, :-1]
+    y00, y10, y11, y01 = y[:, :-1, :-1], y[:, :-1, 1:], y[:, 1:, 1:], y[:, 1:, :-1]
+    xc = 0.25 * ((x00 + x10) + (x11 + x01))
+    yc = 0.25 * ((y00 + y10) + (y11 + y01))
+    vol = 0.5 * ((x11 - x00) * (y01 - y10) - (y11 - y00) * (x01 - x10))
+    # i-face at node column I: from node (I, J-1) to (I, J)
+    six = y[:, 1:, :] - y[:, :-1, :]
+    siy = x[:, :-1, :] - x[:, 1:, :]
+    # j-face at node row J: from node (I-1, J) to (I, J)
+    sjx = y[:, :, :-1] - y[:, :, 1:]
+    sjy = x[:, :, 1:] - x[:, :, :-1]
+    out = {"xc": xc, "yc": yc, "vol": vol, "six": six, "siy": siy, "sjx": sjx, "sjy": sjy}
+    if block.xt is not None:
+        # face grid flux: average of the face's two node velocities . S
+        xt, yt = block.xt, block.yt
+        gi = (0.5 * (xt[:, 1:, :] + xt[:, :-1, :])) * six + (0.5 * (yt[:, 1:, :] + yt[:, :-1, :])) * siy
+        gj = (0.5 * (xt[:, :, :-1] + xt[:, :, 1:])) * sjx + (0.5 * (yt[:, :, :-1] + yt[:, :, 1:])) * sjy
+        out["gi"], out["gj"] = gi, gj
+    return {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in out.items()}
+
+
+def freestream(case):
+    """W_inf per snapshot, shape (P, 4)."""
+    P = case.planes
+    out = np.zeros((P, 4))
+    for n in range(P):
+        a = math.radians(case.dalpha_deg) * math.sin(2 * math.pi * n / P)
+        u, v = case.mach * math.cos(a), case.mach * math.sin(a)
+        p = 1.0 / GAMMA
+        out[n] = (1.0, u, v, p / (GAMMA - 1.0) + 0.5 * (u * u + v * v))
+    return out
+
+
+def initial_state(case, block, seed=13047654):
+    """Freestream with a seeded 1% uniform perturbation per state variable
+    (BASELINE.json), halos zero: shape (P, 4, nj+2NG, ni+2NG)."""
+    P = case.planes
+    winf = freestream(case)
+    rng = np.random.default_rng(seed + block.id)
+    q = np.zeros((P, 4, block.nj + 2 * NG, block.ni + 2 * NG))
+    pert = 1.0 + 0.01 * rng.uniform(-1.0, 1.0, size=(P, 4, block.nj, block.ni))
+    q[:, :, NG:-NG, NG:-NG] = winf[:, :, None, None] * pert
+    return q
+
+
+def spectral_matrix(case):
+    from .hbop import spectral_matrix as sm
+    return np.ascontiguousarray(sm(case.nharms, case.omega).matrix)

@@ -32,7 +32,7 @@ from enum import Enum
 import numpy as np
 
 from . import hbop, native, outio
-from .cutplan import ExchangeMode, ExchangeStrategy, build_cut_plan, predicted_message_count
+from .cutplan import ExchangeMode, ExchangeStrategy, build_cut_plan, predicted_message_count, rank_routes
 from .devlayout import build_rank_layout
 from .exceptions import CollectiveError, DivergenceError, ProtocolError, RankFailure, RunAborted
 from .topology import build_topology, partition_blocks
@@ -114,9 +114,12 @@ class RunSpec:
     # transport (exercises the multi-GPU halo path); "loopback-split" does
     # so with the overlapped boundary / interior schedule of the NCCL engine
     transport: str = "fold"
-    # paired RK stages (hb_pair.cu): None = whenever eligible (P <= 17 and
-    # every block a whole number of strips wide), False = single stages
+    # paired RK stages (hb_pair.cu): None = auto (eligible and from
+    # FUSED_MIN_UNITS units per stage), False = single stages
     fused: bool | None = None
+    # one-launch small schedule (hb_small.cu): None = auto (single rank
+    # without remote cuts, up to SMALL_MAX_UNITS units per stage), False = off
+    small: bool | None = None
 
 
 @dataclass
@@ -197,7 +200,7 @@ class DeviceRank:
     """One rank's blocks resident on one GPU, plus its libhbgpu engine."""
 
     def __init__(self, case, topology, partition, plan, rank=0, device=None, comm=None,
-                 initial=None, tile_rows=None, max_iters=1, pinned_ic=None, fused=None):
+                 initial=None, tile_rows=None, max_iters=1, pinned_ic=None, fused=None, small=None):
         import torch
         self.lib = native.require_cuda()
         self.torch = torch
@@ -209,7 +212,7 @@ class DeviceRank:
         torch.cuda.set_device(self.device)
         t0 = time.perf_counter()
         L = self.layout = build_rank_layout(topology, partition, plan, rank, case.planes, tile_rows,
-                                            fused=fused)
+                                            fused=fused, small=small)
         self.timings = {"layout": time.perf_counter() - t0}
         dev = self.device
         f64 = torch.float64
@@ -341,6 +344,7 @@ class DeviceRank:
         d.post_max_len = int(L.post_dirs["length"].max()) if len(L.post_dirs) else 0
         d.band_segs, d.nband_segs = self.t_band.data_ptr(), len(L.band_segs)
         d.band_max_len, d.fused = int(L.band_max_len), int(L.fused)
+        d.small, d.small_max_cells = int(L.small), int(L.small_max_cells)
         d.edge_q0 = self.edge_q0.data_ptr()
         # multi-GPU overlap: boundary tiles first, remote packs first
         self.t_order = torch.from_numpy(np.ascontiguousarray(L.tile_order, dtype=np.int32)).to(self.device)
@@ -737,7 +741,7 @@ def run_case(spec):
     forces = (ForceCoefficients.from_stack(hist_np[-1]) if iterations > 0
               else ForceCoefficients.zeros(case.planes, case.nbody))
     activations = iterations * (12 if _per_loop(spec.activation) else 1) + len(targets)
-    counters = rank_counters(plan, spec, partition, iterations, activations, layouts, targets)
+    counters = rank_counters(plan, spec, partition, iterations, activations, layouts, targets, world)
     record = None
     if iterations >= 1:
         units = topology.total_cells() * case.planes * 4 * iterations
@@ -757,7 +761,7 @@ def run_case(spec):
 def _new_rank(spec, topology, partition, plan, rank, device, comm, iterations):
     return DeviceRank(spec.case, topology, partition, plan, rank=rank, device=device, comm=comm,
                       initial=spec.initial, tile_rows=spec.tile_rows, max_iters=max(1, iterations),
-                      pinned_ic=spec.initial_state, fused=spec.fused)
+                      pinned_ic=spec.initial_state, fused=spec.fused, small=spec.small)
 
 
 def _history(dr, iterations):
@@ -777,13 +781,22 @@ class CounterSnapshot:
     collective_calls: int
     write_ops: int
     team_activations: int
+    # what the device path itself moved (the fields above are the reference's
+    # counters for the chosen strategies, exchange.py:172-188): one
+    # aggregated payload per peer and exchange (NCCL send or loopback copy),
+    # its bytes, and the NCCL collectives of a multi-GPU run (divergence
+    # consensus per polling chunk, the final status / norm all-reduces, the
+    # force-history all-gather)
+    device_msgs: int = 0
+    device_bytes: int = 0
+    device_collectives: int = 0
 
 
 def _per_loop(activation):
     return getattr(activation, "value", activation) == "per-loop"
 
 
-def rank_counters(plan, spec, partition, iterations, activations, layouts, targets):
+def rank_counters(plan, spec, partition, iterations, activations, layouts, targets, world=1):
     """What each rank of the reference partition sends, receives, reduces and
     writes under spec's strategies -- the reference's counters exactly
     (exchange.py:172-188 message counts, reduce.py:40-46 collectives,
@@ -803,12 +816,38 @@ def rank_counters(plan, spec, partition, iterations, activations, layouts, targe
             sent_bytes[d.sender_rank] += cut.length * cut.datasize * 8 * exchanges
             received[d.recv_rank] += msgs * exchanges
     calls = iterations * spec.reduce.collective_calls(spec.case.planes, spec.case.nbody)
+    dev_msgs, dev_bytes, dev_coll = device_traffic(plan, spec, iterations, world)
     out = []
     for r in range(spec.ranks):
         owned = partition.blocks_of(r)
         ops = sum(outio.write_ops(layouts, owned, mode) for _, mode in targets)
-        out.append(CounterSnapshot(sent[r], sent_bytes[r], received[r], calls, ops, activations))
+        out.append(CounterSnapshot(sent[r], sent_bytes[r], received[r], calls, ops, activations,
+                                   dev_msgs[r], dev_bytes[r], dev_coll))
     return out
+
+
+def device_traffic(plan, spec, iterations, world=1):
+    """Per rank: (payloads sent, bytes sent) by the device path over the run,
+    and the NCCL collectives of the run.  A single-process "fold" run keeps
+    every cut inside one engine (nothing moves between ranks); "loopback"
+    and multi-GPU runs send one aggregated payload per peer and exchange
+    (4 per iteration + the priming one), whatever the reference strategy."""
+    exchanges = 4 * iterations + 1
+    msgs = [0] * spec.ranks
+    nbytes = [0] * spec.ranks
+    moving = world > 1 or spec.transport in ("loopback", "loopback-split")
+    if moving:
+        for r in range(spec.ranks):
+            sends = rank_routes(plan, r).sends
+            msgs[r] = len({d.recv_rank for d in sends}) * exchanges
+            nbytes[r] = sum(d.length for d in sends) * plan.datasize * 8 * exchanges
+    coll = 0
+    if world > 1 and iterations > 0:
+        first = 1 if spec.use_graph and iterations > 1 else 0
+        topology = build_topology(spec.case)
+        chunk = poll_interval(topology, spec.case.planes, iterations)
+        coll = -(-(iterations - first) // chunk) + 3
+    return msgs, nbytes, coll
 
 
 def _output_targets(spec):
@@ -846,7 +885,7 @@ def _execute_single(spec, topology, partition, plan, iterations, out=((), ())):
         torch.cuda.synchronize(dr.device)
         t1 = time.perf_counter()
         LAST_RUN.clear()
-        LAST_RUN.update(iterations_issued=dr.iterations_done(), fused=dr.fused)
+        LAST_RUN.update(iterations_issued=dr.iterations_done(), fused=dr.fused, small=bool(dr.layout.small))
         raise_divergence(dr.divergence())
         fields = dr.fields(0, pinned_out=spec.output)
         hist = _history(dr, iterations)

@@ -32,7 +32,14 @@ def test_reference_arm_json_line(oracle_mod):
     assert BASE_KEYS <= d.keys()
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["config"]["workload"] == "C0"
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["value"] == d["value"]
+    cb = d["cpu_baseline"]
+    assert cb["value"] == d["value"] and cb["cores"] >= 1
+    if os.path.isdir(os.path.join(REPO, "baseline", "_ref", "hbproxy")):
+        # the unmodified reference (numba run_case) with the C port beside it
+        assert cb["kind"] == "reference" and "run_case" in cb["sample"]
+        assert cb["port"]["value"] > 0
+    else:
+        assert cb["kind"] == "port"
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
 
@@ -50,3 +57,12 @@ def test_our_arm_json_line(cuda):
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+def test_our_arm_refuses_library_knobs():
+    """A bench line is never taken with a libhbgpu test knob set unknowingly
+    (HBGPU_GRID_LIMIT, HBGPU_FUSED, ...): the arm exits before touching a GPU."""
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0", HBGPU_GRID_LIMIT="3")
+    out = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--workload", "C0"], cwd=REPO,
+                         env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode != 0 and "refusing to benchmark" in out.stderr

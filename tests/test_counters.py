@@ -71,3 +71,20 @@ def test_counters_of_the_tiny_record():
     assert sum(c.msgs_sent for c in cs) == 2 * 17
     assert sum(c.bytes_sent for c in cs) == 2 * 17 * 4 * 12 * 8
     assert all(c.collective_calls == 4 and c.team_activations == 4 for c in cs)
+
+
+def test_device_counters_report_what_the_device_moves():
+    """The reference counters follow the strategy (per-element: 2L messages
+    per direction); the device_* fields record what the device path moves:
+    one aggregated payload per peer and exchange, the same bytes."""
+    case = cut2500()
+    for mode in ExchangeMode:
+        cs, plan = _counters(case, 2, 3, exchange=ExchangeStrategy(mode), transport="loopback")
+        exchanges = 4 * 3 + 1
+        for c in cs:
+            assert c.device_msgs == exchanges          # one peer
+            assert c.device_bytes == c.bytes_sent       # the same payload bytes
+            assert c.device_collectives == 0
+    cs, _ = _counters(case, 2, 3, exchange=ExchangeStrategy(ExchangeMode.PER_ELEMENT))   # "fold"
+    assert all(c.device_msgs == 0 and c.device_bytes == 0 for c in cs)
+    assert all(c.msgs_sent == 5000 * 13 for c in cs)

@@ -131,3 +131,50 @@ def test_forces_no_bodies(cuda):
     field = blockops.HarmonicField.allocate([spec], 3)
     got = blockops.compute_forces(field, Topology(blocks=(spec,), cuts=(), nbody=0))
     assert got.cl.shape == (3, 0)
+
+
+@pytest.mark.parametrize("ranks", [2, 3])
+def test_exchange_halos_remote_cuts_vs_oracle(ranks, cuda, oracle_mod):
+    """Block-level exchange_halos with remote cuts (exchange.py:382-402 with a
+    rank context): each rank, a thread holding only its own blocks, packs its
+    sends element-major, moves one payload per peer through a HaloContext
+    (LoopbackHub here, NCCL on several GPUs) and unpacks; every halo must
+    equal the all-local oracle exchange."""
+    import threading
+    from paper_1304_7654_b200 import blockops
+    case = lattice_case(3, 2, 9, 6, 1, h=0.1, dtau=0.01)
+    topo = build_topology(case)
+    part = partition_blocks(topo, ranks)
+    plan = build_cut_plan(topo, part, case.nharms, case.npde)
+    assert any(not c.local for c in plan.cuts)
+    full = blockops.HarmonicField.allocate(topo.blocks, case.planes)
+    _seeded(full)
+    qs = {b: bs.q.cpu().numpy().copy() for b, bs in full.blocks.items()}
+    oracle_mod.exchange(qs, topo.cuts)
+    fields = []
+    for r in range(ranks):
+        f = blockops.HarmonicField.allocate([topo.blocks[g] for g in part.blocks_of(r)], case.planes)
+        for g, bs in f.blocks.items():
+            bs.q.copy_(full.blocks[g].q)
+        fields.append(f)
+    hub = blockops.LoopbackHub(ranks)
+    errors = []
+
+    def rank_main(r):
+        try:
+            blockops.exchange_halos(fields[r], plan, blockops.HaloContext(r, hub=hub))
+        except Exception as e:   # noqa: BLE001
+            errors.append(e)
+            hub.barrier.abort()
+
+    threads = [threading.Thread(target=rank_main, args=(r,)) for r in range(ranks)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for f in fields:
+        for g, bs in f.blocks.items():
+            assert np.array_equal(bs.q.cpu().numpy(), qs[g]), f"block {g}"
+    with pytest.raises(Exception, match="HaloContext"):
+        blockops.exchange_halos(fields[0], plan)

@@ -52,19 +52,23 @@ CASES = {
 }
 
 
+@pytest.mark.parametrize("small", [None, False])
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_run_case_matches_oracle(name, cuda, oracle_mod):
+def test_run_case_matches_oracle(name, small, cuda, oracle_mod):
+    """small=None: the auto schedule, the one-launch small kernel for these
+    sizes (hb_small.cu); small=False: the per-stage TMA kernels."""
     build, iters, initial = CASES[name]
     case = build()
-    got = run_case(RunSpec(case=case, ranks=1, iterations=iters, initial=initial))
+    got = run_case(RunSpec(case=case, ranks=1, iterations=iters, initial=initial, small=small))
     want = oracle_mod.run(case, iters, initial=initial)
     assert_parity(got, want, name)
 
 
+@pytest.mark.parametrize("small", [None, False])
 @pytest.mark.parametrize("key,iters", [("C0", 20), ("C1", 2), ("C2", 2)])
-def test_baseline_workloads_match_oracle(key, iters, cuda, oracle_mod):
+def test_baseline_workloads_match_oracle(key, iters, small, cuda, oracle_mod):
     wl = baseline_workload(key)
-    got = run_case(RunSpec(case=wl.case, ranks=1, iterations=iters, initial=wl.initial))
+    got = run_case(RunSpec(case=wl.case, ranks=1, iterations=iters, initial=wl.initial, small=small))
     want = oracle_mod.run(wl.case, iters, initial=wl.initial)
     assert_parity(got, want, key)
 
@@ -76,7 +80,7 @@ def test_ragged_widths_match_oracle(ni, cuda, oracle_mod):
     at or before cell ni, and the forwarded east halo cell ni+1 -- in the same
     granule as cell ni when ni % 8 != 0 -- must survive every stage."""
     case = ring_case(2, ni, 5, 1, h=0.05, dtau=0.0005, nbody=1, bodies=((1, "south", 0),))
-    got = run_case(RunSpec(case=case, ranks=1, iterations=3))
+    got = run_case(RunSpec(case=case, ranks=1, iterations=3, small=False))
     want = oracle_mod.run(case, 3)
     assert_parity(got, want, f"ring2-ni{ni}")
 
@@ -204,7 +208,7 @@ def test_paired_stages_match_oracle_and_single_stages(name, cuda, oracle_mod):
     got = run_case(RunSpec(case=case, ranks=ranks, iterations=iters, tile_rows=tile_rows, initial=initial,
                            transport=transport, fused=True))
     single = run_case(RunSpec(case=case, ranks=ranks, iterations=iters, tile_rows=tile_rows, initial=initial,
-                              transport=transport, fused=False))
+                              transport=transport, fused=False, small=False))
     want = oracle_mod.run(case, iters, initial=initial)
     assert_parity(got, want, name)
     assert got.field_bits_equal(single) and got.forces.equal_bits(single.forces)
@@ -258,7 +262,7 @@ def test_many_tiles_per_cta_match_oracle(name, fused, limit, cuda, oracle_mod, m
     monkeypatch.setenv("HBGPU_GRID_LIMIT", str(limit))
     build, iters, tile_rows = MANY_TILES[name]
     case = build()
-    got = run_case(RunSpec(case=case, ranks=1, iterations=iters, tile_rows=tile_rows, fused=fused))
+    got = run_case(RunSpec(case=case, ranks=1, iterations=iters, tile_rows=tile_rows, fused=fused, small=False))
     want = oracle_mod.run(case, iters)
     assert_parity(got, want, f"{name} fused={fused} limit={limit}")
 
@@ -402,3 +406,28 @@ def test_run_diverges_with_rank_in_error(cuda):
             run_case(RunSpec(case=case, ranks=ranks, iterations=50))
         assert isinstance(err.value.cause, DivergenceError)
         assert err.value.rank in range(ranks)
+
+
+@pytest.mark.parametrize("name", ["tc1-mini-4", "lattice-p7-ragged", "stacked-ns"])
+def test_small_schedule_equals_stage_kernels(name, cuda):
+    """The one-launch small schedule and the per-stage TMA kernels agree
+    bitwise (fields, forces) and on the norms (rtol 1e-13), over several
+    iterations and through the status poller's chunks."""
+    build, iters, initial = CASES[name]
+    case = build()
+    a = run_case(RunSpec(case=case, ranks=1, iterations=iters + 3, small=True))
+    b = run_case(RunSpec(case=case, ranks=1, iterations=iters + 3, small=False))
+    assert a.field_bits_equal(b) and a.forces.equal_bits(b.forces)
+    np.testing.assert_allclose(a.residual_norms, b.residual_norms, rtol=1e-13)
+    from paper_1304_7654_b200 import solver
+    assert solver.LAST_RUN["small"] is False
+
+
+def test_small_schedule_divergence_location(cuda, oracle_mod):
+    case = pair_case(8, 6, 1, h=0.25, dtau=50.0, nbody=0)
+    with pytest.raises(oracle_mod.OracleDivergence) as want:
+        oracle_mod.run(case, 100)
+    with pytest.raises(RankFailure) as got:
+        run_case(RunSpec(case=case, ranks=1, iterations=100, small=True))
+    w, g = want.value, got.value.cause
+    assert (g.block, g.i, g.j, g.p, g.n) == (w.block, w.i, w.j, w.p, w.n)
