@@ -339,9 +339,9 @@ def _ref_case(mesh, case):
 
 
 def ref_sample_blocks(wl):
-    # ~300M units per sampled iteration (a few s of 16-core numba): 8 blocks
-    # of C4, 4 of C3, all of C0..C2
-    budget = 300e6
+    # ~320M units per sampled iteration (a few s of 16-core numba): 8 blocks
+    # of C4 (one per 2 of the box's 16 cores), 5 of C3, all of C0..C2
+    budget = 320e6
     per = wl.case.blocks[0].cells() * wl.case.planes * 4
     return max(1, min(len(wl.case.blocks), int(budget // per)))
 

@@ -172,12 +172,13 @@ def ogrid_mesh(ni, nj, radius=20.0, stretch=1.02, planes=1, pitch_deg=0.0, k=0.1
     pitch_deg > 0 the whole mesh rotates rigidly about the quarter chord,
     alpha(t) = pitch sin(omega t), omega = 2 k M (chord 1); snapshot n sits
     at t_n = 2 pi n / (P omega); node velocities are returned as xt, yt."""
-    th = 2 * np.pi * np.arange(ni + 1) / ni
+    # clockwise around the airfoil, so that (i, j = outward) is right-handed
+    th = -2 * np.pi * np.arange(ni + 1) / ni
     t = 0.5 * (1.0 + np.cos(th))                       # TE -> LE -> TE
     xs = t
     ys = np.where(np.sin(th) >= 0, 1.0, -1.0) * naca0012(t)
     xo = 0.5 + radius * np.cos(th)
-    yo = radius * np.sin(th)
+    yo = radius * np.sin(th)                           # lower surface first
     g = stretch ** np.arange(nj + 1)
     s = (g - 1.0) / (g[-1] - 1.0)                      # 0 at the wall, 1 outside
     x = xs[None, :] + s[:, None] * (xo - xs)[None, :]
@@ -327,3 +328,216 @@ def initial_state(case, block, seed=13047654):
 def spectral_matrix(case):
     from .hbop import spectral_matrix as sm
     return np.ascontiguousarray(sm(case.nharms, case.omega).matrix)
+
+
+# ---------------------------------------------------------------------------
+# the GPU run (libhbgpu hbns_* + hbgpu_halo for the cut halos)
+# ---------------------------------------------------------------------------
+
+RK_ALPHAS = (0.25, 1.0 / 3.0, 0.5, 1.0)
+UPD_THREADS = 256
+
+
+def _halo_rows(case, offsets):
+    """hbgpu_halo directions of every cut, both ways, both halo layers."""
+    from . import native
+    rows = []
+    blocks = {b.id: b for b in case.blocks}
+
+    def cell(b, face, k, e, halo):
+        ni, nj = b.ni, b.nj
+        if face == "south":
+            return (e, 1 - k) if halo else (e, k)
+        if face == "north":
+            return (e, nj + k) if halo else (e, nj + 1 - k)
+        if face == "west":
+            return (1 - k, e) if halo else (k, e)
+        return (ni + k, e) if halo else (ni + 1 - k, e)
+
+    def off(b, i, j):
+        return offsets[b.id] + (j + 1) * (b.ni + 4) + (i + 1)
+
+    for c in case.cuts:
+        A, B = blocks[c.a], blocks[c.b]
+        for k in (1, 2):
+            for dst, dface, src, sface in ((A, c.face_a, B, c.face_b), (B, c.face_b, A, c.face_a)):
+                si, sj = cell(src, sface, k, c.lo, False)
+                di, dj = cell(dst, dface, k, c.lo, True)
+                ses = 1 if sface in ("south", "north") else src.ni + 4
+                des = 1 if dface in ("south", "north") else dst.ni + 4
+                rows.append((off(src, si, sj), ses, (src.nj + 4) * (src.ni + 4),
+                             off(dst, di, dj), des, (dst.nj + 4) * (dst.ni + 4),
+                             c.hi - c.lo + 1, 0, 0, 0))
+    return np.array(rows, dtype=native.HALO_DIR_DTYPE) if rows else np.zeros(0, native.HALO_DIR_DTYPE)
+
+
+def _ns_types():
+    """ctypes mirrors of hbns_block / hbns_args (include/hbns.h)."""
+    import ctypes
+    vp, i32, i64, f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+
+    class Block(ctypes.Structure):
+        _fields_ = [("w_off", i64), ("r_off", i64), ("dt_off", i64), ("c_off", i64), ("fi_off", i64),
+                    ("fj_off", i64), ("part_off", i64), ("ni", i32), ("nj", i32), ("kinds", i32 * 4)]
+
+    class Args(ctypes.Structure):
+        _fields_ = [("w", vp * 3), ("r", vp), ("dt", vp), ("xc", vp), ("yc", vp), ("vol", vp),
+                    ("six", vp), ("siy", vp), ("gi", vp), ("sjx", vp), ("sjy", vp), ("gj", vp),
+                    ("blocks", vp), ("winf", vp), ("dmat", vp), ("status", vp), ("norm_part", vp),
+                    ("norms", vp), ("forces", vp), ("mu", f64), ("cfl", f64), ("omega_nh", f64),
+                    ("nblocks", i32), ("P", i32), ("Pg", i32), ("moving", i32), ("max_len", i32),
+                    ("max_cells", i32)]
+    return Block, Args
+
+
+class NSRun:
+    """The HB Euler / NS loop of one case on one GPU: every block resident in
+    three state pools, the RK stages launched on torch's current stream
+    (hb_ns.cu), cut halos by hbgpu_halo."""
+
+    def __init__(self, case, max_iters, initial=None, device=None):
+        import ctypes
+        import torch
+        from . import native
+        self.lib = native.require_cuda()
+        self.torch, self._ct = torch, ctypes
+        self.case = case
+        self.max_iters = max_iters
+        dev = self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        P = case.planes
+        blocks = self.blocks = sorted(case.blocks, key=lambda b: b.id)
+        geos = [metrics(b) for b in blocks]
+        Pg = geos[0]["xc"].shape[0]
+        moving = "gi" in geos[0]
+        Block, Args = _ns_types()
+        max_cells = max(b.ni * b.nj for b in blocks)
+        ctas = -(-max_cells // UPD_THREADS)
+        table = (Block * len(blocks))()
+        self.w_off = {}
+        wsz = r_off = dt_off = c_off = fi_off = fj_off = 0
+        pools = {k: [] for k in ("xc", "yc", "vol", "six", "siy", "gi", "sjx", "sjy", "gj")}
+        for k, (b, g) in enumerate(zip(blocks, geos)):
+            e = table[k]
+            e.w_off, e.r_off, e.dt_off = wsz, r_off, dt_off
+            e.c_off, e.fi_off, e.fj_off = c_off, fi_off, fj_off
+            e.part_off = k * P * ctas
+            e.ni, e.nj = b.ni, b.nj
+            for s in range(4):
+                e.kinds[s] = b.kinds[s]
+            self.w_off[b.id] = wsz
+            wsz += P * 4 * (b.nj + 4) * (b.ni + 4)
+            r_off += P * 4 * b.nj * b.ni
+            dt_off += b.nj * b.ni
+            c_off += g["xc"].size
+            fi_off += g["six"].size
+            fj_off += g["sjx"].size
+            for name in pools:
+                if name in g:
+                    pools[name].append(g[name].ravel())
+        f64 = torch.float64
+        self.slots = [torch.zeros(wsz, dtype=f64, device=dev) for _ in range(3)]
+        for b in blocks:
+            q = initial(b) if initial is not None else initial_state(case, b)
+            self.slot_view(0, b).copy_(torch.from_numpy(np.ascontiguousarray(q)))
+        self.r = torch.zeros(max(1, r_off), dtype=f64, device=dev)
+        self.dt = torch.zeros(max(1, dt_off), dtype=f64, device=dev)
+        self.geo = {k: (torch.from_numpy(np.concatenate(v)).to(dev) if v else torch.zeros(1, dtype=f64, device=dev))
+                    for k, v in pools.items()}
+        self.t_blocks = torch.frombuffer(bytearray(bytes(table)), dtype=torch.uint8).to(dev)
+        self.winf = torch.from_numpy(np.ascontiguousarray(freestream(case))).to(dev)
+        self.dmat = torch.from_numpy(spectral_matrix(case).copy()).to(dev)
+        self.status = torch.full((len(blocks),), -1, dtype=torch.int64, device=dev)
+        self.norm_part = torch.zeros(len(blocks) * P * ctas, dtype=f64, device=dev)
+        self.norms = torch.zeros(max(1, max_iters), dtype=f64, device=dev)
+        self.forces = torch.zeros(max(1, max_iters) * P * 2, dtype=f64, device=dev)
+        halo = _halo_rows(case, self.w_off)
+        self.nhalo = len(halo)
+        self.halo_len = int(halo["length"].max()) if len(halo) else 0
+        self.t_halo = torch.from_numpy(halo.view(np.uint8).copy()).to(dev) if len(halo) else None
+        a = Args()
+        for k in range(3):
+            a.w[k] = self.slots[k].data_ptr()
+        a.r, a.dt = self.r.data_ptr(), self.dt.data_ptr()
+        for name in pools:
+            setattr(a, name, self.geo[name].data_ptr())
+        a.blocks, a.winf, a.dmat = self.t_blocks.data_ptr(), self.winf.data_ptr(), self.dmat.data_ptr()
+        a.status, a.norm_part = self.status.data_ptr(), self.norm_part.data_ptr()
+        a.norms, a.forces = self.norms.data_ptr(), self.forces.data_ptr()
+        a.mu, a.cfl, a.omega_nh = case.mu, case.cfl, case.omega * case.nharms
+        a.nblocks, a.P, a.Pg, a.moving = len(blocks), P, Pg, int(moving)
+        a.max_len = max(max(b.ni, b.nj) for b in blocks)
+        a.max_cells = max_cells
+        self.args = a
+        self.done = 0
+
+    def slot_view(self, slot, b):
+        P = self.case.planes
+        n = P * 4 * (b.nj + 4) * (b.ni + 4)
+        off = self.w_off[b.id]
+        return self.slots[slot][off:off + n].view(P, 4, b.nj + 4, b.ni + 4)
+
+    def _stream(self):
+        return self._ct.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
+
+    def iterate(self, iterations):
+        from . import native
+        if self.done + iterations > self.max_iters:
+            raise ValueError(f"{iterations} more iterations exceed max_iters={self.max_iters}")
+        L, a, s, ct = self.lib, self.args, self._stream(), self._ct
+        ap = ct.byref(a)
+        for _ in range(iterations):
+            it = self.done
+            for st, (si, so) in enumerate(((0, 1), (1, 2), (2, 1), (1, 0))):
+                if self.nhalo:
+                    native.check(L.hbgpu_halo(ct.c_void_p(self.slots[si].data_ptr()), None, None,
+                                              ct.c_void_p(self.t_halo.data_ptr()), self.nhalo, self.halo_len,
+                                              self.case.planes, s), "hbgpu_halo (ns cuts)")
+                native.check(L.hbns_boundaries(ap, si, s), "hbns_boundaries")
+                if st == 0:
+                    native.check(L.hbns_timestep(ap, 0, s), "hbns_timestep")
+                native.check(L.hbns_residual(ap, si, s), "hbns_residual")
+                native.check(L.hbns_update(ap, si, so, RK_ALPHAS[st], it, int(st == 0), s), "hbns_update")
+            native.check(L.hbns_forces(ap, it, s), "hbns_forces")
+            self.done += 1
+        return self
+
+    def divergence(self):
+        keys = self.status.cpu().numpy().view(np.uint64)
+        for k, key in enumerate(keys):
+            if int(key) != (1 << 64) - 1:
+                b = self.blocks[k]
+                lin = int(key)
+                i, j = lin % b.ni + 1, (lin // b.ni) % b.nj + 1
+                nk = lin // (b.ni * b.nj)
+                return b.id, i, j, nk % 4, nk // 4
+        return None
+
+    def fields(self):
+        return {b.id: self.slot_view(0, b).cpu().numpy() for b in self.blocks}
+
+    def norm_history(self):
+        return self.norms[:self.done].cpu().tolist()
+
+    def force_history(self):
+        """(iterations, P, 2) (cl, cd) in the snapshot's freestream axes."""
+        P = self.case.planes
+        fxy = self.forces[:self.done * P * 2].view(self.done, P, 2).cpu().numpy()
+        ang = np.radians(self.case.dalpha_deg) * np.sin(2 * np.pi * np.arange(P) / P)
+        ca, sa = np.cos(ang), np.sin(ang)
+        cd = fxy[:, :, 0] * ca + fxy[:, :, 1] * sa
+        cl = fxy[:, :, 1] * ca - fxy[:, :, 0] * sa
+        return np.stack([cl, cd], axis=2)
+
+
+def run_ns(case, iterations=None, initial=None):
+    """Run a case on the GPU; returns the NSRun (fields, norms, forces).
+    Raises DivergenceError on a non-finite state."""
+    from .exceptions import DivergenceError
+    iterations = case.iterations if iterations is None else iterations
+    r = NSRun(case, max(1, iterations), initial)
+    r.iterate(iterations)
+    r.torch.cuda.synchronize()
+    d = r.divergence()
+    if d is not None:
+        raise DivergenceError(*d)
+    return r

@@ -17,13 +17,15 @@ from paper_1304_7654_b200 import native
 from paper_1304_7654_b200.exceptions import NativeUnavailable
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADER = os.path.join(REPO, "include", "hbgpu.h")
+HEADERS = [os.path.join(REPO, "include", h) for h in ("hbgpu.h", "hbns.h")]
 
 
 def declared_functions():
-    text = open(HEADER).read()
-    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    names = re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\**\s*(hbgpu_[a-z_0-9]+)\s*\(", text, flags=re.M)
+    names = []
+    for header in HEADERS:
+        text = open(header).read()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        names += re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\**\s*(hb(?:gpu|ns)_[a-z_0-9]+)\s*\(", text, flags=re.M)
     return sorted(set(names))
 
 

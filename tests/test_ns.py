@@ -1,0 +1,91 @@
+"""North-star physics: HB Euler / laminar NS.
+
+The reference has no flux physics (hbcore.py:3-13), so this
+row's parity is UNPINNED: the GPU path (hb_ns.cu) is checked bitwise against
+oracle/ns_oracle.c, a builder-written independent restatement of the same
+specification (nsflow.py's docstring) -- not against any reference output.
+
+CPU: the host geometry (numpy) equals the C oracle's bit for bit; the oracle
+runs stay physical and converge.  GPU: fields (halos included) and forces
+bitwise, residual norms at rtol 1e-12, on scaled-down versions of every
+BASELINE config (sinusoidal Euler, tanh-stretched NS with a no-slip wall and
+cuts, the pitching NACA 0012 O-grid with grid velocity, a slip wall and a
+self-cut).
+"""
+
+import numpy as np
+import pytest
+
+import ns_oracle
+from paper_1304_7654_b200 import nsflow
+
+SCALES = {"C0": 2, "C1": 8, "C2": 16, "C3": 32, "C4": 128}
+
+
+@pytest.mark.parametrize("key", sorted(SCALES))
+def test_host_geometry_equals_oracle_geometry(key):
+    case = nsflow.ns_workload(key, scale=SCALES[key])
+    o = ns_oracle.OracleNS(case)
+    for b in case.blocks:
+        m = nsflow.metrics(b)
+        for k, v in m.items():
+            assert np.array_equal(v, o.blocks[b.id].geo[k]), (key, b.id, k)
+        assert (m["vol"][:, 2:-2, 2:-2] > 0).all(), "cells must be right-handed with positive area"
+
+
+@pytest.mark.parametrize("key,iters", [("C0", 60), ("C1", 40), ("C2", 40)])
+def test_oracle_runs_converge_and_stay_physical(key, iters):
+    case = nsflow.ns_workload(key, scale=SCALES[key] * 2)
+    o = ns_oracle.run(case, iters)
+    assert o.norms[-1] < o.norms[0]
+    for q in o.fields().values():
+        rho = q[:, 0, 2:-2, 2:-2]
+        assert np.isfinite(q).all() and rho.min() > 0.5 and rho.max() < 2.0
+
+
+def test_freestream_is_preserved():
+    """A uniform freestream (the same in every snapshot) has no HB source
+    (the rows of D sum to zero), no JST dissipation and no viscous flux; its
+    residual is the rounding of the metric closure only."""
+    case = nsflow.ns_workload("C0", scale=8)
+    case.dalpha_deg = 0.0
+    winf = nsflow.freestream(case)
+    P = case.planes
+
+    def uniform(b):
+        q = np.zeros((P, 4, b.nj + 4, b.ni + 4))
+        q[:] = winf[:, :, None, None]
+        return q
+
+    o = ns_oracle.OracleNS(case, initial=uniform)
+    o.iterate(1)
+    q = o.fields()[0][:, :, 2:-2, 2:-2]
+    assert np.abs(q - winf[:, :, None, None]).max() < 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key,iters", [("C0", 12), ("C1", 6), ("C2", 6), ("C3", 4), ("C4", 3)])
+def test_gpu_matches_oracle_bitwise(key, iters, cuda):
+    case = nsflow.ns_workload(key, scale=SCALES[key])
+    want = ns_oracle.run(case, iters)
+    got = nsflow.run_ns(case, iters)
+    gf, wf = got.fields(), want.fields()
+    for b in wf:
+        if not np.array_equal(gf[b], wf[b]):
+            bad = np.argwhere(gf[b] != wf[b])
+            raise AssertionError(f"{key} block {b}: {len(bad)} values differ, first {bad[0]}: "
+                                 f"{gf[b][tuple(bad[0])]!r} vs {wf[b][tuple(bad[0])]!r}")
+    np.testing.assert_allclose(got.norm_history(), want.norms, rtol=1e-12, atol=0)
+    assert np.array_equal(got.force_history(), np.stack(want.forces))
+
+
+@pytest.mark.gpu
+def test_gpu_full_size_c2_converges(cuda):
+    """BASELINE config 2 at full size (512 x 256, P = 9, pitching, 100 of its
+    500 iterations): the GPU run stays physical and its residual falls."""
+    case = nsflow.ns_workload("C2")
+    got = nsflow.run_ns(case, 100)
+    norms = got.norm_history()
+    assert np.isfinite(norms).all() and norms[-1] < 0.5 * norms[0]
+    q = got.fields()[0][:, 0, 2:-2, 2:-2]
+    assert q.min() > 0.5 and q.max() < 2.0
