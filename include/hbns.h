@@ -42,6 +42,8 @@ typedef struct hbns_block {
 typedef struct hbns_args {
     double *w[3];                /* state slots: 0 = iteration start         */
     double *r;                   /* residual pool                             */
+    double *prim;                /* primitive pool (u, v, p, c, e) of every
+                                    cell incl. halos: 5/4 of a state pool    */
     double *dt;                  /* local time steps                          */
     const double *xc, *yc, *vol; /* cell geometry                             */
     const double *six, *siy, *gi;/* i-face normals, grid flux (moving)        */

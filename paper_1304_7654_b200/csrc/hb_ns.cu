@@ -16,6 +16,8 @@
 //                       (side, layer, face cell, snapshot)
 //   ns_corner_kernel    corner halos
 //   ns_timestep_kernel  local time step, one thread per cell
+//   ns_prim_kernel      u, v, p, c, e of every cell (halos included) once per
+//                       stage: the flux kernel reads each cell's up to 20 times
 //   ns_residual_kernel  face fluxes -> R, one thread per (cell, snapshot)
 //   ns_update_kernel    HB source + RK update, one thread per (cell,
 //                       snapshot, variable); stage-1 R_rho^2 partials per CTA
@@ -33,12 +35,6 @@ constexpr double PR = 0.72;
 constexpr double K2 = 0.5;
 constexpr double K4 = 1.0 / 64.0;
 constexpr int NV = 4;
-
-struct Blk {
-    const hbns_block *m;
-    int ni, nj, Pg;
-    __device__ Blk(const hbns_block &b, int pg) : m(&b), ni(b.ni), nj(b.nj), Pg(pg) {}
-};
 
 __device__ __forceinline__ int64_t ws(const hbns_block &b, int n, int k, int j, int i) {
     return b.w_off + (((int64_t)n * NV + k) * (b.nj + 4) + (j + 1)) * (b.ni + 4) + (i + 1);
@@ -59,6 +55,12 @@ __device__ __forceinline__ int64_t fj(const hbns_block &b, int g, int j, int i) 
 struct Prim {
     double r, ru, rv, re, u, v, p, c, e;
 };
+
+// the primitive pool (u, v, p, c, e) of every cell of a slot, halos included
+constexpr int NPRIM = 5;
+__device__ __forceinline__ int64_t ps_(const hbns_block &b, int n, int k, int j, int i) {
+    return b.w_off / NV * NPRIM + (((int64_t)n * NPRIM + k) * (b.nj + 4) + (j + 1)) * (b.ni + 4) + (i + 1);
+}
 
 __device__ __forceinline__ Prim prim(const double *w, int64_t stride) {
     Prim q;
@@ -153,15 +155,52 @@ __global__ void ns_corner_kernel(hbns_args a, double *w) {
     w[ws(b, n, k, j, i)] = w[ws(b, n, k, src, i)];
 }
 
+// ---- primitives: one conversion per cell and stage (the flux kernel reads
+// each cell's u, v, p, c, e up to 20 times) -----------------------------------------------
+
+__global__ void ns_prim_kernel(hbns_args a, const double *w) {
+    // grid.y = block, grid.z = snapshot; x over all cells incl. the halo ring
+    const hbns_block &b = a.blocks[blockIdx.y];
+    const int n = blockIdx.z;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int wi = b.ni + 4;
+    if (t >= wi * (b.nj + 4)) return;
+    const int i = t % wi - 1, j = t / wi - 1;
+    const int64_t st = (int64_t)(b.nj + 4) * (b.ni + 4);
+    const Prim q = prim(w + ws(b, n, 0, j, i), st);
+    a.prim[ps_(b, n, 0, j, i)] = q.u;
+    a.prim[ps_(b, n, 1, j, i)] = q.v;
+    a.prim[ps_(b, n, 2, j, i)] = q.p;
+    a.prim[ps_(b, n, 3, j, i)] = q.c;
+    a.prim[ps_(b, n, 4, j, i)] = q.e;
+}
+
+// a cell's state and primitives, the latter from the pool
+__device__ __forceinline__ Prim load_prim(const hbns_args &a, const hbns_block &b, const double *w, int n, int j,
+                                          int i) {
+    const int64_t st = (int64_t)(b.nj + 4) * (b.ni + 4);
+    const double *c = w + ws(b, n, 0, j, i);
+    Prim q;
+    q.r = c[0];
+    q.ru = c[st];
+    q.rv = c[2 * st];
+    q.re = c[3 * st];
+    q.u = a.prim[ps_(b, n, 0, j, i)];
+    q.v = a.prim[ps_(b, n, 1, j, i)];
+    q.p = a.prim[ps_(b, n, 2, j, i)];
+    q.c = a.prim[ps_(b, n, 3, j, i)];
+    q.e = a.prim[ps_(b, n, 4, j, i)];
+    return q;
+}
+
 // ---- fluxes -----------------------------------------------------------------------------
 
 __device__ void face_flux(const hbns_args &a, const hbns_block &b, const double *w, int n, int g, int jL, int iL,
                           int dj, int di, double sx, double sy, double gf, double *out) {
-    const int64_t st = (int64_t)(b.nj + 4) * (b.ni + 4);
     const int jR = jL + dj, iR = iL + di;
-    const Prim L = prim(w + ws(b, n, 0, jL, iL), st), R = prim(w + ws(b, n, 0, jR, iR), st);
-    const Prim LL = prim(w + ws(b, n, 0, jL - dj, iL - di), st);
-    const Prim RR = prim(w + ws(b, n, 0, jR + dj, iR + di), st);
+    const Prim L = load_prim(a, b, w, n, jL, iL), R = load_prim(a, b, w, n, jR, iR);
+    const Prim LL = load_prim(a, b, w, n, jL - dj, iL - di);
+    const Prim RR = load_prim(a, b, w, n, jR + dj, iR + di);
     const double unL = add(mul(L.u, sx), mul(L.v, sy)), unR = add(mul(R.u, sx), mul(R.v, sy));
     const double urL = sub(unL, gf), urR = sub(unR, gf);
     double FL[NV] = {mul(L.r, urL), add(mul(L.ru, urL), mul(L.p, sx)), add(mul(L.rv, urL), mul(L.p, sy)),
@@ -179,8 +218,8 @@ __device__ void face_flux(const hbns_args &a, const hbns_block &b, const double 
     const bool visc = a.mu > 0.0;
     if (visc) {
         const int tj = di, ti = dj;
-        const Prim Lp = prim(w + ws(b, n, 0, jL + tj, iL + ti), st), Rp = prim(w + ws(b, n, 0, jR + tj, iR + ti), st);
-        const Prim Lm = prim(w + ws(b, n, 0, jL - tj, iL - ti), st), Rm = prim(w + ws(b, n, 0, jR - tj, iR - ti), st);
+        const Prim Lp = load_prim(a, b, w, n, jL + tj, iL + ti), Rp = load_prim(a, b, w, n, jR + tj, iR + ti);
+        const Prim Lm = load_prim(a, b, w, n, jL - tj, iL - ti), Rm = load_prim(a, b, w, n, jR - tj, iR - ti);
         const double xL = a.xc[cc(b, g, jL, iL)], xR = a.xc[cc(b, g, jR, iR)];
         const double yL = a.yc[cc(b, g, jL, iL)], yR = a.yc[cc(b, g, jR, iR)];
         const double xLp = a.xc[cc(b, g, jL + tj, iL + ti)], xRp = a.xc[cc(b, g, jR + tj, iR + ti)];
@@ -386,9 +425,11 @@ extern "C" int hbns_timestep(const hbns_args *a, int32_t slot, void *stream) {
 }
 
 extern "C" int hbns_residual(const hbns_args *a, int32_t slot, void *stream) {
-    ns_residual_kernel<<<dim3((a->max_cells + 127) / 128, a->nblocks, a->P), 128, 0, (cudaStream_t)stream>>>(
-        *a, a->w[slot]);
-    hbgpu_count_launch(1);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int halo_cells = (a->max_len + 4) * (a->max_len + 4);
+    ns_prim_kernel<<<dim3((halo_cells + 127) / 128, a->nblocks, a->P), 128, 0, s>>>(*a, a->w[slot]);
+    ns_residual_kernel<<<dim3((a->max_cells + 127) / 128, a->nblocks, a->P), 128, 0, s>>>(*a, a->w[slot]);
+    hbgpu_count_launch(2);
     return check("hbns_residual");
 }
 

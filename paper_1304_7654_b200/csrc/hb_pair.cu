@@ -169,9 +169,15 @@ static_assert(CW == 8, "two consumer warpgroups + one helper warpgroup");
 // per tile geometry: the PT = 4 edge warp carries 3 (side, pde, plane)
 // items per lane and needs more registers.  Budget: 256 * (consumer - 168)
 // <= 128 * (168 - helper) + (65536 - 384 * 168).
+#ifndef HBGPU_PAIR_HELPER_REGS   // measurement builds may move the split
+#define HBGPU_PAIR_HELPER_REGS 64
+#endif
+#ifndef HBGPU_PAIR_CONSUMER_REGS
+#define HBGPU_PAIR_CONSUMER_REGS 216
+#endif
 template <int PT> struct PairRegs {
-    static constexpr int HELPER = PT == 1 ? 64 : 80;
-    static constexpr int CONSUMER = PT == 1 ? 216 : 208;
+    static constexpr int HELPER = PT == 1 ? HBGPU_PAIR_HELPER_REGS : 80;
+    static constexpr int CONSUMER = PT == 1 ? HBGPU_PAIR_CONSUMER_REGS : 208;
     static_assert(256 * (CONSUMER - 168) <= 128 * (168 - HELPER) + (65536 - PAIR_THREADS * 168), "regs");
 };
 

@@ -381,7 +381,7 @@ def _ns_types():
                     ("fj_off", i64), ("part_off", i64), ("ni", i32), ("nj", i32), ("kinds", i32 * 4)]
 
     class Args(ctypes.Structure):
-        _fields_ = [("w", vp * 3), ("r", vp), ("dt", vp), ("xc", vp), ("yc", vp), ("vol", vp),
+        _fields_ = [("w", vp * 3), ("r", vp), ("prim", vp), ("dt", vp), ("xc", vp), ("yc", vp), ("vol", vp),
                     ("six", vp), ("siy", vp), ("gi", vp), ("sjx", vp), ("sjy", vp), ("gj", vp),
                     ("blocks", vp), ("winf", vp), ("dmat", vp), ("status", vp), ("norm_part", vp),
                     ("norms", vp), ("forces", vp), ("mu", f64), ("cfl", f64), ("omega_nh", f64),
@@ -440,6 +440,7 @@ class NSRun:
             q = initial(b) if initial is not None else initial_state(case, b)
             self.slot_view(0, b).copy_(torch.from_numpy(np.ascontiguousarray(q)))
         self.r = torch.zeros(max(1, r_off), dtype=f64, device=dev)
+        self.prim = torch.zeros(wsz // 4 * 5, dtype=f64, device=dev)
         self.dt = torch.zeros(max(1, dt_off), dtype=f64, device=dev)
         self.geo = {k: (torch.from_numpy(np.concatenate(v)).to(dev) if v else torch.zeros(1, dtype=f64, device=dev))
                     for k, v in pools.items()}
@@ -457,7 +458,7 @@ class NSRun:
         a = Args()
         for k in range(3):
             a.w[k] = self.slots[k].data_ptr()
-        a.r, a.dt = self.r.data_ptr(), self.dt.data_ptr()
+        a.r, a.prim, a.dt = self.r.data_ptr(), self.prim.data_ptr(), self.dt.data_ptr()
         for name in pools:
             setattr(a, name, self.geo[name].data_ptr())
         a.blocks, a.winf, a.dmat = self.t_blocks.data_ptr(), self.winf.data_ptr(), self.dmat.data_ptr()
