@@ -20,7 +20,8 @@
 //                       stage: the flux kernel reads each cell's up to 20 times
 //   ns_residual_kernel  face fluxes -> R, one thread per (cell, snapshot)
 //   ns_update_kernel    HB source + RK update, one thread per (cell,
-//                       snapshot, variable); stage-1 R_rho^2 partials per CTA
+//                       variable) for all snapshots; stage-1 R_rho^2 partials
+//                       per CTA, folded by ns_norm_kernel (a warp per block)
 //   ns_forces_kernel    wall pressure forces, one thread per snapshot
 // Cut halos move with hbgpu_halo (two directions per cut and layer).
 
@@ -321,27 +322,38 @@ __global__ void ns_timestep_kernel(hbns_args a, const double *w) {
 
 constexpr int UPD_THREADS = 256;
 
+// one thread per (cell, variable k), all P snapshots: each W_m is loaded once
+// for the P outputs of the HB source
+template <int P>
 __global__ void __launch_bounds__(UPD_THREADS) ns_update_kernel(hbns_args a, const double *w_in, const double *w0,
                                                                   double *w_out, double coef, int want_norm) {
-    // grid.y = block, grid.z = snapshot * 4 + variable; x over interior cells
+    // grid.y = block, grid.z = variable; x over interior cells
     __shared__ double red[UPD_THREADS];
     const hbns_block &b = a.blocks[blockIdx.y];
-    const int n = blockIdx.z / NV, k = blockIdx.z % NV;
-    const int g = a.Pg > 1 ? n : 0;
+    const int k = blockIdx.z;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     double sq = 0.0;
     if (t < b.ni * b.nj) {
         const int i = t % b.ni + 1, j = t / b.ni + 1;
-        const double V = a.vol[cc(b, g, j, i)];
-        double s = mul(a.dmat[n * a.P], w_in[ws(b, 0, k, j, i)]);
-        for (int m = 1; m < a.P; ++m) s = add(s, mul(a.dmat[n * a.P + m], w_in[ws(b, m, k, j, i)]));
-        const double R = add(a.r[rs(b, n, k, j, i)], mul(V, s));
-        if (want_norm && k == 0) sq = mul(R, R);
-        const double v = sub(w0[ws(b, n, k, j, i)], mul(dv(mul(coef, a.dt[b.dt_off + (int64_t)(j - 1) * b.ni + (i - 1)]), V), R));
-        w_out[ws(b, n, k, j, i)] = v;
-        if (!isfinite(v)) {
-            const long long lin = (((long long)(n * NV + k) * b.nj + (j - 1)) * b.ni) + (i - 1);
-            atomicMin(a.status + blockIdx.y, (unsigned long long)lin);
+        double wm[P];
+#pragma unroll
+        for (int m = 0; m < P; ++m) wm[m] = w_in[ws(b, m, k, j, i)];
+        const double dtc = a.dt[b.dt_off + (int64_t)(j - 1) * b.ni + (i - 1)];
+#pragma unroll
+        for (int n = 0; n < P; ++n) {
+            const int g = a.Pg > 1 ? n : 0;
+            const double V = a.vol[cc(b, g, j, i)];
+            double s = mul(a.dmat[n * P], wm[0]);
+#pragma unroll
+            for (int m = 1; m < P; ++m) s = add(s, mul(a.dmat[n * P + m], wm[m]));
+            const double R = add(a.r[rs(b, n, k, j, i)], mul(V, s));
+            if (want_norm && k == 0) sq = __fma_rn(R, R, sq);
+            const double v = sub(w0[ws(b, n, k, j, i)], mul(dv(mul(coef, dtc), V), R));
+            w_out[ws(b, n, k, j, i)] = v;
+            if (!isfinite(v)) {
+                const long long lin = (((long long)(n * NV + k) * b.nj + (j - 1)) * b.ni) + (i - 1);
+                atomicMin(a.status + blockIdx.y, (unsigned long long)lin);
+            }
         }
     }
     if (want_norm && k == 0) {
@@ -351,24 +363,29 @@ __global__ void __launch_bounds__(UPD_THREADS) ns_update_kernel(hbns_args a, con
             if (threadIdx.x < s2) red[threadIdx.x] = add(red[threadIdx.x], red[threadIdx.x + s2]);
             __syncthreads();
         }
-        if (threadIdx.x == 0) a.norm_part[b.part_off + (int64_t)n * gridDim.x + blockIdx.x] = red[0];
+        if (threadIdx.x == 0) a.norm_part[b.part_off + blockIdx.x] = red[0];
     }
 }
 
-// stage-1 norm: every block's per-CTA partials, blocks / snapshots / CTAs in order
+// stage-1 norm: one warp per block folds that block's CTA partials in a fixed
+// lane-strided order and shuffle tree; one thread then folds blocks in order
 __global__ void ns_norm_kernel(hbns_args a, int iter, int ctas) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double s = 0.0;
-    for (int bk = 0; bk < a.nblocks; ++bk) {
+    __shared__ double blk_sum[1024];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int bk = warp; bk < a.nblocks; bk += nw) {
         const hbns_block &b = a.blocks[bk];
-        for (int n = 0; n < a.P; ++n)
-            for (int c = 0; c < ctas; ++c) {
-                const int64_t cells = (int64_t)b.ni * b.nj;
-                if ((int64_t)c * UPD_THREADS >= cells) break;
-                s = add(s, a.norm_part[b.part_off + (int64_t)n * ctas + c]);
-            }
+        const int used = (int)(((int64_t)b.ni * b.nj + UPD_THREADS - 1) / UPD_THREADS);
+        double s = 0.0;
+        for (int c = lane; c < used && c < ctas; c += 32) s = add(s, a.norm_part[b.part_off + c]);
+        for (int o = 16; o > 0; o >>= 1) s = add(s, __shfl_down_sync(0xffffffffu, s, o));
+        if (lane == 0) blk_sum[bk] = s;
     }
-    a.norms[iter] = __dsqrt_rn(s);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int bk = 0; bk < a.nblocks; ++bk) s = add(s, blk_sum[bk]);
+        a.norms[iter] = __dsqrt_rn(s);
+    }
 }
 
 __global__ void ns_forces_kernel(hbns_args a, const double *w, int iter) {
@@ -437,11 +454,24 @@ extern "C" int hbns_update(const hbns_args *a, int32_t slot_in, int32_t slot_out
                            int32_t want_norm, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     const int ctas = (a->max_cells + UPD_THREADS - 1) / UPD_THREADS;
-    ns_update_kernel<<<dim3(ctas, a->nblocks, a->P * NV), UPD_THREADS, 0, s>>>(*a, a->w[slot_in], a->w[0],
-                                                                             a->w[slot_out], coef, want_norm);
+    if (a->nblocks > 1024) {
+        hbgpu_set_error("hbns_update: at most 1024 blocks");
+        return HBGPU_ERR_ARG;
+    }
+    const dim3 grid(ctas, a->nblocks, NV);
+    switch (a->P) {
+        case 1: ns_update_kernel<1><<<grid, UPD_THREADS, 0, s>>>(*a, a->w[slot_in], a->w[0], a->w[slot_out], coef, want_norm); break;
+        case 3: ns_update_kernel<3><<<grid, UPD_THREADS, 0, s>>>(*a, a->w[slot_in], a->w[0], a->w[slot_out], coef, want_norm); break;
+        case 5: ns_update_kernel<5><<<grid, UPD_THREADS, 0, s>>>(*a, a->w[slot_in], a->w[0], a->w[slot_out], coef, want_norm); break;
+        case 7: ns_update_kernel<7><<<grid, UPD_THREADS, 0, s>>>(*a, a->w[slot_in], a->w[0], a->w[slot_out], coef, want_norm); break;
+        case 9: ns_update_kernel<9><<<grid, UPD_THREADS, 0, s>>>(*a, a->w[slot_in], a->w[0], a->w[slot_out], coef, want_norm); break;
+        default:
+            hbgpu_set_error("hbns_update: P = %d not templated (1..9 odd)", a->P);
+            return HBGPU_ERR_UNSUPPORTED;
+    }
     int n = 1;
     if (want_norm) {
-        ns_norm_kernel<<<1, 32, 0, s>>>(*a, iter, ctas);
+        ns_norm_kernel<<<1, 1024, 0, s>>>(*a, iter, ctas);
         ++n;
     }
     hbgpu_count_launch(n);

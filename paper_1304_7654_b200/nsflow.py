@@ -420,7 +420,7 @@ class NSRun:
             e = table[k]
             e.w_off, e.r_off, e.dt_off = wsz, r_off, dt_off
             e.c_off, e.fi_off, e.fj_off = c_off, fi_off, fj_off
-            e.part_off = k * P * ctas
+            e.part_off = k * ctas
             e.ni, e.nj = b.ni, b.nj
             for s in range(4):
                 e.kinds[s] = b.kinds[s]
@@ -448,7 +448,7 @@ class NSRun:
         self.winf = torch.from_numpy(np.ascontiguousarray(freestream(case))).to(dev)
         self.dmat = torch.from_numpy(spectral_matrix(case).copy()).to(dev)
         self.status = torch.full((len(blocks),), -1, dtype=torch.int64, device=dev)
-        self.norm_part = torch.zeros(len(blocks) * P * ctas, dtype=f64, device=dev)
+        self.norm_part = torch.zeros(len(blocks) * ctas, dtype=f64, device=dev)
         self.norms = torch.zeros(max(1, max_iters), dtype=f64, device=dev)
         self.forces = torch.zeros(max(1, max_iters) * P * 2, dtype=f64, device=dev)
         halo = _halo_rows(case, self.w_off)
