@@ -73,18 +73,34 @@ __global__ void hazard_scan_kernel(const double *slot, const hbgpu_block *blocks
 
 // ---- residual norm ----------------------------------------------------------
 
-// per block: sequential sum of its (tile, consumer warp) partials in tile order
-// (sumsq holds max_iters rows: an iteration counter at or past it writes nothing)
-__global__ void norm_fold_kernel(const hbgpu_block *blocks, int nblocks, const double *part,
-                                 double *sumsq, const int32_t *iter, int max_iters) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nblocks || *iter >= max_iters || *iter < 0) return;
+// per block: one CTA folds its (tile, consumer warp) partials -- thread t
+// takes partials t, t + NF, t + 2 NF, ... in order, then a fixed-shape tree
+// over the threads.  Deterministic for a given tile layout (the norm is not a
+// reference quantity; the oracle's fsum agrees to rtol 1e-12).  sumsq holds
+// max_iters rows: an iteration counter at or past it writes nothing.
+constexpr int NF_THREADS = 256;
+
+__global__ void __launch_bounds__(NF_THREADS) norm_fold_kernel(const hbgpu_block *blocks, int nblocks,
+                                                               const double *part, double *sumsq,
+                                                               const int32_t *iter, int max_iters) {
+    __shared__ double red[NF_THREADS];
+    const int b = blockIdx.x;
+    const int it = *iter;
+    if (b >= nblocks || it >= max_iters || it < 0) return;
     const hbgpu_block &blk = blocks[b];
-    double s = 0.0;
-    // one partial per (tile, pde), tiles of a block contiguous
+    // one partial per (tile, consumer warp), tiles of a block contiguous
     constexpr int W = HBGPU_TILE_WARPS;
-    for (int c = 0; c < blk.ntiles * W; ++c) s = radd(s, part[(int64_t)blk.tile_begin * W + c]);
-    sumsq[(int64_t)(*iter) * nblocks + b] = s;
+    const int64_t n = (int64_t)blk.ntiles * W;
+    const double *p = part + (int64_t)blk.tile_begin * W;
+    double s = 0.0;
+    for (int64_t c = threadIdx.x; c < n; c += NF_THREADS) s = radd(s, p[c]);
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = NF_THREADS / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] = radd(red[threadIdx.x], red[threadIdx.x + w]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) sumsq[(int64_t)it * nblocks + b] = red[0];
 }
 
 // one thread per iteration: the rank-global per-block sums of R^2 (columns in
@@ -100,16 +116,28 @@ __global__ void norm_totals_kernel(const double *sumsq, int iters, int nblocks, 
 
 // ---- forces (hbcore.py:359-382) --------------------------------------------
 
-// one thread per (coefficient k, plane n, body): a strict left-to-right fold
-// of h*q over the body's face segments in reference order.  Then one thread
-// advances the device iteration counter (this is the iteration's last kernel).
-// hist holds max_iters rows; an iteration counter at or past it writes no
-// history (the engine refuses to issue such iterations in the first place).
-__global__ void forces_kernel(const double *slot, const hbgpu_force_seg *segs, int nsegs,
-                              int planes, int nbody, double *hist, int32_t *iter, int max_iters) {
+// One warp per (coefficient k, plane n, body) output: a strict left-to-right
+// fold of h*q over the body's face segments in reference order.  The warp
+// loads the face in chunks of FCH cells (lanes on consecutive cells, the next
+// chunk's loads in flight during the fold), forms the products h*q in
+// parallel (each rounded once, as in the reference), and lane 0 adds them in
+// order from shared memory -- the fold itself is the only serial part.  Then
+// one thread advances the device iteration counter (this is the iteration's
+// last kernel).  hist holds max_iters rows; an iteration counter at or past
+// it writes no history (the engine refuses to issue such iterations anyway).
+constexpr int FORCE_WARPS = 32;
+constexpr int FCH = 128;
+constexpr int FU = FCH / 32;
+
+__global__ void __launch_bounds__(FORCE_WARPS * 32) forces_kernel(const double *slot, const hbgpu_force_seg *segs,
+                                                                  int nsegs, int planes, int nbody, double *hist,
+                                                                  int32_t *iter, int max_iters) {
+    __shared__ double prod[FORCE_WARPS][FCH];
     const int it = *iter;
     const int total = (it >= 0 && it < max_iters) ? 3 * planes * nbody : 0;
-    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    double *buf = prod[warp];
+    for (int t = warp; t < total; t += nwarps) {
         const int body = t % nbody;
         const int n = (t / nbody) % planes;
         const int k = t / (nbody * planes);
@@ -118,17 +146,34 @@ __global__ void forces_kernel(const double *slot, const hbgpu_force_seg *segs, i
             const hbgpu_force_seg g = segs[s];
             if (g.body != body) continue;
             const double *f = slot + g.start + (int64_t)(n * NPDE + k) * g.ps;
-            int c = 0;
-            for (; c + 8 <= g.length; c += 8) {
-                double v[8];
+            double v[FU];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = f[(int64_t)(c + u) * g.stride];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) acc = radd(acc, rmul(g.h, v[u]));
+            for (int u = 0; u < FU; ++u) {
+                const int c = lane + 32 * u;
+                v[u] = c < g.length ? f[(int64_t)c * g.stride] : 0.0;
             }
-            for (; c < g.length; ++c) acc = radd(acc, rmul(g.h, f[(int64_t)c * g.stride]));
+            for (int c0 = 0; c0 < g.length; c0 += FCH) {
+#pragma unroll
+                for (int u = 0; u < FU; ++u) buf[lane + 32 * u] = rmul(g.h, v[u]);
+                __syncwarp();
+#pragma unroll
+                for (int u = 0; u < FU; ++u) {
+                    const int c = c0 + FCH + lane + 32 * u;
+                    v[u] = c < g.length ? f[(int64_t)c * g.stride] : 0.0;
+                }
+                if (lane == 0) {
+                    const int m = min(FCH, g.length - c0);
+                    int e = 0;
+                    for (; e + 8 <= m; e += 8) {
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) acc = radd(acc, buf[e + u]);
+                    }
+                    for (; e < m; ++e) acc = radd(acc, buf[e]);
+                }
+                __syncwarp();
+            }
         }
-        hist[(int64_t)it * total + t] = acc;
+        if (lane == 0) hist[(int64_t)it * total + t] = acc;
     }
     __syncthreads();
     if (threadIdx.x == 0) *iter = it + 1;
@@ -261,8 +306,13 @@ extern "C" int hbgpu_norm_totals(const double *sumsq, int32_t iters, int32_t nbl
 
 extern "C" int hbgpu_norm_fold(const hbgpu_block *blocks, int32_t nblocks, const double *norm_part,
                                double *sumsq, const int32_t *iter, int32_t max_iters, void *stream) {
-    norm_fold_kernel<<<(nblocks + 127) / 128, 128, 0, (cudaStream_t)stream>>>(blocks, nblocks, norm_part,
-                                                                            sumsq, iter, max_iters);
+    if (nblocks <= 0) return HBGPU_OK;
+    if (nblocks > 65535) {
+        hbgpu_set_error("hbgpu_norm_fold: %d blocks exceed one CTA per block", nblocks);
+        return HBGPU_ERR_ARG;
+    }
+    norm_fold_kernel<<<(unsigned)nblocks, NF_THREADS, 0, (cudaStream_t)stream>>>(blocks, nblocks, norm_part, sumsq,
+                                                                                iter, max_iters);
     hbgpu_count_launch(1);
     return hbgpu_check_launch("hbgpu_norm_fold");
 }
@@ -270,9 +320,9 @@ extern "C" int hbgpu_norm_fold(const hbgpu_block *blocks, int32_t nblocks, const
 extern "C" int hbgpu_forces(const double *slot, const hbgpu_force_seg *segs, int32_t nsegs,
                             int32_t planes, int32_t nbody, double *hist, int32_t *iter, int32_t max_iters,
                             void *stream) {
-    int threads = 3 * planes * nbody;
-    threads = threads < 32 ? 32 : (threads > 1024 ? 1024 : ((threads + 31) / 32) * 32);
-    forces_kernel<<<1, threads, 0, (cudaStream_t)stream>>>(slot, segs, nsegs, planes, nbody, hist, iter,
+    int warps = 3 * planes * nbody;
+    warps = warps < 1 ? 1 : (warps > FORCE_WARPS ? FORCE_WARPS : warps);
+    forces_kernel<<<1, warps * 32, 0, (cudaStream_t)stream>>>(slot, segs, nsegs, planes, nbody, hist, iter,
                                                            max_iters);
     hbgpu_count_launch(1);
     return hbgpu_check_launch("hbgpu_forces");

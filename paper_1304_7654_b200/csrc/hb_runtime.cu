@@ -231,14 +231,20 @@ struct hbgpu_engine {
     bool split = false;
     cudaStream_t comm_s = nullptr;
     cudaEvent_t ev_pack = nullptr, ev_comm = nullptr;
-    // small schedule: per-CTA stage-0 partials of the cooperative kernel
+    // the stage-0 norm fold runs on aux_s, off the critical path: forked
+    // after the first pass, joined before the forces (which advance the
+    // iteration counter the fold reads); captured into the graph as a branch
+    cudaStream_t aux_s = nullptr;
+    cudaEvent_t ev_nf_fork = nullptr, ev_nf_join = nullptr;
+    // small schedule: per-warp-task stage-0 partials of the cooperative kernel
     double *small_part = nullptr;
-    int small_cap = 0;
+    int small_tasks = 0;
 };
 
 namespace hbgpu {
-int small_iterations(const hbgpu_engine_desc &d, int32_t it0, int32_t iters, cudaStream_t s, double **part_buf,
-                     int *part_cap);
+int small_prepare(const hbgpu_engine_desc &d, int *tasks, double **part_buf);
+int small_iterations(const hbgpu_engine_desc &d, int32_t it0, int32_t iters, cudaStream_t s, double *part_buf,
+                     int tasks);
 }
 
 namespace {
@@ -392,16 +398,28 @@ int halo_moves(const hbgpu_engine_desc &d, double *slot, const hbgpu_halo_dir *d
     return hbgpu_halo(slot, d.sendbuf, d.recvbuf, dirs, n, max_len, d.planes, s);
 }
 
-// stage / phase `st` (+ the norm fold after the first stage, + its halo moves)
-int run_stage(hbgpu_engine *e, int st, cudaStream_t s) {
+// stage / phase `st` (+ the norm fold after the first stage, + its halo moves).
+// fork_norm: the norm fold goes to aux_s (joined by join_norm) instead of
+// between the pass and its halo moves.
+int run_stage(hbgpu_engine *e, int st, cudaStream_t s, bool fork_norm = false) {
     const hbgpu_engine_desc &d = e->d;
     hbgpu_stage_args a;
     if (d.fused) fused_args(d, st, a);
     else single_args(d, st, a);
     if (d.fused && (st == 0 || st == 2)) return hbgpu_band(&a, s);
     int rc = hbgpu_stage(&a, s);
-    if (!rc && a.norm_part != nullptr)
-        rc = hbgpu_norm_fold(d.blocks, d.nblocks, d.norm_part, d.sumsq, d.iter, d.max_iters, s);
+    if (!rc && a.norm_part != nullptr) {
+        if (fork_norm) {
+            if (cudaEventRecord(e->ev_nf_fork, s) != cudaSuccess ||
+                cudaStreamWaitEvent(e->aux_s, e->ev_nf_fork, 0) != cudaSuccess)
+                return hbgpu_check_launch("norm fold fork");
+            rc = hbgpu_norm_fold(d.blocks, d.nblocks, d.norm_part, d.sumsq, d.iter, d.max_iters, e->aux_s);
+            if (!rc && cudaEventRecord(e->ev_nf_join, e->aux_s) != cudaSuccess)
+                rc = hbgpu_check_launch("norm fold record");
+        } else {
+            rc = hbgpu_norm_fold(d.blocks, d.nblocks, d.norm_part, d.sumsq, d.iter, d.max_iters, s);
+        }
+    }
     const PostMoves m = post_moves(d, st);
     if (!rc) rc = halo_moves(d, a.out, m.dirs, m.n, m.max_len, s);
     return rc;
@@ -464,11 +482,14 @@ int one_iteration(hbgpu_engine *e, cudaStream_t s) {
         if (e->split && pass_phase(d, st)) {
             rc = run_split(e, st, s);
         } else {
-            rc = run_stage(e, st, s);
+            rc = run_stage(e, st, s, true);
             if (!rc) rc = exchange_remote(e, d.slot[out_slot(d, st)], s);
         }
         if (rc) return rc;
     }
+    // join the forked norm fold (no-op when the fold ran in line)
+    if (!e->split && cudaStreamWaitEvent(s, e->ev_nf_join, 0) != cudaSuccess)
+        return hbgpu_check_launch("norm fold join");
     return hbgpu_forces(d.slot[0], d.segs, d.nsegs, d.planes, d.nbody, d.force_hist, d.iter, d.max_iters, s);
 }
 
@@ -510,7 +531,10 @@ extern "C" int hbgpu_engine_create(const hbgpu_engine_desc *desc, hbgpu_engine *
     e->d.recvs = nullptr;
     if (cudaStreamCreateWithFlags(&e->work, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&e->ev_in, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&e->ev_out, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&e->ev_out, cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&e->aux_s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_nf_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_nf_join, cudaEventDisableTiming) != cudaSuccess) {
         int rc = hbgpu_check_launch("hbgpu_engine_create");
         hbgpu_engine_destroy(e);
         return rc ? rc : HBGPU_ERR_CUDA;
@@ -525,6 +549,13 @@ extern "C" int hbgpu_engine_create(const hbgpu_engine_desc *desc, hbgpu_engine *
         int rc = hbgpu_check_launch("hbgpu_engine_create (comm stream)");
         hbgpu_engine_destroy(e);
         return rc ? rc : HBGPU_ERR_CUDA;
+    }
+    if (desc->small) {
+        int rc = hbgpu::small_prepare(e->d, &e->small_tasks, &e->small_part);
+        if (rc) {
+            hbgpu_engine_destroy(e);
+            return rc;
+        }
     }
     *out = e;
     return HBGPU_OK;
@@ -654,7 +685,7 @@ extern "C" int hbgpu_engine_iterate(hbgpu_engine *e, int32_t iterations, int32_t
     rc = enter(e, caller);
     if (rc) return rc;
     if (e->d.small)
-        rc = hbgpu::small_iterations(e->d, e->done, iterations, e->work, &e->small_part, &e->small_cap);
+        rc = hbgpu::small_iterations(e->d, e->done, iterations, e->work, e->small_part, e->small_tasks);
     else
         rc = iterate_on(e, iterations, use_graph, e->work);
     if (!rc) e->done += iterations;
@@ -743,6 +774,12 @@ extern "C" int hbgpu_engine_destroy(hbgpu_engine *e) {
     }
     if (e->ev_pack) cudaEventDestroy(e->ev_pack);
     if (e->ev_comm) cudaEventDestroy(e->ev_comm);
+    if (e->aux_s) {
+        cudaStreamSynchronize(e->aux_s);
+        cudaStreamDestroy(e->aux_s);
+    }
+    if (e->ev_nf_fork) cudaEventDestroy(e->ev_nf_fork);
+    if (e->ev_nf_join) cudaEventDestroy(e->ev_nf_join);
     if (e->small_part) cudaFree(e->small_part);
     delete e;
     return HBGPU_OK;

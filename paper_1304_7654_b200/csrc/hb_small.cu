@@ -1,19 +1,22 @@
 // hb_small.cu -- whole iterations of a small single-GPU rank in one launch.
 //
-// For a tiny rank (BASELINE C0: 2048 cells, 0.2 MB per slot) the per-stage
-// TMA kernels spend most of their time in launch, pipeline fill and drain
-// (7 launches per iteration, 28 us at C0).  Here one
-// cooperative launch runs `iters` complete iterations: the 4 RK stages of
-// every block (warps stride over (row, pde, 32-column chunk) tasks of each
-// block; a thread computes one (cell, pde) for all P planes), separated by
-// grid-wide barriers, with
+// For a small rank (BASELINE C0/C1: up to a few MB per slot, L2-resident)
+// the per-stage TMA kernels spend most of their time in launch, pipeline
+// fill and drain.  Here one cooperative launch runs `iters` complete
+// iterations: the 4 RK stages, separated by grid-wide barriers.  Each stage
+// is one flat task list over every block of the rank -- a warp task is
+// (block, row, pde, 32-column chunk), a thread computes one (cell, pde) for
+// all P planes -- strided over all warps of the grid, with
 //   * halo forwarding at write time through the face-target pool (local
 //     cut halo cells of the output slot; the rank has no remote cuts),
 //   * divergence keys per block (hbcore.py:279-284),
-//   * stage 0: per-block sums of R^2 -- per thread in task order, per CTA in
-//     a fixed tree, then over CTAs in order -- deterministic run to run,
-//   * forces of each iteration into the history (CTA 0 after the last
-//     stage; the next iteration's first stage only reads slot A),
+//   * stage 0: one R^2 partial per warp task (fixed shuffle tree), folded per
+//     block at stage 1 by one warp (lane-strided, fixed shuffle tree):
+//     deterministic and independent of the grid size,
+//   * forces of each iteration into the history after the last stage: one
+//     warp per (coefficient, plane, body), the products h*q formed by the
+//     whole warp and folded left to right by lane 0 (the next iteration's
+//     first stage only reads slot A, so the other warps go on),
 // and the iteration counter set once at the end.  Operands come through L1
 // and L2; every rounding is the reference's (strict rmul/radd, the signed
 // zero terms included), so the fields equal the other schedules' bitwise.
@@ -24,12 +27,16 @@
 #include <string.h>
 
 #include <algorithm>
+#include <vector>
 
 namespace cg = cooperative_groups;
 
 namespace hbgpu {
 
-constexpr int SMALL_THREADS = 128;
+constexpr int SMALL_THREADS = 256;
+constexpr int SMALL_WARPS = SMALL_THREADS / 32;
+constexpr int SMALL_MAX_BLOCKS = 256;   // task offsets live in shared memory
+constexpr int SMALL_FCH = 128;          // force chunk per warp
 // slot rotation (hb_runtime.cu kIn / kOut): A -> B -> C -> B -> A
 __device__ __forceinline__ int in_slot_of(int st) { return st == 0 ? 0 : (st == 2 ? 2 : 1); }
 __device__ __forceinline__ int out_slot_of(int st) { return st == 3 ? 0 : (st == 1 ? 2 : 1); }
@@ -42,7 +49,7 @@ struct SmallArgs {
     unsigned long long *status;
     int32_t *iter;
     double *sumsq;           // [max_iters * nblocks]
-    double *cta_part;        // [nblocks * gridDim.x] stage-0 partials
+    double *task_part;       // [total warp tasks] stage-0 partials
     const hbgpu_force_seg *segs;
     double *force_hist;      // [max_iters * 3 * planes * nbody]
     int32_t nblocks, planes, nbody, nsegs;
@@ -100,12 +107,35 @@ __device__ __forceinline__ double small_cell(const SmallArgs &a, const hbgpu_blo
 }
 
 template <int P>
-__global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const __grid_constant__ SmallArgs a) {
+struct SmallBounds {
+    // P <= 7 fits 128 registers (two CTAs per SM); P = 9 keeps its loads in
+    // flight with up to 255 (one CTA)
+    static constexpr int MIN_BLOCKS = P <= 7 ? 2 : 1;
+};
+
+template <int P>
+__global__ void __launch_bounds__(SMALL_THREADS, SmallBounds<P>::MIN_BLOCKS)
+    small_kernel(const __grid_constant__ SmallArgs a) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ double red[SMALL_THREADS];
+    __shared__ int task_off[SMALL_MAX_BLOCKS + 1];
+    __shared__ int chunks_of[SMALL_MAX_BLOCKS];
+    __shared__ double fbuf[SMALL_WARPS][SMALL_FCH];
     const int lane = threadIdx.x & 31;
-    const int nwarps = gridDim.x * (SMALL_THREADS / 32);
-    const int gwarp = blockIdx.x * (SMALL_THREADS / 32) + (threadIdx.x >> 5);
+    const int nwarps = gridDim.x * SMALL_WARPS;
+    const int gwarp = blockIdx.x * SMALL_WARPS + (threadIdx.x >> 5);
+    if (threadIdx.x == 0) {
+        // warp tasks of block b: (row, pde, 32-column chunk), chunk fastest
+        int off = 0;
+        for (int b = 0; b < a.nblocks; ++b) {
+            const int chunks = (a.blocks[b].ni + 31) >> 5;
+            chunks_of[b] = chunks;
+            task_off[b] = off;
+            off += chunks * NPDE * a.blocks[b].nj;
+        }
+        task_off[a.nblocks] = off;
+    }
+    __syncthreads();
+    const int tasks = task_off[a.nblocks];
     const int total_f = 3 * P * a.nbody;
     for (int it = 0; it < a.iters; ++it) {
         const int iter = a.it0 + it;
@@ -114,42 +144,38 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const __grid_const
             const double *q0 = a.slot[0];
             double *out = a.slot[out_slot_of(st)];
             const int gstage = iter * 4 + st + 1;
-            if (st == 1 && blockIdx.x == 0 && threadIdx.x < a.nblocks) {
-                // this iteration's stage-0 partials, CTAs in order
+            if (st == 1 && gwarp < a.nblocks && iter < a.max_iters) {
+                // this iteration's stage-0 partials of block gwarp: lane-strided
+                // in task order, then a fixed shuffle tree
                 double s = 0.0;
-                for (int c = 0; c < (int)gridDim.x; ++c) s = radd(s, a.cta_part[threadIdx.x * gridDim.x + c]);
-                a.sumsq[(int64_t)iter * a.nblocks + threadIdx.x] = s;
+                for (int t = task_off[gwarp] + lane; t < task_off[gwarp + 1]; t += 32) s = radd(s, a.task_part[t]);
+                for (int o = 16; o > 0; o >>= 1) s = radd(s, __shfl_down_sync(0xffffffffu, s, o));
+                if (lane == 0) a.sumsq[(int64_t)iter * a.nblocks + gwarp] = s;
             }
-            for (int bidx = 0; bidx < a.nblocks; ++bidx) {
-                const hbgpu_block b = a.blocks[bidx];
-                // warp tasks: (row j, pde p, 32-column chunk), chunk fastest
-                const int chunks = (b.ni + 31) >> 5;
-                const int tasks = chunks * NPDE * b.nj;
+            int bidx = 0;
+            for (int t = gwarp; t < tasks; t += nwarps) {
+                while (t >= task_off[bidx + 1]) ++bidx;   // tasks ascend per warp
+                const hbgpu_block &b = a.blocks[bidx];
+                const int chunks = chunks_of[bidx];
+                const int r = t - task_off[bidx];
+                const int chunk = r % chunks;
+                const int pj = r / chunks;
+                const int p = pj % NPDE, j = pj / NPDE + 1;
+                const int i = (chunk << 5) + lane + 1;
                 double acc = 0.0;
-                for (int t = gwarp; t < tasks; t += nwarps) {
-                    const int chunk = t % chunks;
-                    const int r = t / chunks;
-                    const int p = r % NPDE, j = r / NPDE + 1;
-                    const int i = (chunk << 5) + lane + 1;
-                    if (i <= b.ni) acc += small_cell<P>(a, b, in, q0, out, st, p, j, i, gstage, bidx);
-                }
+                if (i <= b.ni) acc = small_cell<P>(a, b, in, q0, out, st, p, j, i, gstage, bidx);
                 if (st == 0) {
-                    // fixed-shape tree over the CTA's threads
-                    red[threadIdx.x] = acc;
-                    __syncthreads();
-                    for (int w = SMALL_THREADS / 2; w > 0; w >>= 1) {
-                        if (threadIdx.x < w) red[threadIdx.x] = radd(red[threadIdx.x], red[threadIdx.x + w]);
-                        __syncthreads();
-                    }
-                    if (threadIdx.x == 0) a.cta_part[bidx * gridDim.x + blockIdx.x] = red[0];
-                    __syncthreads();
+                    for (int o = 16; o > 0; o >>= 1) acc = radd(acc, __shfl_down_sync(0xffffffffu, acc, o));
+                    if (lane == 0) a.task_part[t] = acc;
                 }
             }
             grid.sync();
         }
-        if (blockIdx.x == 0 && iter < a.max_iters) {
-            // forces of slot A (hbcore.py:359-382), strict left-to-right folds
-            for (int t = threadIdx.x; t < total_f; t += blockDim.x) {
+        if (iter < a.max_iters) {
+            // forces of slot A (hbcore.py:359-382): one warp per output, strict
+            // left-to-right folds of the products h*q
+            double *buf = fbuf[threadIdx.x >> 5];
+            for (int t = gwarp; t < total_f; t += nwarps) {
                 const int body = t % a.nbody;
                 const int n = (t / a.nbody) % P;
                 const int k = t / (a.nbody * P);
@@ -158,9 +184,21 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const __grid_const
                     const hbgpu_force_seg g = a.segs[s];
                     if (g.body != body) continue;
                     const double *fp = a.slot[0] + g.start + (int64_t)(n * NPDE + k) * g.ps;
-                    for (int c = 0; c < g.length; ++c) f = radd(f, rmul(g.h, fp[(int64_t)c * g.stride]));
+                    for (int c0 = 0; c0 < g.length; c0 += SMALL_FCH) {
+#pragma unroll
+                        for (int u = 0; u < SMALL_FCH / 32; ++u) {
+                            const int c = c0 + lane + 32 * u;
+                            buf[lane + 32 * u] = c < g.length ? rmul(g.h, fp[(int64_t)c * g.stride]) : 0.0;
+                        }
+                        __syncwarp();
+                        if (lane == 0) {
+                            const int m = min(SMALL_FCH, g.length - c0);
+                            for (int e = 0; e < m; ++e) f = radd(f, buf[e]);
+                        }
+                        __syncwarp();
+                    }
                 }
-                a.force_hist[(int64_t)iter * total_f + t] = f;
+                if (lane == 0) a.force_hist[(int64_t)iter * total_f + t] = f;
             }
         }
     }
@@ -174,8 +212,7 @@ struct SmallLaunch {
 };
 
 template <int P>
-static int small_launch_p(const SmallArgs &args, int64_t max_items, cudaStream_t s, double **part_buf,
-                          int *part_cap) {
+static int small_launch_p(const SmallArgs &a, int tasks, cudaStream_t s) {
     static SmallLaunch L_d[HB_MAX_DEVICES];
     const int dev = current_device();
     if (dev < 0) return HBGPU_ERR_CUDA;
@@ -191,20 +228,9 @@ static int small_launch_p(const SmallArgs &args, int64_t max_items, cudaStream_t
         L.grid = sms * per_sm;
         L.ready = true;
     }
-    // one warp task per (row, pde, 32 columns) of the largest block
-    int grid = (int)std::min<int64_t>(L.grid, (max_items / P + SMALL_THREADS - 1) / SMALL_THREADS);
+    // every co-resident CTA, or one warp per task if there are fewer tasks
+    int grid = (int)std::min<int64_t>(L.grid, ((int64_t)tasks + SMALL_WARPS - 1) / SMALL_WARPS);
     grid = std::max(grid, 1);
-    SmallArgs a = args;
-    const int need = a.nblocks * grid;
-    if (*part_cap < need) {
-        if (*part_buf) cudaFree(*part_buf);
-        *part_buf = nullptr;
-        *part_cap = 0;
-        if (cudaMalloc(part_buf, sizeof(double) * (size_t)need) != cudaSuccess)
-            return hbgpu_check_launch("small kernel partials");
-        *part_cap = need;
-    }
-    a.cta_part = *part_buf;
     void *params[] = {(void *)&a};
     cudaError_t e = cudaLaunchCooperativeKernel(L.fn, dim3(grid), dim3(SMALL_THREADS), params, 0, s);
     if (e != cudaSuccess) {
@@ -215,10 +241,32 @@ static int small_launch_p(const SmallArgs &args, int64_t max_items, cudaStream_t
     return HBGPU_OK;
 }
 
+// engine creation: the rank's warp-task count (from the device block table)
+// and the per-task partial buffer
+int small_prepare(const hbgpu_engine_desc &d, int *tasks, double **part_buf) {
+    if (d.nblocks > SMALL_MAX_BLOCKS) {
+        hbgpu_set_error("small schedule: %d blocks exceed %d", d.nblocks, SMALL_MAX_BLOCKS);
+        return HBGPU_ERR_ARG;
+    }
+    std::vector<hbgpu_block> host(d.nblocks);
+    if (cudaMemcpy(host.data(), d.blocks, sizeof(hbgpu_block) * d.nblocks, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return hbgpu_check_launch("small schedule: block table");
+    int64_t n = 0;
+    for (const hbgpu_block &b : host) n += (int64_t)((b.ni + 31) / 32) * NPDE * b.nj;
+    if (n <= 0 || n > INT32_MAX / 2) {
+        hbgpu_set_error("small schedule: %lld warp tasks", (long long)n);
+        return HBGPU_ERR_ARG;
+    }
+    if (cudaMalloc(part_buf, sizeof(double) * (size_t)n) != cudaSuccess)
+        return hbgpu_check_launch("small schedule: partials");
+    *tasks = (int)n;
+    return HBGPU_OK;
+}
+
 // `iters` iterations of the engine described by `d` starting at iteration
 // it0, in one cooperative launch (hb_runtime.cu, engine schedule "small")
-int small_iterations(const hbgpu_engine_desc &d, int32_t it0, int32_t iters, cudaStream_t s, double **part_buf,
-                     int *part_cap) {
+int small_iterations(const hbgpu_engine_desc &d, int32_t it0, int32_t iters, cudaStream_t s, double *part_buf,
+                     int tasks) {
     if (iters <= 0) return HBGPU_OK;
     SmallArgs a;
     memset(&a, 0, sizeof(a));
@@ -241,13 +289,13 @@ int small_iterations(const hbgpu_engine_desc &d, int32_t it0, int32_t iters, cud
     for (int k = 0; k < 4; ++k) a.coef[k] = d.coef[k];
     memcpy(a.D, d.D, sizeof(a.D));
     for (int k = 0; k < HBGPU_MAX_TEMPLATED_P * HBGPU_NPDE; ++k) a.ap[k] = d.ap[k];
-    const int64_t max_items = (int64_t)d.planes * NPDE * (int64_t)d.small_max_cells;
+    a.task_part = part_buf;
     switch (d.planes) {
-        case 1: return small_launch_p<1>(a, max_items, s, part_buf, part_cap);
-        case 3: return small_launch_p<3>(a, max_items, s, part_buf, part_cap);
-        case 5: return small_launch_p<5>(a, max_items, s, part_buf, part_cap);
-        case 7: return small_launch_p<7>(a, max_items, s, part_buf, part_cap);
-        case 9: return small_launch_p<9>(a, max_items, s, part_buf, part_cap);
+        case 1: return small_launch_p<1>(a, tasks, s);
+        case 3: return small_launch_p<3>(a, tasks, s);
+        case 5: return small_launch_p<5>(a, tasks, s);
+        case 7: return small_launch_p<7>(a, tasks, s);
+        case 9: return small_launch_p<9>(a, tasks, s);
         default: break;
     }
     hbgpu_set_error("small schedule: P = %d not templated (1..9 odd)", d.planes);
