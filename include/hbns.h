@@ -42,8 +42,6 @@ typedef struct hbns_block {
 typedef struct hbns_args {
     double *w[3];                /* state slots: 0 = iteration start         */
     double *r;                   /* residual pool                             */
-    double *prim;                /* primitive pool (u, v, p, c, e) of every
-                                    cell incl. halos: 5/4 of a state pool    */
     double *dt;                  /* local time steps                          */
     const double *xc, *yc, *vol; /* cell geometry                             */
     const double *six, *siy, *gi;/* i-face normals, grid flux (moving)        */
@@ -56,8 +54,10 @@ typedef struct hbns_args {
     double *norms;               /* per iteration                             */
     double *forces;              /* per iteration, snapshot: (fx, fy)         */
     double mu, cfl, omega_nh;    /* M/Re (0: Euler), CFL, omega * N_H         */
+    double kq;                   /* (mu * gamma) / Pr, as the host rounds it  */
     int32_t nblocks, P, Pg, moving;
     int32_t max_len, max_cells;  /* largest block side, largest ni * nj       */
+    int32_t max_ni, max_nj;      /* largest ni, largest nj (residual grid)    */
 } hbns_args;
 
 int hbns_boundaries(const hbns_args *a, int32_t slot, void *stream);

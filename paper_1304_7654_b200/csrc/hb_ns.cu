@@ -16,16 +16,17 @@
 //                       (side, layer, face cell, snapshot)
 //   ns_corner_kernel    corner halos
 //   ns_timestep_kernel  local time step, one thread per cell
-//   ns_prim_kernel      u, v, p, c, e of every cell (halos included) once per
-//                       stage: the flux kernel reads each cell's up to 20 times
-//   ns_residual_kernel  face fluxes -> R, one thread per (cell, snapshot)
+//   ns_flux_kernel      R of a TJ x TI tile and one snapshot per CTA: the
+//                       state with its 2-cell ring staged in shared memory,
+//                       primitives once per staged cell, sensors once per
+//                       (cell, direction), every face flux once
 //   ns_update_kernel    HB source + RK update, one thread per (cell,
 //                       variable) for all snapshots; stage-1 R_rho^2 partials
 //                       per CTA, folded by ns_norm_kernel (a warp per block)
 //   ns_forces_kernel    wall pressure forces, one thread per snapshot
 // Cut halos move with hbgpu_halo (two directions per cut and layer).
 
-#include "hb_common.cuh"
+#include "hb_tma.cuh"
 
 #include "hbns.h"
 
@@ -56,12 +57,6 @@ __device__ __forceinline__ int64_t fj(const hbns_block &b, int g, int j, int i) 
 struct Prim {
     double r, ru, rv, re, u, v, p, c, e;
 };
-
-// the primitive pool (u, v, p, c, e) of every cell of a slot, halos included
-constexpr int NPRIM = 5;
-__device__ __forceinline__ int64_t ps_(const hbns_block &b, int n, int k, int j, int i) {
-    return b.w_off / NV * NPRIM + (((int64_t)n * NPRIM + k) * (b.nj + 4) + (j + 1)) * (b.ni + 4) + (i + 1);
-}
 
 __device__ __forceinline__ Prim prim(const double *w, int64_t stride) {
     Prim q;
@@ -156,84 +151,91 @@ __global__ void ns_corner_kernel(hbns_args a, double *w) {
     w[ws(b, n, k, j, i)] = w[ws(b, n, k, src, i)];
 }
 
-// ---- primitives: one conversion per cell and stage (the flux kernel reads
-// each cell's u, v, p, c, e up to 20 times) -----------------------------------------------
+// ---- residual: one CTA per (tile of TJ x TI cells, snapshot) ---------------------------
+//
+// The tile's state with its two-cell halo ring is staged in shared memory;
+// primitives are formed once per staged cell, the JST pressure sensor once per
+// (cell, direction), and every face flux once -- the two cells beside a face
+// read the same value (the thread-per-cell form computed each face twice and
+// each sensor up to four times).  Geometry comes through L1/L2: the face
+// normals are read once per face, the cell centres of the viscous diamond
+// from L1.  The per-point arithmetic is the specification's, operation for
+// operation, so R is bitwise the thread-per-cell kernel's (and the oracle's).
 
-__global__ void ns_prim_kernel(hbns_args a, const double *w) {
-    // grid.y = block, grid.z = snapshot; x over all cells incl. the halo ring
-    const hbns_block &b = a.blocks[blockIdx.y];
-    const int n = blockIdx.z;
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    const int wi = b.ni + 4;
-    if (t >= wi * (b.nj + 4)) return;
-    const int i = t % wi - 1, j = t / wi - 1;
-    const int64_t st = (int64_t)(b.nj + 4) * (b.ni + 4);
-    const Prim q = prim(w + ws(b, n, 0, j, i), st);
-    a.prim[ps_(b, n, 0, j, i)] = q.u;
-    a.prim[ps_(b, n, 1, j, i)] = q.v;
-    a.prim[ps_(b, n, 2, j, i)] = q.p;
-    a.prim[ps_(b, n, 3, j, i)] = q.c;
-    a.prim[ps_(b, n, 4, j, i)] = q.e;
+constexpr int TI = 32, TJ = 8;               // tile columns, rows
+constexpr int RW = TI + 4, RH = TJ + 4;      // staged region with the 2-cell ring
+constexpr int FLUX_THREADS = 288;            // 9 warps: 264 i-faces / 288 j-faces per pass
+
+struct FluxSmem {
+    double w[NV][RH][RW];          // conservative state
+    double pr[5][RH][RW];          // u, v, p, c, e
+    double xc[RH - 2][RW - 2];     // cell centres of the 1-cell ring region (viscous)
+    double yc[RH - 2][RW - 2];
+    double nxi[TJ][TI + 1], nyi[TJ][TI + 1], gfi[TJ][TI + 1];   // i-face normals, grid flux
+    double nxj[TJ + 1][TI], nyj[TJ + 1][TI], gfj[TJ + 1][TI];   // j-face normals, grid flux
+    double nui[TJ][TI + 2];        // sensor along i: tile rows, columns i0-1 .. i0+TI
+    double nuj[TJ + 2][TI];        // sensor along j: rows j0-1 .. j0+TJ, tile columns
+    double fi[NV][TJ][TI + 1];     // i-face fluxes: face k between cells i0-1+k and i0+k
+    double fj[NV][TJ + 1][TI];     // j-face fluxes: face k between rows j0-1+k and j0+k
+};
+
+// one 8-byte global -> shared copy, asynchronous (LDGSTS): a CTA issues all
+// of its staging copies before waiting once
+__device__ __forceinline__ void cp8(double *sdst, const double *gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+__device__ __forceinline__ double sensor(double pm, double pc, double pp) {
+    // nu_X = |(p_{X+1} - 2 p_X) + p_{X-1}| / ((p_{X+1} + 2 p_X) + p_{X-1})
+    return dv(fabs(add(sub(pp, mul(2.0, pc)), pm)), add(add(pp, mul(2.0, pc)), pm));
 }
 
-// a cell's state and primitives, the latter from the pool
-__device__ __forceinline__ Prim load_prim(const hbns_args &a, const hbns_block &b, const double *w, int n, int j,
-                                          int i) {
-    const int64_t st = (int64_t)(b.nj + 4) * (b.ni + 4);
-    const double *c = w + ws(b, n, 0, j, i);
-    Prim q;
-    q.r = c[0];
-    q.ru = c[st];
-    q.rv = c[2 * st];
-    q.re = c[3 * st];
-    q.u = a.prim[ps_(b, n, 0, j, i)];
-    q.v = a.prim[ps_(b, n, 1, j, i)];
-    q.p = a.prim[ps_(b, n, 2, j, i)];
-    q.c = a.prim[ps_(b, n, 3, j, i)];
-    q.e = a.prim[ps_(b, n, 4, j, i)];
-    return q;
-}
-
-// ---- fluxes -----------------------------------------------------------------------------
-
-__device__ void face_flux(const hbns_args &a, const hbns_block &b, const double *w, int n, int g, int jL, int iL,
-                          int dj, int di, double sx, double sy, double gf, double *out) {
-    const int jR = jL + dj, iR = iL + di;
-    const Prim L = load_prim(a, b, w, n, jL, iL), R = load_prim(a, b, w, n, jR, iR);
-    const Prim LL = load_prim(a, b, w, n, jL - dj, iL - di);
-    const Prim RR = load_prim(a, b, w, n, jR + dj, iR + di);
-    const double unL = add(mul(L.u, sx), mul(L.v, sy)), unR = add(mul(R.u, sx), mul(R.v, sy));
+// flux through the face between region cells L = (ry, rx) and R = L + (dj, di)
+template <bool VISC>
+__device__ __forceinline__ void tile_face(const hbns_args &a, const FluxSmem &S, int ry, int rx, int dj, int di,
+                                          double sx, double sy, double gf, double nuL, double nuR, double *out) {
+    const int ryR = ry + dj, rxR = rx + di;
+    const double Lr = S.w[0][ry][rx], Lru = S.w[1][ry][rx], Lrv = S.w[2][ry][rx], Lre = S.w[3][ry][rx];
+    const double Rr = S.w[0][ryR][rxR], Rru = S.w[1][ryR][rxR], Rrv = S.w[2][ryR][rxR], Rre = S.w[3][ryR][rxR];
+    const double Lu = S.pr[0][ry][rx], Lv = S.pr[1][ry][rx], Lp = S.pr[2][ry][rx], Lc = S.pr[3][ry][rx];
+    const double Ru = S.pr[0][ryR][rxR], Rv = S.pr[1][ryR][rxR], Rp = S.pr[2][ryR][rxR], Rc = S.pr[3][ryR][rxR];
+    const double unL = add(mul(Lu, sx), mul(Lv, sy)), unR = add(mul(Ru, sx), mul(Rv, sy));
     const double urL = sub(unL, gf), urR = sub(unR, gf);
-    double FL[NV] = {mul(L.r, urL), add(mul(L.ru, urL), mul(L.p, sx)), add(mul(L.rv, urL), mul(L.p, sy)),
-                     add(mul(L.re, urL), mul(L.p, unL))};
-    double FR[NV] = {mul(R.r, urR), add(mul(R.ru, urR), mul(R.p, sx)), add(mul(R.rv, urR), mul(R.p, sy)),
-                     add(mul(R.re, urR), mul(R.p, unR))};
+    const double FL[NV] = {mul(Lr, urL), add(mul(Lru, urL), mul(Lp, sx)), add(mul(Lrv, urL), mul(Lp, sy)),
+                           add(mul(Lre, urL), mul(Lp, unL))};
+    const double FR[NV] = {mul(Rr, urR), add(mul(Rru, urR), mul(Rp, sx)), add(mul(Rrv, urR), mul(Rp, sy)),
+                           add(mul(Rre, urR), mul(Rp, unR))};
     const double sa = __dsqrt_rn(add(mul(sx, sx), mul(sy, sy)));
-    const double lamL = add(fabs(urL), mul(L.c, sa)), lamR = add(fabs(urR), mul(R.c, sa));
+    const double lamL = add(fabs(urL), mul(Lc, sa)), lamR = add(fabs(urR), mul(Rc, sa));
     const double lam = mul(0.5, add(lamL, lamR));
-    const double nuL = dv(fabs(add(sub(R.p, mul(2.0, L.p)), LL.p)), add(add(R.p, mul(2.0, L.p)), LL.p));
-    const double nuR = dv(fabs(add(sub(RR.p, mul(2.0, R.p)), L.p)), add(add(RR.p, mul(2.0, R.p)), L.p));
     const double eps2 = mul(mul(K2, lam), fmax(nuL, nuR));
     const double eps4 = fmax(0.0, sub(mul(K4, lam), eps2));
     double fv[NV] = {0.0, 0.0, 0.0, 0.0};
-    const bool visc = a.mu > 0.0;
-    if (visc) {
-        const int tj = di, ti = dj;
-        const Prim Lp = load_prim(a, b, w, n, jL + tj, iL + ti), Rp = load_prim(a, b, w, n, jR + tj, iR + ti);
-        const Prim Lm = load_prim(a, b, w, n, jL - tj, iL - ti), Rm = load_prim(a, b, w, n, jR - tj, iR - ti);
-        const double xL = a.xc[cc(b, g, jL, iL)], xR = a.xc[cc(b, g, jR, iR)];
-        const double yL = a.yc[cc(b, g, jL, iL)], yR = a.yc[cc(b, g, jR, iR)];
-        const double xLp = a.xc[cc(b, g, jL + tj, iL + ti)], xRp = a.xc[cc(b, g, jR + tj, iR + ti)];
-        const double xLm = a.xc[cc(b, g, jL - tj, iL - ti)], xRm = a.xc[cc(b, g, jR - tj, iR - ti)];
-        const double yLp = a.yc[cc(b, g, jL + tj, iL + ti)], yRp = a.yc[cc(b, g, jR + tj, iR + ti)];
-        const double yLm = a.yc[cc(b, g, jL - tj, iL - ti)], yRm = a.yc[cc(b, g, jR - tj, iR - ti)];
+    if (VISC) {
+        const int tj = di, ti = dj;   // i-face: rows +-1; j-face: columns +-1
+        // centres: ring-1 region coordinates are the region's minus one
+        const int cy = ry - 1, cx = rx - 1, cyR = ryR - 1, cxR = rxR - 1;
+        const double xL = S.xc[cy][cx], xR = S.xc[cyR][cxR];
+        const double yL = S.yc[cy][cx], yR = S.yc[cyR][cxR];
+        const double xLp = S.xc[cy + tj][cx + ti], xRp = S.xc[cyR + tj][cxR + ti];
+        const double xLm = S.xc[cy - tj][cx - ti], xRm = S.xc[cyR - tj][cxR - ti];
+        const double yLp = S.yc[cy + tj][cx + ti], yRp = S.yc[cyR + tj][cxR + ti];
+        const double yLm = S.yc[cy - tj][cx - ti], yRm = S.yc[cyR - tj][cxR - ti];
         const double x_a = sub(xR, xL), y_a = sub(yR, yL);
         const double x_b = mul(0.25, sub(add(xLp, xRp), add(xLm, xRm)));
         const double y_b = mul(0.25, sub(add(yLp, yRp), add(yLm, yRm)));
         const double jac = sub(mul(x_a, y_b), mul(x_b, y_a));
-        const double ua = sub(R.u, L.u), ub = mul(0.25, sub(add(Lp.u, Rp.u), add(Lm.u, Rm.u)));
-        const double va = sub(R.v, L.v), vb = mul(0.25, sub(add(Lp.v, Rp.v), add(Lm.v, Rm.v)));
-        const double ea = sub(R.e, L.e), eb = mul(0.25, sub(add(Lp.e, Rp.e), add(Lm.e, Rm.e)));
+        // u, v, e of the four diamond cells beside L and R
+        const int pLy = ry + tj, pLx = rx + ti, mLy = ry - tj, mLx = rx - ti;
+        const int pRy = ryR + tj, pRx = rxR + ti, mRy = ryR - tj, mRx = rxR - ti;
+        const double ua = sub(Ru, Lu);
+        const double ub = mul(0.25, sub(add(S.pr[0][pLy][pLx], S.pr[0][pRy][pRx]), add(S.pr[0][mLy][mLx], S.pr[0][mRy][mRx])));
+        const double va = sub(Rv, Lv);
+        const double vb = mul(0.25, sub(add(S.pr[1][pLy][pLx], S.pr[1][pRy][pRx]), add(S.pr[1][mLy][mLx], S.pr[1][mRy][mRx])));
+        const double ea = sub(S.pr[4][ryR][rxR], S.pr[4][ry][rx]);
+        const double eb = mul(0.25, sub(add(S.pr[4][pLy][pLx], S.pr[4][pRy][pRx]), add(S.pr[4][mLy][mLx], S.pr[4][mRy][mRx])));
         const double ux = dv(sub(mul(ua, y_b), mul(ub, y_a)), jac), uy = dv(sub(mul(ub, x_a), mul(ua, x_b)), jac);
         const double vx = dv(sub(mul(va, y_b), mul(vb, y_a)), jac), vy = dv(sub(mul(vb, x_a), mul(va, x_b)), jac);
         const double ex = dv(sub(mul(ea, y_b), mul(eb, y_a)), jac), ey = dv(sub(mul(eb, x_a), mul(ea, x_b)), jac);
@@ -243,44 +245,152 @@ __device__ void face_flux(const hbns_args &a, const hbns_block &b, const double 
         const double txx = mul(mu, sub(mul(2.0, ux), mul(t23, div)));
         const double tyy = mul(mu, sub(mul(2.0, vy), mul(t23, div)));
         const double txy = mul(mu, add(uy, vx));
-        const double kq = dv(mul(mu, GAMMA), PR);
+        const double kq = a.kq;   // (mu * gamma) / Pr, formed once on the host
         const double qx = -mul(kq, ex), qy = -mul(kq, ey);
-        const double uf = mul(0.5, add(L.u, R.u)), vf = mul(0.5, add(L.v, R.v));
+        const double uf = mul(0.5, add(Lu, Ru)), vf = mul(0.5, add(Lv, Rv));
         fv[1] = add(mul(txx, sx), mul(txy, sy));
         fv[2] = add(mul(txy, sx), mul(tyy, sy));
         fv[3] = add(mul(sub(add(mul(uf, txx), mul(vf, txy)), qx), sx), mul(sub(add(mul(uf, txy), mul(vf, tyy)), qy), sy));
     }
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-        const double wl = w[ws(b, n, k, jL, iL)], wr = w[ws(b, n, k, jR, iR)];
-        const double wll = w[ws(b, n, k, jL - dj, iL - di)], wrr = w[ws(b, n, k, jR + dj, iR + di)];
+        const double wl = S.w[k][ry][rx], wr = S.w[k][ryR][rxR];
+        const double wll = S.w[k][ry - dj][rx - di], wrr = S.w[k][ryR + dj][rxR + di];
         const double fc = mul(0.5, add(FL[k], FR[k]));
         const double d = sub(mul(eps2, sub(wr, wl)), mul(eps4, sub(add(sub(wrr, mul(3.0, wr)), mul(3.0, wl)), wll)));
-        out[k] = visc ? sub(sub(fc, d), fv[k]) : sub(fc, d);
+        out[k] = VISC ? sub(sub(fc, d), fv[k]) : sub(fc, d);
     }
 }
 
-__global__ void ns_residual_kernel(hbns_args a, const double *w) {
-    // grid.y = block, grid.z = snapshot; x over interior cells (i fastest)
-    const hbns_block &b = a.blocks[blockIdx.y];
-    const int n = blockIdx.z;
+// one row of `count` (<= 64) staged values, lane-strided; columns past
+// `last` read column `last` (clamped to the block's array)
+__device__ __forceinline__ void stage_row(double *sdst, const double *grow, int count, int last, int lane) {
+    cp8(sdst + lane, grow + min(lane, last));
+    if (lane + 32 < count) cp8(sdst + lane + 32, grow + min(lane + 32, last));
+}
+
+// Thread mapping: lane = tile column, warp = row (TI = 32 = warp width), so
+// staging, primitives, sensors and faces need no index division; the 9th
+// warp takes the 8 east-most i-faces and the last j-face row.
+// CTAs per SM the register budget is sized for: 3 of 9 warps (the register
+// file is split over the 4 schedulers, so <= 72 registers; a few spill, and
+// the extra warps still win: C4 231 -> 223, C3 15.6 -> 15.2 ms/iteration
+// against 2).  HBNS_FLUX_MINB overrides it in measurement builds.
+#ifndef HBNS_FLUX_MINB
+#define HBNS_FLUX_MINB 3
+#endif
+
+template <bool VISC>
+__global__ void __launch_bounds__(FLUX_THREADS, HBNS_FLUX_MINB) ns_flux_kernel(hbns_args a, const double *w) {
+    // grid.x = tile * P + snapshot (snapshots of a tile adjacent: the same
+    // geometry when the mesh is fixed), grid.y = block
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    FluxSmem &S = *reinterpret_cast<FluxSmem *>(smem_raw);
+    const hbns_block b = a.blocks[blockIdx.y];
+    const int n = blockIdx.x % a.P;
+    const int tile = blockIdx.x / a.P;
+    const int tiles_i = (b.ni + TI - 1) / TI;
+    if (tile >= tiles_i * ((b.nj + TJ - 1) / TJ)) return;
+    const int i0 = (tile % tiles_i) * TI + 1, j0 = (tile / tiles_i) * TJ + 1;
     const int g = a.Pg > 1 ? n : 0;
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= b.ni * b.nj) return;
-    const int i = t % b.ni + 1, j = t / b.ni + 1;
-    const double *gi = a.moving ? a.gi : nullptr;
-    const double *gj = a.moving ? a.gj : nullptr;
-    double fe[NV], fw[NV], fn[NV], fs[NV];
-    face_flux(a, b, w, n, g, j, i, 0, 1, a.six[fi(b, g, j, i)], a.siy[fi(b, g, j, i)], gi ? gi[fi(b, g, j, i)] : 0.0,
-              fe);
-    face_flux(a, b, w, n, g, j, i - 1, 0, 1, a.six[fi(b, g, j, i - 1)], a.siy[fi(b, g, j, i - 1)],
-              gi ? gi[fi(b, g, j, i - 1)] : 0.0, fw);
-    face_flux(a, b, w, n, g, j, i, 1, 0, a.sjx[fj(b, g, j, i)], a.sjy[fj(b, g, j, i)], gj ? gj[fj(b, g, j, i)] : 0.0,
-              fn);
-    face_flux(a, b, w, n, g, j - 1, i, 1, 0, a.sjx[fj(b, g, j - 1, i)], a.sjy[fj(b, g, j - 1, i)],
-              gj ? gj[fj(b, g, j - 1, i)] : 0.0, fs);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = FLUX_THREADS / 32;
+    // 1. stage, all copies in flight at once: the state of region cells
+    //    (j0-2 .. j0+TJ+1) x (i0-2 .. i0+TI+1), clamped to the block's array
+    //    (the clamped cells feed no face); the tile's face normals and grid
+    //    fluxes; the cell centres of the 1-cell ring (viscous)
+    {
+        const int ilast = b.ni + 2 - (i0 - 2);   // region column of array column ni+2
+        for (int row = warp; row < NV * RH; row += NW) {
+            const int k = row / RH, r = row - k * RH;
+            stage_row(S.w[k][r], w + ws(b, n, k, min(j0 - 2 + r, b.nj + 2), i0 - 2), RW, ilast, lane);
+        }
+        const int flast = b.ni - (i0 - 1);       // i-face column of face ni
+        for (int r = warp; r < TJ; r += NW) {
+            const int64_t f = fi(b, g, min(j0 + r, b.nj), i0 - 1);
+            stage_row(S.nxi[r], a.six + f, TI + 1, flast, lane);
+            stage_row(S.nyi[r], a.siy + f, TI + 1, flast, lane);
+            if (a.moving) stage_row(S.gfi[r], a.gi + f, TI + 1, flast, lane);
+        }
+        const int jlast = b.ni - i0;             // j-face / tile column of cell ni
+        for (int r = warp; r <= TJ; r += NW) {
+            const int64_t f = fj(b, g, min(j0 - 1 + r, b.nj), i0);
+            stage_row(S.nxj[r], a.sjx + f, TI, jlast, lane);
+            stage_row(S.nyj[r], a.sjy + f, TI, jlast, lane);
+            if (a.moving) stage_row(S.gfj[r], a.gj + f, TI, jlast, lane);
+        }
+        if (VISC) {
+            const int clast = b.ni + 1 - (i0 - 1);
+            for (int r = warp; r < RH - 2; r += NW) {
+                const int64_t o = cc(b, g, min(j0 - 1 + r, b.nj + 1), i0 - 1);
+                stage_row(S.xc[r], a.xc + o, RW - 2, clast, lane);
+                stage_row(S.yc[r], a.yc + o, RW - 2, clast, lane);
+            }
+        }
+    }
+    cp_wait_all();
+    __syncthreads();
+    // 2. primitives of every staged cell (nsflow: u, v, p, c, e)
+    for (int t = threadIdx.x; t < RH * RW; t += FLUX_THREADS) {
+        const int r = t / RW, c = t - r * RW;
+        const double q_r = S.w[0][r][c], q_ru = S.w[1][r][c], q_rv = S.w[2][r][c], q_re = S.w[3][r][c];
+        const double u = dv(q_ru, q_r), v = dv(q_rv, q_r);
+        const double p = mul(GAMMA - 1.0, sub(q_re, mul(0.5, add(mul(q_ru, u), mul(q_rv, v)))));
+        S.pr[0][r][c] = u;
+        S.pr[1][r][c] = v;
+        S.pr[2][r][c] = p;
+        S.pr[3][r][c] = __dsqrt_rn(dv(mul(GAMMA, p), q_r));
+        S.pr[4][r][c] = dv(p, mul(GAMMA - 1.0, q_r));
+    }
+    __syncthreads();
+    // 3. JST sensors of the cells beside the tile's faces
+    constexpr int NSI = TJ * (TI + 2), NSJ = (TJ + 2) * TI;
+    for (int t = threadIdx.x; t < NSI + NSJ; t += FLUX_THREADS) {
+        if (t < NSI) {
+            const int r = t / (TI + 2), c = t - r * (TI + 2);   // cell (j0 + r, i0 - 1 + c)
+            S.nui[r][c] = sensor(S.pr[2][r + 2][c], S.pr[2][r + 2][c + 1], S.pr[2][r + 2][c + 2]);
+        } else {
+            const int u = t - NSI, r = u / TI, c = u % TI;      // cell (j0 - 1 + r, i0 + c)
+            S.nuj[r][c] = sensor(S.pr[2][r][c + 2], S.pr[2][r + 1][c + 2], S.pr[2][r + 2][c + 2]);
+        }
+    }
+    __syncthreads();
+    // 4. face fluxes, one i-face and one j-face per thread, both evaluated
+    //    unconditionally (indices clamped into the staged region) so that the
+    //    two dependency chains interleave; only real faces are stored.
+    //    Warp w < TJ: i-faces of row w (faces 0..31); warp TJ: face 32 of
+    //    every row (lanes 0..TJ-1).  Every warp w: j-face row w.
+    {
+        const bool mv = a.moving != 0;
+        const int ri = warp < TJ ? warp : min(lane, TJ - 1), ci = warp < TJ ? lane : TI;
+        const bool live_i = (warp < TJ || lane < TJ) && j0 + ri <= b.nj && i0 - 1 + ci <= b.ni;
+        const int rj = warp, cj = lane;
+        const bool live_j = j0 - 1 + rj <= b.nj && i0 + cj <= b.ni;
+        double oi[NV], oj[NV];
+        tile_face<VISC>(a, S, ri + 2, ci + 1, 0, 1, S.nxi[ri][ci], S.nyi[ri][ci], mv ? S.gfi[ri][ci] : 0.0,
+                        S.nui[ri][ci], S.nui[ri][ci + 1], oi);
+        tile_face<VISC>(a, S, rj + 1, cj + 2, 1, 0, S.nxj[rj][cj], S.nyj[rj][cj], mv ? S.gfj[rj][cj] : 0.0,
+                        S.nuj[rj][cj], S.nuj[rj + 1][cj], oj);
+        if (live_i) {
 #pragma unroll
-    for (int k = 0; k < NV; ++k) a.r[rs(b, n, k, j, i)] = sub(add(sub(fe[k], fw[k]), fn[k]), fs[k]);
+            for (int k = 0; k < NV; ++k) S.fi[k][ri][ci] = oi[k];
+        }
+        if (live_j) {
+#pragma unroll
+            for (int k = 0; k < NV; ++k) S.fj[k][rj][cj] = oj[k];
+        }
+    }
+    __syncthreads();
+    // 5. R = ((F_{i+1/2} - F_{i-1/2}) + F_{j+1/2}) - F_{j-1/2}
+    if (warp < TJ) {
+        const int r = warp, c = lane;
+        const int j = j0 + r, i = i0 + c;
+        if (j <= b.nj && i <= b.ni) {
+#pragma unroll
+            for (int k = 0; k < NV; ++k)
+                a.r[rs(b, n, k, j, i)] = sub(add(sub(S.fi[k][r][c + 1], S.fi[k][r][c]), S.fj[k][r + 1][c]), S.fj[k][r][c]);
+        }
+    }
 }
 
 __global__ void ns_timestep_kernel(hbns_args a, const double *w) {
@@ -388,32 +498,70 @@ __global__ void ns_norm_kernel(hbns_args a, int iter, int ctas) {
     }
 }
 
-__global__ void ns_forces_kernel(hbns_args a, const double *w, int iter) {
-    const int n = threadIdx.x;
-    if (n >= a.P) return;
+// wall pressure forces: one CTA per snapshot.  The wall faces in the
+// specification's order (blocks ascending, sides south/north/west/east, face
+// cells ascending) are taken in chunks: every thread forms p*Sx and p*Sy of
+// its faces (each product rounded once), then thread 0 adds them in order --
+// the fold is the only serial part.
+constexpr int FORCE_THREADS = 256;
+constexpr int FORCE_CHUNK = 1024;
+constexpr int MAX_WALL_SEGS = 4 * 256;
+
+__global__ void __launch_bounds__(FORCE_THREADS) ns_forces_kernel(hbns_args a, const double *w, int iter) {
+    __shared__ double px[FORCE_CHUNK], py[FORCE_CHUNK];
+    __shared__ int seg_bs[MAX_WALL_SEGS], seg_end[MAX_WALL_SEGS];   // block * 4 + side, running end
+    __shared__ int nseg_s;
+    const int n = blockIdx.x;
     const int g = a.Pg > 1 ? n : 0;
-    double fx = 0.0, fy = 0.0;
-    for (int bk = 0; bk < a.nblocks; ++bk) {
-        const hbns_block &b = a.blocks[bk];
-        const int64_t st = (int64_t)(b.nj + 4) * (b.ni + 4);
-        for (int side = 0; side < 4; ++side) {
-            if (b.kinds[side] != HBNS_NOSLIP && b.kinds[side] != HBNS_SLIP) continue;
-            const int len = side < 2 ? b.ni : b.nj;
-            for (int e = 1; e <= len; ++e) {
-                int ci, cj;
-                double sx, sy;
-                if (side == 0) { ci = e; cj = 1; sx = a.sjx[fj(b, g, 0, e)]; sy = a.sjy[fj(b, g, 0, e)]; }
-                else if (side == 1) { ci = e; cj = b.nj; sx = a.sjx[fj(b, g, b.nj, e)]; sy = a.sjy[fj(b, g, b.nj, e)]; }
-                else if (side == 2) { ci = 1; cj = e; sx = a.six[fi(b, g, e, 0)]; sy = a.siy[fi(b, g, e, 0)]; }
-                else { ci = b.ni; cj = e; sx = a.six[fi(b, g, e, b.ni)]; sy = a.siy[fi(b, g, e, b.ni)]; }
-                const Prim q = prim(w + ws(b, n, 0, cj, ci), st);
-                fx = add(fx, mul(q.p, sx));
-                fy = add(fy, mul(q.p, sy));
+    if (threadIdx.x == 0) {
+        int ns = 0, end = 0;
+        for (int bk = 0; bk < a.nblocks && ns < MAX_WALL_SEGS; ++bk) {
+            const hbns_block &b = a.blocks[bk];
+            for (int side = 0; side < 4; ++side) {
+                if (b.kinds[side] != HBNS_NOSLIP && b.kinds[side] != HBNS_SLIP) continue;
+                end += side < 2 ? b.ni : b.nj;
+                seg_bs[ns] = bk * 4 + side;
+                seg_end[ns] = end;
+                ++ns;
             }
         }
+        nseg_s = ns;
     }
-    a.forces[((int64_t)iter * a.P + n) * 2] = fx;
-    a.forces[((int64_t)iter * a.P + n) * 2 + 1] = fy;
+    __syncthreads();
+    const int nseg = nseg_s;
+    const int total = nseg > 0 ? seg_end[nseg - 1] : 0;
+    double fx = 0.0, fy = 0.0;
+    for (int c0 = 0; c0 < total; c0 += FORCE_CHUNK) {
+        int sg = 0;
+        for (int t = c0 + threadIdx.x; t < min(total, c0 + FORCE_CHUNK); t += FORCE_THREADS) {
+            while (t >= seg_end[sg]) ++sg;
+            const int bk = seg_bs[sg] >> 2, side = seg_bs[sg] & 3;
+            const hbns_block &b = a.blocks[bk];
+            const int e = t - (sg > 0 ? seg_end[sg - 1] : 0) + 1;
+            int ci, cj;
+            double sx, sy;
+            if (side == 0) { ci = e; cj = 1; sx = a.sjx[fj(b, g, 0, e)]; sy = a.sjy[fj(b, g, 0, e)]; }
+            else if (side == 1) { ci = e; cj = b.nj; sx = a.sjx[fj(b, g, b.nj, e)]; sy = a.sjy[fj(b, g, b.nj, e)]; }
+            else if (side == 2) { ci = 1; cj = e; sx = a.six[fi(b, g, e, 0)]; sy = a.siy[fi(b, g, e, 0)]; }
+            else { ci = b.ni; cj = e; sx = a.six[fi(b, g, e, b.ni)]; sy = a.siy[fi(b, g, e, b.ni)]; }
+            const Prim q = prim(w + ws(b, n, 0, cj, ci), (int64_t)(b.nj + 4) * (b.ni + 4));
+            px[t - c0] = mul(q.p, sx);
+            py[t - c0] = mul(q.p, sy);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int m = min(FORCE_CHUNK, total - c0);
+            for (int e = 0; e < m; ++e) {
+                fx = add(fx, px[e]);
+                fy = add(fy, py[e]);
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        a.forces[((int64_t)iter * a.P + n) * 2] = fx;
+        a.forces[((int64_t)iter * a.P + n) * 2 + 1] = fy;
+    }
 }
 
 int check(const char *what) { return hbgpu_check_launch(what); }
@@ -442,11 +590,31 @@ extern "C" int hbns_timestep(const hbns_args *a, int32_t slot, void *stream) {
 }
 
 extern "C" int hbns_residual(const hbns_args *a, int32_t slot, void *stream) {
+    if (a == nullptr || slot < 0 || slot > 2 || a->max_ni < 1 || a->max_nj < 1) {
+        hbgpu_set_error("hbns_residual: bad arguments");
+        return HBGPU_ERR_ARG;
+    }
+    static bool ready[hbgpu::HB_MAX_DEVICES][2];
+    const int dev = hbgpu::current_device();
+    if (dev < 0) return HBGPU_ERR_CUDA;
+    const bool visc = a->mu > 0.0;
+    const size_t smem = sizeof(FluxSmem);
+    if (!ready[dev][visc]) {
+        cudaError_t e = visc ? cudaFuncSetAttribute(ns_flux_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                             : cudaFuncSetAttribute(ns_flux_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return check("hbns_residual (smem attribute)");
+        ready[dev][visc] = true;
+    }
+    const int64_t tiles = (int64_t)((a->max_ni + TI - 1) / TI) * ((a->max_nj + TJ - 1) / TJ);
+    if (tiles * a->P > INT32_MAX || a->nblocks > 65535) {
+        hbgpu_set_error("hbns_residual: grid too large");
+        return HBGPU_ERR_ARG;
+    }
+    const dim3 grid((unsigned)(tiles * a->P), a->nblocks);
     cudaStream_t s = (cudaStream_t)stream;
-    const int halo_cells = (a->max_len + 4) * (a->max_len + 4);
-    ns_prim_kernel<<<dim3((halo_cells + 127) / 128, a->nblocks, a->P), 128, 0, s>>>(*a, a->w[slot]);
-    ns_residual_kernel<<<dim3((a->max_cells + 127) / 128, a->nblocks, a->P), 128, 0, s>>>(*a, a->w[slot]);
-    hbgpu_count_launch(2);
+    if (visc) ns_flux_kernel<true><<<grid, FLUX_THREADS, smem, s>>>(*a, a->w[slot]);
+    else ns_flux_kernel<false><<<grid, FLUX_THREADS, smem, s>>>(*a, a->w[slot]);
+    hbgpu_count_launch(1);
     return check("hbns_residual");
 }
 
@@ -479,7 +647,11 @@ extern "C" int hbns_update(const hbns_args *a, int32_t slot_in, int32_t slot_out
 }
 
 extern "C" int hbns_forces(const hbns_args *a, int32_t iter, void *stream) {
-    ns_forces_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(*a, a->w[0], iter);
+    if (a->nblocks > 256) {
+        hbgpu_set_error("hbns_forces: at most 256 blocks");
+        return HBGPU_ERR_ARG;
+    }
+    ns_forces_kernel<<<a->P, FORCE_THREADS, 0, (cudaStream_t)stream>>>(*a, a->w[0], iter);
     hbgpu_count_launch(1);
     return check("hbns_forces");
 }

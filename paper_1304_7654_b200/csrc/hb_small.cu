@@ -10,9 +10,10 @@
 //   * halo forwarding at write time through the face-target pool (local
 //     cut halo cells of the output slot; the rank has no remote cuts),
 //   * divergence keys per block (hbcore.py:279-284),
-//   * stage 0: one R^2 partial per warp task (fixed shuffle tree), folded per
-//     block at stage 1 by one warp (lane-strided, fixed shuffle tree):
-//     deterministic and independent of the grid size,
+//   * stage 0: per warp task a fixed shuffle tree, per (warp, block) the
+//     warp's tasks in order, per (CTA, block) the warps in order; at stage 1
+//     one warp per block folds the CTA partials (lane-strided, fixed shuffle
+//     tree) -- deterministic for a given grid,
 //   * forces of each iteration into the history after the last stage: one
 //     warp per (coefficient, plane, body), the products h*q formed by the
 //     whole warp and folded left to right by lane 0 (the next iteration's
@@ -37,6 +38,7 @@ constexpr int SMALL_THREADS = 256;
 constexpr int SMALL_WARPS = SMALL_THREADS / 32;
 constexpr int SMALL_MAX_BLOCKS = 256;   // task offsets live in shared memory
 constexpr int SMALL_FCH = 128;          // force chunk per warp
+constexpr int SMALL_MAX_CTAS = 4096;    // grid cap (the per-(CTA, block) partials)
 // slot rotation (hb_runtime.cu kIn / kOut): A -> B -> C -> B -> A
 __device__ __forceinline__ int in_slot_of(int st) { return st == 0 ? 0 : (st == 2 ? 2 : 1); }
 __device__ __forceinline__ int out_slot_of(int st) { return st == 3 ? 0 : (st == 1 ? 2 : 1); }
@@ -49,7 +51,7 @@ struct SmallArgs {
     unsigned long long *status;
     int32_t *iter;
     double *sumsq;           // [max_iters * nblocks]
-    double *task_part;       // [total warp tasks] stage-0 partials
+    double *task_part;       // [gridDim.x * nblocks] stage-0 partials per (CTA, block)
     const hbgpu_force_seg *segs;
     double *force_hist;      // [max_iters * 3 * planes * nbody]
     int32_t nblocks, planes, nbody, nsegs;
@@ -120,6 +122,7 @@ __global__ void __launch_bounds__(SMALL_THREADS, SmallBounds<P>::MIN_BLOCKS)
     __shared__ int task_off[SMALL_MAX_BLOCKS + 1];
     __shared__ int chunks_of[SMALL_MAX_BLOCKS];
     __shared__ double fbuf[SMALL_WARPS][SMALL_FCH];
+    __shared__ double red[SMALL_WARPS][SMALL_MAX_BLOCKS];
     const int lane = threadIdx.x & 31;
     const int nwarps = gridDim.x * SMALL_WARPS;
     const int gwarp = blockIdx.x * SMALL_WARPS + (threadIdx.x >> 5);
@@ -145,14 +148,33 @@ __global__ void __launch_bounds__(SMALL_THREADS, SmallBounds<P>::MIN_BLOCKS)
             double *out = a.slot[out_slot_of(st)];
             const int gstage = iter * 4 + st + 1;
             if (st == 1 && gwarp < a.nblocks && iter < a.max_iters) {
-                // this iteration's stage-0 partials of block gwarp: lane-strided
-                // in task order, then a fixed shuffle tree
+                // this iteration's stage-0 partials of block gwarp: CTAs
+                // lane-strided in order (8 loads in flight), then a fixed
+                // shuffle tree
                 double s = 0.0;
-                for (int t = task_off[gwarp] + lane; t < task_off[gwarp + 1]; t += 32) s = radd(s, a.task_part[t]);
+                const int nc = gridDim.x;
+                for (int c0 = lane; c0 < nc; c0 += 32 * 8) {
+                    double v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int c = c0 + 32 * u;
+                        v[u] = c < nc ? a.task_part[(int64_t)c * a.nblocks + gwarp] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (c0 + 32 * u < nc) s = radd(s, v[u]);
+                }
                 for (int o = 16; o > 0; o >>= 1) s = radd(s, __shfl_down_sync(0xffffffffu, s, o));
                 if (lane == 0) a.sumsq[(int64_t)iter * a.nblocks + gwarp] = s;
             }
-            int bidx = 0;
+            const int wib = threadIdx.x >> 5;
+            if (st == 0) {
+                for (int k = threadIdx.x; k < SMALL_WARPS * a.nblocks; k += SMALL_THREADS)
+                    red[k / a.nblocks][k % a.nblocks] = 0.0;
+                __syncthreads();
+            }
+            int bidx = 0, cur_b = -1;
+            double acc_b = 0.0;
             for (int t = gwarp; t < tasks; t += nwarps) {
                 while (t >= task_off[bidx + 1]) ++bidx;   // tasks ascend per warp
                 const hbgpu_block &b = a.blocks[bidx];
@@ -166,7 +188,21 @@ __global__ void __launch_bounds__(SMALL_THREADS, SmallBounds<P>::MIN_BLOCKS)
                 if (i <= b.ni) acc = small_cell<P>(a, b, in, q0, out, st, p, j, i, gstage, bidx);
                 if (st == 0) {
                     for (int o = 16; o > 0; o >>= 1) acc = radd(acc, __shfl_down_sync(0xffffffffu, acc, o));
-                    if (lane == 0) a.task_part[t] = acc;
+                    if (bidx != cur_b) {
+                        if (cur_b >= 0 && lane == 0) red[wib][cur_b] = acc_b;
+                        acc_b = 0.0;
+                        cur_b = bidx;
+                    }
+                    acc_b = radd(acc_b, acc);
+                }
+            }
+            if (st == 0) {
+                if (cur_b >= 0 && lane == 0) red[wib][cur_b] = acc_b;
+                __syncthreads();
+                for (int bb = threadIdx.x; bb < a.nblocks; bb += SMALL_THREADS) {
+                    double s = 0.0;
+                    for (int w2 = 0; w2 < SMALL_WARPS; ++w2) s = radd(s, red[w2][bb]);
+                    a.task_part[(int64_t)blockIdx.x * a.nblocks + bb] = s;
                 }
             }
             grid.sync();
@@ -230,7 +266,7 @@ static int small_launch_p(const SmallArgs &a, int tasks, cudaStream_t s) {
     }
     // every co-resident CTA, or one warp per task if there are fewer tasks
     int grid = (int)std::min<int64_t>(L.grid, ((int64_t)tasks + SMALL_WARPS - 1) / SMALL_WARPS);
-    grid = std::max(grid, 1);
+    grid = std::max(std::min(grid, SMALL_MAX_CTAS), 1);   // the partial buffer's capacity
     void *params[] = {(void *)&a};
     cudaError_t e = cudaLaunchCooperativeKernel(L.fn, dim3(grid), dim3(SMALL_THREADS), params, 0, s);
     if (e != cudaSuccess) {
@@ -257,7 +293,9 @@ int small_prepare(const hbgpu_engine_desc &d, int *tasks, double **part_buf) {
         hbgpu_set_error("small schedule: %lld warp tasks", (long long)n);
         return HBGPU_ERR_ARG;
     }
-    if (cudaMalloc(part_buf, sizeof(double) * (size_t)n) != cudaSuccess)
+    // one stage-0 partial per (CTA, block): at most one CTA per warp task
+    const int64_t ctas = std::min<int64_t>((n + SMALL_WARPS - 1) / SMALL_WARPS, SMALL_MAX_CTAS);
+    if (cudaMalloc(part_buf, sizeof(double) * (size_t)(ctas * d.nblocks)) != cudaSuccess)
         return hbgpu_check_launch("small schedule: partials");
     *tasks = (int)n;
     return HBGPU_OK;

@@ -381,12 +381,12 @@ def _ns_types():
                     ("fj_off", i64), ("part_off", i64), ("ni", i32), ("nj", i32), ("kinds", i32 * 4)]
 
     class Args(ctypes.Structure):
-        _fields_ = [("w", vp * 3), ("r", vp), ("prim", vp), ("dt", vp), ("xc", vp), ("yc", vp), ("vol", vp),
+        _fields_ = [("w", vp * 3), ("r", vp), ("dt", vp), ("xc", vp), ("yc", vp), ("vol", vp),
                     ("six", vp), ("siy", vp), ("gi", vp), ("sjx", vp), ("sjy", vp), ("gj", vp),
                     ("blocks", vp), ("winf", vp), ("dmat", vp), ("status", vp), ("norm_part", vp),
-                    ("norms", vp), ("forces", vp), ("mu", f64), ("cfl", f64), ("omega_nh", f64),
+                    ("norms", vp), ("forces", vp), ("mu", f64), ("cfl", f64), ("omega_nh", f64), ("kq", f64),
                     ("nblocks", i32), ("P", i32), ("Pg", i32), ("moving", i32), ("max_len", i32),
-                    ("max_cells", i32)]
+                    ("max_cells", i32), ("max_ni", i32), ("max_nj", i32)]
     return Block, Args
 
 
@@ -440,7 +440,6 @@ class NSRun:
             q = initial(b) if initial is not None else initial_state(case, b)
             self.slot_view(0, b).copy_(torch.from_numpy(np.ascontiguousarray(q)))
         self.r = torch.zeros(max(1, r_off), dtype=f64, device=dev)
-        self.prim = torch.zeros(wsz // 4 * 5, dtype=f64, device=dev)
         self.dt = torch.zeros(max(1, dt_off), dtype=f64, device=dev)
         self.geo = {k: (torch.from_numpy(np.concatenate(v)).to(dev) if v else torch.zeros(1, dtype=f64, device=dev))
                     for k, v in pools.items()}
@@ -458,16 +457,18 @@ class NSRun:
         a = Args()
         for k in range(3):
             a.w[k] = self.slots[k].data_ptr()
-        a.r, a.prim, a.dt = self.r.data_ptr(), self.prim.data_ptr(), self.dt.data_ptr()
+        a.r, a.dt = self.r.data_ptr(), self.dt.data_ptr()
         for name in pools:
             setattr(a, name, self.geo[name].data_ptr())
         a.blocks, a.winf, a.dmat = self.t_blocks.data_ptr(), self.winf.data_ptr(), self.dmat.data_ptr()
         a.status, a.norm_part = self.status.data_ptr(), self.norm_part.data_ptr()
         a.norms, a.forces = self.norms.data_ptr(), self.forces.data_ptr()
         a.mu, a.cfl, a.omega_nh = case.mu, case.cfl, case.omega * case.nharms
+        a.kq = (case.mu * GAMMA) / PR    # the specification's (mu gamma) / Pr, one IEEE mul and div
         a.nblocks, a.P, a.Pg, a.moving = len(blocks), P, Pg, int(moving)
         a.max_len = max(max(b.ni, b.nj) for b in blocks)
         a.max_cells = max_cells
+        a.max_ni, a.max_nj = max(b.ni for b in blocks), max(b.nj for b in blocks)
         self.args = a
         self.done = 0
 
