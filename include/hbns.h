@@ -8,8 +8,7 @@
  *
  * One RK stage of the host loop (nsflow.NSRun):
  *   cut halos (hbgpu_halo, two layers) -> hbns_boundaries(slot_in)
- *   -> [stage 1: hbns_timestep(slot 0)] -> hbns_residual(slot_in)
- *   -> hbns_update(slot_in, slot_out, alpha_s)
+ *   -> hbns_stage(slot_in, slot_out, alpha_s)
  * and after the fourth stage hbns_forces.  All pointers are device memory
  * except the args struct itself; every call is asynchronous on `stream`.
  */
@@ -27,6 +26,11 @@ extern "C" {
 #define HBNS_SLIP 2
 #define HBNS_CUT 3
 
+/* hbns_stage tiles: HBNS_TILE_I columns x HBNS_TILE_J rows of a block per
+ * CTA; norm_part holds one partial per tile (part_off per block)          */
+#define HBNS_TILE_I 32
+#define HBNS_TILE_J 8
+
 typedef struct hbns_block {
     int64_t w_off;       /* element offset of the block in every state pool   */
     int64_t r_off;       /* ... in the residual pool (P, 4, nj, ni)            */
@@ -34,9 +38,12 @@ typedef struct hbns_block {
     int64_t c_off;       /* ... in the cell-geometry pools (Pg, nj+4, ni+4)    */
     int64_t fi_off;      /* ... in the i-face pools (Pg, nj+4, ni+5)           */
     int64_t fj_off;      /* ... in the j-face pools (Pg, nj+5, ni+4)           */
-    int64_t part_off;    /* ... in the stage-1 norm partials (P * ctas)        */
+    int64_t part_off;    /* ... in the stage-1 norm partials (one per tile)   */
     int32_t ni, nj;
     int32_t kinds[4];    /* south, north, west, east: HBNS_*                   */
+    int32_t gid;         /* index of the block in the job (ids ascending)      */
+    int32_t wall_off;    /* position of its first wall face in the job's wall
+                            order (blocks ascending, sides S/N/W/E, cells)    */
 } hbns_block;
 
 typedef struct hbns_args {
@@ -53,19 +60,36 @@ typedef struct hbns_args {
     double *norm_part;           /* stage-1 partials                          */
     double *norms;               /* per iteration                             */
     double *forces;              /* per iteration, snapshot: (fx, fy)         */
+    /* multi-rank runs (else null): per iteration the per-block sums of
+     * R_rho^2 at [iter * nglobal + gid], and the wall-face products p S at
+     * [((iter * P + n) * 2 + xy) * nwall + position]; summed over the ranks
+     * they fold (hbgpu_norm_totals, hbns_wall_fold) exactly as one rank's    */
+    double *blk_norms;
+    double *wall_prod;
+    /* non-null: the iteration index is read from this device counter (the
+     * `iter` arguments are ignored) and hbns_forces advances it, so one
+     * captured iteration replays as the next                               */
+    int32_t *iter_dev;
     double mu, cfl, omega_nh;    /* M/Re (0: Euler), CFL, omega * N_H         */
     double kq;                   /* (mu * gamma) / Pr, as the host rounds it  */
     int32_t nblocks, P, Pg, moving;
     int32_t max_len, max_cells;  /* largest block side, largest ni * nj       */
     int32_t max_ni, max_nj;      /* largest ni, largest nj (residual grid)    */
+    int32_t nglobal, nwall;      /* blocks / wall faces of the whole job      */
 } hbns_args;
 
 int hbns_boundaries(const hbns_args *a, int32_t slot, void *stream);
-int hbns_timestep(const hbns_args *a, int32_t slot, void *stream);
-int hbns_residual(const hbns_args *a, int32_t slot, void *stream);
-int hbns_update(const hbns_args *a, int32_t slot_in, int32_t slot_out, double coef, int32_t iter,
-                int32_t want_norm, void *stream);
+/* One RK stage: residual of slot_in (halos filled), HB source, update
+ * W(slot_out) = W(slot 0) - (coef dt / V) R.  first != 0 (stage 1, slot_in
+ * = 0): the local time step is formed from slot 0 into `dt` first, and the
+ * residual norm of iteration `iter` is written to norms[iter].            */
+int hbns_stage(const hbns_args *a, int32_t slot_in, int32_t slot_out, double coef, int32_t iter,
+               int32_t first, void *stream);
 int hbns_forces(const hbns_args *a, int32_t iter, void *stream);
+/* forces[(it * P + n) * 2 + xy] = left-to-right sum over the nwall faces of
+ * wall_prod[((it * P + n) * 2 + xy) * nwall + f], it < iters               */
+int hbns_wall_fold(const double *wall_prod, int32_t iters, int32_t P, int32_t nwall, double *forces,
+                   void *stream);
 
 #ifdef __cplusplus
 }

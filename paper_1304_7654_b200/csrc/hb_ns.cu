@@ -15,15 +15,16 @@
 //   ns_bc_kernel        non-cut sides' two halo layers, one thread per
 //                       (side, layer, face cell, snapshot)
 //   ns_corner_kernel    corner halos
-//   ns_timestep_kernel  local time step, one thread per cell
-//   ns_flux_kernel      R of a TJ x TI tile and one snapshot per CTA: the
-//                       state with its 2-cell ring staged in shared memory,
-//                       primitives once per staged cell, sensors once per
-//                       (cell, direction), every face flux once
-//   ns_update_kernel    HB source + RK update, one thread per (cell,
-//                       variable) for all snapshots; stage-1 R_rho^2 partials
-//                       per CTA, folded by ns_norm_kernel (a warp per block)
-//   ns_forces_kernel    wall pressure forces, one thread per snapshot
+//   ns_stage_kernel     one RK stage of a TJ x TI tile, all snapshots, per
+//                       CTA: per snapshot the state with its 2-cell ring
+//                       staged in shared memory, primitives once per staged
+//                       cell, sensors once per (cell, direction), every face
+//                       flux once, R_n to an L2-resident scratch (stage 1:
+//                       the local time step folded over the snapshots); then
+//                       HB source + RK update of the tile and the stage-1
+//                       norm partial (folded by ns_norm_kernel)
+//   ns_norm_kernel      per block the tile partials (a warp), blocks in order
+//   ns_forces_kernel    wall pressure forces, one CTA per snapshot
 // Cut halos move with hbgpu_halo (two directions per cut and layer).
 
 #include "hb_tma.cuh"
@@ -162,7 +163,7 @@ __global__ void ns_corner_kernel(hbns_args a, double *w) {
 // from L1.  The per-point arithmetic is the specification's, operation for
 // operation, so R is bitwise the thread-per-cell kernel's (and the oracle's).
 
-constexpr int TI = 32, TJ = 8;               // tile columns, rows
+constexpr int TI = HBNS_TILE_I, TJ = HBNS_TILE_J;   // tile columns, rows
 constexpr int RW = TI + 4, RH = TJ + 4;      // staged region with the 2-cell ring
 constexpr int FLUX_THREADS = 288;            // 9 warps: 264 i-faces / 288 j-faces per pass
 
@@ -177,6 +178,7 @@ struct FluxSmem {
     double nuj[TJ + 2][TI];        // sensor along j: rows j0-1 .. j0+TJ, tile columns
     double fi[NV][TJ][TI + 1];     // i-face fluxes: face k between cells i0-1+k and i0+k
     double fj[NV][TJ + 1][TI];     // j-face fluxes: face k between rows j0-1+k and j0+k
+    double dmat[HBGPU_MAX_TEMPLATED_P * HBGPU_MAX_TEMPLATED_P];   // HB matrix D (stage kernel)
 };
 
 // one 8-byte global -> shared copy, asynchronous (LDGSTS): a CTA issues all
@@ -272,223 +274,258 @@ __device__ __forceinline__ void stage_row(double *sdst, const double *grow, int 
 // Thread mapping: lane = tile column, warp = row (TI = 32 = warp width), so
 // staging, primitives, sensors and faces need no index division; the 9th
 // warp takes the 8 east-most i-faces and the last j-face row.
-// CTAs per SM the register budget is sized for: 3 of 9 warps (the register
-// file is split over the 4 schedulers, so <= 72 registers; a few spill, and
-// the extra warps still win: C4 231 -> 223, C3 15.6 -> 15.2 ms/iteration
-// against 2).  HBNS_FLUX_MINB overrides it in measurement builds.
-#ifndef HBNS_FLUX_MINB
-#define HBNS_FLUX_MINB 3
+// CTAs per SM the register budget is sized for (9 warps each; the register
+// file is split over the 4 schedulers, so 3 CTAs mean <= 72 registers and 2
+// <= 96).  Measured on the fused stage kernel: Euler 3 (C4 201 vs 210 ms per
+// iteration with 2), viscous 2 (C3 13.9 vs 14.9, C1 0.44 vs 0.50 ms).
+// HBNS_FLUX_MINB overrides both in measurement builds.
+#ifdef HBNS_FLUX_MINB
+#define HBNS_MINB(VISC) HBNS_FLUX_MINB
+#else
+#define HBNS_MINB(VISC) ((VISC) ? 2 : 3)
 #endif
 
-template <bool VISC>
-__global__ void __launch_bounds__(FLUX_THREADS, HBNS_FLUX_MINB) ns_flux_kernel(hbns_args a, const double *w) {
-    // grid.x = tile * P + snapshot (snapshots of a tile adjacent: the same
-    // geometry when the mesh is fixed), grid.y = block
+// The RK stage of one TJ x TI tile, all snapshots, in one CTA (grid.x =
+// tile, grid.y = block).  Per snapshot n: stage W_n with its 2-cell ring
+// (and, once per tile unless the mesh moves, the face normals and cell
+// centres), form the face fluxes, write R_n = sum of face fluxes to the
+// residual pool -- an L2-resident scratch: this CTA reads it back moments
+// later -- and, in the first stage, fold the cell's local time step (the
+// specification's dt, min over snapshots, from the iteration's start state
+// that stage 1 reads).  Then the update of the tile, thread = cell, for
+// every (variable, snapshot): the HB source V sum_m D[n][m] W_m (m
+// ascending) added to R_n, W^(s) = W^0 - (alpha_s dt / V) R.  The time-step
+// and update kernels of the unfused schedule are gone: their inputs are
+// already on chip (primitives, normals) or in L2 (R, W_m).
+template <bool VISC, int P>
+__global__ void __launch_bounds__(FLUX_THREADS, HBNS_MINB(VISC))
+    ns_stage_kernel(hbns_args a, const double *w, const double *w0, double *w_out, double coef, int first) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     FluxSmem &S = *reinterpret_cast<FluxSmem *>(smem_raw);
+    __shared__ double red[FLUX_THREADS / 32];
     const hbns_block b = a.blocks[blockIdx.y];
-    const int n = blockIdx.x % a.P;
-    const int tile = blockIdx.x / a.P;
+    const int tile = blockIdx.x;
     const int tiles_i = (b.ni + TI - 1) / TI;
     if (tile >= tiles_i * ((b.nj + TJ - 1) / TJ)) return;
     const int i0 = (tile % tiles_i) * TI + 1, j0 = (tile / tiles_i) * TJ + 1;
-    const int g = a.Pg > 1 ? n : 0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int NW = FLUX_THREADS / 32;
-    // 1. stage, all copies in flight at once: the state of region cells
-    //    (j0-2 .. j0+TJ+1) x (i0-2 .. i0+TI+1), clamped to the block's array
-    //    (the clamped cells feed no face); the tile's face normals and grid
-    //    fluxes; the cell centres of the 1-cell ring (viscous)
-    {
-        const int ilast = b.ni + 2 - (i0 - 2);   // region column of array column ni+2
-        for (int row = warp; row < NV * RH; row += NW) {
-            const int k = row / RH, r = row - k * RH;
-            stage_row(S.w[k][r], w + ws(b, n, k, min(j0 - 2 + r, b.nj + 2), i0 - 2), RW, ilast, lane);
-        }
-        const int flast = b.ni - (i0 - 1);       // i-face column of face ni
-        for (int r = warp; r < TJ; r += NW) {
-            const int64_t f = fi(b, g, min(j0 + r, b.nj), i0 - 1);
-            stage_row(S.nxi[r], a.six + f, TI + 1, flast, lane);
-            stage_row(S.nyi[r], a.siy + f, TI + 1, flast, lane);
-            if (a.moving) stage_row(S.gfi[r], a.gi + f, TI + 1, flast, lane);
-        }
-        const int jlast = b.ni - i0;             // j-face / tile column of cell ni
-        for (int r = warp; r <= TJ; r += NW) {
-            const int64_t f = fj(b, g, min(j0 - 1 + r, b.nj), i0);
-            stage_row(S.nxj[r], a.sjx + f, TI, jlast, lane);
-            stage_row(S.nyj[r], a.sjy + f, TI, jlast, lane);
-            if (a.moving) stage_row(S.gfj[r], a.gj + f, TI, jlast, lane);
-        }
-        if (VISC) {
-            const int clast = b.ni + 1 - (i0 - 1);
-            for (int r = warp; r < RH - 2; r += NW) {
-                const int64_t o = cc(b, g, min(j0 - 1 + r, b.nj + 1), i0 - 1);
-                stage_row(S.xc[r], a.xc + o, RW - 2, clast, lane);
-                stage_row(S.yc[r], a.yc + o, RW - 2, clast, lane);
+    const bool mv = a.moving != 0;
+    // this thread's cell in the update and time-step steps (warps 0..TJ-1)
+    const int cr = warp, cc_ = lane;
+    const int cj = j0 + cr, ci = i0 + cc_;
+    const bool cell_live = warp < TJ && cj <= b.nj && ci <= b.ni;
+    double best = 0.0;   // stage 1: the cell's time step, min over snapshots
+    for (int t = threadIdx.x; t < P * P; t += FLUX_THREADS) S.dmat[t] = a.dmat[t];
+    for (int n = 0; n < P; ++n) {
+        const int g = a.Pg > 1 ? n : 0;
+        const bool geo = n == 0 || a.Pg > 1;   // stage the geometry of snapshot g
+        __syncthreads();                        // the previous snapshot's reads of S are done
+        // 1. stage, all copies in flight at once: the state of region cells
+        //    (j0-2 .. j0+TJ+1) x (i0-2 .. i0+TI+1), clamped to the block's
+        //    array (the clamped cells feed no face); the tile's face normals
+        //    and grid fluxes; the cell centres of the 1-cell ring (viscous)
+        {
+            const int ilast = b.ni + 2 - (i0 - 2);   // region column of array column ni+2
+            for (int row = warp; row < NV * RH; row += NW) {
+                const int k = row / RH, r = row - k * RH;
+                stage_row(S.w[k][r], w + ws(b, n, k, min(j0 - 2 + r, b.nj + 2), i0 - 2), RW, ilast, lane);
+            }
+            if (geo) {
+                const int flast = b.ni - (i0 - 1);       // i-face column of face ni
+                for (int r = warp; r < TJ; r += NW) {
+                    const int64_t f = fi(b, g, min(j0 + r, b.nj), i0 - 1);
+                    stage_row(S.nxi[r], a.six + f, TI + 1, flast, lane);
+                    stage_row(S.nyi[r], a.siy + f, TI + 1, flast, lane);
+                    if (mv) stage_row(S.gfi[r], a.gi + f, TI + 1, flast, lane);
+                }
+                const int jlast = b.ni - i0;             // j-face / tile column of cell ni
+                for (int r = warp; r <= TJ; r += NW) {
+                    const int64_t f = fj(b, g, min(j0 - 1 + r, b.nj), i0);
+                    stage_row(S.nxj[r], a.sjx + f, TI, jlast, lane);
+                    stage_row(S.nyj[r], a.sjy + f, TI, jlast, lane);
+                    if (mv) stage_row(S.gfj[r], a.gj + f, TI, jlast, lane);
+                }
+                if (VISC) {
+                    const int clast = b.ni + 1 - (i0 - 1);
+                    for (int r = warp; r < RH - 2; r += NW) {
+                        const int64_t o = cc(b, g, min(j0 - 1 + r, b.nj + 1), i0 - 1);
+                        stage_row(S.xc[r], a.xc + o, RW - 2, clast, lane);
+                        stage_row(S.yc[r], a.yc + o, RW - 2, clast, lane);
+                    }
+                }
             }
         }
-    }
-    cp_wait_all();
-    __syncthreads();
-    // 2. primitives of every staged cell (nsflow: u, v, p, c, e)
-    for (int t = threadIdx.x; t < RH * RW; t += FLUX_THREADS) {
-        const int r = t / RW, c = t - r * RW;
-        const double q_r = S.w[0][r][c], q_ru = S.w[1][r][c], q_rv = S.w[2][r][c], q_re = S.w[3][r][c];
-        const double u = dv(q_ru, q_r), v = dv(q_rv, q_r);
-        const double p = mul(GAMMA - 1.0, sub(q_re, mul(0.5, add(mul(q_ru, u), mul(q_rv, v)))));
-        S.pr[0][r][c] = u;
-        S.pr[1][r][c] = v;
-        S.pr[2][r][c] = p;
-        S.pr[3][r][c] = __dsqrt_rn(dv(mul(GAMMA, p), q_r));
-        S.pr[4][r][c] = dv(p, mul(GAMMA - 1.0, q_r));
-    }
-    __syncthreads();
-    // 3. JST sensors of the cells beside the tile's faces
-    constexpr int NSI = TJ * (TI + 2), NSJ = (TJ + 2) * TI;
-    for (int t = threadIdx.x; t < NSI + NSJ; t += FLUX_THREADS) {
-        if (t < NSI) {
-            const int r = t / (TI + 2), c = t - r * (TI + 2);   // cell (j0 + r, i0 - 1 + c)
-            S.nui[r][c] = sensor(S.pr[2][r + 2][c], S.pr[2][r + 2][c + 1], S.pr[2][r + 2][c + 2]);
-        } else {
-            const int u = t - NSI, r = u / TI, c = u % TI;      // cell (j0 - 1 + r, i0 + c)
-            S.nuj[r][c] = sensor(S.pr[2][r][c + 2], S.pr[2][r + 1][c + 2], S.pr[2][r + 2][c + 2]);
+        cp_wait_all();
+        __syncthreads();
+        // 2. primitives of every staged cell (nsflow: u, v, p, c, e)
+        for (int t = threadIdx.x; t < RH * RW; t += FLUX_THREADS) {
+            const int r = t / RW, c = t - r * RW;
+            const double q_r = S.w[0][r][c], q_ru = S.w[1][r][c], q_rv = S.w[2][r][c], q_re = S.w[3][r][c];
+            const double u = dv(q_ru, q_r), v = dv(q_rv, q_r);
+            const double p = mul(GAMMA - 1.0, sub(q_re, mul(0.5, add(mul(q_ru, u), mul(q_rv, v)))));
+            S.pr[0][r][c] = u;
+            S.pr[1][r][c] = v;
+            S.pr[2][r][c] = p;
+            S.pr[3][r][c] = __dsqrt_rn(dv(mul(GAMMA, p), q_r));
+            S.pr[4][r][c] = dv(p, mul(GAMMA - 1.0, q_r));
         }
-    }
-    __syncthreads();
-    // 4. face fluxes, one i-face and one j-face per thread, both evaluated
-    //    unconditionally (indices clamped into the staged region) so that the
-    //    two dependency chains interleave; only real faces are stored.
-    //    Warp w < TJ: i-faces of row w (faces 0..31); warp TJ: face 32 of
-    //    every row (lanes 0..TJ-1).  Every warp w: j-face row w.
-    {
-        const bool mv = a.moving != 0;
-        const int ri = warp < TJ ? warp : min(lane, TJ - 1), ci = warp < TJ ? lane : TI;
-        const bool live_i = (warp < TJ || lane < TJ) && j0 + ri <= b.nj && i0 - 1 + ci <= b.ni;
-        const int rj = warp, cj = lane;
-        const bool live_j = j0 - 1 + rj <= b.nj && i0 + cj <= b.ni;
-        double oi[NV], oj[NV];
-        tile_face<VISC>(a, S, ri + 2, ci + 1, 0, 1, S.nxi[ri][ci], S.nyi[ri][ci], mv ? S.gfi[ri][ci] : 0.0,
-                        S.nui[ri][ci], S.nui[ri][ci + 1], oi);
-        tile_face<VISC>(a, S, rj + 1, cj + 2, 1, 0, S.nxj[rj][cj], S.nyj[rj][cj], mv ? S.gfj[rj][cj] : 0.0,
-                        S.nuj[rj][cj], S.nuj[rj + 1][cj], oj);
-        if (live_i) {
+        __syncthreads();
+        // 3. JST sensors of the cells beside the tile's faces
+        constexpr int NSI = TJ * (TI + 2), NSJ = (TJ + 2) * TI;
+        for (int t = threadIdx.x; t < NSI + NSJ; t += FLUX_THREADS) {
+            if (t < NSI) {
+                const int r = t / (TI + 2), c = t - r * (TI + 2);   // cell (j0 + r, i0 - 1 + c)
+                S.nui[r][c] = sensor(S.pr[2][r + 2][c], S.pr[2][r + 2][c + 1], S.pr[2][r + 2][c + 2]);
+            } else {
+                const int u = t - NSI, r = u / TI, c = u % TI;      // cell (j0 - 1 + r, i0 + c)
+                S.nuj[r][c] = sensor(S.pr[2][r][c + 2], S.pr[2][r + 1][c + 2], S.pr[2][r + 2][c + 2]);
+            }
+        }
+        __syncthreads();
+        // 4. face fluxes, one i-face and one j-face per thread, both evaluated
+        //    unconditionally (indices clamped into the staged region) so that
+        //    the two dependency chains interleave; only real faces are stored.
+        //    Warp w < TJ: i-faces of row w (faces 0..31); warp TJ: face 32 of
+        //    every row (lanes 0..TJ-1).  Every warp w: j-face row w.
+        {
+            const int ri = warp < TJ ? warp : min(lane, TJ - 1), ci2 = warp < TJ ? lane : TI;
+            const bool live_i = (warp < TJ || lane < TJ) && j0 + ri <= b.nj && i0 - 1 + ci2 <= b.ni;
+            const int rj = warp, cj2 = lane;
+            const bool live_j = j0 - 1 + rj <= b.nj && i0 + cj2 <= b.ni;
+            double oi[NV], oj[NV];
+            tile_face<VISC>(a, S, ri + 2, ci2 + 1, 0, 1, S.nxi[ri][ci2], S.nyi[ri][ci2], mv ? S.gfi[ri][ci2] : 0.0,
+                            S.nui[ri][ci2], S.nui[ri][ci2 + 1], oi);
+            tile_face<VISC>(a, S, rj + 1, cj2 + 2, 1, 0, S.nxj[rj][cj2], S.nyj[rj][cj2], mv ? S.gfj[rj][cj2] : 0.0,
+                            S.nuj[rj][cj2], S.nuj[rj + 1][cj2], oj);
+            if (live_i) {
 #pragma unroll
-            for (int k = 0; k < NV; ++k) S.fi[k][ri][ci] = oi[k];
-        }
-        if (live_j) {
+                for (int k = 0; k < NV; ++k) S.fi[k][ri][ci2] = oi[k];
+            }
+            if (live_j) {
 #pragma unroll
-            for (int k = 0; k < NV; ++k) S.fj[k][rj][cj] = oj[k];
+                for (int k = 0; k < NV; ++k) S.fj[k][rj][cj2] = oj[k];
+            }
         }
-    }
-    __syncthreads();
-    // 5. R = ((F_{i+1/2} - F_{i-1/2}) + F_{j+1/2}) - F_{j-1/2}
-    if (warp < TJ) {
-        const int r = warp, c = lane;
-        const int j = j0 + r, i = i0 + c;
-        if (j <= b.nj && i <= b.ni) {
+        __syncthreads();
+        // 5. R_n = ((F_{i+1/2} - F_{i-1/2}) + F_{j+1/2}) - F_{j-1/2}; stage 1:
+        //    the local time step of snapshot n (nsflow: lambda_i, lambda_j,
+        //    lambda_v, omega N_H V), folded into the min over snapshots
+        if (cell_live) {
+            const int r = cr, c = cc_;
 #pragma unroll
             for (int k = 0; k < NV; ++k)
-                a.r[rs(b, n, k, j, i)] = sub(add(sub(S.fi[k][r][c + 1], S.fi[k][r][c]), S.fj[k][r + 1][c]), S.fj[k][r][c]);
-        }
-    }
-}
-
-__global__ void ns_timestep_kernel(hbns_args a, const double *w) {
-    const hbns_block &b = a.blocks[blockIdx.y];
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= b.ni * b.nj) return;
-    const int i = t % b.ni + 1, j = t / b.ni + 1;
-    const int64_t st = (int64_t)(b.nj + 4) * (b.ni + 4);
-    const bool mv = a.moving != 0;
-    double best = 0.0;
-    for (int n = 0; n < a.P; ++n) {
-        const int g = a.Pg > 1 ? n : 0;
-        const Prim q = prim(w + ws(b, n, 0, j, i), st);
-        const double ax = a.six[fi(b, g, j, i - 1)], ay = a.siy[fi(b, g, j, i - 1)];
-        const double bx = a.six[fi(b, g, j, i)], by = a.siy[fi(b, g, j, i)];
-        const double cx = a.sjx[fj(b, g, j - 1, i)], cy = a.sjy[fj(b, g, j - 1, i)];
-        const double dx = a.sjx[fj(b, g, j, i)], dy = a.sjy[fj(b, g, j, i)];
-        const double ga = mv ? a.gi[fi(b, g, j, i - 1)] : 0.0, gb = mv ? a.gi[fi(b, g, j, i)] : 0.0;
-        const double gc = mv ? a.gj[fj(b, g, j - 1, i)] : 0.0, gd = mv ? a.gj[fj(b, g, j, i)] : 0.0;
-        const double la = add(fabs(sub(add(mul(q.u, ax), mul(q.v, ay)), ga)), mul(q.c, __dsqrt_rn(add(mul(ax, ax), mul(ay, ay)))));
-        const double lb = add(fabs(sub(add(mul(q.u, bx), mul(q.v, by)), gb)), mul(q.c, __dsqrt_rn(add(mul(bx, bx), mul(by, by)))));
-        const double lc = add(fabs(sub(add(mul(q.u, cx), mul(q.v, cy)), gc)), mul(q.c, __dsqrt_rn(add(mul(cx, cx), mul(cy, cy)))));
-        const double ld = add(fabs(sub(add(mul(q.u, dx), mul(q.v, dy)), gd)), mul(q.c, __dsqrt_rn(add(mul(dx, dx), mul(dy, dy)))));
-        const double V = a.vol[cc(b, g, j, i)];
-        double den = add(mul(0.5, add(la, lb)), mul(0.5, add(lc, ld)));
-        if (a.mu > 0.0) {
-            const double sxi = mul(0.5, add(ax, bx)), syi = mul(0.5, add(ay, by));
-            const double sxj = mul(0.5, add(cx, dx)), syj = mul(0.5, add(cy, dy));
-            const double lv = mul(dv(mul(mul(2.0, GAMMA), a.mu), mul(PR, q.r)),
-                                  dv(add(add(mul(sxi, sxi), mul(syi, syi)), add(mul(sxj, sxj), mul(syj, syj))), V));
-            den = add(den, lv);
-        }
-        den = add(den, mul(a.omega_nh, V));
-        const double tn = dv(mul(a.cfl, V), den);
-        best = n == 0 ? tn : fmin(best, tn);
-    }
-    a.dt[b.dt_off + (int64_t)(j - 1) * b.ni + (i - 1)] = best;
-}
-
-constexpr int UPD_THREADS = 256;
-
-// one thread per (cell, variable k), all P snapshots: each W_m is loaded once
-// for the P outputs of the HB source
-template <int P>
-__global__ void __launch_bounds__(UPD_THREADS) ns_update_kernel(hbns_args a, const double *w_in, const double *w0,
-                                                                  double *w_out, double coef, int want_norm) {
-    // grid.y = block, grid.z = variable; x over interior cells
-    __shared__ double red[UPD_THREADS];
-    const hbns_block &b = a.blocks[blockIdx.y];
-    const int k = blockIdx.z;
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    double sq = 0.0;
-    if (t < b.ni * b.nj) {
-        const int i = t % b.ni + 1, j = t / b.ni + 1;
-        double wm[P];
-#pragma unroll
-        for (int m = 0; m < P; ++m) wm[m] = w_in[ws(b, m, k, j, i)];
-        const double dtc = a.dt[b.dt_off + (int64_t)(j - 1) * b.ni + (i - 1)];
-#pragma unroll
-        for (int n = 0; n < P; ++n) {
-            const int g = a.Pg > 1 ? n : 0;
-            const double V = a.vol[cc(b, g, j, i)];
-            double s = mul(a.dmat[n * P], wm[0]);
-#pragma unroll
-            for (int m = 1; m < P; ++m) s = add(s, mul(a.dmat[n * P + m], wm[m]));
-            const double R = add(a.r[rs(b, n, k, j, i)], mul(V, s));
-            if (want_norm && k == 0) sq = __fma_rn(R, R, sq);
-            const double v = sub(w0[ws(b, n, k, j, i)], mul(dv(mul(coef, dtc), V), R));
-            w_out[ws(b, n, k, j, i)] = v;
-            if (!isfinite(v)) {
-                const long long lin = (((long long)(n * NV + k) * b.nj + (j - 1)) * b.ni) + (i - 1);
-                atomicMin(a.status + blockIdx.y, (unsigned long long)lin);
+                a.r[rs(b, n, k, cj, ci)] = sub(add(sub(S.fi[k][r][c + 1], S.fi[k][r][c]), S.fj[k][r + 1][c]), S.fj[k][r][c]);
+            if (first) {
+                const double qu = S.pr[0][r + 2][c + 2], qv = S.pr[1][r + 2][c + 2], qc = S.pr[3][r + 2][c + 2];
+                const double ax = S.nxi[r][c], ay = S.nyi[r][c], bx = S.nxi[r][c + 1], by = S.nyi[r][c + 1];
+                const double cx = S.nxj[r][c], cy = S.nyj[r][c], dx = S.nxj[r + 1][c], dy = S.nyj[r + 1][c];
+                const double ga = mv ? S.gfi[r][c] : 0.0, gb = mv ? S.gfi[r][c + 1] : 0.0;
+                const double gc = mv ? S.gfj[r][c] : 0.0, gd = mv ? S.gfj[r + 1][c] : 0.0;
+                const double la = add(fabs(sub(add(mul(qu, ax), mul(qv, ay)), ga)), mul(qc, __dsqrt_rn(add(mul(ax, ax), mul(ay, ay)))));
+                const double lb = add(fabs(sub(add(mul(qu, bx), mul(qv, by)), gb)), mul(qc, __dsqrt_rn(add(mul(bx, bx), mul(by, by)))));
+                const double lc = add(fabs(sub(add(mul(qu, cx), mul(qv, cy)), gc)), mul(qc, __dsqrt_rn(add(mul(cx, cx), mul(cy, cy)))));
+                const double ld = add(fabs(sub(add(mul(qu, dx), mul(qv, dy)), gd)), mul(qc, __dsqrt_rn(add(mul(dx, dx), mul(dy, dy)))));
+                const double V = a.vol[cc(b, g, cj, ci)];
+                double den = add(mul(0.5, add(la, lb)), mul(0.5, add(lc, ld)));
+                if (VISC) {
+                    const double sxi = mul(0.5, add(ax, bx)), syi = mul(0.5, add(ay, by));
+                    const double sxj = mul(0.5, add(cx, dx)), syj = mul(0.5, add(cy, dy));
+                    const double lv = mul(dv(mul(mul(2.0, GAMMA), a.mu), mul(PR, S.w[0][r + 2][c + 2])),
+                                          dv(add(add(mul(sxi, sxi), mul(syi, syi)), add(mul(sxj, sxj), mul(syj, syj))), V));
+                    den = add(den, lv);
+                }
+                den = add(den, mul(a.omega_nh, V));
+                const double tn = dv(mul(a.cfl, V), den);
+                best = n == 0 ? tn : fmin(best, tn);
             }
         }
     }
-    if (want_norm && k == 0) {
-        red[threadIdx.x] = sq;
-        __syncthreads();
-        for (int s2 = UPD_THREADS / 2; s2 > 0; s2 >>= 1) {
-            if (threadIdx.x < s2) red[threadIdx.x] = add(red[threadIdx.x], red[threadIdx.x + s2]);
-            __syncthreads();
+    __syncthreads();   // R of every snapshot written (CTA-visible)
+    // 6. HB source + RK update, thread = cell, for every (variable, snapshot).
+    //    All of a variable's inputs are loaded before its first store (the
+    //    output may be W^0 itself, stage 4), so the loads overlap.
+    double sq = 0.0;
+    if (cell_live) {
+        const int64_t dti = b.dt_off + (int64_t)(cj - 1) * b.ni + (ci - 1);
+        double dtc;
+        if (first) {
+            a.dt[dti] = best;
+            dtc = best;
+        } else {
+            dtc = a.dt[dti];
         }
-        if (threadIdx.x == 0) a.norm_part[b.part_off + blockIdx.x] = red[0];
+        // V and alpha_s dt / V: one value on a fixed mesh, per snapshot on a
+        // moving one (recomputed per variable there: no register arrays)
+        const double V0 = a.vol[cc(b, 0, cj, ci)];
+        const double cdt0 = dv(mul(coef, dtc), V0);
+        for (int k = 0; k < NV; ++k) {
+            double wm[P], rn[P], qn[P];
+#pragma unroll
+            for (int m = 0; m < P; ++m) {
+                wm[m] = w[ws(b, m, k, cj, ci)];
+                rn[m] = a.r[rs(b, m, k, cj, ci)];
+                qn[m] = w0[ws(b, m, k, cj, ci)];
+            }
+#pragma unroll
+            for (int n = 0; n < P; ++n) {
+                const double V = a.Pg > 1 ? a.vol[cc(b, n, cj, ci)] : V0;
+                const double cdt = a.Pg > 1 ? dv(mul(coef, dtc), V) : cdt0;
+                double s = mul(S.dmat[n * P], wm[0]);
+#pragma unroll
+                for (int m = 1; m < P; ++m) s = add(s, mul(S.dmat[n * P + m], wm[m]));
+                const double R = add(rn[n], mul(V, s));
+                if (first && k == 0) sq = __fma_rn(R, R, sq);
+                const double v = sub(qn[n], mul(cdt, R));
+                w_out[ws(b, n, k, cj, ci)] = v;
+                if (!isfinite(v)) {
+                    const long long lin = (((long long)(n * NV + k) * b.nj + (cj - 1)) * b.ni) + (ci - 1);
+                    atomicMin(a.status + blockIdx.y, (unsigned long long)lin);
+                }
+            }
+        }
+    }
+    // the tile's residual rows are consumed: drop their L2 lines without a
+    // write-back (only whole 128-B lines inside this tile's row segments)
+    __syncthreads();
+    for (int t = threadIdx.x; t < P * NV * TJ; t += FLUX_THREADS) {
+        const int r = t % TJ, k = (t / TJ) % NV, n = t / (TJ * NV);
+        if (j0 + r > b.nj) continue;
+        const int len = min(TI, b.ni - i0 + 1) * 8;
+        const uintptr_t s0 = (uintptr_t)(a.r + rs(b, n, k, j0 + r, i0));
+        for (uintptr_t l = (s0 + 127) & ~(uintptr_t)127; l + 128 <= s0 + len; l += 128)
+            asm volatile("discard.global.L2 [%0], 128;" ::"l"(l) : "memory");
+    }
+    if (first) {
+        // stage-1 norm partial of the tile: fixed shuffle tree per warp, warps in order
+        for (int o = 16; o > 0; o >>= 1) sq = add(sq, __shfl_down_sync(0xffffffffu, sq, o));
+        if (lane == 0) red[warp] = sq;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int k = 0; k < NW; ++k) t = add(t, red[k]);
+            a.norm_part[b.part_off + tile] = t;
+        }
     }
 }
 
-// stage-1 norm: one warp per block folds that block's CTA partials in a fixed
-// lane-strided order and shuffle tree; one thread then folds blocks in order
-__global__ void ns_norm_kernel(hbns_args a, int iter, int ctas) {
+// stage-1 norm: one warp per block folds that block's tile partials in a
+// fixed lane-strided order and shuffle tree; one thread then folds blocks in
+// order
+__global__ void ns_norm_kernel(hbns_args a, int iter) {
     __shared__ double blk_sum[1024];
+    if (a.iter_dev) iter = *a.iter_dev;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int bk = warp; bk < a.nblocks; bk += nw) {
         const hbns_block &b = a.blocks[bk];
-        const int used = (int)(((int64_t)b.ni * b.nj + UPD_THREADS - 1) / UPD_THREADS);
+        const int used = ((b.ni + TI - 1) / TI) * ((b.nj + TJ - 1) / TJ);
         double s = 0.0;
-        for (int c = lane; c < used && c < ctas; c += 32) s = add(s, a.norm_part[b.part_off + c]);
+        for (int c = lane; c < used; c += 32) s = add(s, a.norm_part[b.part_off + c]);
         for (int o = 16; o > 0; o >>= 1) s = add(s, __shfl_down_sync(0xffffffffu, s, o));
-        if (lane == 0) blk_sum[bk] = s;
+        if (lane == 0) {
+            blk_sum[bk] = s;
+            if (a.blk_norms) a.blk_norms[(int64_t)iter * a.nglobal + b.gid] = s;
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -508,8 +545,10 @@ constexpr int FORCE_CHUNK = 1024;
 constexpr int MAX_WALL_SEGS = 4 * 256;
 
 __global__ void __launch_bounds__(FORCE_THREADS) ns_forces_kernel(hbns_args a, const double *w, int iter) {
+    if (a.iter_dev) iter = *a.iter_dev;
     __shared__ double px[FORCE_CHUNK], py[FORCE_CHUNK];
     __shared__ int seg_bs[MAX_WALL_SEGS], seg_end[MAX_WALL_SEGS];   // block * 4 + side, running end
+    __shared__ int seg_gpos[MAX_WALL_SEGS];                            // job-wide position of its first face
     __shared__ int nseg_s;
     const int n = blockIdx.x;
     const int g = a.Pg > 1 ? n : 0;
@@ -517,11 +556,15 @@ __global__ void __launch_bounds__(FORCE_THREADS) ns_forces_kernel(hbns_args a, c
         int ns = 0, end = 0;
         for (int bk = 0; bk < a.nblocks && ns < MAX_WALL_SEGS; ++bk) {
             const hbns_block &b = a.blocks[bk];
+            int gpos = b.wall_off;
             for (int side = 0; side < 4; ++side) {
                 if (b.kinds[side] != HBNS_NOSLIP && b.kinds[side] != HBNS_SLIP) continue;
-                end += side < 2 ? b.ni : b.nj;
+                const int len = side < 2 ? b.ni : b.nj;
+                end += len;
                 seg_bs[ns] = bk * 4 + side;
                 seg_end[ns] = end;
+                seg_gpos[ns] = gpos;
+                gpos += len;
                 ++ns;
             }
         }
@@ -545,9 +588,16 @@ __global__ void __launch_bounds__(FORCE_THREADS) ns_forces_kernel(hbns_args a, c
             else if (side == 2) { ci = 1; cj = e; sx = a.six[fi(b, g, e, 0)]; sy = a.siy[fi(b, g, e, 0)]; }
             else { ci = b.ni; cj = e; sx = a.six[fi(b, g, e, b.ni)]; sy = a.siy[fi(b, g, e, b.ni)]; }
             const Prim q = prim(w + ws(b, n, 0, cj, ci), (int64_t)(b.nj + 4) * (b.ni + 4));
+            if (a.wall_prod) {   // multi-rank: the products at their job-wide positions
+                const int64_t pos = seg_gpos[sg] + e - 1;
+                a.wall_prod[((int64_t)iter * a.P + n) * 2 * a.nwall + pos] = mul(q.p, sx);
+                a.wall_prod[(((int64_t)iter * a.P + n) * 2 + 1) * a.nwall + pos] = mul(q.p, sy);
+                continue;
+            }
             px[t - c0] = mul(q.p, sx);
             py[t - c0] = mul(q.p, sy);
         }
+        if (a.wall_prod) continue;
         __syncthreads();
         if (threadIdx.x == 0) {
             const int m = min(FORCE_CHUNK, total - c0);
@@ -563,6 +613,24 @@ __global__ void __launch_bounds__(FORCE_THREADS) ns_forces_kernel(hbns_args a, c
         a.forces[((int64_t)iter * a.P + n) * 2 + 1] = fy;
     }
 }
+
+// job-wide wall forces of a multi-rank run: one thread per (iteration,
+// snapshot), the specification's left-to-right folds over the summed products
+__global__ void ns_wall_fold_kernel(const double *prod, int iters, int P, int nwall, double *forces) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= iters * P) return;
+    const double *px = prod + (int64_t)t * 2 * nwall, *py = px + nwall;
+    double fx = 0.0, fy = 0.0;
+    for (int f = 0; f < nwall; ++f) {
+        fx = add(fx, px[f]);
+        fy = add(fy, py[f]);
+    }
+    forces[(int64_t)t * 2] = fx;
+    forces[(int64_t)t * 2 + 1] = fy;
+}
+
+// the device iteration counter (graph replays): advanced after the forces
+__global__ void ns_iter_advance_kernel(int32_t *iter) { *iter += 1; }
 
 int check(const char *what) { return hbgpu_check_launch(what); }
 
@@ -583,67 +651,75 @@ extern "C" int hbns_boundaries(const hbns_args *a, int32_t slot, void *stream) {
     return check("hbns_boundaries");
 }
 
-extern "C" int hbns_timestep(const hbns_args *a, int32_t slot, void *stream) {
-    ns_timestep_kernel<<<dim3((a->max_cells + 127) / 128, a->nblocks), 128, 0, (cudaStream_t)stream>>>(*a, a->w[slot]);
-    hbgpu_count_launch(1);
-    return check("hbns_timestep");
-}
-
-extern "C" int hbns_residual(const hbns_args *a, int32_t slot, void *stream) {
-    if (a == nullptr || slot < 0 || slot > 2 || a->max_ni < 1 || a->max_nj < 1) {
-        hbgpu_set_error("hbns_residual: bad arguments");
-        return HBGPU_ERR_ARG;
-    }
-    static bool ready[hbgpu::HB_MAX_DEVICES][2];
+template <bool VISC, int P>
+static int stage_launch(const hbns_args *a, int32_t slot_in, int32_t slot_out, double coef, int first,
+                        cudaStream_t s) {
+    static bool ready[hbgpu::HB_MAX_DEVICES];
     const int dev = hbgpu::current_device();
     if (dev < 0) return HBGPU_ERR_CUDA;
-    const bool visc = a->mu > 0.0;
     const size_t smem = sizeof(FluxSmem);
-    if (!ready[dev][visc]) {
-        cudaError_t e = visc ? cudaFuncSetAttribute(ns_flux_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                             : cudaFuncSetAttribute(ns_flux_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return check("hbns_residual (smem attribute)");
-        ready[dev][visc] = true;
+    if (!ready[dev]) {
+        if (cudaFuncSetAttribute(ns_stage_kernel<VISC, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+            return check("hbns_stage (smem attribute)");
+        ready[dev] = true;
     }
     const int64_t tiles = (int64_t)((a->max_ni + TI - 1) / TI) * ((a->max_nj + TJ - 1) / TJ);
-    if (tiles * a->P > INT32_MAX || a->nblocks > 65535) {
-        hbgpu_set_error("hbns_residual: grid too large");
-        return HBGPU_ERR_ARG;
-    }
-    const dim3 grid((unsigned)(tiles * a->P), a->nblocks);
-    cudaStream_t s = (cudaStream_t)stream;
-    if (visc) ns_flux_kernel<true><<<grid, FLUX_THREADS, smem, s>>>(*a, a->w[slot]);
-    else ns_flux_kernel<false><<<grid, FLUX_THREADS, smem, s>>>(*a, a->w[slot]);
-    hbgpu_count_launch(1);
-    return check("hbns_residual");
+    ns_stage_kernel<VISC, P><<<dim3((unsigned)tiles, a->nblocks), FLUX_THREADS, smem, s>>>(
+        *a, a->w[slot_in], a->w[0], a->w[slot_out], coef, first);
+    return HBGPU_OK;
 }
 
-extern "C" int hbns_update(const hbns_args *a, int32_t slot_in, int32_t slot_out, double coef, int32_t iter,
-                           int32_t want_norm, void *stream) {
-    cudaStream_t s = (cudaStream_t)stream;
-    const int ctas = (a->max_cells + UPD_THREADS - 1) / UPD_THREADS;
-    if (a->nblocks > 1024) {
-        hbgpu_set_error("hbns_update: at most 1024 blocks");
+template <bool VISC>
+static int stage_dispatch(const hbns_args *a, int32_t slot_in, int32_t slot_out, double coef, int first,
+                          cudaStream_t s) {
+    switch (a->P) {
+        case 1: return stage_launch<VISC, 1>(a, slot_in, slot_out, coef, first, s);
+        case 3: return stage_launch<VISC, 3>(a, slot_in, slot_out, coef, first, s);
+        case 5: return stage_launch<VISC, 5>(a, slot_in, slot_out, coef, first, s);
+        case 7: return stage_launch<VISC, 7>(a, slot_in, slot_out, coef, first, s);
+        case 9: return stage_launch<VISC, 9>(a, slot_in, slot_out, coef, first, s);
+        default: break;
+    }
+    hbgpu_set_error("hbns_stage: P = %d not templated (1..9 odd)", a->P);
+    return HBGPU_ERR_UNSUPPORTED;
+}
+
+extern "C" int hbns_stage(const hbns_args *a, int32_t slot_in, int32_t slot_out, double coef, int32_t iter,
+                          int32_t first, void *stream) {
+    if (a == nullptr || slot_in < 0 || slot_in > 2 || slot_out < 0 || slot_out > 2 || a->max_ni < 1 ||
+        a->max_nj < 1) {
+        hbgpu_set_error("hbns_stage: bad arguments");
         return HBGPU_ERR_ARG;
     }
-    const dim3 grid(ctas, a->nblocks, NV);
-    switch (a->P) {
-        case 1: ns_update_kernel<1><<<grid, UPD_THREADS, 0, s>>>(*a, a->w[slot_in], a->w[0], a->w[slot_out], coef, want_norm); break;
-        case 3: ns_update_kernel<3><<<grid, UPD_THREADS, 0, s>>>(*a, a->w[slot_in], a->w[0], a->w[slot_out], coef, want_norm); break;
-        case 5: ns_update_kernel<5><<<grid, UPD_THREADS, 0, s>>>(*a, a->w[slot_in], a->w[0], a->w[slot_out], coef, want_norm); break;
-        case 7: ns_update_kernel<7><<<grid, UPD_THREADS, 0, s>>>(*a, a->w[slot_in], a->w[0], a->w[slot_out], coef, want_norm); break;
-        case 9: ns_update_kernel<9><<<grid, UPD_THREADS, 0, s>>>(*a, a->w[slot_in], a->w[0], a->w[slot_out], coef, want_norm); break;
-        default:
-            hbgpu_set_error("hbns_update: P = %d not templated (1..9 odd)", a->P);
-            return HBGPU_ERR_UNSUPPORTED;
+    const int64_t tiles = (int64_t)((a->max_ni + TI - 1) / TI) * ((a->max_nj + TJ - 1) / TJ);
+    if (tiles > INT32_MAX || a->nblocks > 1024) {
+        hbgpu_set_error("hbns_stage: grid too large (%lld tiles, %d blocks)", (long long)tiles, a->nblocks);
+        return HBGPU_ERR_ARG;
     }
+    cudaStream_t s = (cudaStream_t)stream;
+    int rc = a->mu > 0.0 ? stage_dispatch<true>(a, slot_in, slot_out, coef, first != 0, s)
+                         : stage_dispatch<false>(a, slot_in, slot_out, coef, first != 0, s);
+    if (rc) return rc;
     int n = 1;
-    if (want_norm) {
-        ns_norm_kernel<<<1, 1024, 0, s>>>(*a, iter, ctas);
+    if (first) {
+        ns_norm_kernel<<<1, 1024, 0, s>>>(*a, iter);
         ++n;
     }
     hbgpu_count_launch(n);
-    return check("hbns_update");
+    return check("hbns_stage");
+}
+
+extern "C" int hbns_wall_fold(const double *wall_prod, int32_t iters, int32_t P, int32_t nwall, double *forces,
+                              void *stream) {
+    if (iters <= 0 || P <= 0) return HBGPU_OK;
+    if (wall_prod == nullptr || forces == nullptr || nwall < 0) {
+        hbgpu_set_error("hbns_wall_fold: bad arguments");
+        return HBGPU_ERR_ARG;
+    }
+    ns_wall_fold_kernel<<<(iters * P + 127) / 128, 128, 0, (cudaStream_t)stream>>>(wall_prod, iters, P, nwall, forces);
+    hbgpu_count_launch(1);
+    return check("hbns_wall_fold");
 }
 
 extern "C" int hbns_forces(const hbns_args *a, int32_t iter, void *stream) {
@@ -652,6 +728,10 @@ extern "C" int hbns_forces(const hbns_args *a, int32_t iter, void *stream) {
         return HBGPU_ERR_ARG;
     }
     ns_forces_kernel<<<a->P, FORCE_THREADS, 0, (cudaStream_t)stream>>>(*a, a->w[0], iter);
+    if (a->iter_dev) {
+        ns_iter_advance_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(a->iter_dev);
+        hbgpu_count_launch(1);
+    }
     hbgpu_count_launch(1);
     return check("hbns_forces");
 }

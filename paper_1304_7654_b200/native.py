@@ -145,10 +145,9 @@ SIGNATURES = {
     "hbgpu_comm_abort": (c_i32, [c_vp]),
     "hbgpu_norm_totals": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_vp]),
     "hbns_boundaries": (c_i32, [c_vp, c_i32, c_vp]),
-    "hbns_timestep": (c_i32, [c_vp, c_i32, c_vp]),
-    "hbns_residual": (c_i32, [c_vp, c_i32, c_vp]),
-    "hbns_update": (c_i32, [c_vp, c_i32, c_i32, c_f64, c_i32, c_i32, c_vp]),
+    "hbns_stage": (c_i32, [c_vp, c_i32, c_i32, c_f64, c_i32, c_i32, c_vp]),
     "hbns_forces": (c_i32, [c_vp, c_i32, c_vp]),
+    "hbns_wall_fold": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "hbgpu_abi_version": (c_i32, []),
     "hbgpu_last_error": (ctypes.c_char_p, []),
     "hbgpu_launch_count": (ctypes.c_uint64, []),

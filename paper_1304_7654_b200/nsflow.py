@@ -335,40 +335,118 @@ def spectral_matrix(case):
 # ---------------------------------------------------------------------------
 
 RK_ALPHAS = (0.25, 1.0 / 3.0, 0.5, 1.0)
-UPD_THREADS = 256
+TILE_I, TILE_J = 32, 8        # hbns_stage tiles (include/hbns.h HBNS_TILE_I/J)
+
+
+def ns_partition(case, nranks):
+    """Blocks -> ranks, the proxy path's greedy LPT rule (topology.
+    partition_blocks): blocks in descending cell count (ties: lower id) each
+    to the least-loaded rank (ties: lower rank).  Returns owner[block id]."""
+    import heapq
+    if not 1 <= nranks <= len(case.blocks):
+        raise ValueError(f"{nranks} ranks for {len(case.blocks)} blocks")
+    loads = [(0, r) for r in range(nranks)]
+    owner = {}
+    for b in sorted(case.blocks, key=lambda b: (-b.ni * b.nj, b.id)):
+        load, r = heapq.heappop(loads)
+        owner[b.id] = r
+        heapq.heappush(loads, (load + b.ni * b.nj, r))
+    return owner
+
+
+class HaloPlan:
+    """The cut-halo moves of one rank (hbgpu_halo directions, both halo
+    layers, both ways per cut), in one global order -- cuts as listed, layer
+    1 then 2, a <- b then b <- a -- which every rank enumerates alike:
+      local   both blocks on this rank: slot -> slot;
+      pack    source here, destination on peer q: slot -> send buffer;
+      unpack  source on peer q, destination here: receive buffer -> slot.
+    A peer's payload is its directions in that order, each element-major
+    (the 4P values of a face cell contiguous).  sends / recvs: (peer,
+    offset, count) in doubles, peers ascending."""
+
+    def __init__(self, case, offsets, owner=None, rank=0):
+        from . import native
+        P = case.planes
+        nv = 4 * P
+        blocks = {b.id: b for b in case.blocks}
+        owner = owner or {b.id: 0 for b in case.blocks}
+
+        def cell(b, face, k, e, halo):
+            ni, nj = b.ni, b.nj
+            if face == "south":
+                return (e, 1 - k) if halo else (e, k)
+            if face == "north":
+                return (e, nj + k) if halo else (e, nj + 1 - k)
+            if face == "west":
+                return (1 - k, e) if halo else (k, e)
+            return (ni + k, e) if halo else (ni + 1 - k, e)
+
+        def off(b, i, j):
+            return offsets[b.id] + (j + 1) * (b.ni + 4) + (i + 1)
+
+        local, pack, unpack = [], {}, {}
+        for c in case.cuts:
+            A, B = blocks[c.a], blocks[c.b]
+            n = c.hi - c.lo + 1
+            for k in (1, 2):
+                for dst, dface, src, sface in ((A, c.face_a, B, c.face_b), (B, c.face_b, A, c.face_a)):
+                    ps, pd = owner[src.id], owner[dst.id]
+                    if rank not in (ps, pd):
+                        continue
+                    si, sj = cell(src, sface, k, c.lo, False)
+                    di, dj = cell(dst, dface, k, c.lo, True)
+                    ses = 1 if sface in ("south", "north") else src.ni + 4
+                    des = 1 if dface in ("south", "north") else dst.ni + 4
+                    svs = (src.nj + 4) * (src.ni + 4)
+                    dvs = (dst.nj + 4) * (dst.ni + 4)
+                    if ps == rank and pd == rank:
+                        local.append((off(src, si, sj), ses, svs, off(dst, di, dj), des, dvs, n, 0, 0, 0))
+                    elif ps == rank:
+                        pack.setdefault(pd, []).append((off(src, si, sj), ses, svs, n))
+                    else:
+                        unpack.setdefault(ps, []).append((off(dst, di, dj), des, dvs, n))
+        rows_pack, rows_unpack, self.sends, self.recvs = [], [], [], []
+        o = 0
+        for q in sorted(pack):
+            start = o
+            for so, ses, svs, n in pack[q]:
+                rows_pack.append((so, ses, svs, o, nv, 1, n, 0, 1, 0))   # dst_kind 1: send buffer
+                o += n * nv
+            self.sends.append((q, start, o - start))
+        self.nsend = o
+        o = 0
+        for q in sorted(unpack):
+            start = o
+            for do, des, dvs, n in unpack[q]:
+                rows_unpack.append((o, nv, 1, do, des, dvs, n, 2, 0, 0))  # src_kind 2: receive buffer
+                o += n * nv
+            self.recvs.append((q, start, o - start))
+        self.nrecv = o
+        dt = native.HALO_DIR_DTYPE
+        # the first exchange launch: local copies and packs (one hbgpu_halo)
+        self.first = np.array(local + rows_pack, dtype=dt) if local or rows_pack else np.zeros(0, dt)
+        self.unpack = np.array(rows_unpack, dtype=dt) if rows_unpack else np.zeros(0, dt)
+        self.nlocal = len(local)
 
 
 def _halo_rows(case, offsets):
-    """hbgpu_halo directions of every cut, both ways, both halo layers."""
-    from . import native
-    rows = []
-    blocks = {b.id: b for b in case.blocks}
+    """hbgpu_halo directions of every cut, both ways, both halo layers (one
+    rank holding every block)."""
+    return HaloPlan(case, offsets).first
 
-    def cell(b, face, k, e, halo):
-        ni, nj = b.ni, b.nj
-        if face == "south":
-            return (e, 1 - k) if halo else (e, k)
-        if face == "north":
-            return (e, nj + k) if halo else (e, nj + 1 - k)
-        if face == "west":
-            return (1 - k, e) if halo else (k, e)
-        return (ni + k, e) if halo else (ni + 1 - k, e)
 
-    def off(b, i, j):
-        return offsets[b.id] + (j + 1) * (b.ni + 4) + (i + 1)
-
-    for c in case.cuts:
-        A, B = blocks[c.a], blocks[c.b]
-        for k in (1, 2):
-            for dst, dface, src, sface in ((A, c.face_a, B, c.face_b), (B, c.face_b, A, c.face_a)):
-                si, sj = cell(src, sface, k, c.lo, False)
-                di, dj = cell(dst, dface, k, c.lo, True)
-                ses = 1 if sface in ("south", "north") else src.ni + 4
-                des = 1 if dface in ("south", "north") else dst.ni + 4
-                rows.append((off(src, si, sj), ses, (src.nj + 4) * (src.ni + 4),
-                             off(dst, di, dj), des, (dst.nj + 4) * (dst.ni + 4),
-                             c.hi - c.lo + 1, 0, 0, 0))
-    return np.array(rows, dtype=native.HALO_DIR_DTYPE) if rows else np.zeros(0, native.HALO_DIR_DTYPE)
+def wall_layout(case):
+    """Global wall-face order of the force folds (blocks ascending, sides
+    south / north / west / east, face cells ascending): per block the
+    position of its first wall face, and the total."""
+    off, n = {}, 0
+    for b in sorted(case.blocks, key=lambda b: b.id):
+        off[b.id] = n
+        for side in range(4):
+            if b.kinds[side] in (NOSLIP, SLIP):
+                n += b.ni if side < 2 else b.nj
+    return off, n
 
 
 def _ns_types():
@@ -378,24 +456,33 @@ def _ns_types():
 
     class Block(ctypes.Structure):
         _fields_ = [("w_off", i64), ("r_off", i64), ("dt_off", i64), ("c_off", i64), ("fi_off", i64),
-                    ("fj_off", i64), ("part_off", i64), ("ni", i32), ("nj", i32), ("kinds", i32 * 4)]
+                    ("fj_off", i64), ("part_off", i64), ("ni", i32), ("nj", i32), ("kinds", i32 * 4),
+                    ("gid", i32), ("wall_off", i32)]
 
     class Args(ctypes.Structure):
         _fields_ = [("w", vp * 3), ("r", vp), ("dt", vp), ("xc", vp), ("yc", vp), ("vol", vp),
                     ("six", vp), ("siy", vp), ("gi", vp), ("sjx", vp), ("sjy", vp), ("gj", vp),
                     ("blocks", vp), ("winf", vp), ("dmat", vp), ("status", vp), ("norm_part", vp),
-                    ("norms", vp), ("forces", vp), ("mu", f64), ("cfl", f64), ("omega_nh", f64), ("kq", f64),
+                    ("norms", vp), ("forces", vp), ("blk_norms", vp), ("wall_prod", vp), ("iter_dev", vp), ("mu", f64), ("cfl", f64), ("omega_nh", f64), ("kq", f64),
                     ("nblocks", i32), ("P", i32), ("Pg", i32), ("moving", i32), ("max_len", i32),
-                    ("max_cells", i32), ("max_ni", i32), ("max_nj", i32)]
+                    ("max_cells", i32), ("max_ni", i32), ("max_nj", i32), ("nglobal", i32), ("nwall", i32)]
     return Block, Args
 
 
 class NSRun:
-    """The HB Euler / NS loop of one case on one GPU: every block resident in
-    three state pools, the RK stages launched on torch's current stream
-    (hb_ns.cu), cut halos by hbgpu_halo."""
+    """The HB Euler / NS loop of one rank's blocks on one GPU: the blocks
+    resident in three state pools, the RK stages launched on torch's current
+    stream (hb_ns.cu), cut halos by hbgpu_halo.
 
-    def __init__(self, case, max_iters, initial=None, device=None):
+    owner (block id -> rank, ns_partition) and rank select this rank's
+    blocks; with several ranks, each stage's cut halos are an exchange --
+    exchange_begin (local copies + packs), the transport moving `sends` /
+    `recvs` between the ranks' send and receive buffers, exchange_end
+    (unpacks) -- and the residual norms and wall forces are kept as per-block
+    sums and per-face products in global order (blk_norms, wall_prod), to be
+    summed over the ranks and folded like one rank's (run_ns_ranks)."""
+
+    def __init__(self, case, max_iters, initial=None, device=None, owner=None, rank=0):
         import ctypes
         import torch
         from . import native
@@ -403,15 +490,23 @@ class NSRun:
         self.torch, self._ct = torch, ctypes
         self.case = case
         self.max_iters = max_iters
+        self.rank = rank
+        owner = owner or {b.id: 0 for b in case.blocks}
+        self.multi = len(set(owner.values())) > 1
         dev = self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         P = case.planes
-        blocks = self.blocks = sorted(case.blocks, key=lambda b: b.id)
+        all_blocks = sorted(case.blocks, key=lambda b: b.id)
+        gid = {b.id: k for k, b in enumerate(all_blocks)}
+        wall_off, nwall = wall_layout(case)
+        blocks = self.blocks = [b for b in all_blocks if owner[b.id] == rank]
+        if not blocks:
+            raise ValueError(f"rank {rank} owns no block")
         geos = [metrics(b) for b in blocks]
         Pg = geos[0]["xc"].shape[0]
         moving = "gi" in geos[0]
         Block, Args = _ns_types()
         max_cells = max(b.ni * b.nj for b in blocks)
-        ctas = -(-max_cells // UPD_THREADS)
+        ctas = max(-(-b.ni // TILE_I) * -(-b.nj // TILE_J) for b in blocks)   # tiles per block
         table = (Block * len(blocks))()
         self.w_off = {}
         wsz = r_off = dt_off = c_off = fi_off = fj_off = 0
@@ -422,8 +517,9 @@ class NSRun:
             e.c_off, e.fi_off, e.fj_off = c_off, fi_off, fj_off
             e.part_off = k * ctas
             e.ni, e.nj = b.ni, b.nj
-            for s in range(4):
-                e.kinds[s] = b.kinds[s]
+            for sd in range(4):
+                e.kinds[sd] = b.kinds[sd]
+            e.gid, e.wall_off = gid[b.id], wall_off[b.id]
             self.w_off[b.id] = wsz
             wsz += P * 4 * (b.nj + 4) * (b.ni + 4)
             r_off += P * 4 * b.nj * b.ni
@@ -450,10 +546,19 @@ class NSRun:
         self.norm_part = torch.zeros(len(blocks) * ctas, dtype=f64, device=dev)
         self.norms = torch.zeros(max(1, max_iters), dtype=f64, device=dev)
         self.forces = torch.zeros(max(1, max_iters) * P * 2, dtype=f64, device=dev)
-        halo = _halo_rows(case, self.w_off)
-        self.nhalo = len(halo)
-        self.halo_len = int(halo["length"].max()) if len(halo) else 0
-        self.t_halo = torch.from_numpy(halo.view(np.uint8).copy()).to(dev) if len(halo) else None
+        self.nglobal, self.nwall = len(all_blocks), nwall
+        if self.multi:
+            self.blk_norms = torch.zeros(max(1, max_iters) * len(all_blocks), dtype=f64, device=dev)
+            self.wall_prod = torch.zeros(max(1, max_iters * P * 2 * nwall), dtype=f64, device=dev)
+        plan = self.plan = HaloPlan(case, self.w_off, owner, rank)
+        self.t_first = torch.from_numpy(plan.first.view(np.uint8).copy()).to(dev) if len(plan.first) else None
+        self.t_unpack = torch.from_numpy(plan.unpack.view(np.uint8).copy()).to(dev) if len(plan.unpack) else None
+        self.first_len = int(plan.first["length"].max()) if len(plan.first) else 0
+        self.unpack_len = int(plan.unpack["length"].max()) if len(plan.unpack) else 0
+        self.iter_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.graph = None
+        self.sendbuf = torch.zeros(max(1, plan.nsend), dtype=f64, device=dev)
+        self.recvbuf = torch.zeros(max(1, plan.nrecv), dtype=f64, device=dev)
         a = Args()
         for k in range(3):
             a.w[k] = self.slots[k].data_ptr()
@@ -463,12 +568,17 @@ class NSRun:
         a.blocks, a.winf, a.dmat = self.t_blocks.data_ptr(), self.winf.data_ptr(), self.dmat.data_ptr()
         a.status, a.norm_part = self.status.data_ptr(), self.norm_part.data_ptr()
         a.norms, a.forces = self.norms.data_ptr(), self.forces.data_ptr()
+        if self.multi:
+            a.blk_norms, a.wall_prod = self.blk_norms.data_ptr(), self.wall_prod.data_ptr()
+        else:
+            a.iter_dev = self.iter_dev.data_ptr()
         a.mu, a.cfl, a.omega_nh = case.mu, case.cfl, case.omega * case.nharms
         a.kq = (case.mu * GAMMA) / PR    # the specification's (mu gamma) / Pr, one IEEE mul and div
         a.nblocks, a.P, a.Pg, a.moving = len(blocks), P, Pg, int(moving)
         a.max_len = max(max(b.ni, b.nj) for b in blocks)
         a.max_cells = max_cells
         a.max_ni, a.max_nj = max(b.ni for b in blocks), max(b.nj for b in blocks)
+        a.nglobal, a.nwall = len(all_blocks), nwall
         self.args = a
         self.done = 0
 
@@ -481,25 +591,69 @@ class NSRun:
     def _stream(self):
         return self._ct.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
 
-    def iterate(self, iterations):
+    def _vp(self, t):
+        return self._ct.c_void_p(t.data_ptr())
+
+    def exchange_begin(self, slot):
+        """Cut halos of `slot`: local copies, and the packs of the payloads
+        this rank sends."""
         from . import native
+        if self.t_first is not None:
+            native.check(self.lib.hbgpu_halo(self._vp(self.slots[slot]), self._vp(self.sendbuf), None,
+                                             self._vp(self.t_first), len(self.plan.first), self.first_len,
+                                             self.case.planes, self._stream()), "hbgpu_halo (ns cuts)")
+
+    def exchange_end(self, slot):
+        """Unpack the received payloads into `slot`'s halos."""
+        from . import native
+        if self.t_unpack is not None:
+            native.check(self.lib.hbgpu_halo(self._vp(self.slots[slot]), None, self._vp(self.recvbuf),
+                                             self._vp(self.t_unpack), len(self.plan.unpack), self.unpack_len,
+                                             self.case.planes, self._stream()), "hbgpu_halo (ns unpack)")
+
+    def stage(self, st):
+        """Boundary halos of stage st's input, then the fused stage kernel."""
+        from . import native
+        si, so = STAGE_SLOTS[st]
+        ap, s = self._ct.byref(self.args), self._stream()
+        native.check(self.lib.hbns_boundaries(ap, si, s), "hbns_boundaries")
+        native.check(self.lib.hbns_stage(ap, si, so, RK_ALPHAS[st], self.done, int(st == 0), s), "hbns_stage")
+
+    def finish_iteration(self):
+        from . import native
+        native.check(self.lib.hbns_forces(self._ct.byref(self.args), self.done, self._stream()), "hbns_forces")
+        self.done += 1
+
+    def _one_iteration(self):
+        for st in range(4):
+            self.exchange_begin(STAGE_SLOTS[st][0])
+            self.stage(st)
+        self.finish_iteration()
+
+    def iterate(self, iterations, use_graph=True):
+        """`iterations` iterations of a run whose blocks are all on this rank.
+        use_graph: the first iteration runs eagerly and is then captured once
+        as a CUDA graph (its ~20 launches; the iteration index lives in a
+        device counter), which every later iteration replays."""
+        if self.multi:
+            raise ValueError("a multi-rank NSRun iterates through run_ns_ranks / run_ns_distributed")
         if self.done + iterations > self.max_iters:
             raise ValueError(f"{iterations} more iterations exceed max_iters={self.max_iters}")
-        L, a, s, ct = self.lib, self.args, self._stream(), self._ct
-        ap = ct.byref(a)
+        torch = self.torch
         for _ in range(iterations):
-            it = self.done
-            for st, (si, so) in enumerate(((0, 1), (1, 2), (2, 1), (1, 0))):
-                if self.nhalo:
-                    native.check(L.hbgpu_halo(ct.c_void_p(self.slots[si].data_ptr()), None, None,
-                                              ct.c_void_p(self.t_halo.data_ptr()), self.nhalo, self.halo_len,
-                                              self.case.planes, s), "hbgpu_halo (ns cuts)")
-                native.check(L.hbns_boundaries(ap, si, s), "hbns_boundaries")
-                if st == 0:
-                    native.check(L.hbns_timestep(ap, 0, s), "hbns_timestep")
-                native.check(L.hbns_residual(ap, si, s), "hbns_residual")
-                native.check(L.hbns_update(ap, si, so, RK_ALPHAS[st], it, int(st == 0), s), "hbns_update")
-            native.check(L.hbns_forces(ap, it, s), "hbns_forces")
+            if not use_graph or (self.graph is None and self.done == 0):
+                self._one_iteration()
+                continue
+            if self.graph is None:
+                side = torch.cuda.Stream(self.device)
+                side.wait_stream(torch.cuda.current_stream(self.device))
+                self.graph = torch.cuda.CUDAGraph()
+                with torch.cuda.stream(side), torch.cuda.graph(self.graph, stream=side):
+                    done = self.done
+                    self._one_iteration()
+                    self.done = done   # capture launches nothing
+                torch.cuda.current_stream(self.device).wait_stream(side)
+            self.graph.replay()
             self.done += 1
         return self
 
@@ -522,13 +676,171 @@ class NSRun:
 
     def force_history(self):
         """(iterations, P, 2) (cl, cd) in the snapshot's freestream axes."""
-        P = self.case.planes
-        fxy = self.forces[:self.done * P * 2].view(self.done, P, 2).cpu().numpy()
-        ang = np.radians(self.case.dalpha_deg) * np.sin(2 * np.pi * np.arange(P) / P)
-        ca, sa = np.cos(ang), np.sin(ang)
-        cd = fxy[:, :, 0] * ca + fxy[:, :, 1] * sa
-        cl = fxy[:, :, 1] * ca - fxy[:, :, 0] * sa
-        return np.stack([cl, cd], axis=2)
+        return _lift_drag(self.case, self.forces[:self.done * self.case.planes * 2].cpu().numpy(), self.done)
+
+
+# stage s reads slot STAGE_SLOTS[s][0], writes STAGE_SLOTS[s][1] (0 = W^0)
+STAGE_SLOTS = ((0, 1), (1, 2), (2, 1), (1, 0))
+
+
+def _lift_drag(case, fxy, iterations):
+    P = case.planes
+    fxy = np.asarray(fxy).reshape(iterations, P, 2)
+    ang = np.radians(case.dalpha_deg) * np.sin(2 * np.pi * np.arange(P) / P)
+    ca, sa = np.cos(ang), np.sin(ang)
+    cd = fxy[:, :, 0] * ca + fxy[:, :, 1] * sa
+    cl = fxy[:, :, 1] * ca - fxy[:, :, 0] * sa
+    return np.stack([cl, cd], axis=2)
+
+
+class NSRanksResult:
+    """A multi-rank run's results, the job-wide view: fields of every block,
+    the residual norms and wall forces folded exactly as one rank's, the
+    first divergence in block order."""
+
+    def __init__(self, case, runs, norms, forces, iterations):
+        self.case, self.runs, self._norms, self._forces, self.done = case, runs, norms, forces, iterations
+
+    def fields(self):
+        out = {}
+        for r in self.runs:
+            out.update(r.fields())
+        return out
+
+    def norm_history(self):
+        return self._norms.cpu().tolist()
+
+    def force_history(self):
+        return _lift_drag(self.case, self._forces.cpu().numpy(), self.done)
+
+    def divergence(self):
+        hits = [d for d in (r.divergence() for r in self.runs) if d is not None]
+        return min(hits) if hits else None
+
+
+def _fold_job(case, lib, blk_norms, wall_prod, iterations, stream, ctypes_mod):
+    """Job-wide norms (hbgpu_norm_totals over global block ids) and wall
+    forces (hbns_wall_fold over the global wall-face order) from the summed
+    per-block sums and per-face products."""
+    import torch
+    from . import native
+    P = case.planes
+    nb = len(case.blocks)
+    norms = torch.zeros(max(1, iterations), dtype=torch.float64, device=blk_norms.device)
+    forces = torch.zeros(max(1, iterations * P * 2), dtype=torch.float64, device=blk_norms.device)
+    vp = ctypes_mod.c_void_p
+    if iterations:
+        native.check(lib.hbgpu_norm_totals(vp(blk_norms.data_ptr()), iterations, nb, vp(norms.data_ptr()), stream),
+                     "hbgpu_norm_totals")
+        native.check(lib.hbns_wall_fold(vp(wall_prod.data_ptr()), iterations, P, wall_layout(case)[1],
+                                        vp(forces.data_ptr()), stream), "hbns_wall_fold")
+    return norms[:iterations], forces[:iterations * P * 2]
+
+
+def run_ns_ranks(case, iterations=None, nranks=2, initial=None):
+    """The case split over `nranks` ranks (ns_partition) run as engines of one
+    process on one GPU, their cut-halo payloads moved by device copies
+    (loopback transport) -- the exchange a multi-GPU run does over NCCL
+    (run_ns_distributed), step for step.  Returns an NSRanksResult."""
+    import ctypes
+    import torch
+    from .exceptions import DivergenceError
+    iterations = case.iterations if iterations is None else iterations
+    owner = ns_partition(case, nranks)
+    runs = [NSRun(case, max(1, iterations), initial, owner=owner, rank=r) for r in range(nranks)]
+    if nranks == 1:
+        runs[0].iterate(iterations)
+        torch.cuda.synchronize()
+        res = NSRanksResult(case, runs, runs[0].norms[:iterations], runs[0].forces[:iterations * case.planes * 2],
+                            iterations)
+    else:
+        send_at = [{q: (o, c) for q, o, c in r.plan.sends} for r in runs]
+        for _ in range(iterations):
+            for st in range(4):
+                si = STAGE_SLOTS[st][0]
+                for r in runs:
+                    r.exchange_begin(si)
+                for r in runs:   # the transport: peer send-buffer segments -> receive buffer
+                    for q, off, cnt in r.plan.recvs:
+                        so, sc = send_at[q][r.rank]
+                        if sc != cnt:
+                            raise RuntimeError(f"rank {q} -> {r.rank}: {sc} != {cnt} doubles")
+                        r.recvbuf[off:off + cnt].copy_(runs[q].sendbuf[so:so + sc])
+                for r in runs:
+                    r.exchange_end(si)
+                    r.stage(st)
+            for r in runs:
+                r.finish_iteration()
+        blk = sum(r.blk_norms for r in runs)       # one nonzero contributor per entry: exact
+        prod = sum(r.wall_prod for r in runs)
+        norms, forces = _fold_job(case, runs[0].lib, blk, prod, iterations, runs[0]._stream(), ctypes)
+        torch.cuda.synchronize()
+        res = NSRanksResult(case, runs, norms, forces, iterations)
+    d = res.divergence()
+    if d is not None:
+        raise DivergenceError(*d)
+    return res
+
+
+def run_ns_distributed(case, iterations=None, initial=None):
+    """One rank of a multi-GPU run under torchrun (one process per GPU,
+    torch.distributed initialised): this rank's blocks (ns_partition), the
+    cut-halo payloads of every stage over NCCL (grouped ncclSend/ncclRecv per
+    peer, hbgpu_comm_exchange), then the per-block norm sums and per-face
+    force products summed over the ranks (ncclAllReduce; exact, one
+    contributor per entry) and folded as one rank's.  Every rank returns the
+    job-wide norms and forces and its own blocks' fields."""
+    import ctypes
+    import torch
+    import torch.distributed as dist
+    from . import native
+    from .blockops import HaloContext
+    from .exceptions import DivergenceError
+    from .solver import make_comm
+    iterations = case.iterations if iterations is None else iterations
+    rank, world = dist.get_rank(), dist.get_world_size()
+    dev = torch.cuda.current_device()
+    if world == 1:
+        return run_ns_ranks(case, iterations, 1, initial)
+    owner = ns_partition(case, world)
+    run = NSRun(case, max(1, iterations), initial, owner=owner, rank=rank)
+    comm = make_comm(rank, world, dev)
+    try:
+        ctx = HaloContext(rank, comm=comm)
+        for _ in range(iterations):
+            for st in range(4):
+                si = STAGE_SLOTS[st][0]
+                run.exchange_begin(si)
+                ctx.transfer(run.sendbuf, run.plan.sends, run.recvbuf, run.plan.recvs)
+                run.exchange_end(si)
+                run.stage(st)
+            run.finish_iteration()
+        s = run._stream()
+        for t in (run.blk_norms, run.wall_prod):
+            native.check(run.lib.hbgpu_comm_allreduce(comm, ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(t.data_ptr()),
+                                                      t.numel(), native.REDUCE_SUM_F64, s), "hbgpu_comm_allreduce")
+        keys = torch.full((len(case.blocks),), -1, dtype=torch.int64, device=run.device)
+        keys[torch.tensor(_gids(case, run.blocks), device=run.device)] = run.status
+        native.check(run.lib.hbgpu_comm_allreduce(comm, ctypes.c_void_p(keys.data_ptr()),
+                                                  ctypes.c_void_p(keys.data_ptr()), keys.numel(),
+                                                  native.REDUCE_MIN_U64, s), "hbgpu_comm_allreduce")
+        norms, forces = _fold_job(case, run.lib, run.blk_norms, run.wall_prod, iterations, s, ctypes)
+        torch.cuda.synchronize()
+    finally:
+        native.load().hbgpu_comm_destroy(comm)
+    res = NSRanksResult(case, [run], norms, forces, iterations)
+    ordered = sorted(case.blocks, key=lambda b: b.id)
+    for gidx, key in enumerate(keys.cpu().numpy().view(np.uint64)):
+        if int(key) != (1 << 64) - 1:
+            b, lin = ordered[gidx], int(key)
+            nk = lin // (b.ni * b.nj)
+            raise DivergenceError(b.id, lin % b.ni + 1, (lin // b.ni) % b.nj + 1, nk % 4, nk // 4)
+    return res
+
+
+def _gids(case, blocks):
+    order = {b.id: k for k, b in enumerate(sorted(case.blocks, key=lambda b: b.id))}
+    return [order[b.id] for b in blocks]
 
 
 def run_ns(case, iterations=None, initial=None):

@@ -4,8 +4,9 @@ GPU, BASELINE configs at full size.
 One unit = one interior cell x one HB snapshot x one RK stage (4 conservative
 variables), as for the proxy path; value = units / CUDA-event time of K
 iterations after W warm-up ones (L2 flushed implicitly: every config but C0
-exceeds L2).  The NS kernels (hb_ns.cu) are plain thread-per-(cell, snapshot)
-kernels: a correct, measured first version, not yet tiled.
+exceeds L2).  One iteration = per stage the boundary and cut halos and one
+hbns_stage launch (the fused tile kernel of hb_ns.cu), plus the stage-1 norm
+fold and the wall forces.
 
     python profiles/ns_bench.py --configs C0,C1,C2,C3,C4 --steps 5 --warmup 2
 """
@@ -25,6 +26,7 @@ def main():
     ap.add_argument("--configs", default="C0,C1,C2,C3,C4")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--out", default=None, help="also write the rows as a JSON list")
     args = ap.parse_args()
     rows = []
     for key in args.configs.split(","):
@@ -49,6 +51,9 @@ def main():
         rows.append(row)
         del run
         torch.cuda.empty_cache()
+    if args.out:
+        with open(args.out, "w") as fh:
+            json.dump(rows, fh, indent=1)
 
 
 if __name__ == "__main__":
