@@ -537,7 +537,7 @@ def run_ours(args, wl):
                            "schedule": "paired RK stages (band + pair kernels)" if fused
                                        else ("one-launch small schedule (hb_small.cu)" if small
                                              else "single RK stages"),
-                           "l2": f"inputs larger than L2: {dr_slot_gb(case, mine):.1f} GB per state slot"},
+                           "l2": l2_note(dr_slot_gb(case, mine))},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
                 "gpu_launches": int(launches),
                 "env": {"hbgpu_knobs": knobs, "library": native.LIB_PATH,
@@ -547,6 +547,16 @@ def run_ours(args, wl):
     if world > 1:
         dist.destroy_process_group()
     np.random.seed(0)
+
+
+def l2_note(slot_gb):
+    """The timing rule's L2 statement: C3/C4 stream slots far larger than the
+    126 MB L2; the small configs' three slots fit in it, and are not flushed
+    between iterations (a solver's own iterations reuse them the same way)."""
+    if 3 * slot_gb * 1e3 > 126:
+        return f"inputs larger than L2: {slot_gb:.2f} GB per state slot (3 slots)"
+    return (f"inputs fit in L2 ({slot_gb * 1e3:.0f} MB per state slot, 3 slots); not flushed between "
+            "iterations: the workload's own iteration-to-iteration reuse")
 
 
 def dr_slot_gb(case, blocks):
