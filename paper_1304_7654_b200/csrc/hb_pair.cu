@@ -170,10 +170,10 @@ static_assert(CW == 8, "two consumer warpgroups + one helper warpgroup");
 // items per lane and needs more registers.  Budget: 256 * (consumer - 168)
 // <= 128 * (168 - helper) + (65536 - 384 * 168).
 #ifndef HBGPU_PAIR_HELPER_REGS   // measurement builds may move the split
-#define HBGPU_PAIR_HELPER_REGS 64
+#define HBGPU_PAIR_HELPER_REGS 72
 #endif
 #ifndef HBGPU_PAIR_CONSUMER_REGS
-#define HBGPU_PAIR_CONSUMER_REGS 216
+#define HBGPU_PAIR_CONSUMER_REGS 208
 #endif
 template <int PT> struct PairRegs {
     static constexpr int HELPER = PT == 1 ? HBGPU_PAIR_HELPER_REGS : 80;

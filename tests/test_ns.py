@@ -89,3 +89,34 @@ def test_gpu_full_size_c2_converges(cuda):
     assert np.isfinite(norms).all() and norms[-1] < 0.5 * norms[0]
     q = got.fields()[0][:, 0, 2:-2, 2:-2]
     assert q.min() > 0.5 and q.max() < 2.0
+
+
+def _ragged_case():
+    """Two 40 x 13 blocks side by side (viscous, a no-slip wall below, one
+    cut): neither dimension a multiple of the stage kernel's 32 x 8 tiles, so
+    both tile directions end in partial tiles and the residual scratch rows
+    are not whole L2 lines."""
+    ni, nj = 40, 13
+    blocks = []
+    for c in range(2):
+        x, y = nsflow.tanh_mesh(ni, nj, c * 1.0, 0.0, 1.0, 0.4)
+        kinds = [nsflow.NOSLIP, nsflow.FARFIELD, nsflow.FARFIELD, nsflow.FARFIELD]
+        kinds[3 if c == 0 else 2] = nsflow.CUT
+        blocks.append(nsflow.NSBlock(c, ni, nj, x, y, tuple(kinds)))
+    cuts = [nsflow.NSCut(0, "east", 1, "west", 1, nj)]
+    return nsflow.NSCase("ragged-ns", 1, 0.3, 1.0, 1e3, 1.0, blocks, cuts, iterations=5)
+
+
+@pytest.mark.gpu
+def test_gpu_ragged_tiles_match_oracle(cuda):
+    case = _ragged_case()
+    want = ns_oracle.run(case, 5)
+    got = nsflow.run_ns(case, 5)
+    for b, q in want.fields().items():
+        assert np.array_equal(got.fields()[b], q), f"block {b}"
+    np.testing.assert_allclose(got.norm_history(), want.norms, rtol=1e-12, atol=0)
+    assert np.array_equal(got.force_history(), np.stack(want.forces))
+    split = nsflow.run_ns_ranks(case, 5, 2)
+    for b, q in want.fields().items():
+        assert np.array_equal(split.fields()[b], q), f"block {b} (2 ranks)"
+    assert np.array_equal(split.force_history(), got.force_history())
