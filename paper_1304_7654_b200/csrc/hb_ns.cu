@@ -279,6 +279,9 @@ __device__ __forceinline__ void stage_row(double *sdst, const double *grow, int 
 // <= 96).  Measured on the fused stage kernel: Euler 3 (C4 201 vs 210 ms per
 // iteration with 2), viscous 2 (C3 13.9 vs 14.9, C1 0.44 vs 0.50 ms).
 // HBNS_FLUX_MINB overrides both in measurement builds.
+#ifndef HBNS_DISCARD   // measurement builds may keep the residual scratch's write-backs
+#define HBNS_DISCARD 1
+#endif
 #ifdef HBNS_FLUX_MINB
 #define HBNS_MINB(VISC) HBNS_FLUX_MINB
 #else
@@ -459,25 +462,32 @@ __global__ void __launch_bounds__(FLUX_THREADS, HBNS_MINB(VISC))
         // moving one (recomputed per variable there: no register arrays)
         const double V0 = a.vol[cc(b, 0, cj, ci)];
         const double cdt0 = dv(mul(coef, dtc), V0);
+        const bool per_n = a.Pg > 1;
+        const int64_t wstride = (int64_t)NV * (b.nj + 4) * (b.ni + 4);   // snapshot stride, state pools
+        const int64_t rstride = (int64_t)NV * b.nj * b.ni;               // snapshot stride, residual pool
         for (int k = 0; k < NV; ++k) {
+            const int64_t wo = ws(b, 0, k, cj, ci), ro = rs(b, 0, k, cj, ci);
             double wm[P], rn[P], qn[P];
 #pragma unroll
             for (int m = 0; m < P; ++m) {
-                wm[m] = w[ws(b, m, k, cj, ci)];
-                rn[m] = a.r[rs(b, m, k, cj, ci)];
-                qn[m] = w0[ws(b, m, k, cj, ci)];
+                wm[m] = w[wo + m * wstride];
+                rn[m] = a.r[ro + m * rstride];
+                qn[m] = w0[wo + m * wstride];
             }
 #pragma unroll
             for (int n = 0; n < P; ++n) {
-                const double V = a.Pg > 1 ? a.vol[cc(b, n, cj, ci)] : V0;
-                const double cdt = a.Pg > 1 ? dv(mul(coef, dtc), V) : cdt0;
+                double V = V0, cdt = cdt0;
+                if (per_n) {
+                    V = a.vol[cc(b, n, cj, ci)];
+                    cdt = dv(mul(coef, dtc), V);
+                }
                 double s = mul(S.dmat[n * P], wm[0]);
 #pragma unroll
                 for (int m = 1; m < P; ++m) s = add(s, mul(S.dmat[n * P + m], wm[m]));
                 const double R = add(rn[n], mul(V, s));
                 if (first && k == 0) sq = __fma_rn(R, R, sq);
                 const double v = sub(qn[n], mul(cdt, R));
-                w_out[ws(b, n, k, cj, ci)] = v;
+                w_out[wo + n * wstride] = v;
                 if (!isfinite(v)) {
                     const long long lin = (((long long)(n * NV + k) * b.nj + (cj - 1)) * b.ni) + (ci - 1);
                     atomicMin(a.status + blockIdx.y, (unsigned long long)lin);
@@ -487,6 +497,7 @@ __global__ void __launch_bounds__(FLUX_THREADS, HBNS_MINB(VISC))
     }
     // the tile's residual rows are consumed: drop their L2 lines without a
     // write-back (only whole 128-B lines inside this tile's row segments)
+#if HBNS_DISCARD
     __syncthreads();
     for (int t = threadIdx.x; t < P * NV * TJ; t += FLUX_THREADS) {
         const int r = t % TJ, k = (t / TJ) % NV, n = t / (TJ * NV);
@@ -496,6 +507,7 @@ __global__ void __launch_bounds__(FLUX_THREADS, HBNS_MINB(VISC))
         for (uintptr_t l = (s0 + 127) & ~(uintptr_t)127; l + 128 <= s0 + len; l += 128)
             asm volatile("discard.global.L2 [%0], 128;" ::"l"(l) : "memory");
     }
+#endif
     if (first) {
         // stage-1 norm partial of the tile: fixed shuffle tree per warp, warps in order
         for (int o = 16; o > 0; o >>= 1) sq = add(sq, __shfl_down_sync(0xffffffffu, sq, o));
