@@ -56,7 +56,7 @@ typedef struct hbns_args {
     const hbns_block *blocks;
     const double *winf;          /* freestream state per snapshot (P x 4)     */
     const double *dmat;          /* HB matrix D (P x P)                       */
-    unsigned long long *status;  /* per block: first non-finite lin, ~0 none  */
+    unsigned long long *status;  /* per block: first non-finite key, ~0 none  */
     double *norm_part;           /* stage-1 partials                          */
     double *norms;               /* per iteration                             */
     double *forces;              /* per iteration, snapshot: (fx, fy)         */
@@ -76,6 +76,10 @@ typedef struct hbns_args {
     int32_t max_len, max_cells;  /* largest block side, largest ni * nj       */
     int32_t max_ni, max_nj;      /* largest ni, largest nj (residual grid)    */
     int32_t nglobal, nwall;      /* blocks / wall faces of the whole job      */
+    int32_t stage, pad_;         /* RK stage (0..3) of the next hbns_stage:
+                                    status keys are ((iter*4 + stage + 1) << 40)
+                                    | (n, k, j, i) index, an atomicMin keeps the
+                                    first offending stage, then cell          */
 } hbns_args;
 
 int hbns_boundaries(const hbns_args *a, int32_t slot, void *stream);

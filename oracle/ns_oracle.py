@@ -122,7 +122,9 @@ def cut_exchange(blocks, cuts, slot):
 
 
 class NSDivergence(Exception):
-    pass
+    def __init__(self, block, iteration, stage):
+        self.block, self.iteration, self.stage = block, iteration, stage
+        super().__init__(f"non-finite state in block {block} at iteration {iteration}, stage {stage}")
 
 
 class OracleNS:
@@ -162,8 +164,7 @@ class OracleNS:
                                       _p(ob.r), _p(ob.dt), _p(self.dmat), RK_ALPHAS[st], int(st == 0),
                                       ctypes.byref(sumsq))
                     if bad:
-                        raise NSDivergence(f"non-finite state in block {bid} at iteration {self.done}, "
-                                           f"stage {st}")
+                        raise NSDivergence(bid, self.done, st)
                 if st == 0:
                     self.norms.append(math.sqrt(float(sumsq.value)))
             self.forces.append(self.force_coefficients())

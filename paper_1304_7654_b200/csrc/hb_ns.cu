@@ -302,7 +302,7 @@ __device__ __forceinline__ void stage_row(double *sdst, const double *grow, int 
 // already on chip (primitives, normals) or in L2 (R, W_m).
 template <bool VISC, int P>
 __global__ void __launch_bounds__(FLUX_THREADS, HBNS_MINB(VISC))
-    ns_stage_kernel(hbns_args a, const double *w, const double *w0, double *w_out, double coef, int first) {
+    ns_stage_kernel(hbns_args a, const double *w, const double *w0, double *w_out, double coef, int first, int iter) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     FluxSmem &S = *reinterpret_cast<FluxSmem *>(smem_raw);
     __shared__ double red[FLUX_THREADS / 32];
@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(FLUX_THREADS, HBNS_MINB(VISC))
     const int cj = j0 + cr, ci = i0 + cc_;
     const bool cell_live = warp < TJ && cj <= b.nj && ci <= b.ni;
     double best = 0.0;   // stage 1: the cell's time step, min over snapshots
+    const int gstage = (a.iter_dev ? *a.iter_dev : iter) * 4 + a.stage + 1;
     for (int t = threadIdx.x; t < P * P; t += FLUX_THREADS) S.dmat[t] = a.dmat[t];
     for (int n = 0; n < P; ++n) {
         const int g = a.Pg > 1 ? n : 0;
@@ -490,7 +491,7 @@ __global__ void __launch_bounds__(FLUX_THREADS, HBNS_MINB(VISC))
                 w_out[wo + n * wstride] = v;
                 if (!isfinite(v)) {
                     const long long lin = (((long long)(n * NV + k) * b.nj + (cj - 1)) * b.ni) + (ci - 1);
-                    atomicMin(a.status + blockIdx.y, (unsigned long long)lin);
+                    atomicMin(a.status + blockIdx.y, hbgpu::divergence_key(gstage, lin));
                 }
             }
         }
@@ -664,7 +665,7 @@ extern "C" int hbns_boundaries(const hbns_args *a, int32_t slot, void *stream) {
 }
 
 template <bool VISC, int P>
-static int stage_launch(const hbns_args *a, int32_t slot_in, int32_t slot_out, double coef, int first,
+static int stage_launch(const hbns_args *a, int32_t slot_in, int32_t slot_out, double coef, int first, int iter,
                         cudaStream_t s) {
     static bool ready[hbgpu::HB_MAX_DEVICES];
     const int dev = hbgpu::current_device();
@@ -678,19 +679,19 @@ static int stage_launch(const hbns_args *a, int32_t slot_in, int32_t slot_out, d
     }
     const int64_t tiles = (int64_t)((a->max_ni + TI - 1) / TI) * ((a->max_nj + TJ - 1) / TJ);
     ns_stage_kernel<VISC, P><<<dim3((unsigned)tiles, a->nblocks), FLUX_THREADS, smem, s>>>(
-        *a, a->w[slot_in], a->w[0], a->w[slot_out], coef, first);
+        *a, a->w[slot_in], a->w[0], a->w[slot_out], coef, first, iter);
     return HBGPU_OK;
 }
 
 template <bool VISC>
-static int stage_dispatch(const hbns_args *a, int32_t slot_in, int32_t slot_out, double coef, int first,
+static int stage_dispatch(const hbns_args *a, int32_t slot_in, int32_t slot_out, double coef, int first, int iter,
                           cudaStream_t s) {
     switch (a->P) {
-        case 1: return stage_launch<VISC, 1>(a, slot_in, slot_out, coef, first, s);
-        case 3: return stage_launch<VISC, 3>(a, slot_in, slot_out, coef, first, s);
-        case 5: return stage_launch<VISC, 5>(a, slot_in, slot_out, coef, first, s);
-        case 7: return stage_launch<VISC, 7>(a, slot_in, slot_out, coef, first, s);
-        case 9: return stage_launch<VISC, 9>(a, slot_in, slot_out, coef, first, s);
+        case 1: return stage_launch<VISC, 1>(a, slot_in, slot_out, coef, first, iter, s);
+        case 3: return stage_launch<VISC, 3>(a, slot_in, slot_out, coef, first, iter, s);
+        case 5: return stage_launch<VISC, 5>(a, slot_in, slot_out, coef, first, iter, s);
+        case 7: return stage_launch<VISC, 7>(a, slot_in, slot_out, coef, first, iter, s);
+        case 9: return stage_launch<VISC, 9>(a, slot_in, slot_out, coef, first, iter, s);
         default: break;
     }
     hbgpu_set_error("hbns_stage: P = %d not templated (1..9 odd)", a->P);
@@ -710,8 +711,12 @@ extern "C" int hbns_stage(const hbns_args *a, int32_t slot_in, int32_t slot_out,
         return HBGPU_ERR_ARG;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    int rc = a->mu > 0.0 ? stage_dispatch<true>(a, slot_in, slot_out, coef, first != 0, s)
-                         : stage_dispatch<false>(a, slot_in, slot_out, coef, first != 0, s);
+    if (a->stage < 0 || a->stage > 3) {
+        hbgpu_set_error("hbns_stage: args->stage %d is not an RK stage (0..3)", a->stage);
+        return HBGPU_ERR_ARG;
+    }
+    int rc = a->mu > 0.0 ? stage_dispatch<true>(a, slot_in, slot_out, coef, first != 0, iter, s)
+                         : stage_dispatch<false>(a, slot_in, slot_out, coef, first != 0, iter, s);
     if (rc) return rc;
     int n = 1;
     if (first) {

@@ -465,7 +465,8 @@ def _ns_types():
                     ("blocks", vp), ("winf", vp), ("dmat", vp), ("status", vp), ("norm_part", vp),
                     ("norms", vp), ("forces", vp), ("blk_norms", vp), ("wall_prod", vp), ("iter_dev", vp), ("mu", f64), ("cfl", f64), ("omega_nh", f64), ("kq", f64),
                     ("nblocks", i32), ("P", i32), ("Pg", i32), ("moving", i32), ("max_len", i32),
-                    ("max_cells", i32), ("max_ni", i32), ("max_nj", i32), ("nglobal", i32), ("nwall", i32)]
+                    ("max_cells", i32), ("max_ni", i32), ("max_nj", i32), ("nglobal", i32), ("nwall", i32),
+                    ("stage", i32), ("pad_", i32)]
     return Block, Args
 
 
@@ -615,6 +616,7 @@ class NSRun:
         """Boundary halos of stage st's input, then the fused stage kernel."""
         from . import native
         si, so = STAGE_SLOTS[st]
+        self.args.stage = st   # the launch copies the arguments (and a graph keeps the copy)
         ap, s = self._ct.byref(self.args), self._stream()
         native.check(self.lib.hbns_boundaries(ap, si, s), "hbns_boundaries")
         native.check(self.lib.hbns_stage(ap, si, so, RK_ALPHAS[st], self.done, int(st == 0), s), "hbns_stage")
@@ -658,15 +660,10 @@ class NSRun:
         return self
 
     def divergence(self):
-        keys = self.status.cpu().numpy().view(np.uint64)
-        for k, key in enumerate(keys):
-            if int(key) != (1 << 64) - 1:
-                b = self.blocks[k]
-                lin = int(key)
-                i, j = lin % b.ni + 1, (lin // b.ni) % b.nj + 1
-                nk = lin // (b.ni * b.nj)
-                return b.id, i, j, nk % 4, nk // 4
-        return None
+        """The first non-finite value: earliest (iteration, stage), then the
+        lowest block id, then the first (snapshot, variable, j, i) --
+        (block, i, j, variable, snapshot, iteration, stage), or None."""
+        return _first_divergence(self.status.cpu().numpy().view(np.uint64), self.blocks)
 
     def fields(self):
         return {b.id: self.slot_view(0, b).cpu().numpy() for b in self.blocks}
@@ -677,6 +674,29 @@ class NSRun:
     def force_history(self):
         """(iterations, P, 2) (cl, cd) in the snapshot's freestream axes."""
         return _lift_drag(self.case, self.forces[:self.done * self.case.planes * 2].cpu().numpy(), self.done)
+
+
+def _first_divergence(keys, blocks):
+    """Decode per-block status keys ((gstage << 40) | lin, all-ones: none)."""
+    hits = []
+    for b, key in zip(blocks, keys):
+        key = int(key)
+        if key == (1 << 64) - 1:
+            continue
+        gstage, lin = key >> 40, key & ((1 << 40) - 1)
+        hits.append((gstage, b.id, lin, b))
+    if not hits:
+        return None
+    gstage, bid, lin, b = min(hits, key=lambda h: h[:3])
+    nk = lin // (b.ni * b.nj)
+    return bid, lin % b.ni + 1, (lin // b.ni) % b.nj + 1, nk % 4, nk // 4, (gstage - 1) // 4, (gstage - 1) % 4
+
+
+def _raise_divergence(d):
+    from .exceptions import DivergenceError
+    err = DivergenceError(*d[:5])
+    err.iteration, err.stage = d[5], d[6]
+    raise err
 
 
 # stage s reads slot STAGE_SLOTS[s][0], writes STAGE_SLOTS[s][1] (0 = W^0)
@@ -714,8 +734,8 @@ class NSRanksResult:
         return _lift_drag(self.case, self._forces.cpu().numpy(), self.done)
 
     def divergence(self):
-        hits = [d for d in (r.divergence() for r in self.runs) if d is not None]
-        return min(hits) if hits else None
+        keys = np.concatenate([r.status.cpu().numpy().view(np.uint64) for r in self.runs])
+        return _first_divergence(keys, [b for r in self.runs for b in r.blocks])
 
 
 def _fold_job(case, lib, blk_norms, wall_prod, iterations, stream, ctypes_mod):
@@ -744,7 +764,6 @@ def run_ns_ranks(case, iterations=None, nranks=2, initial=None):
     (run_ns_distributed), step for step.  Returns an NSRanksResult."""
     import ctypes
     import torch
-    from .exceptions import DivergenceError
     iterations = case.iterations if iterations is None else iterations
     owner = ns_partition(case, nranks)
     runs = [NSRun(case, max(1, iterations), initial, owner=owner, rank=r) for r in range(nranks)]
@@ -778,7 +797,7 @@ def run_ns_ranks(case, iterations=None, nranks=2, initial=None):
         res = NSRanksResult(case, runs, norms, forces, iterations)
     d = res.divergence()
     if d is not None:
-        raise DivergenceError(*d)
+        _raise_divergence(d)
     return res
 
 
@@ -795,7 +814,6 @@ def run_ns_distributed(case, iterations=None, initial=None):
     import torch.distributed as dist
     from . import native
     from .blockops import HaloContext
-    from .exceptions import DivergenceError
     from .solver import make_comm
     iterations = case.iterations if iterations is None else iterations
     rank, world = dist.get_rank(), dist.get_world_size()
@@ -829,12 +847,9 @@ def run_ns_distributed(case, iterations=None, initial=None):
     finally:
         native.load().hbgpu_comm_destroy(comm)
     res = NSRanksResult(case, [run], norms, forces, iterations)
-    ordered = sorted(case.blocks, key=lambda b: b.id)
-    for gidx, key in enumerate(keys.cpu().numpy().view(np.uint64)):
-        if int(key) != (1 << 64) - 1:
-            b, lin = ordered[gidx], int(key)
-            nk = lin // (b.ni * b.nj)
-            raise DivergenceError(b.id, lin % b.ni + 1, (lin // b.ni) % b.nj + 1, nk % 4, nk // 4)
+    d = _first_divergence(keys.cpu().numpy().view(np.uint64), sorted(case.blocks, key=lambda b: b.id))
+    if d is not None:
+        _raise_divergence(d)
     return res
 
 
@@ -843,15 +858,20 @@ def _gids(case, blocks):
     return [order[b.id] for b in blocks]
 
 
-def run_ns(case, iterations=None, initial=None):
+def run_ns(case, iterations=None, initial=None, poll=16):
     """Run a case on the GPU; returns the NSRun (fields, norms, forces).
-    Raises DivergenceError on a non-finite state."""
-    from .exceptions import DivergenceError
+    The status keys are read every `poll` iterations: a non-finite state
+    stops the run there and raises DivergenceError (block, i, j, variable,
+    snapshot; .iteration and .stage) for the first offending stage."""
     iterations = case.iterations if iterations is None else iterations
     r = NSRun(case, max(1, iterations), initial)
-    r.iterate(iterations)
+    done = 0
+    while done < iterations:
+        step = min(poll, iterations - done)
+        r.iterate(step)
+        done += step
+        d = r.divergence()   # synchronises
+        if d is not None:
+            _raise_divergence(d)
     r.torch.cuda.synchronize()
-    d = r.divergence()
-    if d is not None:
-        raise DivergenceError(*d)
     return r

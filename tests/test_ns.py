@@ -120,3 +120,26 @@ def test_gpu_ragged_tiles_match_oracle(cuda):
     for b, q in want.fields().items():
         assert np.array_equal(split.fields()[b], q), f"block {b} (2 ranks)"
     assert np.array_equal(split.force_history(), got.force_history())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key,scale,cfl", [("C0", 2, 5.0), ("C0", 2, 30.0), ("C1", 8, 5.0), ("C1", 8, 10.0)])
+def test_gpu_divergence_stops_at_the_oracles_stage(key, scale, cfl, cuda):
+    """Too large a CFL number: the oracle stops at the first stage that writes
+    a non-finite value; the GPU run raises DivergenceError for the same
+    block, iteration and stage, within its status-polling chunk, and the
+    split run names the same place."""
+    from paper_1304_7654_b200.exceptions import DivergenceError
+    case = nsflow.ns_workload(key, scale=scale)
+    case.cfl = cfl
+    with pytest.raises(ns_oracle.NSDivergence) as want:
+        ns_oracle.run(case, 30)
+    with pytest.raises(DivergenceError) as got:
+        nsflow.run_ns(case, 30, poll=4)
+    assert (got.value.block, got.value.iteration, got.value.stage) == \
+        (want.value.block, want.value.iteration, want.value.stage)
+    if len(case.blocks) > 1:
+        with pytest.raises(DivergenceError) as split:
+            nsflow.run_ns_ranks(case, want.value.iteration + 1, 2)
+        assert (split.value.block, split.value.iteration, split.value.stage, split.value.i, split.value.j) == \
+            (got.value.block, got.value.iteration, got.value.stage, got.value.i, got.value.j)
