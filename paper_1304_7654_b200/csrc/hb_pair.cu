@@ -152,9 +152,15 @@ struct PairSmem {
     static constexpr int QSLOT = P * PT * G::TCOLS;
     static constexpr int NQ = PB ? Q : 0;
     static constexpr int NV = 3;                                          // v1 rows in flight
+    // a v1 row holds, per (plane, pde), the strip's columns plus the two edge
+    // columns i0-1 (index 0) and i0+TCOLS (index TCOLS+1), which the edge
+    // warp writes: every consumer lane then reads its west / east v1
+    // neighbour at the same compile-time offsets
+    static constexpr int VPITCH = G::TCOLS + 2;
+    static constexpr int VROW = P * PT * VPITCH;
     static constexpr size_t V1_OFF = ((size_t)R * SLOT + (size_t)NQ * QSLOT) * 8;
-    static constexpr size_t BAR_OFF = V1_OFF + (size_t)NV * QSLOT * 8;
-    static constexpr size_t BYTES = BAR_OFF + (size_t)(3 * R + 3 * NQ) * 8;
+    static constexpr size_t BAR_OFF = V1_OFF + ((size_t)NV * VROW * 8 + 15) / 16 * 16;
+    static constexpr size_t BYTES = BAR_OFF + (size_t)(2 * R + 3 * NQ) * 8;
     static_assert((SLOT * 8) % 128 == 0 && (QSLOT * 8) % 128 == 0, "TMA slots need 128-B alignment");
 };
 
@@ -190,8 +196,10 @@ __device__ __forceinline__ void consumer_regs() {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(PairRegs<PT>::CONSUMER));
 }
 
+// the consumers and the edge warp meet once per row step (v1(r) of every
+// column, the edge columns included, is in the v1 ring) and at each tile end
 __device__ __forceinline__ void consumer_sync() {
-    asm volatile("bar.sync 1, %0;" ::"n"(HBGPU_TILE_WARPS * 32) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"((HBGPU_TILE_WARPS + 1) * 32) : "memory");
 }
 
 // o = residual, v = base - coef * o: the reference's per-point rounding
@@ -281,14 +289,12 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
     uint64_t *full_q = empty_in + R;
     uint64_t *empty_q = full_q + S::NQ;   // q0 slot stored out and free (store warp)
     uint64_t *staged = empty_q + S::NQ;   // v2 row written over it (consumers)
-    uint64_t *edge_ready = staged + S::NQ;   // per stencil slot: edge v1 written (edge warp)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int k = 0; k < R; ++k) {
             mbar_init(full_in + k, 1);
             mbar_init(empty_in + k, CW + 1);   // consumers + the edge warp
-            mbar_init(edge_ready + k, 1);
         }
         for (int k = 0; k < S::NQ; ++k) {
             mbar_init(full_q + k, 1);
@@ -384,39 +390,53 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
 
     if (warp == CW + 2) {
         // ------------------------------ edge warp ------------------------------
-        // v1 of the strip's two edge columns (i0-1, i0+TCOLS) where they lie
-        // inside the block: per row r, once rows r-1..r+1 are in the ring,
-        // lane k = (side, pde, plane n) accumulates plane n's residual in the
-        // reference order (hbcore.py:197-221: stencil, m ascending, forcing)
-        // from the stencil slots, and writes v1 into the slot's edge granule
-        // where the consumers' second stage reads it.
+        // v1 of the strip's two edge columns (i0-1, i0+TCOLS), written into
+        // the v1 ring's edge columns before the row step's barrier:
+        //  * inside the block, lane k = (side, pde, plane n) accumulates plane
+        //    n's residual in the reference order (hbcore.py:197-221: stencil,
+        //    m ascending, forcing) from the stencil slots;
+        //  * on a block face, v1 is the band slot's halo value, which the
+        //    producer's TMA brought into the row's slot as an edge granule.
+        // The south value of each item is kept from the previous row step, so
+        // row r's slot is released as soon as row r's v1 is written: the
+        // consumers and this warp free a slot one row earlier than a
+        // three-row stencil read would, and the ring looks one row further.
         constexpr int NE = 2 * PT * P;
         constexpr int KE = (NE + 31) / 32;   // (side, pde, plane) items per lane
         // per item: its plane's D row and forcing amplitude (fixed), and the
         // forcing / q0 values of the next row, loaded one row ahead
         double drow[KE][P];
-        int side_k[KE], pp_k[KE], n_k[KE];
+        int side_k[KE], pp_k[KE], n_k[KE], off_k[KE], vcol_k[KE], gran_k[KE];
 #pragma unroll
         for (int c = 0; c < KE; ++c) {
             const int k = lane + 32 * c;
             side_k[c] = k < NE ? k / (PT * P) : 2;
             pp_k[c] = (k / P) % PT;
             n_k[c] = k % P;
+            const int side = side_k[c], pp = pp_k[c], n = n_k[c];
+            // smem column of the edge cell inside the stencil box
+            const int region = side == 0 ? 0 : G::NSPLIT - 1;
+            const int idx = side == 0 ? 1 : G::TCOLS - region * (G::TCOLS / G::NSPLIT) + 2;
+            off_k[c] = region * S::REGION + pp * G::BW + idx + n * PT * G::BW;
+            vcol_k[c] = (n * PT + pp) * S::VPITCH + (side == 0 ? 0 : G::TCOLS + 1);
+            gran_k[c] = side == 0 ? S::EDGE_W + (n * PT + pp) * 8 + 7 : S::EDGE_E + (n * PT + pp) * 8;
 #pragma unroll
-            for (int m = 0; m < P; ++m) drow[c][m] = k < NE ? a.D[n_k[c] * P + m] : 0.0;
+            for (int m = 0; m < P; ++m) drow[c][m] = k < NE ? a.D[n * P + m] : 0.0;
         }
         RingPos cin{0, 0};
+        int vr = 0;   // v1 ring row of v1(r), in step with the consumers
         for (int k = a.tile_lo + blockIdx.x; k < ntile; k += gridDim.x) {
             const int t = tile_at(a, k);
             const Tile tl = decode_tile<PT>(a, t);
             const hbgpu_block b = a.blocks[tl.bidx];
             const bool west_in = tl.i0 > 1, east_in = tl.i0 + G::TCOLS <= b.ni;
             const int64_t erow = (int64_t)t * a.tile_rows;   // this tile's rows in edge_q0
-            bool act[KE];
+            bool act[KE], live[KE];
             int ie_k[KE];
-            double ap_k[KE], sv_n[KE], bs_n[KE];
+            double ap_k[KE], sv_n[KE], bs_n[KE], south[KE];
 #pragma unroll
             for (int c = 0; c < KE; ++c) {
+                live[c] = side_k[c] < 2;
                 act[c] = side_k[c] == 0 ? west_in : side_k[c] == 1 ? east_in : false;
                 ie_k[c] = side_k[c] == 0 ? tl.i0 - 1 : tl.i0 + G::TCOLS;
                 ap_k[c] = act[c] ? a.ap[n_k[c] * NPDE + tl.pde0 + pp_k[c]] : 0.0;
@@ -433,14 +453,17 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
                 }
             };
             fetch(tl.j0);
-            RingPos cprev = cin;
-            cin = advance<R>(cin);
-            // every slot fill gets one edge_ready arrival (rows j0-1 and j1+1
-            // carry no edges) so the barrier's phase follows the fills; an
-            // arrival only once its fill has landed, or it could complete the
-            // next phase before the consumers waited on the previous one
-            mbar_wait_idle(full_in + cprev.slot, cprev.phase);
-            if (lane == 0) mbar_arrive(edge_ready + cprev.slot);
+            {
+                // row j0-1: only its centre values are used (v1(j0)'s south)
+                mbar_wait_idle(full_in + cin.slot, cin.phase);
+                const double *ru = ring + cin.slot * S::SLOT;
+#pragma unroll
+                for (int c = 0; c < KE; ++c)
+                    if (act[c]) south[c] = ru[off_k[c]];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty_in + cin.slot);
+                cin = advance<R>(cin);
+            }
             for (int r = tl.j0; r <= tl.j1; ++r) {
                 double sv_c[KE], bs_c[KE];
 #pragma unroll
@@ -450,51 +473,45 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
                 }
                 if (r < tl.j1) fetch(r + 1);
                 const RingPos nx = advance<R>(cin);
-                // row r-1 was waited for at the tile start or as the previous
-                // step's row r; row r as the previous step's row r+1, except at
-                // the tile's first row: the ring's fills complete in any order,
-                // so row j0+1 having landed says nothing about row j0
+                // row r as the previous step's row r+1, except at the tile's
+                // first row: the ring's fills complete in any order, so row
+                // j0+1 having landed says nothing about row j0
                 if (r == tl.j0) mbar_wait_idle(full_in + cin.slot, cin.phase);
                 mbar_wait_idle(full_in + nx.slot, nx.phase);
+                const double *rc = ring + cin.slot * S::SLOT;
+                const double *rn = ring + nx.slot * S::SLOT;
+                double *vrow = v1ring + vr * S::VROW;
 #pragma unroll
                 for (int c = 0; c < KE; ++c) {
-                    if (!act[c]) continue;
-                    const int side = side_k[c], pp = pp_k[c], n = n_k[c];
-                    // smem column of the edge cell inside the stencil box
-                    const int region = side == 0 ? 0 : G::NSPLIT - 1;
-                    const int idx = side == 0 ? 1 : G::TCOLS - region * (G::TCOLS / G::NSPLIT) + 2;
-                    const int off = region * S::REGION + pp * G::BW + idx;
-                    const double *rc = ring + cin.slot * S::SLOT + off;
-                    const double *ru = ring + cprev.slot * S::SLOT + off;
-                    const double *rn = ring + nx.slot * S::SLOT + off;
-                    double o = stencil(rc[n * PT * G::BW], rc[n * PT * G::BW - 1], rc[n * PT * G::BW + 1],
-                                       ru[n * PT * G::BW], rn[n * PT * G::BW], b.nu_h2, b.adv_2h);
+                    if (!live[c]) continue;
+                    double v;
+                    if (act[c]) {
+                        const double *cc = rc + off_k[c];
+                        const double cen = cc[0];
+                        double o = stencil(cen, cc[-1], cc[1], south[c], rn[off_k[c]], b.nu_h2, b.adv_2h);
+                        const double *cm = rc + off_k[c] - n_k[c] * PT * G::BW;   // plane 0 of the column
 #pragma unroll
-                    for (int m = 0; m < P; ++m) o = radd(o, rmul(drow[c][m], rc[m * PT * G::BW]));
-                    o = radd(o, rmul(ap_k[c], sv_c[c]));
-                    const double base = PB ? bs_c[c] : rc[n * PT * G::BW];
-                    if (!PB) a.edge_q0[(erow + r - tl.j0) * NE + lane + 32 * c] = base;   // q0 (pass A: in)
-                    const double v = rsub(base, rmul(a.coef, o));
-                    ring[cin.slot * S::SLOT + (side == 0 ? S::EDGE_W + (n * PT + pp) * 8 + 7
-                                                            : S::EDGE_E + (n * PT + pp) * 8)] = v;
+                        for (int m = 0; m < P; ++m) o = radd(o, rmul(drow[c][m], cm[m * PT * G::BW]));
+                        o = radd(o, rmul(ap_k[c], sv_c[c]));
+                        const double base = PB ? bs_c[c] : cen;
+                        if (!PB) a.edge_q0[(erow + r - tl.j0) * NE + lane + 32 * c] = base;   // q0 (pass A: in)
+                        v = rsub(base, rmul(a.coef, o));
+                        south[c] = cen;
+                    } else {
+                        v = rc[gran_k[c]];   // block face: the band slot's halo value
+                    }
+                    vrow[vcol_k[c]] = v;
                 }
-                // a later fill of this slot may TMA a face granule over the
-                // same words: order these generic-proxy writes before it
-                fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(edge_ready + cin.slot);
-                    mbar_arrive(empty_in + cprev.slot);   // row r-1: read for the last time
-                }
-                cprev = cin;
+                if (lane == 0) mbar_arrive(empty_in + cin.slot);   // row r: read for the last time
+                consumer_sync();   // the consumers' barrier of row step r
                 cin = nx;
+                vr = vr == S::NV - 1 ? 0 : vr + 1;
             }
+            // row j1+1 was read as the last row's north only
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(edge_ready + cin.slot);   // row j1+1
-                mbar_arrive(empty_in + cprev.slot);   // row j1
-                mbar_arrive(empty_in + cin.slot);     // row j1+1
-            }
+            if (lane == 0) mbar_arrive(empty_in + cin.slot);
+            consumer_sync();   // the consumers' tile-end barrier
             cin = advance<R>(cin);
         }
         return;
@@ -508,13 +525,10 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
     const int col0 = 32 * cw + lane;
     const int in_off = (cw / G::CWPR) * S::REGION + pp * G::BW + 32 * (cw % G::CWPR) + lane + 2;
     const int q_off = pp * G::TCOLS + col0;
-    // this lane's west / east v1 neighbour for the second stage: the shared v1
-    // row, or the band granule at the strip's edges (element 7 / 0 of it)
-    const bool west_edge = col0 == 0, east_edge = col0 == G::TCOLS - 1;
-    const int w_off = west_edge ? S::EDGE_W + pp * 8 + 7 : q_off - 1;      // + n * (PT*8 | PT*TCOLS)
-    const int e_off = east_edge ? S::EDGE_E + pp * 8 : q_off + 1;
-    const int w_nstride = west_edge ? PT * 8 : PT * G::TCOLS;
-    const int e_nstride = east_edge ? PT * 8 : PT * G::TCOLS;
+    // this lane's column in a v1 ring row; its west / east v1 neighbours for
+    // the second stage sit at -1 / +1 (the edge warp's columns at the strip's
+    // edges)
+    const int v_off = pp * S::VPITCH + 1 + col0;
     const int gstage = (*a.iter) * 4 + a.stage + 1;   // first stage of the pair; +1 for the second
     const double coef1 = a.coef, coef2 = a.coef2;
     double dk[P / 2 + 1];
@@ -550,24 +564,25 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
         FaceHit trow = PB ? FaceHit{0, 0} : row_target(a.faces, b, i, tl.j0, true);
         double nrm = 0.0;
         double sv_prev = 0.0;
-        RingPos cprev{0, 0};   // stencil entry of row r-1
         // input window: this lane's column of `in` at rows r-1, r, r+1 stays
         // in registers, so a row step loads only the new row's centre and
         // the current row's west / east neighbours from the ring
         double xa[P], xb[P], xc[P];
         {
-            // row j0-1 entry: only its stencil row is used (as v1(j0)'s south)
-            cprev = cin;
+            // row j0-1 entry: only its centre row is used (as v1(j0)'s south)
+            const RingPos cu = cin;
             cin = advance<R>(cin);
-            mbar_wait(full_in + cprev.slot, cprev.phase);
+            mbar_wait(full_in + cu.slot, cu.phase);
             mbar_wait(full_in + cin.slot, cin.phase);
-            const double *ru = ring + cprev.slot * S::SLOT + in_off;
+            const double *ru = ring + cu.slot * S::SLOT + in_off;
             const double *rc = ring + cin.slot * S::SLOT + in_off;
 #pragma unroll
             for (int n = 0; n < P; ++n) {
                 xa[n] = ru[n * PT * G::BW];
                 xb[n] = rc[n * PT * G::BW];
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty_in + cu.slot);   // row j0-1: read for the last time
         }
         // one row step: v1(r) and, one row behind, v2(r-1).  Input window on
         // entry: ia = in(r-1), ib = in(r); ic <- in(r+1)
@@ -602,23 +617,19 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
                 for (int n = 0; n < P; ++n) nrm = __fma_rn(o[n], o[n], nrm);
             }
             record_nonfinite<P>(pc, a, tl.bidx, b, p, r, i, gstage);
-            double *vrow = v1ring + vr * S::QSLOT + q_off;
+            double *vrow = v1ring + vr * S::VROW + v_off;
 #pragma unroll
-            for (int n = 0; n < P; ++n) vrow[n * PT * G::TCOLS] = pc[n];
-#ifndef HBGPU_MEASURE_NOBARRIER   // measurement builds only: wrong results, barrier cost
+            for (int n = 0; n < P; ++n) vrow[n * PT * S::VPITCH] = pc[n];
             consumer_sync();
-#endif
             if (r > tl.j0) {
                 // second stage at row r-1
-                mbar_wait(edge_ready + cprev.slot, cprev.phase);
                 const int vp = vr == 0 ? S::NV - 1 : vr - 1;   // v1 ring row of v1(r-1)
-                const double *vw = west_edge ? ring + cprev.slot * S::SLOT + w_off : v1ring + vp * S::QSLOT + w_off;
-                const double *ve = east_edge ? ring + cprev.slot * S::SLOT + e_off : v1ring + vp * S::QSLOT + e_off;
+                const double *vv = v1ring + vp * S::VROW + v_off;
                 double w2[P], e2[P], base2[P];
 #pragma unroll
                 for (int n = 0; n < P; ++n) {
-                    w2[n] = vw[n * w_nstride];
-                    e2[n] = ve[n * e_nstride];
+                    w2[n] = vv[n * PT * S::VPITCH - 1];
+                    e2[n] = vv[n * PT * S::VPITCH + 1];
                 }
                 if (PB) {
                     // q0 of row r-1: the previous q slot
@@ -649,8 +660,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
             }
             sv_prev = sv;
             __syncwarp();
-            if (lane == 0) mbar_arrive(empty_in + cprev.slot);   // row r-1 no longer read
-            cprev = cin;
+            if (lane == 0) mbar_arrive(empty_in + cin.slot);   // row r no longer read
             cin = nx;
             if (PB) cq = advance<Q>(cq);
             vr = vr == S::NV - 1 ? 0 : vr + 1;
@@ -663,21 +673,19 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
             row_step(r + 2, vc, va, vb, xc, xa, xb);
         }
         // last second-stage row: v2(j1) from the window (A, B) = (v1(j1-1),
-        // v1(j1)) and v1(j1+1) from the band slot; cprev is the entry of row
-        // j1 (v1(j1)'s edge granules); X = in(j1) (pass A: q0 row j1)
+        // v1(j1)) and v1(j1+1) from the band slot; X = in(j1) (pass A: q0
+        // row j1)
         auto last_step = [&](double(&A)[P], double(&B)[P], double(&X)[P]) {
             double vd[P];
 #pragma unroll
             for (int n = 0; n < P; ++n) vd[n] = __ldg(a.band + colbase + n * ps4 + (int64_t)(tl.j1 + 1) * b.rs);
-            mbar_wait(edge_ready + cprev.slot, cprev.phase);
             const int vp = vr == 0 ? S::NV - 1 : vr - 1;   // v1 ring row of v1(j1)
-            const double *vw = west_edge ? ring + cprev.slot * S::SLOT + w_off : v1ring + vp * S::QSLOT + w_off;
-            const double *ve = east_edge ? ring + cprev.slot * S::SLOT + e_off : v1ring + vp * S::QSLOT + e_off;
+            const double *vv = v1ring + vp * S::VROW + v_off;
             double w2[P], e2[P], base2[P], o[P], v[P];
 #pragma unroll
             for (int n = 0; n < P; ++n) {
-                w2[n] = vw[n * w_nstride];
-                e2[n] = ve[n * e_nstride];
+                w2[n] = vv[n * PT * S::VPITCH - 1];
+                e2[n] = vv[n * PT * S::VPITCH + 1];
             }
             if (PB) {
                 const RingPos cqp = cq.slot == 0 ? RingPos{Q - 1, cq.phase ^ 1u} : RingPos{cq.slot - 1, cq.phase};
@@ -718,10 +726,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
         // tile's first row overwrites it
         consumer_sync();
         __syncwarp();
-        if (lane == 0) {
-            mbar_arrive(empty_in + cprev.slot);   // row j1
-            mbar_arrive(empty_in + cin.slot);     // row j1+1
-        }
+        if (lane == 0) mbar_arrive(empty_in + cin.slot);   // row j1+1 (row j1 left with its row step)
         cin = advance<R>(cin);
         if (!PB && a.norm_part != nullptr) {
             const double s = warp_sum(nrm);
