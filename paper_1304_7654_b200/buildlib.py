@@ -11,6 +11,7 @@ import glob
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 REPO_DIR = os.path.dirname(PKG_DIR)
@@ -53,18 +54,22 @@ def build(force=False, verbose=False):
     objdir = os.path.join(PKG_DIR, "build")
     os.makedirs(objdir, exist_ok=True)
     inc = ["-I", os.path.join(REPO_DIR, "include"), "-I", CSRC, "-I", _nccl_include()]
-    objs = []
-    logs = []
-    for src in sources():
+    # HBGPU_NVCC_EXTRA: extra flags for measurement builds (e.g. -D overrides)
+    extra = os.environ.get("HBGPU_NVCC_EXTRA", "").split()
+
+    def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        # HBGPU_NVCC_EXTRA: extra flags for measurement builds (e.g. -D overrides)
-        extra = os.environ.get("HBGPU_NVCC_EXTRA", "").split()
         cmd = [nvcc, *ARCH_FLAGS, *NVCC_FLAGS, *extra, *inc, "-c", src, "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
-        logs.append(res.stdout + res.stderr)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
-        objs.append(obj)
+        return obj, res.stdout + res.stderr
+
+    # one nvcc per source, side by side (the template-heavy files take a minute each)
+    with ThreadPoolExecutor(max_workers=min(len(sources()), os.cpu_count() or 1)) as pool:
+        done = list(pool.map(compile_one, sources()))
+    objs = [o for o, _ in done]
+    logs = [l for _, l in done]
     tmp = LIB_PATH + ".tmp"
     cmd = [nvcc, *ARCH_FLAGS, "-shared", "-o", tmp, *objs, "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)

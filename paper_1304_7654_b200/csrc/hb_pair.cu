@@ -561,7 +561,6 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
         double va[P], vb[P], vc[P];
 #pragma unroll
         for (int n = 0; n < P; ++n) vb[n] = __ldg(a.band + colbase + n * ps4 + (int64_t)(tl.j0 - 1) * b.rs);
-        FaceHit trow = PB ? FaceHit{0, 0} : row_target(a.faces, b, i, tl.j0, true);
         double nrm = 0.0;
         double sv_prev = 0.0;
         // input window: this lane's column of `in` at rows r-1, r, r+1 stays
@@ -650,11 +649,6 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
                     const int64_t row = (int64_t)(r - 1) * b.rs;
 #pragma unroll
                     for (int n = 0; n < P; ++n) a.out[colbase + n * ps4 + row] = v[n];
-                    if (trow.ps != 0) {
-#pragma unroll
-                        for (int n = 0; n < P; ++n) forward(trow, a.out, a.sendbuf, n, p, v[n]);
-                    }
-                    trow = row_target(a.faces, b, i, r, true);
                 }
                 record_nonfinite<P>(v, a, tl.bidx, b, p, r - 1, i, gstage + 1);
             }
@@ -705,10 +699,6 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
                 const int64_t row = (int64_t)tl.j1 * b.rs;
 #pragma unroll
                 for (int n = 0; n < P; ++n) a.out[colbase + n * ps4 + row] = v[n];
-                if (trow.ps != 0) {
-#pragma unroll
-                    for (int n = 0; n < P; ++n) forward(trow, a.out, a.sendbuf, n, p, v[n]);
-                }
             }
             record_nonfinite<P>(v, a, tl.bidx, b, p, tl.j1, i, gstage + 1);
         };
@@ -721,6 +711,24 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1) pair_tma_kernel(const __grid_
             row_step(r, va, vb, vc, xa, xb, xc);
             row_step(r + 1, vb, vc, va, xb, xc, xa);
             last_step(vc, va, xc);
+        }
+        if (!PB) {
+            // pass A forwards the block's south / north face rows (a full halo
+            // pass follows pass B).  Out of the row loop: the lane reads back
+            // the v2 values it stored itself (same thread, program order) for
+            // the at most two face rows of the tile, instead of testing for a
+            // face row in every row step.
+            auto forward_row = [&](int j) {
+                const FaceHit trow = row_target(a.faces, b, i, j, true);
+                if (trow.ps == 0) return;
+                double v[P];
+#pragma unroll
+                for (int n = 0; n < P; ++n) v[n] = a.out[colbase + n * ps4 + (int64_t)j * b.rs];
+#pragma unroll
+                for (int n = 0; n < P; ++n) forward(trow, a.out, a.sendbuf, n, p, v[n]);
+            };
+            if (tl.j0 == 1) forward_row(1);
+            if (tl.j1 == b.nj && b.nj > 1) forward_row(b.nj);
         }
         // every consumer is past its reads of the v1 ring before the next
         // tile's first row overwrites it
