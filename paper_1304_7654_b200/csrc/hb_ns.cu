@@ -279,6 +279,13 @@ __device__ __forceinline__ void stage_row(double *sdst, const double *grow, int 
 // <= 96).  Measured on the fused stage kernel: Euler 3 (C4 201 vs 210 ms per
 // iteration with 2), viscous 2 (C3 13.9 vs 14.9, C1 0.44 vs 0.50 ms).
 // HBNS_FLUX_MINB overrides both in measurement builds.
+#ifndef HBNS_UPDATE_LAZY   // update-step load schedule (see the update step), Euler / viscous
+#define HBNS_UPDATE_LAZY 2
+#endif
+#ifndef HBNS_UPDATE_LAZY_VISC
+#define HBNS_UPDATE_LAZY_VISC 0
+#endif
+
 #ifndef HBNS_DISCARD   // measurement builds may keep the residual scratch's write-backs
 #define HBNS_DISCARD 1
 #endif
@@ -320,6 +327,14 @@ __global__ void __launch_bounds__(FLUX_THREADS, HBNS_MINB(VISC))
     const bool cell_live = warp < TJ && cj <= b.nj && ci <= b.ni;
     double best = 0.0;   // stage 1: the cell's time step, min over snapshots
     const int gstage = (a.iter_dev ? *a.iter_dev : iter) * 4 + a.stage + 1;
+    // Index arithmetic in 32 bits: offsets inside one snapshot of one block
+    // (below 2^31 values: nsflow.NSRun refuses larger blocks) are ints; only the
+    // per-snapshot base pointers are 64-bit, formed once per snapshot.
+    const int wrow = b.ni + 4;                    // state / centre row pitch
+    const int wplane = (b.nj + 4) * wrow;         // one (snapshot, variable) plane; one geometry snapshot of xc/yc/vol
+    const int rplane = b.nj * b.ni;               // one residual plane
+    const int cell_w = (cj + 1) * wrow + ci + 1;  // this thread's cell in a state plane (ws / cc)
+    const int cell_r = (cj - 1) * b.ni + ci - 1;  // ... in a residual plane (rs)
     for (int t = threadIdx.x; t < P * P; t += FLUX_THREADS) S.dmat[t] = a.dmat[t];
     for (int n = 0; n < P; ++n) {
         const int g = a.Pg > 1 ? n : 0;
@@ -331,9 +346,11 @@ __global__ void __launch_bounds__(FLUX_THREADS, HBNS_MINB(VISC))
         //    and grid fluxes; the cell centres of the 1-cell ring (viscous)
         {
             const int ilast = b.ni + 2 - (i0 - 2);   // region column of array column ni+2
+            const double *wn = w + b.w_off + (int64_t)n * NV * wplane + (i0 - 1);   // (n, 0, j = -1, i0 - 2)
+#pragma unroll 1   // unrolled, the six row copies cost more (C4 185.8 vs 180.8 ms per iteration)
             for (int row = warp; row < NV * RH; row += NW) {
                 const int k = row / RH, r = row - k * RH;
-                stage_row(S.w[k][r], w + ws(b, n, k, min(j0 - 2 + r, b.nj + 2), i0 - 2), RW, ilast, lane);
+                stage_row(S.w[k][r], wn + k * wplane + min(j0 - 1 + r, b.nj + 3) * wrow, RW, ilast, lane);
             }
             if (geo) {
                 const int flast = b.ni - (i0 - 1);       // i-face column of face ni
@@ -417,9 +434,10 @@ __global__ void __launch_bounds__(FLUX_THREADS, HBNS_MINB(VISC))
         //    lambda_v, omega N_H V), folded into the min over snapshots
         if (cell_live) {
             const int r = cr, c = cc_;
+            double *rn_ = a.r + b.r_off + (int64_t)n * NV * rplane + cell_r;
 #pragma unroll
             for (int k = 0; k < NV; ++k)
-                a.r[rs(b, n, k, cj, ci)] = sub(add(sub(S.fi[k][r][c + 1], S.fi[k][r][c]), S.fj[k][r + 1][c]), S.fj[k][r][c]);
+                rn_[k * rplane] = sub(add(sub(S.fi[k][r][c + 1], S.fi[k][r][c]), S.fj[k][r + 1][c]), S.fj[k][r][c]);
             if (first) {
                 const double qu = S.pr[0][r + 2][c + 2], qv = S.pr[1][r + 2][c + 2], qc = S.pr[3][r + 2][c + 2];
                 const double ax = S.nxi[r][c], ay = S.nyi[r][c], bx = S.nxi[r][c + 1], by = S.nyi[r][c + 1];
@@ -430,7 +448,7 @@ __global__ void __launch_bounds__(FLUX_THREADS, HBNS_MINB(VISC))
                 const double lb = add(fabs(sub(add(mul(qu, bx), mul(qv, by)), gb)), mul(qc, __dsqrt_rn(add(mul(bx, bx), mul(by, by)))));
                 const double lc = add(fabs(sub(add(mul(qu, cx), mul(qv, cy)), gc)), mul(qc, __dsqrt_rn(add(mul(cx, cx), mul(cy, cy)))));
                 const double ld = add(fabs(sub(add(mul(qu, dx), mul(qv, dy)), gd)), mul(qc, __dsqrt_rn(add(mul(dx, dx), mul(dy, dy)))));
-                const double V = a.vol[cc(b, g, cj, ci)];
+                const double V = a.vol[b.c_off + (int64_t)g * wplane + cell_w];
                 double den = add(mul(0.5, add(la, lb)), mul(0.5, add(lc, ld)));
                 if (VISC) {
                     const double sxi = mul(0.5, add(ax, bx)), syi = mul(0.5, add(ay, by));
@@ -461,33 +479,54 @@ __global__ void __launch_bounds__(FLUX_THREADS, HBNS_MINB(VISC))
         }
         // V and alpha_s dt / V: one value on a fixed mesh, per snapshot on a
         // moving one (recomputed per variable there: no register arrays)
-        const double V0 = a.vol[cc(b, 0, cj, ci)];
+        const double *volc = a.vol + b.c_off + cell_w;   // this cell, geometry snapshot 0
+        const double V0 = volc[0];
         const double cdt0 = dv(mul(coef, dtc), V0);
         const bool per_n = a.Pg > 1;
-        const int64_t wstride = (int64_t)NV * (b.nj + 4) * (b.ni + 4);   // snapshot stride, state pools
-        const int64_t rstride = (int64_t)NV * b.nj * b.ni;               // snapshot stride, residual pool
+        const int64_t wstride = (int64_t)NV * wplane;   // snapshot stride, state pools
+        const int64_t rstride = (int64_t)NV * rplane;   // snapshot stride, residual pool
         for (int k = 0; k < NV; ++k) {
-            const int64_t wo = ws(b, 0, k, cj, ci), ro = rs(b, 0, k, cj, ci);
-            double wm[P], rn[P], qn[P];
+            const int64_t wo = b.w_off + k * wplane + cell_w, ro = b.r_off + k * rplane + cell_r;
+            // W_m of every snapshot first (they feed every n).  LAZY 0: R_n
+            // and W^0_n of every snapshot loaded up front as well (3 P values
+            // held); 1: W^0_n one snapshot ahead of its use; 2: R_n too (P + 4
+            // values held).  W^0_n is always loaded before the store that may
+            // replace it (stage 4 writes W^0's slot).
+            constexpr int LAZY = VISC ? HBNS_UPDATE_LAZY_VISC : HBNS_UPDATE_LAZY;
+            double wm[P], rn[LAZY < 2 ? P : 1], qn[LAZY < 1 ? P : 1];
 #pragma unroll
             for (int m = 0; m < P; ++m) {
                 wm[m] = w[wo + m * wstride];
-                rn[m] = a.r[ro + m * rstride];
-                qn[m] = w0[wo + m * wstride];
+                if (LAZY < 2) rn[m] = a.r[ro + m * rstride];
+                if (LAZY < 1) qn[m] = w0[wo + m * wstride];
             }
+            double rn_next = LAZY == 2 ? a.r[ro] : 0.0, qn_next = LAZY >= 1 ? w0[wo] : 0.0;
 #pragma unroll
             for (int n = 0; n < P; ++n) {
+                double qn_n, rn_n;
+                if (LAZY >= 1) {
+                    qn_n = qn_next;
+                    if (n + 1 < P) qn_next = w0[wo + (n + 1) * wstride];
+                } else {
+                    qn_n = qn[n];
+                }
+                if (LAZY == 2) {
+                    rn_n = rn_next;
+                    if (n + 1 < P) rn_next = a.r[ro + (n + 1) * rstride];
+                } else {
+                    rn_n = rn[n];
+                }
                 double V = V0, cdt = cdt0;
                 if (per_n) {
-                    V = a.vol[cc(b, n, cj, ci)];
+                    V = volc[(int64_t)n * wplane];
                     cdt = dv(mul(coef, dtc), V);
                 }
                 double s = mul(S.dmat[n * P], wm[0]);
 #pragma unroll
                 for (int m = 1; m < P; ++m) s = add(s, mul(S.dmat[n * P + m], wm[m]));
-                const double R = add(rn[n], mul(V, s));
+                const double R = add(rn_n, mul(V, s));
                 if (first && k == 0) sq = __fma_rn(R, R, sq);
-                const double v = sub(qn[n], mul(cdt, R));
+                const double v = sub(qn_n, mul(cdt, R));
                 w_out[wo + n * wstride] = v;
                 if (!isfinite(v)) {
                     const long long lin = (((long long)(n * NV + k) * b.nj + (cj - 1)) * b.ni) + (ci - 1);

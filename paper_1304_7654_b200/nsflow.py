@@ -518,6 +518,10 @@ class NSRun:
             e.c_off, e.fi_off, e.fj_off = c_off, fi_off, fj_off
             e.part_off = k * ctas
             e.ni, e.nj = b.ni, b.nj
+            # the stage kernel indexes inside one snapshot of a block in 32 bits
+            if 4 * (b.nj + 4) * (b.ni + 4) >= 2 ** 31:
+                from .exceptions import ConfigError
+                raise ConfigError(f"block {b.id}: {b.ni} x {b.nj} cells exceed the NS kernel's 32-bit plane offsets")
             for sd in range(4):
                 e.kinds[sd] = b.kinds[sd]
             e.gid, e.wall_off = gid[b.id], wall_off[b.id]

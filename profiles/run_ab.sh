@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-rm -f gpurun_out/ab.jsonl
-for i in 1 2 3; do
-python bench.py --no-e2e --no-cpu-baseline >> gpurun_out/ab.jsonl 2>> gpurun_out/ab.err
-done
+python -m pytest tests/test_ns.py tests/test_ns_multirank.py -m gpu -x -q > gpurun_out/ns_tests.log 2>&1
+tail -2 gpurun_out/ns_tests.log
+ncu --set full --clock-control none --import-source on -k regex:ns_stage -s 4 -c 2 -o gpurun_out/ns_c4 -f python profiles/ns_bench.py --configs C4 --steps 1 --warmup 1 > gpurun_out/ncu_ns4.log 2>&1
