@@ -166,6 +166,7 @@ __global__ void ns_corner_kernel(hbns_args a, double *w) {
 constexpr int TI = HBNS_TILE_I, TJ = HBNS_TILE_J;   // tile columns, rows
 constexpr int RW = TI + 4, RH = TJ + 4;      // staged region with the 2-cell ring
 constexpr int FLUX_THREADS = 288;            // 9 warps: 264 i-faces / 288 j-faces per pass
+static_assert(RW % 2 == 0, "16-byte staging chunks");
 
 struct FluxSmem {
     double w[NV][RH][RW];          // conservative state
@@ -186,6 +187,11 @@ struct FluxSmem {
 __device__ __forceinline__ void cp8(double *sdst, const double *gsrc) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+// 16-byte form (both addresses 16-byte aligned), past L1: staged values are read once per CTA
+__device__ __forceinline__ void cp16(double *sdst, const double *gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
@@ -335,6 +341,10 @@ __global__ void __launch_bounds__(FLUX_THREADS, HBNS_MINB(VISC))
     const int rplane = b.nj * b.ni;               // one residual plane
     const int cell_w = (cj + 1) * wrow + ci + 1;  // this thread's cell in a state plane (ws / cc)
     const int cell_r = (cj - 1) * b.ni + ci - 1;  // ... in a residual plane (rs)
+    // 16-byte staging copies: even row pitch (every plane offset is then even,
+    // i0 - 1 is a multiple of 32 and the pools are 256-byte aligned) and no
+    // column clamp (the region ends inside the block's array)
+    const bool wide = (b.ni & 1) == 0 && i0 + TI + 1 <= b.ni + 2 && ((uintptr_t)w & 15) == 0 && (b.w_off & 1) == 0;
     for (int t = threadIdx.x; t < P * P; t += FLUX_THREADS) S.dmat[t] = a.dmat[t];
     for (int n = 0; n < P; ++n) {
         const int g = a.Pg > 1 ? n : 0;
@@ -347,6 +357,18 @@ __global__ void __launch_bounds__(FLUX_THREADS, HBNS_MINB(VISC))
         {
             const int ilast = b.ni + 2 - (i0 - 2);   // region column of array column ni+2
             const double *wn = w + b.w_off + (int64_t)n * NV * wplane + (i0 - 1);   // (n, 0, j = -1, i0 - 2)
+            if (wide) {
+                // the region's NV * RH rows of RW values as 16-byte chunks, lane-
+                // contiguous over the whole CTA (864 chunks: 3 per thread);
+                // S.w is dense, so chunk c lands at value 2 c
+                constexpr int CPR = RW / 2;   // chunks per row
+#pragma unroll
+                for (int c = threadIdx.x; c < NV * RH * CPR; c += FLUX_THREADS) {
+                    const int row = c / CPR, k = row / RH, r = row - k * RH;
+                    cp16(&S.w[0][0][0] + 2 * c,
+                         wn + k * wplane + min(j0 - 1 + r, b.nj + 3) * wrow + 2 * (c - row * CPR));
+                }
+            } else
 #pragma unroll 1   // unrolled, the six row copies cost more (C4 185.8 vs 180.8 ms per iteration)
             for (int row = warp; row < NV * RH; row += NW) {
                 const int k = row / RH, r = row - k * RH;
@@ -389,7 +411,7 @@ __global__ void __launch_bounds__(FLUX_THREADS, HBNS_MINB(VISC))
             S.pr[1][r][c] = v;
             S.pr[2][r][c] = p;
             S.pr[3][r][c] = __dsqrt_rn(dv(mul(GAMMA, p), q_r));
-            S.pr[4][r][c] = dv(p, mul(GAMMA - 1.0, q_r));
+            if (VISC) S.pr[4][r][c] = dv(p, mul(GAMMA - 1.0, q_r));   // e: the viscous heat flux only
         }
         __syncthreads();
         // 3. JST sensors of the cells beside the tile's faces
