@@ -78,8 +78,17 @@ struct Smem {
 
 // ---- the pipelined kernel -----------------------------------------------------------
 
+// Resident CTAs per SM the kernel is compiled for: small P needs few
+// registers and short rings, and a second CTA per SM halves the rows each
+// CTA walks in the small, L2-resident cases (C1: 4 x 256 x 128 cells give a
+// CTA ~14 rows of a stage, so its time is the row loop's latency)
+#ifndef HBGPU_SMALL_P_CTAS
+#define HBGPU_SMALL_P_CTAS 2
+#endif
+constexpr int stage_ctas_per_sm(int P) { return P <= 5 ? HBGPU_SMALL_P_CTAS : 1; }
+
 template <int P, bool FIRST, int R, int Q, int PT, int MODE>
-__global__ void __launch_bounds__(THREADS, 1) stage_tma_kernel(const __grid_constant__ hbgpu_stage_args a) {
+__global__ void __launch_bounds__(THREADS, stage_ctas_per_sm(P)) stage_tma_kernel(const __grid_constant__ hbgpu_stage_args a) {
     using S = Smem<P, FIRST, R, Q, PT>;
     using G = Geo<PT>;
     static_assert(R >= 3 && Q >= 2, "ring too short");
@@ -541,9 +550,15 @@ static int prepare(Launch &L) {
 template <int P> struct Depth {
     static constexpr int R = HBGPU_DEPTH_R, RF = HBGPU_DEPTH_RF, Q = HBGPU_DEPTH_Q;
 };
+#if HBGPU_SMALL_P_CTAS == 2   // two CTAs per SM: at most ~113 KB each
+template <> struct Depth<1> { static constexpr int R = 6, RF = 8, Q = 4; };
+template <> struct Depth<3> { static constexpr int R = 5, RF = 8, Q = 4; };
+template <> struct Depth<5> { static constexpr int R = 4, RF = 6, Q = 3; };
+#else
 template <> struct Depth<1> { static constexpr int R = 8, RF = 12, Q = 6; };
 template <> struct Depth<3> { static constexpr int R = 8, RF = 12, Q = 6; };
 template <> struct Depth<5> { static constexpr int R = 6, RF = 10, Q = 5; };
+#endif
 template <> struct Depth<13> { static constexpr int R = 4, RF = 6, Q = 2; };
 template <> struct Depth<15> { static constexpr int R = 4, RF = 5, Q = 2; };
 template <> struct Depth<17> { static constexpr int R = 4, RF = 5, Q = 2; };

@@ -41,6 +41,8 @@ NPDE = native.NPDE
 WIDE_MIN_NI = 192         # blocks at least this wide use 256-column, 1-pde tiles
 BLOCK_ALIGN = 32          # elements (256 B)
 GRID_CTAS = 148           # persistent CTAs of the stage / pair kernels (B200: 1 per SM)
+SMALL_P_CTAS = 2          # resident single-stage CTAs per SM for P <= SMALL_P_MAX (hb_stage.cu)
+SMALL_P_MAX = 5
 TILE_OVERHEAD_ROWS = 4    # a tile's cost beyond its rows: 2 halo rows, ring fill, band rows
 MAX_TILE_ROWS = 1024
 MIN_TILE_ROWS = 8
@@ -92,6 +94,17 @@ def _makespan(shape, tile_rows, ctas):
     costs = np.concatenate(costs)
     costs = np.concatenate([costs, np.zeros((-len(costs)) % ctas)])
     return float(costs.reshape(-1, ctas).sum(axis=0).max())
+
+
+def stage_grid_ctas(blocks, planes, tile_pdes, fused):
+    """Persistent CTAs the rank's stage kernels run with: the single-stage
+    kernel is compiled for SMALL_P_CTAS resident CTAs per SM up to
+    SMALL_P_MAX planes (hb_stage.cu stage_ctas_per_sm), the paired kernel
+    always for one."""
+    units = sum(b.ni * b.nj for b in blocks) * planes * NPDE
+    paired = (fused is not False and fused_eligible(blocks, planes, tile_pdes)
+              and (bool(fused) or units >= FUSED_MIN_UNITS))
+    return GRID_CTAS * (SMALL_P_CTAS if planes <= SMALL_P_MAX and not paired else 1)
 
 
 def choose_tile_rows(blocks, tile_pdes=4, ctas=GRID_CTAS):
@@ -197,7 +210,7 @@ def build_rank_layout(topology, partition, plan, rank, planes, tile_rows=None,
         raise ValueError(f"rank {rank} owns no blocks")
     local_index = {b.id: k for k, b in enumerate(owned)}
     tpd = tile_pdes or choose_tile_pdes(owned)
-    tj = tile_rows or choose_tile_rows(owned, tpd)
+    tj = tile_rows or choose_tile_rows(owned, tpd, stage_grid_ctas(owned, planes, tpd, fused))
     inter = INTERLEAVED if interleaved is None else bool(interleaved)
 
     pitch, ps, rs, base = [], [], [], []
