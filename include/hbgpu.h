@@ -256,6 +256,14 @@ int hbgpu_stage(const hbgpu_stage_args *args, void *stream);
  * CUDA graph capture (hbgpu_engine_create calls it) */
 int hbgpu_stage_prepare(int32_t planes);
 
+/* 1 when the first RK stage of the single-stage schedule (args->stage == 0,
+ * args->pair == 0) forwards its own west / east face columns for this
+ * snapshot count, as stages 1..3 always do; 0 when a column-halo pass
+ * (hbgpu_halo over the post directions) must follow that launch.  The
+ * reference exchanges every face after every stage (exchange.py:295-316);
+ * this only says which launch moves the column faces. */
+int hbgpu_stage_first_forwards(int32_t planes);
+
 /* TMA descriptors for the stage kernel: 4-D tensor maps (columns, rows,
  * pde, plane) over each block's part of a slot, written as CUtensorMap
  * (128 B) #(set*nblocks + b) into out_host (caller uploads it to device

@@ -368,7 +368,8 @@ void single_args(const hbgpu_engine_desc &d, int st, hbgpu_stage_args &a) {
 
 // The halo moves that follow a stage kernel, split in the remote packs
 // (the first `remote` of `dirs`, dst_kind 1) and the local copies:
-//   single stage 0 and pass A: west / east face columns (post_dirs);
+//   pass A, and single stage 0 unless it forwards them itself
+//   (hbgpu_stage_first_forwards): west / east face columns (post_dirs);
 //   pass B: the full halo pass (prime_dirs), pass B forwarding nothing
 //   itself because it writes q4 over q0, which other tiles still read.
 struct PostMoves {
@@ -378,7 +379,7 @@ struct PostMoves {
 
 PostMoves post_moves(const hbgpu_engine_desc &d, int st) {
     PostMoves m;
-    if (d.fused ? st == 1 : st == 0) {
+    if (d.fused ? st == 1 : (st == 0 && !hbgpu_stage_first_forwards(d.planes))) {
         m.dirs = d.post_dirs;
         m.n = d.npost;
         m.remote = d.post_remote;

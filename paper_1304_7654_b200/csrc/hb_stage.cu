@@ -50,13 +50,18 @@
 namespace hbgpu {
 
 // Output rows of the update stages leave by TMA store from the q0 slot they
-// replace.  The first stage is fp64-issue bound: its plain stores cost less
-// than staging + proxy fence, so NOUT = 0 keeps them (a measurement build can
-// set HBGPU_FIRST_STAGING=2 to stage its rows in two extra slots).
+// replace.  The first stage has no q0 ring; it stages its rows in NOUT own
+// slots, so that its store warp forwards the west / east face columns as in
+// the other stages and no column-halo pass follows the launch (the engine
+// asks hbgpu_stage_first_forwards).  Staging costs the issue-bound first
+// stage ~8% at C4's size against plain stores + a 0.23 ms halo pass, but the
+// single-stage schedule serves the small cases, where that extra launch is
+// 5 of ~60-100 us per iteration (C1, C2).  P > 9 (rings near the shared-
+// memory limit) keeps plain stores and the halo pass.
 #ifndef HBGPU_FIRST_STAGING
-#define HBGPU_FIRST_STAGING 0
+#define HBGPU_FIRST_STAGING 2
 #endif
-constexpr int NOUT = HBGPU_FIRST_STAGING;
+constexpr int first_staging(int P) { return P <= 9 ? HBGPU_FIRST_STAGING : 0; }
 
 template <int P, bool FIRST, int R, int Q, int PT>
 struct Smem {
@@ -68,8 +73,8 @@ struct Smem {
     static constexpr int QSLOT = P * PT * G::TCOLS;                      // q0 slot
     static constexpr int NQ = FIRST ? 0 : Q;
     // output rows are staged for the TMA store in the q0 slot they replace;
-    // the first stage has no q0 ring: NOUT own slots, or plain stores
-    static constexpr int NO = FIRST ? NOUT : 0;
+    // the first stage has no q0 ring: first_staging(P) own slots, or plain stores
+    static constexpr int NO = FIRST ? first_staging(P) : 0;
     static constexpr int NS = FIRST ? NO : NQ;   // staging slots (either kind)
     static constexpr size_t BAR_OFF = ((size_t)R * SLOT + (size_t)(NQ + NO) * QSLOT) * 8;
     static constexpr size_t BYTES = BAR_OFF + (size_t)(2 * (R + NQ) + NS + NO) * 8;
@@ -700,6 +705,11 @@ extern "C" int hbgpu_stage_prepare(int32_t planes) {
         }
     }
     return rc;
+}
+
+extern "C" int hbgpu_stage_first_forwards(int32_t planes) {
+    // the templated TMA kernels (odd P) with first-stage staging slots
+    return planes >= 1 && planes <= 9 && (planes & 1) && hbgpu::first_staging(planes) > 0 ? 1 : 0;
 }
 
 extern "C" int hbgpu_stage(const hbgpu_stage_args *args, void *stream) {

@@ -117,6 +117,7 @@ SIGNATURES = {
     "hbgpu_stage": (c_i32, [ctypes.POINTER(StageArgs), c_vp]),
     "hbgpu_band": (c_i32, [ctypes.POINTER(StageArgs), c_vp]),
     "hbgpu_stage_prepare": (c_i32, [c_i32]),
+    "hbgpu_stage_first_forwards": (c_i32, [c_i32]),
     "hbgpu_encode_tensor_maps": (c_i32, [c_vp * 3, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_i64]),
     "hbgpu_halo": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "hbgpu_hazard_scan": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp]),
