@@ -216,3 +216,24 @@ def test_baseline_workloads_shapes():
     assert ic.shape == (5, 4, 128, 256)
     qinf0 = 1.0
     assert np.all(np.abs(ic[:, 0] / qinf0 - 1.0) <= 0.01 + 1e-15)
+
+
+def test_tile_rows_follow_the_stage_kernel_grid():
+    """The single-stage kernel runs two CTAs per SM up to SMALL_P_MAX planes
+    (hb_stage.cu stage_ctas_per_sm), the paired kernel always one: the tile
+    rows are chosen for that grid."""
+    from paper_1304_7654_b200 import baseline_workload, devlayout
+
+    c1 = baseline_workload("C1").case
+    tpd = devlayout.choose_tile_pdes(c1.blocks)
+    assert devlayout.stage_grid_ctas(c1.blocks, c1.planes, tpd, None) == 2 * devlayout.GRID_CTAS
+    assert devlayout.stage_grid_ctas(c1.blocks, c1.planes, tpd, True) == devlayout.GRID_CTAS   # paired
+    rows = devlayout.choose_tile_rows(c1.blocks, tpd, 2 * devlayout.GRID_CTAS)
+    tiles = sum(-(-b.nj // rows) * devlayout.tiles_per_row(c1.blocks, tpd)[b.id] for b in c1.blocks)
+    assert tiles <= 2 * devlayout.GRID_CTAS < 2 * tiles          # one wave, more than half the CTAs busy
+    c2 = baseline_workload("C2").case                             # P = 9: one CTA per SM
+    assert devlayout.stage_grid_ctas(c2.blocks, c2.planes, devlayout.choose_tile_pdes(c2.blocks), None) \
+        == devlayout.GRID_CTAS
+    c3 = baseline_workload("C3").case                             # paired by size
+    assert devlayout.stage_grid_ctas(c3.blocks, c3.planes, devlayout.choose_tile_pdes(c3.blocks), None) \
+        == devlayout.GRID_CTAS
