@@ -1,8 +1,9 @@
 mkdir -p gpurun_out
-rm -f gpurun_out/small_ab.jsonl
-for w in C1 C2 C1 C2; do
-python bench.py --workload $w --steps 50 --warmup 5 --no-e2e --no-cpu-baseline >> gpurun_out/small_ab.jsonl 2>> gpurun_out/small_ab.err
-done
-python bench.py --workload C4 --schedule single --steps 5 --warmup 3 --no-e2e --no-cpu-baseline >> gpurun_out/small_ab.jsonl 2>> gpurun_out/small_ab.err
-python -m pytest tests -m gpu -x -q > gpurun_out/ab_tests.log 2>&1
-tail -3 gpurun_out/ab_tests.log
+python -m pytest tests/test_ns.py tests/test_ns_multirank.py -m gpu -x -q > gpurun_out/ns_tests.log 2>&1
+tail -2 gpurun_out/ns_tests.log
+python profiles/ns_bench.py --configs C0,C1,C2,C3,C4 --steps 5 --warmup 2 2>&1 | python -c "
+import sys,json
+for l in sys.stdin:
+    try: d=json.loads(l); print(d['config'], d['ms_per_iteration'])
+    except Exception: print(l.strip()[:200])
+"

@@ -80,6 +80,25 @@ def test_gpu_matches_oracle_bitwise(key, iters, cuda):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("key,iters", [("C0", 100), ("C1", 12), ("C2", 8)])
+def test_gpu_full_size_matches_oracle_bitwise(key, iters, cuda):
+    """BASELINE configs at full size: C0 (64 x 32, P = 3) at its stated 100
+    iterations; C1 (4 blocks of 256 x 128, viscous, P = 5) and C2 (the
+    pitching 512 x 256 O-grid, P = 9) for as many iterations as the
+    single-threaded oracle finishes in seconds (profiles/ns_soak.py runs
+    them at their stated 200 and 500).  Full-size tiles take the 16-byte
+    staging path of the stage kernel; the scaled cases above mostly do not."""
+    case = nsflow.ns_workload(key)
+    want = ns_oracle.run(case, iters)
+    got = nsflow.run_ns(case, iters)
+    gf, wf = got.fields(), want.fields()
+    for b in wf:
+        assert np.array_equal(gf[b], wf[b]), f"{key} block {b} differs"
+    np.testing.assert_allclose(got.norm_history(), want.norms, rtol=1e-12, atol=0)
+    assert np.array_equal(got.force_history(), np.stack(want.forces))
+
+
+@pytest.mark.gpu
 def test_gpu_full_size_c2_converges(cuda):
     """BASELINE config 2 at full size (512 x 256, P = 9, pitching, 100 of its
     500 iterations): the GPU run stays physical and its residual falls."""
