@@ -295,11 +295,6 @@ __device__ __forceinline__ void stage_row(double *sdst, const double *grow, int 
 #ifndef HBNS_DISCARD   // measurement builds may keep the residual scratch's write-backs
 #define HBNS_DISCARD 1
 #endif
-#ifdef HBNS_FLUX_MINB
-#define HBNS_MINB(VISC) HBNS_FLUX_MINB
-#else
-#define HBNS_MINB(VISC) ((VISC) ? 2 : 3)
-#endif
 
 // The RK stage of one TJ x TI tile, all snapshots, in one CTA (grid.x =
 // tile, grid.y = block).  Per snapshot n: stage W_n with its 2-cell ring
@@ -313,8 +308,8 @@ __device__ __forceinline__ void stage_row(double *sdst, const double *grow, int 
 // ascending) added to R_n, W^(s) = W^0 - (alpha_s dt / V) R.  The time-step
 // and update kernels of the unfused schedule are gone: their inputs are
 // already on chip (primitives, normals) or in L2 (R, W_m).
-template <bool VISC, int P>
-__global__ void __launch_bounds__(FLUX_THREADS, HBNS_MINB(VISC))
+template <bool VISC, int P, int MINB>
+__global__ void __launch_bounds__(FLUX_THREADS, MINB)
     ns_stage_kernel(hbns_args a, const double *w, const double *w0, double *w_out, double coef, int first, int iter) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     FluxSmem &S = *reinterpret_cast<FluxSmem *>(smem_raw);
@@ -725,23 +720,48 @@ extern "C" int hbns_boundaries(const hbns_args *a, int32_t slot, void *stream) {
     return check("hbns_boundaries");
 }
 
-template <bool VISC, int P>
-static int stage_launch(const hbns_args *a, int32_t slot_in, int32_t slot_out, double coef, int first, int iter,
-                        cudaStream_t s) {
+template <bool VISC, int P, int MINB>
+static int stage_launch_k(const hbns_args *a, int32_t slot_in, int32_t slot_out, double coef, int first, int iter,
+                          int64_t tiles, cudaStream_t s) {
     static bool ready[hbgpu::HB_MAX_DEVICES];
     const int dev = hbgpu::current_device();
     if (dev < 0) return HBGPU_ERR_CUDA;
     const size_t smem = sizeof(FluxSmem);
     if (!ready[dev]) {
-        if (cudaFuncSetAttribute(ns_stage_kernel<VISC, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess)
+        if (cudaFuncSetAttribute(ns_stage_kernel<VISC, P, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
             return check("hbns_stage (smem attribute)");
         ready[dev] = true;
     }
-    const int64_t tiles = (int64_t)((a->max_ni + TI - 1) / TI) * ((a->max_nj + TJ - 1) / TJ);
-    ns_stage_kernel<VISC, P><<<dim3((unsigned)tiles, a->nblocks), FLUX_THREADS, smem, s>>>(
+    ns_stage_kernel<VISC, P, MINB><<<dim3((unsigned)tiles, a->nblocks), FLUX_THREADS, smem, s>>>(
         *a, a->w[slot_in], a->w[0], a->w[slot_out], coef, first, iter);
     return HBGPU_OK;
+}
+
+// CTAs per SM the kernel variant is compiled for.  Viscous: 2 (96 registers).
+// Euler: 3 (72 registers) on a grid of many waves -- C4: 170 vs 187 ms per
+// iteration -- but 2 (96 registers, fewer spills: a tile takes ~0.73 of the
+// time) when the grid is so small that both fill the same number of waves --
+// C2, 512 tiles: 0.58 vs 0.71 ms.  The rule compares waves x tile time.
+template <bool VISC, int P>
+static int stage_launch(const hbns_args *a, int32_t slot_in, int32_t slot_out, double coef, int first, int iter,
+                        cudaStream_t s) {
+    const int64_t tiles = (int64_t)((a->max_ni + TI - 1) / TI) * ((a->max_nj + TJ - 1) / TJ);
+#ifdef HBNS_FLUX_MINB
+    return stage_launch_k<VISC, P, HBNS_FLUX_MINB>(a, slot_in, slot_out, coef, first, iter, tiles, s);
+#else
+    if (VISC) return stage_launch_k<VISC, P, 2>(a, slot_in, slot_out, coef, first, iter, tiles, s);
+    static int sms[hbgpu::HB_MAX_DEVICES];
+    const int dev = hbgpu::current_device();
+    if (dev < 0) return HBGPU_ERR_CUDA;
+    if (sms[dev] == 0 && cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        return check("hbns_stage (SM count)");
+    const int64_t total = tiles * a->nblocks;
+    const int64_t waves3 = (total + 3 * sms[dev] - 1) / (3 * sms[dev]), waves2 = (total + 2 * sms[dev] - 1) / (2 * sms[dev]);
+    if (0.733 * (double)waves2 < (double)waves3)
+        return stage_launch_k<VISC, P, 2>(a, slot_in, slot_out, coef, first, iter, tiles, s);
+    return stage_launch_k<VISC, P, 3>(a, slot_in, slot_out, coef, first, iter, tiles, s);
+#endif
 }
 
 template <bool VISC>
