@@ -172,28 +172,75 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled during the timed region: NVML (the
+    source nvidia-smi reads) polled every few ms from a thread -- the default
+    timed region is ~0.2 s, two samples of `nvidia-smi -lms 100` -- with the
+    nvidia-smi loop of the profiling recipe as the fallback."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # nvmlClocksThrottleReason* / nvmlClocksEventReason* bits
+    NVML_REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+                    0x4: "sw_power_cap"}
 
-    def __init__(self, index):
+    def __init__(self, index, period_s=0.005):
         self.index = index
+        self.period_s = period_s
         self.proc = None
+        self.thread = None
+        self.samples = []       # (sm_mhz, reason bits)
+        self.smax = None
+        self.source = None
+
+    def _nvml_loop(self, nv, handle):
+        reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append((float(nv.nvmlDeviceGetClockInfo(handle, nv.NVML_CLOCK_SM)),
+                                     int(reasons(handle))))
+            except Exception:
+                break
+            self._stop.wait(self.period_s)
 
     def __enter__(self):
+        try:
+            import threading
+
+            import pynvml as nv
+            nv.nvmlInit()
+            # torch's device index follows CUDA_VISIBLE_DEVICES; NVML's does not
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = self.index
+            if vis:
+                ids = [v.strip() for v in vis.split(",") if v.strip()]
+                if self.index < len(ids) and ids[self.index].isdigit():
+                    phys = int(ids[self.index])
+            handle = nv.nvmlDeviceGetHandleByIndex(phys)
+            self.smax = float(nv.nvmlDeviceGetMaxClockInfo(handle, nv.NVML_CLOCK_SM))
+            self._stop = threading.Event()
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, handle), daemon=True)
+            self.thread.start()
+            self.source = "nvml"
+            return self
+        except Exception:
+            self.thread = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.source = "nvidia-smi"
         except Exception:
             self.proc = None
         return self
 
     def __exit__(self, *exc):
         self.lines = []
+        if self.thread is not None:
+            self._stop.set()
+            self.thread.join(timeout=2)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -205,7 +252,10 @@ class ClockSampler:
 
     def summary(self):
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm, smax, reasons = [], None, set()
+        sm, smax, reasons = [], self.smax, set()
+        for mhz, bits in self.samples:
+            sm.append(mhz)
+            reasons.update(name for bit, name in self.NVML_REASONS.items() if bits & bit)
         for ln in getattr(self, "lines", []):
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
@@ -221,7 +271,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": self.source}
 
 
 def library_knobs():
