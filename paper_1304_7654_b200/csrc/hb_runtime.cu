@@ -225,6 +225,7 @@ struct hbgpu_engine {
     std::vector<hbgpu_peer_msg> sends, recvs;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
+    bool graph_failed = false;   // capture or instantiation failed once: eager iterations from then on
     int32_t done = 0;   // iterations issued (rows of sumsq / force_hist used)
     // multi-GPU overlap: boundary tiles -> remote pack -> NCCL on `comm_s`
     // while the interior tiles run on the work stream (run_split)
@@ -712,7 +713,7 @@ extern "C" int hbgpu_engine_rewind(hbgpu_engine *e, void *stream) {
 }
 
 static int iterate_on(hbgpu_engine *e, int32_t iterations, int32_t use_graph, cudaStream_t s) {
-    if (!use_graph) {
+    if (!use_graph || e->graph_failed) {
         for (int it = 0; it < iterations; ++it) {
             int rc = one_iteration(e, s);
             if (rc) return rc;
@@ -731,19 +732,18 @@ static int iterate_on(hbgpu_engine *e, int32_t iterations, int32_t use_graph, cu
         ce = cudaStreamEndCapture(s, &g);
         // captured launches are counted when the graph replays
         g_launches.store(before);
-        if (rc) {
+        if (!rc && ce == cudaSuccess) ce = cudaGraphInstantiate(&e->exec, g, 0);
+        if (rc || ce != cudaSuccess) {
+            // Nothing of the iteration has run (it was only being recorded).
+            // An operation that cannot be captured -- e.g. a collective of a
+            // communicator library that refuses stream capture -- must not
+            // end the run: this engine issues its iterations eagerly from now
+            // on; a real error shows again there and is returned.
             if (g) cudaGraphDestroy(g);
-            return rc;
-        }
-        if (ce != cudaSuccess) {
-            hbgpu_set_error("cudaStreamEndCapture: %s", cudaGetErrorString(ce));
-            return HBGPU_ERR_CUDA;
-        }
-        ce = cudaGraphInstantiate(&e->exec, g, 0);
-        if (ce != cudaSuccess) {
-            cudaGraphDestroy(g);
-            hbgpu_set_error("cudaGraphInstantiate: %s", cudaGetErrorString(ce));
-            return HBGPU_ERR_CUDA;
+            e->exec = nullptr;
+            cudaGetLastError();
+            e->graph_failed = true;
+            return iterate_on(e, iterations, 0, s);
         }
         e->graph = g;
     }
