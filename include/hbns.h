@@ -46,6 +46,8 @@ typedef struct hbns_block {
                             order (blocks ascending, sides S/N/W/E, cells)    */
 } hbns_block;
 
+#define HBNS_FLAG_D_CIRCULANT 1
+
 typedef struct hbns_args {
     double *w[3];                /* state slots: 0 = iteration start         */
     double *r;                   /* residual pool                             */
@@ -76,10 +78,16 @@ typedef struct hbns_args {
     int32_t max_len, max_cells;  /* largest block side, largest ni * nj       */
     int32_t max_ni, max_nj;      /* largest ni, largest nj (residual grid)    */
     int32_t nglobal, nwall;      /* blocks / wall faces of the whole job      */
-    int32_t stage, pad_;         /* RK stage (0..3) of the next hbns_stage:
+    int32_t stage, flags;        /* RK stage (0..3) of the next hbns_stage:
                                     status keys are ((iter*4 + stage + 1) << 40)
                                     | (n, k, j, i) index, an atomicMin keeps the
                                     first offending stage, then cell          */
+    /* flags: HBNS_FLAG_D_CIRCULANT (1) = dmat is bitwise circulant and
+     * antisymmetric with a +0 diagonal, as the reference's spectral_matrix
+     * (hbcore.py:88-94) is: the update then multiplies by the N_H constants
+     * D[k][0] and shares each product between rows m + k and m - k -- the
+     * same values, as (-d) w == -(d w) and s + (-x) == s - x in IEEE
+     * arithmetic.  Only set it after checking the matrix on the host.       */
 } hbns_args;
 
 int hbns_boundaries(const hbns_args *a, int32_t slot, void *stream);

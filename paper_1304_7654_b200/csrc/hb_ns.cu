@@ -308,7 +308,7 @@ __device__ __forceinline__ void stage_row(double *sdst, const double *grow, int 
 // ascending) added to R_n, W^(s) = W^0 - (alpha_s dt / V) R.  The time-step
 // and update kernels of the unfused schedule are gone: their inputs are
 // already on chip (primitives, normals) or in L2 (R, W_m).
-template <bool VISC, int P, int MINB>
+template <bool VISC, int P, int MINB, bool DSHARE>
 __global__ void __launch_bounds__(FLUX_THREADS, MINB)
     ns_stage_kernel(hbns_args a, const double *w, const double *w0, double *w_out, double coef, int first, int iter) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -502,6 +502,9 @@ __global__ void __launch_bounds__(FLUX_THREADS, MINB)
         const bool per_n = a.Pg > 1;
         const int64_t wstride = (int64_t)NV * wplane;   // snapshot stride, state pools
         const int64_t rstride = (int64_t)NV * rplane;   // snapshot stride, residual pool
+        double dk[P / 2 + 1];   // d_k = D[k][0] (DSHARE)
+#pragma unroll
+        for (int kk = 1; kk <= P / 2; ++kk) dk[kk] = DSHARE ? S.dmat[kk * P] : 0.0;
         for (int k = 0; k < NV; ++k) {
             const int64_t wo = b.w_off + k * wplane + cell_w, ro = b.r_off + k * rplane + cell_r;
             // W_m of every snapshot first (they feed every n).  LAZY 0: R_n
@@ -518,6 +521,33 @@ __global__ void __launch_bounds__(FLUX_THREADS, MINB)
                 if (LAZY < 1) qn[m] = w0[wo + m * wstride];
             }
             double rn_next = LAZY == 2 ? a.r[ro] : 0.0, qn_next = LAZY >= 1 ? w0[wo] : 0.0;
+            // sum_m D[n][m] W_m for every n at once when D is circulant and
+            // antisymmetric (HBNS_FLAG_D_CIRCULANT): D[m+k][m] = d_k and
+            // D[m-k][m] = -d_k bitwise, so one product d_k W_m serves row m + k
+            // (added) and row m - k (subtracted) -- (-d) w == -(d w) and
+            // s + (-x) == s - x exactly -- and the +0 diagonal term is the zero
+            // carrying W_m's sign.  Every row still receives its terms in m
+            // ascending order, the first one (m = 0) unadded, as specified.
+            double hb[DSHARE ? P : 1];
+            if (DSHARE) {
+                hb[0] = hbgpu::zero_times(wm[0]);
+#pragma unroll
+                for (int kk = 1; kk <= P / 2; ++kk) {
+                    const double prod = mul(dk[kk], wm[0]);
+                    hb[kk] = prod;
+                    hb[P - kk] = -prod;
+                }
+#pragma unroll
+                for (int m = 1; m < P; ++m) {
+#pragma unroll
+                    for (int kk = 1; kk <= P / 2; ++kk) {
+                        const double prod = mul(dk[kk], wm[m]);
+                        hb[(m + kk) % P] = add(hb[(m + kk) % P], prod);
+                        hb[(m + P - kk) % P] = sub(hb[(m + P - kk) % P], prod);
+                    }
+                    hb[m] = add(hb[m], hbgpu::zero_times(wm[m]));
+                }
+            }
 #pragma unroll
             for (int n = 0; n < P; ++n) {
                 double qn_n, rn_n;
@@ -538,9 +568,14 @@ __global__ void __launch_bounds__(FLUX_THREADS, MINB)
                     V = volc[(int64_t)n * wplane];
                     cdt = dv(mul(coef, dtc), V);
                 }
-                double s = mul(S.dmat[n * P], wm[0]);
+                double s;
+                if (DSHARE) {
+                    s = hb[n];
+                } else {
+                    s = mul(S.dmat[n * P], wm[0]);
 #pragma unroll
-                for (int m = 1; m < P; ++m) s = add(s, mul(S.dmat[n * P + m], wm[m]));
+                    for (int m = 1; m < P; ++m) s = add(s, mul(S.dmat[n * P + m], wm[m]));
+                }
                 const double R = add(rn_n, mul(V, s));
                 if (first && k == 0) sq = __fma_rn(R, R, sq);
                 const double v = sub(qn_n, mul(cdt, R));
@@ -720,22 +755,30 @@ extern "C" int hbns_boundaries(const hbns_args *a, int32_t slot, void *stream) {
     return check("hbns_boundaries");
 }
 
-template <bool VISC, int P, int MINB>
-static int stage_launch_k(const hbns_args *a, int32_t slot_in, int32_t slot_out, double coef, int first, int iter,
+template <bool VISC, int P, int MINB, bool DSHARE>
+static int stage_launch_kd(const hbns_args *a, int32_t slot_in, int32_t slot_out, double coef, int first, int iter,
                           int64_t tiles, cudaStream_t s) {
     static bool ready[hbgpu::HB_MAX_DEVICES];
     const int dev = hbgpu::current_device();
     if (dev < 0) return HBGPU_ERR_CUDA;
     const size_t smem = sizeof(FluxSmem);
     if (!ready[dev]) {
-        if (cudaFuncSetAttribute(ns_stage_kernel<VISC, P, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(ns_stage_kernel<VISC, P, MINB, DSHARE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem) != cudaSuccess)
             return check("hbns_stage (smem attribute)");
         ready[dev] = true;
     }
-    ns_stage_kernel<VISC, P, MINB><<<dim3((unsigned)tiles, a->nblocks), FLUX_THREADS, smem, s>>>(
+    ns_stage_kernel<VISC, P, MINB, DSHARE><<<dim3((unsigned)tiles, a->nblocks), FLUX_THREADS, smem, s>>>(
         *a, a->w[slot_in], a->w[0], a->w[slot_out], coef, first, iter);
     return HBGPU_OK;
+}
+
+template <bool VISC, int P, int MINB>
+static int stage_launch_k(const hbns_args *a, int32_t slot_in, int32_t slot_out, double coef, int first, int iter,
+                          int64_t tiles, cudaStream_t s) {
+    if (a->flags & HBNS_FLAG_D_CIRCULANT)
+        return stage_launch_kd<VISC, P, MINB, true>(a, slot_in, slot_out, coef, first, iter, tiles, s);
+    return stage_launch_kd<VISC, P, MINB, false>(a, slot_in, slot_out, coef, first, iter, tiles, s);
 }
 
 // CTAs per SM the kernel variant is compiled for.  Viscous: 2 (96 registers).
@@ -750,17 +793,20 @@ static int stage_launch(const hbns_args *a, int32_t slot_in, int32_t slot_out, d
 #ifdef HBNS_FLUX_MINB
     return stage_launch_k<VISC, P, HBNS_FLUX_MINB>(a, slot_in, slot_out, coef, first, iter, tiles, s);
 #else
-    if (VISC) return stage_launch_k<VISC, P, 2>(a, slot_in, slot_out, coef, first, iter, tiles, s);
-    static int sms[hbgpu::HB_MAX_DEVICES];
-    const int dev = hbgpu::current_device();
-    if (dev < 0) return HBGPU_ERR_CUDA;
-    if (sms[dev] == 0 && cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-        return check("hbns_stage (SM count)");
-    const int64_t total = tiles * a->nblocks;
-    const int64_t waves3 = (total + 3 * sms[dev] - 1) / (3 * sms[dev]), waves2 = (total + 2 * sms[dev] - 1) / (2 * sms[dev]);
-    if (0.733 * (double)waves2 < (double)waves3)
+    if constexpr (VISC) {
         return stage_launch_k<VISC, P, 2>(a, slot_in, slot_out, coef, first, iter, tiles, s);
-    return stage_launch_k<VISC, P, 3>(a, slot_in, slot_out, coef, first, iter, tiles, s);
+    } else {
+        static int sms[hbgpu::HB_MAX_DEVICES];
+        const int dev = hbgpu::current_device();
+        if (dev < 0) return HBGPU_ERR_CUDA;
+        if (sms[dev] == 0 && cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            return check("hbns_stage (SM count)");
+        const int64_t total = tiles * a->nblocks;
+        const int64_t waves3 = (total + 3 * sms[dev] - 1) / (3 * sms[dev]), waves2 = (total + 2 * sms[dev] - 1) / (2 * sms[dev]);
+        if (0.733 * (double)waves2 < (double)waves3)
+            return stage_launch_k<VISC, P, 2>(a, slot_in, slot_out, coef, first, iter, tiles, s);
+        return stage_launch_k<VISC, P, 3>(a, slot_in, slot_out, coef, first, iter, tiles, s);
+    }
 #endif
 }
 

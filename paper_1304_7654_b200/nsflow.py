@@ -325,6 +325,11 @@ def initial_state(case, block, seed=13047654):
     return q
 
 
+def circulant_antisymmetric(mat):
+    from .hbop import circulant_antisymmetric as ca
+    return ca(mat)
+
+
 def spectral_matrix(case):
     from .hbop import spectral_matrix as sm
     return np.ascontiguousarray(sm(case.nharms, case.omega).matrix)
@@ -466,7 +471,7 @@ def _ns_types():
                     ("norms", vp), ("forces", vp), ("blk_norms", vp), ("wall_prod", vp), ("iter_dev", vp), ("mu", f64), ("cfl", f64), ("omega_nh", f64), ("kq", f64),
                     ("nblocks", i32), ("P", i32), ("Pg", i32), ("moving", i32), ("max_len", i32),
                     ("max_cells", i32), ("max_ni", i32), ("max_nj", i32), ("nglobal", i32), ("nwall", i32),
-                    ("stage", i32), ("pad_", i32)]
+                    ("stage", i32), ("flags", i32)]
     return Block, Args
 
 
@@ -546,7 +551,10 @@ class NSRun:
                     for k, v in pools.items()}
         self.t_blocks = torch.frombuffer(bytearray(bytes(table)), dtype=torch.uint8).to(dev)
         self.winf = torch.from_numpy(np.ascontiguousarray(freestream(case))).to(dev)
-        self.dmat = torch.from_numpy(spectral_matrix(case).copy()).to(dev)
+        dmat_host = spectral_matrix(case).copy()
+        self.dmat = torch.from_numpy(dmat_host).to(dev)
+        # HBNS_FLAG_D_CIRCULANT: the update may share D products between rows m +- k
+        self.d_circulant = bool(circulant_antisymmetric(dmat_host))
         self.status = torch.full((len(blocks),), -1, dtype=torch.int64, device=dev)
         self.norm_part = torch.zeros(len(blocks) * ctas, dtype=f64, device=dev)
         self.norms = torch.zeros(max(1, max_iters), dtype=f64, device=dev)
@@ -580,6 +588,7 @@ class NSRun:
         a.mu, a.cfl, a.omega_nh = case.mu, case.cfl, case.omega * case.nharms
         a.kq = (case.mu * GAMMA) / PR    # the specification's (mu gamma) / Pr, one IEEE mul and div
         a.nblocks, a.P, a.Pg, a.moving = len(blocks), P, Pg, int(moving)
+        a.flags = 1 if self.d_circulant else 0   # HBNS_FLAG_D_CIRCULANT
         a.max_len = max(max(b.ni, b.nj) for b in blocks)
         a.max_cells = max_cells
         a.max_ni, a.max_nj = max(b.ni for b in blocks), max(b.nj for b in blocks)
