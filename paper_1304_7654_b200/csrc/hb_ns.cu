@@ -31,6 +31,8 @@
 
 #include "hbns.h"
 
+#include <type_traits>
+
 namespace hbns {
 
 constexpr double GAMMA = 1.4;
@@ -505,87 +507,94 @@ __global__ void __launch_bounds__(FLUX_THREADS, MINB)
         double dk[P / 2 + 1];   // d_k = D[k][0] (DSHARE)
 #pragma unroll
         for (int kk = 1; kk <= P / 2; ++kk) dk[kk] = DSHARE ? S.dmat[kk * P] : 0.0;
-        for (int k = 0; k < NV; ++k) {
-            const int64_t wo = b.w_off + k * wplane + cell_w, ro = b.r_off + k * rplane + cell_r;
-            // W_m of every snapshot first (they feed every n).  LAZY 0: R_n
-            // and W^0_n of every snapshot loaded up front as well (3 P values
-            // held); 1: W^0_n one snapshot ahead of its use; 2: R_n too (P + 4
-            // values held).  W^0_n is always loaded before the store that may
-            // replace it (stage 4 writes W^0's slot).
-            constexpr int LAZY = VISC ? HBNS_UPDATE_LAZY_VISC : HBNS_UPDATE_LAZY;
-            double wm[P], rn[LAZY < 2 ? P : 1], qn[LAZY < 1 ? P : 1];
-#pragma unroll
-            for (int m = 0; m < P; ++m) {
-                wm[m] = w[wo + m * wstride];
-                if (LAZY < 2) rn[m] = a.r[ro + m * rstride];
-                if (LAZY < 1) qn[m] = w0[wo + m * wstride];
-            }
-            double rn_next = LAZY == 2 ? a.r[ro] : 0.0, qn_next = LAZY >= 1 ? w0[wo] : 0.0;
-            // sum_m D[n][m] W_m for every n at once when D is circulant and
-            // antisymmetric (HBNS_FLAG_D_CIRCULANT): D[m+k][m] = d_k and
-            // D[m-k][m] = -d_k bitwise, so one product d_k W_m serves row m + k
-            // (added) and row m - k (subtracted) -- (-d) w == -(d w) and
-            // s + (-x) == s - x exactly -- and the +0 diagonal term is the zero
-            // carrying W_m's sign.  Every row still receives its terms in m
-            // ascending order, the first one (m = 0) unadded, as specified.
-            double hb[DSHARE ? P : 1];
-            if (DSHARE) {
-                hb[0] = hbgpu::zero_times(wm[0]);
-#pragma unroll
-                for (int kk = 1; kk <= P / 2; ++kk) {
-                    const double prod = mul(dk[kk], wm[0]);
-                    hb[kk] = prod;
-                    hb[P - kk] = -prod;
+        // the loop in two copies, selected once: a run-time per_n inside it made the
+        // compiler form the moving-mesh division for every (variable, snapshot)
+        auto update = [&](auto per_n_tag) {
+            constexpr bool PER_N = decltype(per_n_tag)::value;
+            for (int k = 0; k < NV; ++k) {
+                const int64_t wo = b.w_off + k * wplane + cell_w, ro = b.r_off + k * rplane + cell_r;
+                // W_m of every snapshot first (they feed every n).  LAZY 0: R_n
+                // and W^0_n of every snapshot loaded up front as well (3 P values
+                // held); 1: W^0_n one snapshot ahead of its use; 2: R_n too (P + 4
+                // values held).  W^0_n is always loaded before the store that may
+                // replace it (stage 4 writes W^0's slot).
+                constexpr int LAZY = VISC ? HBNS_UPDATE_LAZY_VISC : HBNS_UPDATE_LAZY;
+                double wm[P], rn[LAZY < 2 ? P : 1], qn[LAZY < 1 ? P : 1];
+    #pragma unroll
+                for (int m = 0; m < P; ++m) {
+                    wm[m] = w[wo + m * wstride];
+                    if (LAZY < 2) rn[m] = a.r[ro + m * rstride];
+                    if (LAZY < 1) qn[m] = w0[wo + m * wstride];
                 }
-#pragma unroll
-                for (int m = 1; m < P; ++m) {
-#pragma unroll
-                    for (int kk = 1; kk <= P / 2; ++kk) {
-                        const double prod = mul(dk[kk], wm[m]);
-                        hb[(m + kk) % P] = add(hb[(m + kk) % P], prod);
-                        hb[(m + P - kk) % P] = sub(hb[(m + P - kk) % P], prod);
-                    }
-                    hb[m] = add(hb[m], hbgpu::zero_times(wm[m]));
-                }
-            }
-#pragma unroll
-            for (int n = 0; n < P; ++n) {
-                double qn_n, rn_n;
-                if (LAZY >= 1) {
-                    qn_n = qn_next;
-                    if (n + 1 < P) qn_next = w0[wo + (n + 1) * wstride];
-                } else {
-                    qn_n = qn[n];
-                }
-                if (LAZY == 2) {
-                    rn_n = rn_next;
-                    if (n + 1 < P) rn_next = a.r[ro + (n + 1) * rstride];
-                } else {
-                    rn_n = rn[n];
-                }
-                double V = V0, cdt = cdt0;
-                if (per_n) {
-                    V = volc[(int64_t)n * wplane];
-                    cdt = dv(mul(coef, dtc), V);
-                }
-                double s;
+                double rn_next = LAZY == 2 ? a.r[ro] : 0.0, qn_next = LAZY >= 1 ? w0[wo] : 0.0;
+                // sum_m D[n][m] W_m for every n at once when D is circulant and
+                // antisymmetric (HBNS_FLAG_D_CIRCULANT): D[m+k][m] = d_k and
+                // D[m-k][m] = -d_k bitwise, so one product d_k W_m serves row m + k
+                // (added) and row m - k (subtracted) -- (-d) w == -(d w) and
+                // s + (-x) == s - x exactly -- and the +0 diagonal term is the zero
+                // carrying W_m's sign.  Every row still receives its terms in m
+                // ascending order, the first one (m = 0) unadded, as specified.
+                double hb[DSHARE ? P : 1];
                 if (DSHARE) {
-                    s = hb[n];
-                } else {
-                    s = mul(S.dmat[n * P], wm[0]);
-#pragma unroll
-                    for (int m = 1; m < P; ++m) s = add(s, mul(S.dmat[n * P + m], wm[m]));
+                    hb[0] = hbgpu::zero_times(wm[0]);
+    #pragma unroll
+                    for (int kk = 1; kk <= P / 2; ++kk) {
+                        const double prod = mul(dk[kk], wm[0]);
+                        hb[kk] = prod;
+                        hb[P - kk] = -prod;
+                    }
+    #pragma unroll
+                    for (int m = 1; m < P; ++m) {
+    #pragma unroll
+                        for (int kk = 1; kk <= P / 2; ++kk) {
+                            const double prod = mul(dk[kk], wm[m]);
+                            hb[(m + kk) % P] = add(hb[(m + kk) % P], prod);
+                            hb[(m + P - kk) % P] = sub(hb[(m + P - kk) % P], prod);
+                        }
+                        hb[m] = add(hb[m], hbgpu::zero_times(wm[m]));
+                    }
                 }
-                const double R = add(rn_n, mul(V, s));
-                if (first && k == 0) sq = __fma_rn(R, R, sq);
-                const double v = sub(qn_n, mul(cdt, R));
-                w_out[wo + n * wstride] = v;
-                if (!isfinite(v)) {
-                    const long long lin = (((long long)(n * NV + k) * b.nj + (cj - 1)) * b.ni) + (ci - 1);
-                    atomicMin(a.status + blockIdx.y, hbgpu::divergence_key(gstage, lin));
+    #pragma unroll
+                for (int n = 0; n < P; ++n) {
+                    double qn_n, rn_n;
+                    if (LAZY >= 1) {
+                        qn_n = qn_next;
+                        if (n + 1 < P) qn_next = w0[wo + (n + 1) * wstride];
+                    } else {
+                        qn_n = qn[n];
+                    }
+                    if (LAZY == 2) {
+                        rn_n = rn_next;
+                        if (n + 1 < P) rn_next = a.r[ro + (n + 1) * rstride];
+                    } else {
+                        rn_n = rn[n];
+                    }
+                    double V = V0, cdt = cdt0;
+                    if (PER_N) {
+                        V = volc[(int64_t)n * wplane];
+                        cdt = dv(mul(coef, dtc), V);
+                    }
+                    double s;
+                    if (DSHARE) {
+                        s = hb[n];
+                    } else {
+                        s = mul(S.dmat[n * P], wm[0]);
+    #pragma unroll
+                        for (int m = 1; m < P; ++m) s = add(s, mul(S.dmat[n * P + m], wm[m]));
+                    }
+                    const double R = add(rn_n, mul(V, s));
+                    if (first && k == 0) sq = __fma_rn(R, R, sq);
+                    const double v = sub(qn_n, mul(cdt, R));
+                    w_out[wo + n * wstride] = v;
+                    if (!isfinite(v)) {
+                        const long long lin = (((long long)(n * NV + k) * b.nj + (cj - 1)) * b.ni) + (ci - 1);
+                        atomicMin(a.status + blockIdx.y, hbgpu::divergence_key(gstage, lin));
+                    }
                 }
             }
-        }
+        };
+        if (per_n) update(std::true_type{});
+        else update(std::false_type{});
     }
     // the tile's residual rows are consumed: drop their L2 lines without a
     // write-back (only whole 128-B lines inside this tile's row segments)
