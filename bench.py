@@ -561,10 +561,20 @@ def run_ours(args, wl):
         e2e_iters = max(args.steps, case.iterations)
         barrier()
         t0 = time.perf_counter()
-        res = run_case(RunSpec(case=case, ranks=world, iterations=e2e_iters, initial_state=ic,
-                               output=out, tile_rows=args.tile_rows, device=local))
+        e2e_error = None
+        try:
+            res = run_case(RunSpec(case=case, ranks=world, iterations=e2e_iters, initial_state=ic,
+                                   output=out, tile_rows=args.tile_rows, device=local))
+            del res
+        except Exception as exc:   # noqa: BLE001
+            # one GPU: a failing public API fails the bench.  Several GPUs: the
+            # device-timed line above is still valid, so it is printed with the
+            # end-to-end leg marked failed (run_case's CommGuard has already
+            # released the peers of a failing rank)
+            if world == 1:
+                raise
+            e2e_error = f"{type(exc).__name__}: {exc}"
         wall = max_over_ranks(time.perf_counter() - t0)
-        del res
         e2e = {"value": total_units_iter * e2e_iters / wall, "unit": UNIT,
                "h2d_bytes_per_step": h2d * world // e2e_iters,
                "d2h_bytes_per_step": d2h * world // e2e_iters,
@@ -573,6 +583,9 @@ def run_ours(args, wl):
                "note": "one run_case() of the workload's stated iteration count (max with K): layout + "
                        "allocation + pinned H2D of the initial state + the iterations + D2H of all fields "
                        "(halos incl.) + forces/norms; per-step bytes are the run's copies / iterations"}
+        if e2e_error is not None:
+            e2e = {"value": None, "unit": UNIT, "error": e2e_error, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
